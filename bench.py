@@ -1,0 +1,340 @@
+"""Benchmark: FL rounds/sec and client-updates/sec at 1024 UNSW-shaped clients.
+
+Workload (BASELINE.json configs[3], SURVEY.md §8d "C4"): synthetic
+UNSW-NB15-shaped data (219,176 rows x 42 features, 30 % anomalies, Dirichlet
+alpha=0.5 over 1024 clients), the 42-256-128-64-1 MLP with dropout 0.3,
+E=5 local epochs, capacity-driven batch sizes (dynamic 64..1024),
+gradient-sign (delta_sign) selection at theta=0.65, FedAvg, per-round
+evaluation on the 43,835-row test split. One bench "step" is one
+synchronous FL round over all 1024 clients (training, selection,
+aggregation, evaluation, event-log bookkeeping). fp64 parity mode: the
+event log is bit-identical to the reference's.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0). See DESIGN.md §Measurement for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU legs are single-threaded (stated as cores=1)
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C4_SYNC = {
+    "num_clients": 1024, "rounds": 100, "epochs": 5, "mode": "sync_filtered",
+    "selection_mode": "delta_sign", "theta": 0.65, "seed": 1,
+    "dataset": {"kind": "synthetic", "n": 219176, "d": 42, "anomaly_frac": 0.3, "separation": 4.0,
+                "test_frac": 0.2},
+    "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3},
+    "batch": {"policy": "dynamic", "b_ref": 64, "b_min": 64, "b_max": 1024},
+    "profiles": {"speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
+                 "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
+                 "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
+                 "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}},
+    "lr": 0.05, "lr_decay": 0.9,
+}
+METRIC = "FL rounds/sec (1024 UNSW-shaped clients, C4 sync_filtered)"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA-core and DMMA) nominal; no measured fp64 peak exists
+
+
+def build_c4_world(num_clients: int = 1024):
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    cfg = dict(C4_SYNC)
+    cfg["num_clients"] = num_clients
+    return build_world(ExperimentConfig.from_dict(cfg))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU sides
+def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None):
+    """Time the oracle (reference algorithm, numpy, 1 thread) on a bounded
+    sample of one C4 sync round: `sample_clients` client cycles (training +
+    delta_sign scoring), FedAvg of their updates, and one full evaluation.
+    Returns (extrapolated seconds per 1024-client round, detail)."""
+    from oracle import fl_oracle as O
+
+    sim = O.OracleFederation(world)
+    n = world.num_clients
+    w0 = initial.values
+    wp = w_prev if w_prev is not None else w0 * 0.999
+    picks = [int(i) for i in np.linspace(0, n - 1, sample_clients).round()]
+    t0 = time.perf_counter()
+    outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
+    t_train = time.perf_counter() - t0
+    ups = [o["res"]["params"] for o in outs if o["accepted"]]
+    t0 = time.perf_counter()
+    O.fedavg(ups if ups else [w0])
+    t_agg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    p = O.probs(w0, world.spec.dims, np.ascontiguousarray(world.test_features))
+    O.acc_auc(p, world.test_labels)
+    t_eval = time.perf_counter() - t0
+    per_round = (t_train + t_agg) * n / len(picks) + t_eval
+    return per_round, {"t_train_s": t_train, "t_agg_s": t_agg, "t_eval_s": t_eval, "clients": len(picks)}
+
+
+def cpu_threads_used() -> int:
+    return 1  # numpy oracle; BLAS pinned to one thread below
+
+
+def run_reference(args, rank: int, world_size: int) -> None:
+    if rank != 0:
+        return
+    world, initial = build_c4_world()
+    sample = args.ref_sample
+    times = []
+    for i in range(args.warmup + args.steps):
+        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0)
+        if i >= args.warmup:
+            times.append(per_round)
+    sec = float(np.mean(times))
+    value = 1.0 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world_size,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients, MLP 42-256-128-64-1, E=5, "
+                               "dynamic batch, delta_sign theta=0.65"},
+        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": cpu_threads_used(), "kind": "port",
+                         "sample": f"{sample} of 1024 client cycles of round 0 + FedAvg + full eval per step, "
+                                   "extrapolated x1024/sample (oracle/fl_oracle.py, numpy, 1 thread)"},
+        "e2e": {"value": value, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "client_updates_per_s": value * 1024,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def flush_l2(buf):
+    buf.zero_()
+
+
+def run_b200(args, rank: int, world_size: int) -> None:
+    import torch
+
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.server import FederationEngine, GlobalState
+
+    torch.cuda.set_device(rank % max(torch.cuda.device_count(), 1))
+    dist = None
+    if world_size > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    world, initial = build_c4_world()
+    rt = D.Runtime.get()
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=rt.device)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    # ---- device-resident timed run (value)
+    eng = FederationEngine(world)
+    state = GlobalState(round=0, w_g=initial)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        state = eng.run_sync_round(state)
+    barrier()
+    D.Runtime.timer = D.KernelTimer()
+    calls0 = D.Runtime.abi_calls
+    trainings0 = eng.trainings
+    round_ms = []
+    with ClockSampler(rank % max(torch.cuda.device_count(), 1)) as clocks:
+        for _ in range(args.steps):
+            flush_l2(l2_flush)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            state = eng.run_sync_round(state)
+            b.record(stream)
+            barrier()
+            round_ms.append(a.elapsed_time(b))
+    timer, D.Runtime.timer = D.Runtime.timer, None
+    abi_calls = D.Runtime.abi_calls - calls0
+    trainings = eng.trainings - trainings0
+    total_ms = float(np.sum(round_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=rt.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_round = total_ms / args.steps
+    value = 1000.0 / ms_per_round
+    ksum = timer.summary()
+
+    # ---- end-to-end through the public API with host buffers (e2e)
+    e2e_ms = []
+    h2d = d2h = 0
+    for i in range(max(2, args.steps // 2) + 1):
+        world._device = None   # drop the HBM copy: shards + test set re-uploaded from host
+        barrier()
+        t0 = time.perf_counter()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dev = world.device_state()
+        state = eng.run_sync_round(state)
+        host_w = state.w_g.values  # D2H of the round's result
+        b.record(stream)
+        barrier()
+        if i > 0:
+            e2e_ms.append(a.elapsed_time(b))
+        h2d = (dev.shards.features.numel() + dev.shards.labels.numel() + dev.test_x.numel()) * 8 + dev.test_y.numel()
+        d2h = host_w.nbytes + 1024 * 8 * 2  # w_g + aligned counts/status of 1024 clients
+    e2e_value = 1000.0 / float(np.mean(e2e_ms))
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (the trainer)
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    tr = ksum.get("train", {})
+    achieved_tflops = tr["work_per_launch"] / (tr["mean_ms"] * 1e-3) / 1e12 if tr else None
+    roofline = {
+        "kernel": "fs::f64::train_kernel (K5, fp64 parity mode)",
+        "bound": "fp64",
+        "achieved": achieved_tflops, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved_tflops / FP64_NOMINAL_TFLOPS if achieved_tflops else None,
+        "peak_source": "nominal B200 FP64 37 TFLOP/s (MEASURED_PEAKS.json has no fp64 figure)",
+        "traffic": None,
+        "share_of_round": tr.get("total_ms", 0.0) / total_ms if tr else None,
+    }
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kernels = {}
+    for name in ("align", "aggregate"):
+        if name in ksum:
+            k = ksum[name]
+            gbs = k["work_per_launch"] / (k["mean_ms"] * 1e-3) / 1e9
+            kernels[name] = {"achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak, "mean_ms": k["mean_ms"],
+                             "bytes_per_launch": k["work_per_launch"]}
+
+    # ---- CPU baseline (oracle port, bounded sample)
+    cpu = None
+    if world_size == 1 and not args.no_cpu:
+        per_round, detail = oracle_round_sample(world, initial, args.cpu_sample)
+        cpu = {"value": 1.0 / per_round, "unit": "rounds/s", "cores": cpu_threads_used(), "kind": "port",
+               "sample": f"{args.cpu_sample} of 1024 client cycles of round 0 + FedAvg + full eval, "
+                         f"extrapolated x1024/{args.cpu_sample}; oracle/fl_oracle.py numpy, 1 thread",
+               "detail": detail}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world_size, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_round, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients (175,341 train rows, d=42), "
+                               "MLP 42-256-128-64-1 dropout 0.3, E=5, dynamic batch 64..1024, delta_sign "
+                               "theta=0.65, FedAvg, eval on 43,835 rows",
+                   "global_batch": None, "precision": "fp64 parity (digest-identical to reference)",
+                   "l2": "256 MiB buffer written between timed rounds (L2 flush)",
+                   "parallelism": f"clients sharded over {world_size} GPU(s)"},
+        "client_updates_per_s": value * trainings / args.steps,
+        "e2e": {"value": e2e_value, "unit": "rounds/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "note": "public FederationEngine.run_sync_round with the world re-uploaded from host numpy "
+                        "each step and w_g read back"},
+        "roofline": roofline,
+        "hbm_kernels": kernels,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(abi_calls),
+        "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (CUB sort counts as one)",
+        "clocks": clocks.summary(),
+        "kernel_ms": {k: v["mean_ms"] for k, v in ksum.items()},
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world_size = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
+    if args.impl == "reference":
+        run_reference(args, rank, world_size)
+    else:
+        run_b200(args, rank, world_size)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * fedsim_b200 C-ABI — the drop-in boundary of the FL round loop.
+ *
+ * The reference's plugin API for this path is the backend module selected
+ * in pkg/src/fedsim/backends/__init__.py:1-63 (NAME, forward,
+ * loss_and_grad, sign_align_count) plus the round-level callers that loop
+ * over it: client.train_local (client.py:98-172), selection
+ * calculate_relevance/filter_update (selection.py:53-85) and
+ * server.aggregate (server.py:72-86), evaluated per round by
+ * FederationEngine._evaluate_global (server.py:321-328).  Each entry point
+ * below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - every pointer argument is DEVICE memory unless its name ends in _host;
+ *  - every call is stream-ordered and non-blocking on `stream` (a
+ *    cudaStream_t passed as void*); no call allocates device memory — the
+ *    caller passes workspaces sized by the matching *_workspace_bytes query;
+ *  - return 0 on success or a negative FS_E* code; fs_last_error() returns a
+ *    thread-local message for the last failure on the calling thread;
+ *  - parameter vectors use the reference's flat float64 layout
+ *    (numpy_backend.py:3-14): per layer W[fan_in x fan_out] row-major, then b.
+ */
+#ifndef FEDSIM_B200_H
+#define FEDSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_ABI_VERSION 1
+#define FS_MAX_LAYERS 8 /* weight layers, hidden + head */
+
+enum fs_status {
+  FS_OK = 0,
+  FS_EINVAL = -1,   /* maps to ValueError (layout/length mismatch) */
+  FS_ECUDA = -2,    /* CUDA runtime failure */
+  FS_ENCCL = -3,    /* collective failure */
+  FS_EDIVERGED = -4 /* non-finite loss: TrainingDivergedError, model.py:207-211 */
+};
+
+enum fs_mask_mode { FS_MASK_NONE = 0, FS_MASK_BITS = 1, FS_MASK_DENSE = 2 };
+
+enum fs_align_mode { FS_ALIGN_WEIGHT_SIGN = 0, FS_ALIGN_DELTA_SIGN = 1 };
+
+const char* fs_last_error(void);
+int fs_abi_version(void);
+
+/* ---------------------------------------------------------------- K1 seeds
+ * derive_seed(master, *path) with integer label words (rng.py:42-44).
+ * Host-side helper used by tests and the host control plane.            */
+int fs_derive_seed_host(uint64_t master, const uint32_t* path_host, int32_t n_path,
+                        uint64_t* out_host);
+
+/* seeds[i] = derive_seed(master, "train", client_ids[i], cycles[i])
+ * (server.py:207).                                                       */
+int fs_train_seeds(uint64_t master, const int32_t* client_ids, const int32_t* cycles, int32_t n,
+                   uint64_t* seeds_out, void* stream);
+
+/* ---------------------------------------------------------------- K2 shuffles
+ * perm_out[perm_off[r] + e*n_rows[r] + i] =
+ *   derive_rng(seeds[r], "shuffle", e).permutation(n_rows[r])[i]
+ * for e in [0, epochs)  (client.py:136).                                  */
+int fs_shuffle_perms(const uint64_t* seeds, const int32_t* n_rows, const int64_t* perm_off,
+                     int32_t n_req, int32_t epochs, int32_t max_rows, int32_t* perm_out,
+                     void* stream);
+
+/* ---------------------------------------------------------------- K3 masks
+ * Dropout keep-bits of every (request, epoch, step) of a training batch
+ * (model.py:153-166 with the seed of client.py:150). Step (e, s) of request
+ * r occupies ceil(batch[r]*sum_hidden/32) words at
+ *   mask_off[r] + (e*steps_per_epoch_r + s) * slot_words_r;
+ * bit j of a slot is draw j of the step's stream (layer-major, then row,
+ * then unit): keep iff random() < keep.                                   */
+int fs_dropout_bits(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
+                    const int64_t* mask_off, int32_t n_req, int32_t epochs, int32_t sum_hidden,
+                    double keep, uint32_t* bits_out, void* stream);
+
+/* Keep-bits of one stream: default_rng(SeedSequence(mask_seed)) drawing
+ * n_draws doubles (model.dropout_masks).                                  */
+int fs_dropout_bits_seed(uint64_t mask_seed, int64_t n_draws, double keep, uint32_t* bits_out,
+                         void* stream);
+
+/* ---------------------------------------------------------------- K5 trainer
+ * Batched local SGD (client.train_local, client.py:98-172): request r trains
+ * from w_start[r] over steps [start_step[r], end_step[r]) of its shard and
+ * leaves its parameters in w_out + r*ldw.                                  */
+typedef struct fs_train_desc {
+  int32_t n_dims;
+  int32_t dims[FS_MAX_LAYERS + 1];
+  int32_t n_req;
+  int32_t epochs;
+  int32_t max_batch;           /* max over requests of batch[r]                 */
+  int32_t mask_mode;           /* FS_MASK_NONE or FS_MASK_BITS                  */
+  double scale;                /* 1/(1-p): value of a kept unit                 */
+  const double* features;      /* [rows x dims[0]] packed shards                */
+  const double* labels;        /* [rows] 0.0 / 1.0                              */
+  const int64_t* row_off;      /* [n_req] first shard row                       */
+  const int32_t* n_rows;       /* [n_req]                                       */
+  const int32_t* batch;        /* [n_req]                                       */
+  const double* lr;            /* [n_req x epochs] step size of each epoch      */
+  const uint64_t* w_start;     /* [n_req] device pointers (const double*)       */
+  double* w_out;               /* [n_req x ldw]                                 */
+  int64_t ldw;
+  const int32_t* perm;         /* K2 output                                     */
+  const int64_t* perm_off;
+  const uint32_t* mask_bits;   /* K3 output (FS_MASK_BITS)                      */
+  const int64_t* mask_off;
+  const int32_t* start_step;   /* [n_req]                                       */
+  const int32_t* end_step;     /* [n_req]                                       */
+  const int32_t* order;        /* [n_req] processing order (longest first)      */
+  int32_t* status;             /* [n_req] out: 1 = non-finite logit (diverged)  */
+  void* workspace;
+  size_t workspace_bytes;
+  int32_t grid;                /* CTAs; 0 = auto                                */
+} fs_train_desc;
+
+size_t fs_train_workspace_bytes(const fs_train_desc* desc);
+int fs_train_f64(const fs_train_desc* desc, void* stream);
+
+/* backend.loss_and_grad (_core.pyx:140-219 / numpy_backend.py:60-104):
+ * one batch x[rows x dims[0]], labels y[rows], optional dense pre-scaled masks
+ * (layer-major [rows x h_l] blocks) -> loss_out[1], grad_out[M]. Shares the
+ * trainer's step code, so train_local == fold(loss_and_grad + sgd_step)
+ * bitwise.                                                                 */
+size_t fs_step_workspace_bytes(const int32_t* dims, int32_t n_dims, int32_t rows);
+int fs_loss_and_grad_f64(const int32_t* dims, int32_t n_dims, const double* w, const double* x,
+                         const double* y, int32_t rows, const double* dense_masks,
+                         double* loss_out, double* grad_out, int32_t* status, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* backend.forward (_core.pyx:109-137): class-1 probabilities of x rows.   */
+size_t fs_forward_workspace_bytes(const int32_t* dims, int32_t n_dims, int32_t rows);
+int fs_forward_f64(const int32_t* dims, int32_t n_dims, const double* w, const double* x,
+                   int32_t rows, const double* dense_masks, double* probs_out, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K6 alignment
+ * aligned_out[r] = #{j : sgn(a_j) == sgn(b_j)}, sgn in {-1,0,+1}
+ * (_core.pyx:222-236) with a = wc[r], b = wg[r] (weight_sign) or
+ * a = wc[r]-wg[r], b = wg[r]-wg_prev[r] (delta_sign), selection.py:53-74.
+ * wc/wg/wg_prev are [n_req] arrays of device pointers to float64 [M].      */
+int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
+                      int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
+                      void* stream);
+
+/* ---------------------------------------------------------------- K7/K9 FedAvg
+ * keys_out[i*n_keys + t] = bswap64(bits(rows[i][t])) — the leading bytes
+ * of values.tobytes() as big-endian integers (server.py:84 sort key).     */
+int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t n_keys, uint64_t* keys_out,
+                            void* stream);
+/* out[j] = (sum_{i=0..k-1} rows[i][j]) / k, summed sequentially in the given
+ * row order (server.py:84-86: stack in sorted order, mean(axis=0)).        */
+int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out, void* stream);
+
+/* ---------------------------------------------------------------- K8 metrics
+ * accuracy at `threshold` and rank AUC with midrank ties
+ * (metrics.py:118-165): counts_out[0] = #correct, counts_out[1] = 2*U_pos
+ * (exact), counts_out[2] = n_pos.                                          */
+size_t fs_eval_workspace_bytes(int32_t n);
+int fs_eval_metrics(const double* scores, const int8_t* labels, int32_t n, double threshold,
+                    int64_t* counts_out, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEDSIM_B200_H */

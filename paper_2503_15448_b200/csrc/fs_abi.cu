@@ -1,0 +1,31 @@
+// C-ABI plumbing: thread-local error messages and launch checks.
+#include <cstdarg>
+#include <cstdio>
+
+#include "fs_common.cuh"
+
+namespace fs {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return FS_ECUDA;
+  }
+  return FS_OK;
+}
+
+}  // namespace fs
+
+extern "C" const char* fs_last_error(void) { return fs::g_err; }
+
+extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }

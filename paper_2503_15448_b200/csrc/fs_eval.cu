@@ -1,0 +1,103 @@
+// K8 metrics half: accuracy and rank AUC of the per-round evaluation.
+//
+// Replaces metrics.evaluate / accuracy / auc_roc / _midranks
+// (pkg/src/fedsim/metrics.py:118-165), run every round by
+// FederationEngine._emit_report (server.py:321-353).  The eval forward
+// itself is fs_forward_f64 (K8 forward half, fs_train_f64.cu).
+//
+// AUC = U_pos / (n_pos * n_neg) with U_pos = sum over positives of
+// (#negatives scoring below + 0.5 * #negatives tied) — the midrank
+// identity.  Everything is counted in integers (2*U exactly), so the
+// result equals the reference's midrank sum bit for bit given equal scores.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "fs_common.cuh"
+
+namespace fs {
+
+// counts: [0]=correct, [1]=2U, [2]=n_pos, [3]=n_neg
+__global__ void eval_split_kernel(const double* scores, const int8_t* labels, int n, double thr,
+                                  double* neg_keys, unsigned long long* counts) {
+  unsigned correct = 0, pos = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double s = scores[i];
+    const bool is_pos = labels[i] == 1;
+    correct += ((s >= thr) == is_pos);
+    pos += is_pos;
+    neg_keys[i] = is_pos ? __longlong_as_double(0x7ff0000000000000LL) : s;  // +inf sorts last
+  }
+  correct = __reduce_add_sync(0xffffffffu, correct);
+  pos = __reduce_add_sync(0xffffffffu, pos);
+  if ((threadIdx.x & 31) == 0) {
+    if (correct) atomicAdd(counts + 0, (unsigned long long)correct);
+    if (pos) atomicAdd(counts + 2, (unsigned long long)pos);
+  }
+}
+
+__global__ void eval_rank_kernel(const double* scores, const int8_t* labels, int n,
+                                 const double* sorted_neg, unsigned long long* counts) {
+  const int n_neg = n - (int)counts[2];
+  unsigned long long twice_u = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (labels[i] != 1) continue;
+    const double s = scores[i];
+    int lo = 0, hi = n_neg;  // first index with key >= s
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sorted_neg[mid] < s) lo = mid + 1; else hi = mid;
+    }
+    int lo2 = lo, hi2 = n_neg;  // first index with key > s
+    while (lo2 < hi2) {
+      const int mid = (lo2 + hi2) >> 1;
+      if (sorted_neg[mid] <= s) lo2 = mid + 1; else hi2 = mid;
+    }
+    twice_u += 2ull * (unsigned long long)lo + (unsigned long long)(lo2 - lo);
+  }
+  for (int o = 16; o > 0; o >>= 1) twice_u += __shfl_xor_sync(0xffffffffu, twice_u, o);
+  if ((threadIdx.x & 31) == 0 && twice_u) atomicAdd(counts + 1, twice_u);
+}
+
+static size_t cub_temp_bytes(int n) {
+  size_t t = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, t, (const double*)nullptr, (double*)nullptr, n);
+  return t;
+}
+
+}  // namespace fs
+
+using namespace fs;
+
+extern "C" size_t fs_eval_workspace_bytes(int32_t n) {
+  if (n < 1) return 0;
+  return 256 + 2 * (size_t)n * sizeof(double) + cub_temp_bytes(n) + 256;
+}
+
+extern "C" int fs_eval_metrics(const double* scores, const int8_t* labels, int32_t n,
+                               double threshold, int64_t* counts_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (n < 1 || workspace_bytes < fs_eval_workspace_bytes(n)) {
+    set_error("fs_eval_metrics: empty input or workspace too small");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = reinterpret_cast<char*>(workspace);
+  auto* counts = reinterpret_cast<unsigned long long*>(ws);
+  double* keys = reinterpret_cast<double*>(ws + 256);
+  double* sorted = keys + n;
+  void* temp = reinterpret_cast<void*>(reinterpret_cast<char*>(sorted + n));
+  size_t temp_bytes = cub_temp_bytes(n);
+  if (cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess)
+    return check_launch("memset counts");
+  int blocks = (n + 255) / 256;
+  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+  eval_split_kernel<<<blocks, 256, 0, st>>>(scores, labels, n, threshold, keys, counts);
+  if (int rc = check_launch("eval_split_kernel")) return rc;
+  if (cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys, sorted, n, 0, 64, st) != cudaSuccess)
+    return check_launch("cub sort");
+  eval_rank_kernel<<<blocks, 256, 0, st>>>(scores, labels, n, sorted, counts);
+  if (int rc = check_launch("eval_rank_kernel")) return rc;
+  if (cudaMemcpyAsync(counts_out, counts, 3 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st) !=
+      cudaSuccess)
+    return check_launch("copy counts");
+  return FS_OK;
+}

@@ -1,0 +1,227 @@
+// K6 sign-alignment, K9 FedAvg sort keys, K7 FedAvg mean.
+//
+//   K6 fs_sign_align_f64   selection.calculate_relevance  selection.py:53-74
+//                          backend sign_align_count        _core.pyx:222-236
+//   K9 fs_gather_sort_keys server.aggregate's tobytes() sort key  server.py:84
+//   K7 fs_aggregate_f64    server.aggregate's stacked mean   server.py:84-86
+//
+// Both K6 and K7 are HBM-streaming integer/float reductions: coalesced
+// 16-byte loads, many independent loads in flight per thread, integer
+// counts reduced with warp shuffles and one atomic per CTA.
+#include "fs_common.cuh"
+
+namespace fs {
+
+constexpr int ALIGN_THREADS = 256;
+constexpr int ALIGN_UNROLL = 4;                                    // double2 per thread per pass
+constexpr int ALIGN_TILE = ALIGN_THREADS * ALIGN_UNROLL * 2;        // doubles per CTA pass
+
+__device__ __forceinline__ int sgn(double x) { return (x > 0.0) - (x < 0.0); }
+// sign(a - b) for finite a, b: IEEE subtraction with gradual underflow is
+// zero iff a == b and otherwise carries the ordering of a and b.
+__device__ __forceinline__ int sgn_diff(double a, double b) { return (a > b) - (a < b); }
+
+template <int MODE>
+__device__ __forceinline__ int aligned1(double c, double g, double p) {
+  if (MODE == FS_ALIGN_WEIGHT_SIGN) return sgn(c) == sgn(g);
+  return sgn_diff(c, g) == sgn_diff(g, p);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(ALIGN_THREADS)
+    sign_align_kernel(const uint64_t* wc, const uint64_t* wg, const uint64_t* wgp, int64_t M,
+                      int blocks_per_req, unsigned long long* out) {
+  const int r = blockIdx.x / blocks_per_req;
+  const int blk = blockIdx.x % blocks_per_req;
+  const double* c = reinterpret_cast<const double*>(wc[r]);
+  const double* g = reinterpret_cast<const double*>(wg[r]);
+  const double* p = MODE == FS_ALIGN_DELTA_SIGN ? reinterpret_cast<const double*>(wgp[r]) : nullptr;
+  unsigned cnt = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(p)) & 15) == 0;
+  const int64_t span = (M + blocks_per_req - 1) / blocks_per_req;
+  int64_t lo = (int64_t)blk * span;
+  const int64_t hi = min(M, lo + span);
+  if (vec) {
+    // 16-byte aligned bulk of [lo, hi): lo is rounded to an even index
+    int64_t v0 = (lo + 1) & ~(int64_t)1;
+    int64_t v1 = hi & ~(int64_t)1;
+    if (v0 > v1) v0 = v1;
+    for (int64_t j = lo + threadIdx.x; j < v0; j += ALIGN_THREADS)
+      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
+    const double2* c2 = reinterpret_cast<const double2*>(c + v0);
+    const double2* g2 = reinterpret_cast<const double2*>(g + v0);
+    const double2* p2 = p ? reinterpret_cast<const double2*>(p + v0) : nullptr;
+    const int64_t n2 = (v1 - v0) / 2;
+    int64_t i = threadIdx.x;
+    for (; i + (ALIGN_UNROLL - 1) * ALIGN_THREADS < n2; i += ALIGN_UNROLL * ALIGN_THREADS) {
+      double2 cv[ALIGN_UNROLL], gv[ALIGN_UNROLL], pv[ALIGN_UNROLL];
+#pragma unroll
+      for (int u = 0; u < ALIGN_UNROLL; ++u) {
+        cv[u] = __ldcs(c2 + i + u * ALIGN_THREADS);
+        gv[u] = __ldg(g2 + i + u * ALIGN_THREADS);
+        if (MODE == FS_ALIGN_DELTA_SIGN) pv[u] = __ldg(p2 + i + u * ALIGN_THREADS);
+      }
+#pragma unroll
+      for (int u = 0; u < ALIGN_UNROLL; ++u) {
+        const double px = MODE == FS_ALIGN_DELTA_SIGN ? pv[u].x : 0.0;
+        const double py = MODE == FS_ALIGN_DELTA_SIGN ? pv[u].y : 0.0;
+        cnt += aligned1<MODE>(cv[u].x, gv[u].x, px);
+        cnt += aligned1<MODE>(cv[u].y, gv[u].y, py);
+      }
+    }
+    for (; i < n2; i += ALIGN_THREADS) {
+      const double2 cv = c2[i], gv = g2[i];
+      const double2 pv = p2 ? p2[i] : make_double2(0.0, 0.0);
+      cnt += aligned1<MODE>(cv.x, gv.x, pv.x);
+      cnt += aligned1<MODE>(cv.y, gv.y, pv.y);
+    }
+    for (int64_t j = v1 + threadIdx.x; j < hi; j += ALIGN_THREADS)
+      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
+  } else {
+    for (int64_t j = lo + threadIdx.x; j < hi; j += ALIGN_THREADS)
+      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  __shared__ unsigned warp_sums[ALIGN_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned v = threadIdx.x < ALIGN_THREADS / 32 ? warp_sums[threadIdx.x] : 0u;
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (threadIdx.x == 0 && v) atomicAdd(out + r, (unsigned long long)v);
+  }
+}
+
+__global__ void sort_keys_kernel(const uint64_t* rows, int k, int n_keys, uint64_t* keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k * n_keys) return;
+  const int row = i / n_keys, t = i % n_keys;
+  const unsigned long long bits =
+      (unsigned long long)__double_as_longlong(reinterpret_cast<const double*>(rows[row])[t]);
+  keys[i] = __byte_perm((unsigned)(bits >> 32), 0, 0x0123) |
+            ((uint64_t)__byte_perm((unsigned)bits, 0, 0x0123) << 32);
+}
+
+constexpr int AGG_THREADS = 128;
+constexpr int AGG_UNROLL = 8;
+
+// out[j] = ((rows[0][j] + rows[1][j]) + ...) / k : numpy's mean(axis=0) of
+// the stacked (k x M) updates adds rows in order, then true-divides by k.
+__global__ void __launch_bounds__(AGG_THREADS)
+    aggregate_kernel(const uint64_t* rows, int k, int64_t M, double* out) {
+  extern __shared__ const double* sh_rows[];
+  for (int i = threadIdx.x; i < k; i += AGG_THREADS)
+    sh_rows[i] = reinterpret_cast<const double*>(rows[i]);
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * AGG_THREADS + threadIdx.x;
+  if (j >= M) return;
+  double acc = __ldcs(sh_rows[0] + j);
+  int i = 1;
+  for (; i + AGG_UNROLL <= k; i += AGG_UNROLL) {
+    double v[AGG_UNROLL];
+#pragma unroll
+    for (int u = 0; u < AGG_UNROLL; ++u) v[u] = __ldcs(sh_rows[i + u] + j);
+#pragma unroll
+    for (int u = 0; u < AGG_UNROLL; ++u) acc += v[u];
+  }
+  for (; i < k; ++i) acc += __ldcs(sh_rows[i] + j);
+  out[j] = acc / (double)k;
+}
+
+// M == 1: a single stacked column reduces pairwise (np.sum semantics).
+__device__ double pairwise_rows(const uint64_t* rows, int lo, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r += reinterpret_cast<const double*>(rows[lo + i])[0];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = reinterpret_cast<const double*>(rows[lo + j])[0];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += reinterpret_cast<const double*>(rows[lo + i + j])[0];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += reinterpret_cast<const double*>(rows[lo + i])[0];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_rows(rows, lo, n2) + pairwise_rows(rows, lo + n2, n - n2);
+}
+
+__global__ void aggregate_single_kernel(const uint64_t* rows, int k, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = pairwise_rows(rows, 0, k) / (double)k;
+}
+
+}  // namespace fs
+
+using namespace fs;
+
+extern "C" int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
+                                 int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
+                                 void* stream) {
+  if (n_req < 0 || M < 0 || (mode != FS_ALIGN_WEIGHT_SIGN && mode != FS_ALIGN_DELTA_SIGN) ||
+      (mode == FS_ALIGN_DELTA_SIGN && !wg_prev)) {
+    set_error("fs_sign_align_f64: invalid arguments");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_req == 0) return FS_OK;
+  if (cudaMemsetAsync(aligned_out, 0, sizeof(int64_t) * n_req, st) != cudaSuccess)
+    return check_launch("memset aligned");
+  if (M == 0) return FS_OK;
+  int bpr = (int)((M + ALIGN_TILE - 1) / ALIGN_TILE);
+  // keep >= 2 waves of 8 resident CTAs per SM even for few requests
+  const int64_t want = (int64_t)kNumSMs * 8 * 2;
+  if ((int64_t)bpr * n_req < want) {
+    const int64_t b2 = (want + n_req - 1) / n_req;
+    const int64_t cap = (M + 255) / 256;
+    bpr = (int)(b2 < cap ? b2 : cap);
+    if (bpr < 1) bpr = 1;
+  }
+  const unsigned nblk = (unsigned)bpr * (unsigned)n_req;
+  auto* out = reinterpret_cast<unsigned long long*>(aligned_out);
+  if (mode == FS_ALIGN_WEIGHT_SIGN)
+    sign_align_kernel<FS_ALIGN_WEIGHT_SIGN><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
+  else
+    sign_align_kernel<FS_ALIGN_DELTA_SIGN><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
+  return check_launch("sign_align_kernel");
+}
+
+extern "C" int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t n_keys,
+                                       uint64_t* keys_out, void* stream) {
+  if (k < 0 || n_keys < 0) {
+    set_error("fs_gather_sort_keys_f64: invalid sizes");
+    return FS_EINVAL;
+  }
+  const int total = k * n_keys;
+  if (total == 0) return FS_OK;
+  sort_keys_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(rows, k, n_keys, keys_out);
+  return check_launch("sort_keys_kernel");
+}
+
+extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out,
+                                void* stream) {
+  if (k < 1 || M < 0) {
+    set_error("fs_aggregate_f64: need k >= 1 updates");
+    return FS_EINVAL;
+  }
+  if (M == 0) return FS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M == 1) {
+    aggregate_single_kernel<<<1, 32, 0, st>>>(rows, k, out);
+    return check_launch("aggregate_single_kernel");
+  }
+  const size_t smem = (size_t)k * sizeof(double*);
+  if (smem > 200 * 1024) {
+    set_error("fs_aggregate_f64: k=%d updates exceed the staged pointer table", k);
+    return FS_EINVAL;
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
+  aggregate_kernel<<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  return check_launch("aggregate_kernel");
+}

@@ -1,0 +1,408 @@
+"""Device runtime: resident shard store and the batched round-level operators.
+
+The reference runs its round loop one client at a time (server.py:409-417
+-> client.train_local -> backend.loss_and_grad per batch). Here the engines
+hand a whole round (or a deferred batch of async trainings) to the GPU:
+
+    train_requests   K1 seeds -> K2 shuffles -> K3 dropout bits -> K5 trainer
+    align_requests   K6 sign-alignment counts (one launch for all clients)
+    aggregate_rows   K9 sort keys -> host sort -> K7 ordered mean
+    evaluate_global  K8 eval forward + accuracy/AUC counts
+
+Only per-request metadata crosses the PCIe bus (one packed H2D per launch
+group) plus the integer results the event log needs (aligned counts,
+divergence flags). Parameters, shards, permutations and masks stay in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class KernelTimer:
+    """Optional CUDA-event brackets around the hot launches (bench/profiling).
+
+    ``record(name, work)`` returns a context manager that records events on
+    the launching stream; ``summary()`` reports mean duration per launch and
+    the algorithmic work (FLOPs or bytes) each launch carried.
+    """
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+        self.launches = 0
+
+    def record(self, name: str, work: float, stream):
+        timer = self
+
+        class _Ctx:
+            def __enter__(self_inner):
+                self_inner.a = torch.cuda.Event(enable_timing=True)
+                self_inner.b = torch.cuda.Event(enable_timing=True)
+                self_inner.a.record(stream)
+
+            def __exit__(self_inner, *exc):
+                self_inner.b.record(stream)
+                timer.events.setdefault(name, []).append((self_inner.a, self_inner.b, work))
+
+        return _Ctx()
+
+    def summary(self) -> dict:
+        out = {}
+        for name, evs in self.events.items():
+            ms = [a.elapsed_time(b) for a, b, _ in evs]
+            work = [w for _, _, w in evs]
+            out[name] = {"launches": len(evs), "mean_ms": float(np.mean(ms)), "total_ms": float(np.sum(ms)),
+                         "work_per_launch": float(np.mean(work)), "work_total": float(np.sum(work))}
+        return out
+
+
+class Runtime:
+    """Per-device state: stream handle and growable scratch buffers."""
+
+    timer: KernelTimer | None = None   # set by bench.py to time hot launches
+    abi_calls = 0                      # kernel-launching C-ABI calls issued
+
+    _instances: dict[int, "Runtime"] = {}
+
+    def __init__(self, index: int):
+        self.lib = N.load(require_gpu=True)
+        self.index = index
+        self.device = torch.device("cuda", index)
+        self._ws: dict[str, torch.Tensor] = {}
+
+    @classmethod
+    def get(cls, index: int | None = None) -> "Runtime":
+        N.load(require_gpu=True)
+        if index is None:
+            index = torch.cuda.current_device()
+        rt = cls._instances.get(index)
+        if rt is None:
+            rt = cls(index)
+            cls._instances[index] = rt
+        return rt
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def scratch(self, name: str, nbytes: int) -> torch.Tensor:
+        """A cached uint8 device buffer of at least ``nbytes`` (stream-ordered reuse)."""
+        nbytes = max(int(nbytes), 1)
+        buf = self._ws.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),
+                              dtype=torch.uint8, device=self.device)
+            self._ws[name] = buf
+        return buf
+
+    def h2d(self, arr: np.ndarray) -> torch.Tensor:
+        """Pinned host copy -> device tensor (async on the current stream)."""
+        src = torch.from_numpy(np.ascontiguousarray(arr))
+        if src.numel() == 0:
+            return torch.empty(0, dtype=src.dtype, device=self.device)
+        return src.pin_memory().to(self.device, non_blocking=True)
+
+    def call(self, rc: int, what: str) -> None:
+        Runtime.abi_calls += 1
+        N.check(rc, what)
+
+    def timed(self, name: str, work: float):
+        t = Runtime.timer
+        if t is None:
+            return _NULL_CTX
+        return t.record(name, work, torch.cuda.current_stream(self.device))
+
+
+class _Null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULL_CTX = _Null()
+
+
+def mlp_flops_per_sample(dims) -> int:
+    """Algorithmic fwd+bwd FLOPs per sample: 4*sum f_l f_l+1 over
+    all layers for forward + weight gradients, plus 2*sum over layers l>=1 for
+    the input gradients of every layer but the first."""
+    pairs = [a * b for a, b in zip(dims[:-1], dims[1:])]
+    return 4 * sum(pairs) + 2 * sum(pairs[1:])
+
+
+def dims_array(dims) -> tuple[ctypes.Array, int]:
+    arr = (ctypes.c_int32 * len(dims))(*[int(d) for d in dims])
+    return arr, len(dims)
+
+
+# --------------------------------------------------------------------- shards
+class DeviceShards:
+    """All client shards packed row-wise in HBM ([rows x d] float64 + labels).
+
+    The reference keeps one numpy shard per WorldClient (server.py:89-106);
+    here they are concatenated once at world build so a training launch
+    addresses any client by (row offset, rows).
+    """
+
+    def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], rt: Runtime | None = None):
+        self.rt = rt or Runtime.get()
+        n_rows = np.array([f.shape[0] for f in features], dtype=np.int64)
+        self.n_rows = n_rows.astype(np.int32)
+        self.row_off = np.zeros(len(features), dtype=np.int64)
+        if len(features) > 1:
+            self.row_off[1:] = np.cumsum(n_rows)[:-1]
+        d = features[0].shape[1] if features else 0
+        host_x = np.ascontiguousarray(np.concatenate(features, axis=0), dtype=np.float64) if features else np.zeros((0, d))
+        host_y = np.ascontiguousarray(np.concatenate([np.asarray(l, dtype=np.float64) for l in labels])) if labels else np.zeros(0)
+        self.dim = d
+        self.features = self.rt.h2d(host_x.reshape(-1, d) if d else host_x)
+        self.labels = self.rt.h2d(host_y)
+
+    def __len__(self) -> int:
+        return len(self.n_rows)
+
+
+# --------------------------------------------------------------- training
+@dataclass
+class TrainRequest:
+    """One local training: shard `client` from `w_start` over steps [start, end)."""
+
+    client: int
+    seed: int               # train seed (derive_seed(master, "train", cid, cycle))
+    lr: np.ndarray          # [epochs] step size of each epoch
+    w_start: torch.Tensor   # float64 [M] on device
+    batch: int
+    start_step: int = 0
+    end_step: int | None = None
+
+
+def steps_per_epoch(n: int, b: int) -> int:
+    return -(-n // b)
+
+
+def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], epochs: int,
+                   dropout_rate: float, w_out: torch.Tensor | None = None,
+                   rt: Runtime | None = None):
+    """Batched K2 -> K3 -> K5. Returns (w_out [n x M] float64, status int32 [n] on device)."""
+    rt = rt or Runtime.get()
+    lib = rt.lib
+    n = len(reqs)
+    dims = tuple(int(x) for x in spec_dims)
+    M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
+    if w_out is None:
+        w_out = torch.empty((n, M), dtype=torch.float64, device=rt.device)
+    status = torch.zeros(n, dtype=torch.int32, device=rt.device)
+    if n == 0:
+        return w_out, status
+    sum_hidden = sum(dims[1:-1])
+    cl = np.array([r.client for r in reqs], dtype=np.int64)
+    n_rows = shards.n_rows[cl].astype(np.int64)
+    batch = np.array([r.batch for r in reqs], dtype=np.int64)
+    spe = -(-n_rows // batch)
+    total = epochs * spe
+    start = np.array([r.start_step for r in reqs], dtype=np.int64)
+    end = np.array([total[i] if r.end_step is None else r.end_step for i, r in enumerate(reqs)], dtype=np.int64)
+    perm_len = epochs * n_rows
+    perm_off = np.zeros(n, dtype=np.int64)
+    if n > 1:
+        perm_off[1:] = np.cumsum(perm_len)[:-1]
+    use_masks = dropout_rate > 0.0
+    slot = (batch * sum_hidden + 31) // 32
+    mask_len = total * slot if use_masks else np.zeros(n, dtype=np.int64)
+    mask_off = np.zeros(n, dtype=np.int64)
+    if n > 1:
+        mask_off[1:] = np.cumsum(mask_len)[:-1]
+    # longest client first (LPT) so the critical path starts at t=0
+    work = (end - start) * batch
+    order = np.argsort(-work, kind="stable").astype(np.int64)
+
+    i64 = np.concatenate([
+        shards.row_off[cl], perm_off, mask_off,
+        np.array([r.w_start.data_ptr() for r in reqs], dtype=np.uint64).view(np.int64),
+        np.array([r.seed for r in reqs], dtype=np.uint64).view(np.int64),
+    ])
+    i32 = np.concatenate([n_rows, batch, start, end, order]).astype(np.int32)
+    lr = np.stack([np.broadcast_to(np.asarray(r.lr, dtype=np.float64), (epochs,)) for r in reqs]) if epochs else np.zeros((n, 1))
+    d_i64 = rt.h2d(i64)
+    d_i32 = rt.h2d(i32)
+    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64))
+    p64 = d_i64.data_ptr()
+    p32 = d_i32.data_ptr()
+    row_off_p, perm_off_p, mask_off_p, wstart_p, seeds_p = (p64 + 8 * n * k for k in range(5))
+    n_rows_p, batch_p, start_p, end_p, order_p = (p32 + 4 * n * k for k in range(5))
+
+    perm = torch.empty(max(int(perm_len.sum()), 1), dtype=torch.int32, device=rt.device)
+    stream = rt.stream
+    if epochs > 0:
+        rt.call(lib.fs_shuffle_perms(seeds_p, n_rows_p, perm_off_p, n, epochs,
+                                     int(n_rows.max()), perm.data_ptr(), stream), "fs_shuffle_perms")
+    mask_ptr = None
+    scale = 1.0
+    if use_masks and epochs > 0:
+        keep = 1.0 - dropout_rate
+        scale = 1.0 / keep
+        bits = torch.empty(max(int(mask_len.sum()), 1), dtype=torch.int32, device=rt.device)
+        rt.call(lib.fs_dropout_bits(seeds_p, n_rows_p, batch_p, mask_off_p, n, epochs, sum_hidden,
+                                    keep, bits.data_ptr(), stream), "fs_dropout_bits")
+        mask_ptr = bits.data_ptr()
+
+    desc = N.TrainDesc()
+    desc.n_dims = len(dims)
+    for i, v in enumerate(dims):
+        desc.dims[i] = v
+    desc.n_req = n
+    desc.epochs = epochs
+    desc.max_batch = int(batch.max())
+    desc.mask_mode = N.FS_MASK_BITS if mask_ptr else N.FS_MASK_NONE
+    desc.scale = scale
+    desc.features = shards.features.data_ptr()
+    desc.labels = shards.labels.data_ptr()
+    desc.row_off = row_off_p
+    desc.n_rows = n_rows_p
+    desc.batch = batch_p
+    desc.lr = d_lr.data_ptr()
+    desc.w_start = wstart_p
+    desc.w_out = w_out.data_ptr()
+    desc.ldw = w_out.stride(0)
+    desc.perm = perm.data_ptr()
+    desc.perm_off = perm_off_p
+    desc.mask_bits = mask_ptr
+    desc.mask_off = mask_off_p
+    desc.start_step = start_p
+    desc.end_step = end_p
+    desc.order = order_p
+    desc.status = status.data_ptr()
+    desc.grid = 0
+    need = lib.fs_train_workspace_bytes(ctypes.byref(desc))
+    ws = rt.scratch("train", need)
+    desc.workspace = ws.data_ptr()
+    desc.workspace_bytes = ws.numel()
+    work = 0.0
+    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
+        last = end // spe - start // spe   # epoch-final (partial) steps in [start, end)
+        rows = (end - start - last) * batch + last * (n_rows - (spe - 1) * batch)
+        work = float(rows.sum()) * mlp_flops_per_sample(dims)
+    with rt.timed("train", work):
+        rt.call(lib.fs_train_f64(ctypes.byref(desc), stream), "fs_train_f64")
+    # staging tensors may be released now: torch's caching allocator only
+    # reuses their blocks for later work on this same stream
+    return w_out, status
+
+
+# --------------------------------------------------------------- alignment
+def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | None = None) -> torch.Tensor:
+    """K6: aligned counts [n] int64 (device)."""
+    rt = rt or Runtime.get()
+    n = len(wc_ptrs)
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if n == 0:
+        return out[:0]
+    m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
+    ptrs = [np.asarray(wc_ptrs, dtype=np.uint64), np.asarray(wg_ptrs, dtype=np.uint64)]
+    if m == N.FS_ALIGN_DELTA_SIGN:
+        ptrs.append(np.asarray(wgp_ptrs, dtype=np.uint64))
+    d = rt.h2d(np.concatenate(ptrs).view(np.int64))
+    p = d.data_ptr()
+    with rt.timed("align", 8.0 * M * (n + (2 if m else 1))):
+        rt.call(rt.lib.fs_sign_align_f64(p, p + 8 * n, (p + 16 * n) if m else None, n, M, m,
+                                     out.data_ptr(), rt.stream), "fs_sign_align_f64")
+    return out[:n]
+
+
+# --------------------------------------------------------------- FedAvg
+_N_KEYS = 4
+
+
+def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
+    """Indices of ``rows`` sorted by ``values.tobytes()`` (server.py:84).
+
+    K9 gathers the leading elements as big-endian integer keys; rows tied on
+    that prefix fall back to a full-row byte comparison (rare).
+    """
+    k = len(rows)
+    if k <= 1:
+        return list(range(k))
+    nk = min(_N_KEYS, M)
+    d = rt.h2d(np.asarray([r.data_ptr() for r in rows], dtype=np.uint64).view(np.int64))
+    keys = torch.empty(k * nk, dtype=torch.int64, device=rt.device)
+    rt.call(rt.lib.fs_gather_sort_keys_f64(d.data_ptr(), k, nk, keys.data_ptr(), rt.stream),
+            "fs_gather_sort_keys_f64")
+    kh = keys.cpu().numpy().view(np.uint64).reshape(k, nk)
+    order = list(np.lexsort([kh[:, t] for t in range(nk - 1, -1, -1)]))
+    if nk == M:
+        return [int(x) for x in order]
+    out: list[int] = []
+    i = 0
+    while i < k:
+        j = i + 1
+        while j < k and np.array_equal(kh[order[j]], kh[order[i]]):
+            j += 1
+        group = order[i:j]
+        if len(group) > 1:
+            full = {g: rows[g].cpu().numpy().tobytes() for g in group}
+            group = sorted(group, key=lambda g: full[g])
+        out.extend(int(g) for g in group)
+        i = j
+    return out
+
+
+def aggregate_rows(rows: list[torch.Tensor], M: int, rt: Runtime | None = None) -> torch.Tensor:
+    """K9 + K7: mean of k device rows in canonical byte order (server.aggregate)."""
+    rt = rt or Runtime.get()
+    k = len(rows)
+    order = canonical_order(rows, M, rt)
+    d = rt.h2d(np.asarray([rows[i].data_ptr() for i in order], dtype=np.uint64).view(np.int64))
+    out = torch.empty(M, dtype=torch.float64, device=rt.device)
+    with rt.timed("aggregate", 8.0 * M * (k + 1)):
+        rt.call(rt.lib.fs_aggregate_f64(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate_f64")
+    return out
+
+
+# --------------------------------------------------------------- eval
+def forward_probs(spec_dims, w: torch.Tensor, x: torch.Tensor, dense_masks: torch.Tensor | None = None,
+                  rt: Runtime | None = None) -> torch.Tensor:
+    rt = rt or Runtime.get()
+    dims_c, nd = dims_array(spec_dims)
+    rows = x.shape[0]
+    probs = torch.empty(rows, dtype=torch.float64, device=rt.device)
+    need = rt.lib.fs_forward_workspace_bytes(dims_c, nd, rows)
+    ws = rt.scratch("forward", need)
+    rt.call(rt.lib.fs_forward_f64(dims_c, nd, w.data_ptr(), x.data_ptr(), rows, _ptr(dense_masks),
+                                  probs.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream), "fs_forward_f64")
+    return probs
+
+
+def eval_counts(scores: torch.Tensor, labels_i8: torch.Tensor, threshold: float, rt: Runtime | None = None) -> torch.Tensor:
+    """K8 metrics: device int64 [3] = (#correct, 2*U_pos, n_pos)."""
+    rt = rt or Runtime.get()
+    n = scores.shape[0]
+    out = torch.empty(3, dtype=torch.int64, device=rt.device)
+    need = rt.lib.fs_eval_workspace_bytes(n)
+    ws = rt.scratch("eval", need)
+    rt.call(rt.lib.fs_eval_metrics(scores.data_ptr(), labels_i8.data_ptr(), n, float(threshold),
+                                   out.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream), "fs_eval_metrics")
+    return out
+
+
+def metrics_from_counts(counts: np.ndarray, n: int) -> tuple[float, float, int, int]:
+    """(accuracy, auc, n_pos, n_neg) exactly as metrics.evaluate computes them."""
+    correct, twice_u, n_pos = (int(c) for c in counts[:3])
+    n_neg = n - n_pos
+    acc = correct / n
+    if n_pos == 0 or n_neg == 0:
+        raise ValueError("AUC needs at least one example of each class")
+    auc = (twice_u / 2.0) / (n_pos * n_neg)
+    return acc, auc, n_pos, n_neg

@@ -1,0 +1,263 @@
+"""Parity of the CUDA path against the reference (golden vectors) and the oracle.
+
+Bars: bit-exact for integer/index work (seeds, permutations, mask bits,
+alignment counts, aggregation order and the event-log digest); float64
+results within 1e-12 relative (the reference's own compiled-vs-numpy
+backends differ by up to ~3e-16); aggregation bitwise for equal inputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+RUN_NAMES = ["sync_weight", "sync_delta_dyn", "sync_baseline", "sync_fail_ckpt",
+             "async_fail_lost", "async_weight", "async_delta_dyn", "unsw_sync_delta"]
+
+
+def rel_err(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0))) if a.size else 0.0
+
+
+# --------------------------------------------------------------------- K1-K3
+def test_rng_kernels_bit_exact(golden):
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, dropout_mask_bits
+
+    rt = D.Runtime.get()
+    g = golden("rng.npz")
+    meta = g["train_seeds"]
+    for m in np.unique(meta[:, 0]):
+        sel = meta[:, 0] == m
+        cid = rt.h2d(meta[sel, 1].astype(np.int32))
+        cyc = rt.h2d(meta[sel, 2].astype(np.int32))
+        out = torch.empty(int(sel.sum()), dtype=torch.int64, device=rt.device)
+        rt.call(rt.lib.fs_train_seeds(int(m), cid.data_ptr(), cyc.data_ptr(), int(sel.sum()), out.data_ptr(),
+                                      rt.stream), "seeds")
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), g["train_seed_out"][sel])
+
+    at = 0
+    for ts, e, n in g["perm_meta"]:
+        n, e = int(n), int(e)
+        seeds = rt.h2d(np.array([ts], dtype=np.uint64).view(np.int64))
+        nr = rt.h2d(np.array([n], dtype=np.int32))
+        off = rt.h2d(np.array([0], dtype=np.int64))
+        perm = torch.empty(n * (e + 1), dtype=torch.int32, device=rt.device)
+        rt.call(rt.lib.fs_shuffle_perms(seeds.data_ptr(), nr.data_ptr(), off.data_ptr(), 1, e + 1, n,
+                                        perm.data_ptr(), rt.stream), "perms")
+        assert np.array_equal(perm.cpu().numpy()[e * n:(e + 1) * n], g["perm_flat"][at:at + n])
+        at += n
+
+    spec = ModelSpec(input_dim=42, hidden_dims=(256, 128, 64), dropout_rate=0.3)
+    at = 0
+    for ts, e, s, b, ms in g["mask_meta"]:
+        words = dropout_mask_bits(spec, int(b), int(ms)).cpu().numpy().view(np.uint32)
+        nbits = int(b) * 448
+        bits = ((words[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).ravel()[:nbits]
+        nbytes = (nbits + 7) // 8
+        assert np.array_equal(np.packbits(bits, bitorder="little"), g["mask_bits"][at:at + nbytes])
+        at += nbytes
+
+
+# --------------------------------------------------------------------- backend kernels
+def test_backend_kernels_match_reference(golden):
+    from paper_2503_15448_b200.backends import get_backend
+    from oracle.fl_oracle import keep_masks
+
+    be = get_backend()
+    k = golden("kernels.npz")
+    t = 0
+    while f"c{t}_dims" in k:
+        dims = tuple(int(v) for v in k[f"c{t}_dims"])
+        x, y, w = k[f"c{t}_x"], k[f"c{t}_y"], k[f"c{t}_w"]
+        ms = int(k[f"c{t}_mseed"])
+        masks = keep_masks(dims[1:-1], float(k[f"c{t}_rate"]), x.shape[0], ms) if ms >= 0 else None
+        loss, grad = be.loss_and_grad(w, dims, x, y, masks)
+        assert loss == pytest.approx(float(k[f"c{t}_loss"]), rel=1e-12, abs=1e-14)
+        assert rel_err(grad, k[f"c{t}_grad"]) < 1e-12
+        assert np.max(np.abs(be.forward(w, dims, x, masks) - k[f"c{t}_fwd"])) < 1e-12
+        t += 1
+    t = 0
+    while f"s{t}_a" in k:
+        assert be.sign_align_count(k[f"s{t}_a"], k[f"s{t}_b"]) == int(k[f"s{t}_count"])
+        t += 1
+
+
+def test_sign_align_edge_cases():
+    from paper_2503_15448_b200.backends import get_backend
+    from paper_2503_15448_b200.model import ParamVector
+    from paper_2503_15448_b200.selection import calculate_relevance
+
+    be = get_backend()
+    assert be.sign_align_count(np.array([-0.0, 0.0, 1.0, -1.0]), np.array([0.0, -0.0, 2.0, -3.0])) == 4
+    assert be.sign_align_count(np.array([1.0]), np.array([-1.0])) == 0
+    with pytest.raises(ValueError):
+        be.sign_align_count(np.ones(3), np.ones(4))
+    # reference known answers (tests/test_selection.py:45-54, 86-106)
+    pv = lambda v: ParamVector(np.asarray(v, dtype=float), "d")
+    assert calculate_relevance(pv([1, -1, 1, -1]), pv([1, 1, -1, -1])).ratio == 0.5
+    s = calculate_relevance(pv([1.0, 2.0, 3.0]), pv([0.5, 1.0, 4.0]), pv([0.0, 2.0, 3.5]), "delta_sign")
+    assert s.aligned == 2
+    # odd lengths / unaligned starts / large M across the vector path
+    rng = np.random.default_rng(4)
+    for n in (1, 2, 3, 1023, 4097, 52225, 300001):
+        a = np.round(rng.normal(size=n), 1)
+        b = np.round(rng.normal(size=n), 1)
+        assert be.sign_align_count(a, b) == int(np.count_nonzero(np.sign(a) == np.sign(b)))
+        assert be.sign_align_count(a[1:], b[1:]) == int(np.count_nonzero(np.sign(a[1:]) == np.sign(b[1:])))
+
+
+def test_aggregate_bitwise(golden):
+    from paper_2503_15448_b200.model import ParamVector
+    from paper_2503_15448_b200.server import aggregate
+
+    ag = golden("agg.npz")
+    t = 0
+    while f"a{t}_in" in ag:
+        vecs = [ParamVector(v, "d") for v in ag[f"a{t}_in"]]
+        assert np.array_equal(aggregate(vecs).values, ag[f"a{t}_out"])
+        rev = aggregate(vecs[::-1]).values
+        assert np.array_equal(rev, ag[f"a{t}_out"])
+        t += 1
+    assert aggregate([]) is None
+    with pytest.raises(ValueError):
+        aggregate([ParamVector(np.ones(1), "d"), ParamVector(np.ones(2), "d")])
+
+
+# --------------------------------------------------------------------- trainer
+def test_train_local_matches_reference(golden):
+    from paper_2503_15448_b200.client import ClientProfile, train_local
+    from paper_2503_15448_b200.model import ModelSpec, ParamVector
+
+    tr = golden("train.npz")
+    prof = ClientProfile(id=0, speed=50.0, up_latency_s=1.0, down_latency_s=1.0, capacity=1.0)
+    t = 0
+    while f"t{t}_dims" in tr:
+        dims = tuple(int(v) for v in tr[f"t{t}_dims"])
+        spec = ModelSpec(input_dim=dims[0], hidden_dims=dims[1:-1], dropout_rate=float(tr[f"t{t}_rate"]))
+        ep, bs, seed = (int(v) for v in tr[f"t{t}_meta"])
+        w0 = ParamVector(tr[f"t{t}_w0"], spec.digest())
+        upd = train_local(spec, prof, w0, tr[f"t{t}_x"], tr[f"t{t}_y"], ep, bs, lambda e: 0.05 * (0.9 ** e), seed)
+        assert upd.steps == int(tr[f"t{t}_steps"])
+        assert rel_err(upd.params.values, tr[f"t{t}_out"]) < 1e-12
+        t += 1
+
+
+def _small():
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=4, hidden_dims=(8, 5), dropout_rate=0.3)
+    rng = np.random.default_rng(0)
+    return spec, init_params(spec, 3), rng.normal(size=(40, 4)), rng.integers(0, 2, 40).astype(np.int8)
+
+
+def test_train_local_equals_fold_of_loss_and_grad_bitwise():
+    # reference tests/test_client.py:83-120: batched trainer == per-step API
+    from paper_2503_15448_b200.client import ClientProfile, batch_count, train_local
+    from paper_2503_15448_b200.model import Batch, loss_and_grad, sgd_step
+    from paper_2503_15448_b200.rng import derive_rng, derive_seed
+
+    spec, w0, x, y = _small()
+    prof = ClientProfile(id=0, speed=50.0, up_latency_s=1.0, down_latency_s=1.0, capacity=1.0)
+    epochs, bs, lr, seed = 2, 16, 0.05, 11
+    upd = train_local(spec, prof, w0, x, y, epochs, bs, lambda e: lr, seed=seed)
+    params = w0
+    for e in range(epochs):
+        perm = derive_rng(seed, "shuffle", e).permutation(40)
+        for b in range(batch_count(40, bs)):
+            idx = perm[b * bs:(b + 1) * bs]
+            _, g = loss_and_grad(spec, params, Batch(x[idx], y[idx].astype(np.float64)),
+                                 dropout_seed=derive_seed(seed, "mask", e, b))
+            params = sgd_step(params, g, lr)
+    assert np.array_equal(upd.params.values, params.values)
+
+
+def test_stop_resume_bitwise():
+    # reference tests/test_client.py:122-156
+    from paper_2503_15448_b200.client import ClientProfile, TrainingProgress, train_local
+
+    spec, w0, x, y = _small()
+    prof = ClientProfile(id=0, speed=50.0, up_latency_s=1.0, down_latency_s=1.0, capacity=1.0)
+    full = train_local(spec, prof, w0, x, y, 3, 8, lambda e: 0.1, seed=13)
+    for cut in (1, 4, 7, full.steps - 1):
+        part = train_local(spec, prof, w0, x, y, 3, 8, lambda e: 0.1, seed=13, stop_after_steps=cut)
+        assert isinstance(part, TrainingProgress) and part.steps_done == cut
+        res = train_local(spec, prof, w0, x, y, 3, 8, lambda e: 0.1, seed=13, resume=part)
+        assert np.array_equal(res.params.values, full.params.values)
+        assert res.steps == full.steps
+
+
+def test_divergence_raises():
+    from paper_2503_15448_b200.client import ClientProfile, train_local
+    from paper_2503_15448_b200.model import ParamVector, TrainingDivergedError
+
+    spec, w0, x, y = _small()
+    prof = ClientProfile(id=0, speed=50.0, up_latency_s=1.0, down_latency_s=1.0, capacity=1.0)
+    big = ParamVector(w0.values * 1e300, spec.digest())
+    with pytest.raises(TrainingDivergedError):
+        train_local(spec, prof, big, x * 1e10, y, 1, 8, lambda e: 1.0, seed=1)
+
+
+# --------------------------------------------------------------------- eval
+def test_eval_metrics_match_oracle():
+    from oracle.fl_oracle import acc_auc
+    from paper_2503_15448_b200.metrics import evaluate
+
+    rng = np.random.default_rng(9)
+    for n in (2, 17, 1000, 43835):
+        s = np.round(rng.random(n), 3)  # heavy ties
+        s[: n // 10] = 1.0
+        lab = rng.integers(0, 2, n).astype(np.int8)
+        lab[0], lab[-1] = 0, 1
+        res = evaluate(s, lab)
+        acc, auc = acc_auc(s, lab)
+        assert res.accuracy == acc and res.auc == auc
+
+
+# --------------------------------------------------------------------- engines
+@pytest.mark.parametrize("name", RUN_NAMES)
+def test_engine_replays_reference_digest(golden, name):
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    run = golden("runs.json")[name]
+    world, init = build_world(ExperimentConfig.from_dict(run["config"]))
+    eng = FederationEngine(world)
+    state = eng.run(init)
+    assert eng.timeline.digest() == run["digest"]
+    want = golden("runs_wg.npz")[name]
+    assert rel_err(state.w_g.values, want) < 1e-12
+    for got, ref in zip(eng.reports, run["reports"]):
+        rec = got.to_record()
+        for key in ("accepted", "rejected", "failures", "updates", "aggregations", "sgd_steps", "round"):
+            assert rec[key] == ref[key], key
+        assert rec["accuracy"] == pytest.approx(ref["accuracy"], abs=1e-9)
+        assert rec["auc"] == pytest.approx(ref["auc"], abs=1e-9)
+
+
+def test_engine_matches_oracle_at_unsw_shape():
+    """Teacher-free end-to-end check at the UNSW MLP shape (fp64 mode)."""
+    from oracle.fl_oracle import OracleFederation
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    cfg = {"num_clients": 24, "rounds": 2, "epochs": 1, "dataset": {"n": 20000, "d": 42},
+           "mode": "async_filtered", "selection_mode": "delta_sign",
+           "batch": {"policy": "dynamic"}, "seed": 4,
+           "profiles": {"speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
+                        "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
+                        "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
+                        "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}}}
+    world, init = build_world(ExperimentConfig.from_dict(cfg))
+    eng = FederationEngine(world)
+    st = eng.run(init)
+    sim = OracleFederation(world)
+    wg = sim.run(init.values)
+    assert eng.timeline.digest() == sim.digest()
+    assert rel_err(st.w_g.values, wg) < 1e-12
