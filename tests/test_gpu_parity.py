@@ -100,8 +100,20 @@ def test_sign_align_edge_cases():
     # reference known answers (tests/test_selection.py:45-54, 86-106)
     pv = lambda v: ParamVector(np.asarray(v, dtype=float), "d")
     assert calculate_relevance(pv([1, -1, 1, -1]), pv([1, 1, -1, -1])).ratio == 0.5
-    s = calculate_relevance(pv([1.0, 2.0, 3.0]), pv([0.5, 1.0, 4.0]), pv([0.0, 2.0, 3.5]), "delta_sign")
+    s = calculate_relevance(pv([2.0, -2.0, 0.5, -0.5]), pv([1.0, -1.0, 1.0, -1.0]), pv([0.0] * 4), "delta_sign")
     assert s.aligned == 2
+    with pytest.raises(ValueError):
+        calculate_relevance(pv([2.0]), pv([1.0]), None, "delta_sign")
+    from paper_2503_15448_b200.selection import SelectionPolicy, filter_update
+
+    class _U:
+        def __init__(self, p):
+            self.params = p
+
+    b = np.ones(20)
+    b[13:] = -1.0
+    ok, sc = filter_update(_U(pv(np.ones(20))), pv(b), None, SelectionPolicy(theta=0.65))
+    assert sc.ratio == 0.65 and ok  # inclusive boundary 13/20
     # odd lengths / unaligned starts / large M across the vector path
     rng = np.random.default_rng(4)
     for n in (1, 2, 3, 1023, 4097, 52225, 300001):
