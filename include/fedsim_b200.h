@@ -54,6 +54,10 @@ int fs_abi_version(void);
 int fs_derive_seed_host(uint64_t master, const uint32_t* path_host, int32_t n_path,
                         uint64_t* out_host);
 
+/* Host-side batch of train seeds (all pointers host memory).            */
+int fs_train_seeds_host(uint64_t master, const int32_t* client_ids_host, const int32_t* cycles_host,
+                        int32_t n, uint64_t* seeds_out_host);
+
 /* seeds[i] = derive_seed(master, "train", client_ids[i], cycles[i])
  * (server.py:207).                                                       */
 int fs_train_seeds(uint64_t master, const int32_t* client_ids, const int32_t* cycles, int32_t n,

@@ -76,6 +76,7 @@ _SIGNATURES = {
     "fs_last_error": (ctypes.c_char_p, []),
     "fs_abi_version": (ctypes.c_int, []),
     "fs_derive_seed_host": (ctypes.c_int, [_c_u64, ctypes.POINTER(ctypes.c_uint32), _c_i32, ctypes.POINTER(_c_u64)]),
+    "fs_train_seeds_host": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),
     "fs_shuffle_perms": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_dropout_bits": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i32, _c_f64, _c_vp, _c_vp]),

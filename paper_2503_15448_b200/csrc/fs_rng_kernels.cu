@@ -103,6 +103,17 @@ extern "C" int fs_derive_seed_host(uint64_t master, const uint32_t* path, int32_
   return FS_OK;
 }
 
+extern "C" int fs_train_seeds_host(uint64_t master, const int32_t* client_ids, const int32_t* cycles,
+                                   int32_t n, uint64_t* out) {
+  if (n < 0 || (n > 0 && (!client_ids || !cycles || !out))) {
+    set_error("fs_train_seeds_host: invalid arguments");
+    return FS_EINVAL;
+  }
+  for (int32_t i = 0; i < n; ++i)
+    out[i] = derive_train_seed(master, (uint32_t)client_ids[i], (uint32_t)cycles[i]);
+  return FS_OK;
+}
+
 extern "C" int fs_train_seeds(uint64_t master, const int32_t* client_ids, const int32_t* cycles,
                               int32_t n, uint64_t* seeds_out, void* stream) {
   if (n < 0) {

@@ -196,55 +196,75 @@ def steps_per_epoch(n: int, b: int) -> int:
 def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], epochs: int,
                    dropout_rate: float, w_out: torch.Tensor | None = None,
                    rt: Runtime | None = None):
-    """Batched K2 -> K3 -> K5. Returns (w_out [n x M] float64, status int32 [n] on device)."""
+    """List-of-requests front end of :func:`train_batch`."""
+    n = len(reqs)
+    return train_batch(
+        spec_dims, shards,
+        clients=np.array([r.client for r in reqs], dtype=np.int64),
+        seeds=np.array([r.seed for r in reqs], dtype=np.uint64),
+        lr=np.stack([np.broadcast_to(np.asarray(r.lr, dtype=np.float64), (epochs,)) for r in reqs])
+        if n and epochs else np.zeros((n, max(epochs, 1))),
+        w_start=np.array([r.w_start.data_ptr() for r in reqs], dtype=np.uint64),
+        batch=np.array([r.batch for r in reqs], dtype=np.int64),
+        epochs=epochs, dropout_rate=dropout_rate,
+        start=np.array([r.start_step for r in reqs], dtype=np.int64),
+        end=np.array([-1 if r.end_step is None else r.end_step for r in reqs], dtype=np.int64),
+        w_out=w_out, rt=rt)
+
+
+def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.ndarray, lr: np.ndarray,
+                w_start: np.ndarray, batch: np.ndarray, epochs: int, dropout_rate: float,
+                start: np.ndarray | None = None, end: np.ndarray | None = None,
+                w_out: torch.Tensor | None = None, rt: Runtime | None = None):
+    """Batched K2 -> K3 -> K5 over n requests given as arrays.
+
+    clients [n] shard index, seeds [n] uint64 train seeds, lr [n x epochs],
+    w_start [n] device pointers of the start parameters, batch [n]; optional
+    start/end global step (end < 0 = all E*ceil(n_i/b_i) steps).
+    Returns (w_out [n x M] float64, status int32 [n]) on the device.
+    """
     rt = rt or Runtime.get()
     lib = rt.lib
-    n = len(reqs)
+    n = int(len(clients))
     dims = tuple(int(x) for x in spec_dims)
     M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
     if w_out is None:
         w_out = torch.empty((n, M), dtype=torch.float64, device=rt.device)
-    status = torch.zeros(n, dtype=torch.int32, device=rt.device)
+    status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
     if n == 0:
         return w_out, status
     sum_hidden = sum(dims[1:-1])
-    cl = np.array([r.client for r in reqs], dtype=np.int64)
+    cl = np.asarray(clients, dtype=np.int64)
     n_rows = shards.n_rows[cl].astype(np.int64)
-    batch = np.array([r.batch for r in reqs], dtype=np.int64)
+    batch = np.asarray(batch, dtype=np.int64)
     spe = -(-n_rows // batch)
     total = epochs * spe
-    start = np.array([r.start_step for r in reqs], dtype=np.int64)
-    end = np.array([total[i] if r.end_step is None else r.end_step for i, r in enumerate(reqs)], dtype=np.int64)
+    start = np.zeros(n, dtype=np.int64) if start is None else np.asarray(start, dtype=np.int64)
+    end = total.copy() if end is None else np.where(np.asarray(end) < 0, total, end).astype(np.int64)
     perm_len = epochs * n_rows
     perm_off = np.zeros(n, dtype=np.int64)
-    if n > 1:
-        perm_off[1:] = np.cumsum(perm_len)[:-1]
+    np.cumsum(perm_len[:-1], out=perm_off[1:])
     use_masks = dropout_rate > 0.0
     slot = (batch * sum_hidden + 31) // 32
     mask_len = total * slot if use_masks else np.zeros(n, dtype=np.int64)
     mask_off = np.zeros(n, dtype=np.int64)
-    if n > 1:
-        mask_off[1:] = np.cumsum(mask_len)[:-1]
+    np.cumsum(mask_len[:-1], out=mask_off[1:])
     # longest client first (LPT) so the critical path starts at t=0
-    work = (end - start) * batch
-    order = np.argsort(-work, kind="stable").astype(np.int64)
+    order = np.argsort(-((end - start) * batch), kind="stable")
 
-    i64 = np.concatenate([
-        shards.row_off[cl], perm_off, mask_off,
-        np.array([r.w_start.data_ptr() for r in reqs], dtype=np.uint64).view(np.int64),
-        np.array([r.seed for r in reqs], dtype=np.uint64).view(np.int64),
-    ])
+    i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off,
+                          np.asarray(w_start, dtype=np.uint64).view(np.int64),
+                          np.asarray(seeds, dtype=np.uint64).view(np.int64)])
     i32 = np.concatenate([n_rows, batch, start, end, order]).astype(np.int32)
-    lr = np.stack([np.broadcast_to(np.asarray(r.lr, dtype=np.float64), (epochs,)) for r in reqs]) if epochs else np.zeros((n, 1))
     d_i64 = rt.h2d(i64)
     d_i32 = rt.h2d(i32)
-    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64))
+    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
     p64 = d_i64.data_ptr()
     p32 = d_i32.data_ptr()
     row_off_p, perm_off_p, mask_off_p, wstart_p, seeds_p = (p64 + 8 * n * k for k in range(5))
     n_rows_p, batch_p, start_p, end_p, order_p = (p32 + 4 * n * k for k in range(5))
 
-    perm = torch.empty(max(int(perm_len.sum()), 1), dtype=torch.int32, device=rt.device)
+    perm = rt.scratch("perm", 4 * max(int(perm_len.sum()), 1))
     stream = rt.stream
     if epochs > 0:
         rt.call(lib.fs_shuffle_perms(seeds_p, n_rows_p, perm_off_p, n, epochs,
@@ -254,7 +274,7 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
     if use_masks and epochs > 0:
         keep = 1.0 - dropout_rate
         scale = 1.0 / keep
-        bits = torch.empty(max(int(mask_len.sum()), 1), dtype=torch.int32, device=rt.device)
+        bits = rt.scratch("mask_bits", 4 * max(int(mask_len.sum()), 1))
         rt.call(lib.fs_dropout_bits(seeds_p, n_rows_p, batch_p, mask_off_p, n, epochs, sum_hidden,
                                     keep, bits.data_ptr(), stream), "fs_dropout_bits")
         mask_ptr = bits.data_ptr()
@@ -285,7 +305,7 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
     desc.end_step = end_p
     desc.order = order_p
     desc.status = status.data_ptr()
-    desc.grid = 0
+    desc.grid = TRAIN_GRID
     need = lib.fs_train_workspace_bytes(ctypes.byref(desc))
     ws = rt.scratch("train", need)
     desc.workspace = ws.data_ptr()
@@ -302,6 +322,9 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
     return w_out, status
 
 
+TRAIN_GRID = int(__import__("os").environ.get("FS_TRAIN_GRID", "0"))
+
+
 # --------------------------------------------------------------- alignment
 def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | None = None) -> torch.Tensor:
     """K6: aligned counts [n] int64 (device)."""
@@ -311,9 +334,9 @@ def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | 
     if n == 0:
         return out[:0]
     m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
-    ptrs = [np.asarray(wc_ptrs, dtype=np.uint64), np.asarray(wg_ptrs, dtype=np.uint64)]
+    ptrs = [np.asarray(wc_ptrs, dtype=np.uint64).ravel(), np.asarray(wg_ptrs, dtype=np.uint64).ravel()]
     if m == N.FS_ALIGN_DELTA_SIGN:
-        ptrs.append(np.asarray(wgp_ptrs, dtype=np.uint64))
+        ptrs.append(np.asarray(wgp_ptrs, dtype=np.uint64).ravel())
     d = rt.h2d(np.concatenate(ptrs).view(np.int64))
     p = d.data_ptr()
     with rt.timed("align", 8.0 * M * (n + (2 if m else 1))):
