@@ -51,13 +51,13 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA-core and DMMA) nominal; no measured fp64 peak exists
 
 
-def build_c4_world(num_clients: int = 1024):
+def build_c4_world(num_clients: int = 1024, precision: str = "fp64"):
     from paper_2503_15448_b200.config import ExperimentConfig
     from paper_2503_15448_b200.experiment import build_world
 
     cfg = dict(C4_SYNC)
     cfg["num_clients"] = num_clients
-    return build_world(ExperimentConfig.from_dict(cfg))
+    return build_world(ExperimentConfig.from_dict(cfg), precision=precision)
 
 
 # ------------------------------------------------------------------ clocks
@@ -190,7 +190,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl")
-    world, initial = build_c4_world()
+    world, initial = build_c4_world(precision=args.precision)
     rt = D.Runtime.get()
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=rt.device)
 
@@ -327,6 +327,7 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--ref-sample", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))

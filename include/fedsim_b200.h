@@ -124,6 +124,19 @@ typedef struct fs_train_desc {
 size_t fs_train_workspace_bytes(const fs_train_desc* desc);
 int fs_train_f64(const fs_train_desc* desc, void* stream);
 
+/* bf16 mixed-precision trainer (tcgen05/TMEM): same descriptor, but
+ * w_start[r] points to float32 parameters and w_out is a float32 [n_req x
+ * ldw] buffer (fp32 master weights, bf16 GEMM operands, fp32 accumulate).
+ * Features/labels come pre-converted by fs_prep_features_bf16 (desc->features
+ * and desc->labels are ignored). Hidden widths must be multiples of 32 (<=256),
+ * input width <= 256, at most 4 hidden layers.                              */
+int fs_bf16_supported(const int32_t* dims, int32_t n_dims);
+int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
+                          void* xb_out, float* y_out, void* stream);
+size_t fs_train_bf16_workspace_bytes(const fs_train_desc* desc);
+int fs_train_bf16(const fs_train_desc* desc, const void* features_bf16, const float* labels_f32,
+                  void* stream);
+
 /* backend.loss_and_grad (_core.pyx:140-219 / numpy_backend.py:60-104):
  * one batch x[rows x dims[0]], labels y[rows], optional dense pre-scaled masks
  * (layer-major [rows x h_l] blocks) -> loss_out[1], grad_out[M]. Shares the
@@ -150,6 +163,11 @@ int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg
                       int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
                       void* stream);
 
+/* float32 variant (bf16 mixed-precision mode: fp32 parameter vectors).   */
+int fs_sign_align_f32(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
+                      int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
+                      void* stream);
+
 /* ---------------------------------------------------------------- K7/K9 FedAvg
  * keys_out[i*n_keys + t] = bswap64(bits(rows[i][t])) — the leading bytes
  * of values.tobytes() as big-endian integers (server.py:84 sort key).     */
@@ -158,6 +176,12 @@ int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t n_keys, uin
 /* out[j] = (sum_{i=0..k-1} rows[i][j]) / k, summed sequentially in the given
  * row order (server.py:84-86: stack in sorted order, mean(axis=0)).        */
 int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out, void* stream);
+
+/* float32 variants (bf16 mode): keys are bswap32 of the leading floats;
+ * the mean is accumulated in float64 and rounded once to float32.         */
+int fs_gather_sort_keys_f32(const uint64_t* rows, int32_t k, int32_t n_keys, uint64_t* keys_out,
+                            void* stream);
+int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, void* stream);
 
 /* ---------------------------------------------------------------- K8 metrics
  * accuracy at `threshold` and rank AUC with midrank ties

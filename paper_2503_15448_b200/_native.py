@@ -83,6 +83,10 @@ _SIGNATURES = {
     "fs_dropout_bits_seed": (ctypes.c_int, [_c_u64, _c_i64, _c_f64, _c_vp, _c_vp]),
     "fs_train_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
     "fs_train_f64": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp]),
+    "fs_bf16_supported": (ctypes.c_int, [_c_vp, _c_i32]),
+    "fs_prep_features_bf16": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp]),
+    "fs_train_bf16_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
+    "fs_train_bf16": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp, _c_vp, _c_vp]),
     "fs_step_workspace_bytes": (_c_sz, [_c_vp, _c_i32, _c_i32]),
     "fs_loss_and_grad_f64": (
         ctypes.c_int,
@@ -91,6 +95,9 @@ _SIGNATURES = {
     "fs_forward_workspace_bytes": (_c_sz, [_c_vp, _c_i32, _c_i32]),
     "fs_forward_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_sign_align_f64": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "fs_sign_align_f32": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "fs_gather_sort_keys_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
+    "fs_aggregate_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_gather_sort_keys_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_eval_workspace_bytes": (_c_sz, [_c_i32]),

@@ -16,72 +16,86 @@ constexpr int ALIGN_THREADS = 256;
 constexpr int ALIGN_UNROLL = 4;                                    // double2 per thread per pass
 constexpr int ALIGN_TILE = ALIGN_THREADS * ALIGN_UNROLL * 2;        // doubles per CTA pass
 
-__device__ __forceinline__ int sgn(double x) { return (x > 0.0) - (x < 0.0); }
+template <class T>
+__device__ __forceinline__ int sgn(T x) { return (x > T(0)) - (x < T(0)); }
 // sign(a - b) for finite a, b: IEEE subtraction with gradual underflow is
 // zero iff a == b and otherwise carries the ordering of a and b.
-__device__ __forceinline__ int sgn_diff(double a, double b) { return (a > b) - (a < b); }
+template <class T>
+__device__ __forceinline__ int sgn_diff(T a, T b) { return (a > b) - (a < b); }
 
-template <int MODE>
-__device__ __forceinline__ int aligned1(double c, double g, double p) {
+template <int MODE, class T>
+__device__ __forceinline__ int aligned1(T c, T g, T p) {
   if (MODE == FS_ALIGN_WEIGHT_SIGN) return sgn(c) == sgn(g);
   return sgn_diff(c, g) == sgn_diff(g, p);
 }
 
-template <int MODE>
+template <class T> struct Vec16;                       // 16-byte vector of T
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+
+template <int MODE, class T>
+__device__ __forceinline__ unsigned aligned_vec(const typename Vec16<T>::type& c, const typename Vec16<T>::type& g,
+                                                const typename Vec16<T>::type& p) {
+  const T* cc = reinterpret_cast<const T*>(&c);
+  const T* gg = reinterpret_cast<const T*>(&g);
+  const T* pp = reinterpret_cast<const T*>(&p);
+  unsigned n = 0;
+#pragma unroll
+  for (int i = 0; i < Vec16<T>::n; ++i) n += aligned1<MODE, T>(cc[i], gg[i], pp[i]);
+  return n;
+}
+
+template <int MODE, class T>
 __global__ void __launch_bounds__(ALIGN_THREADS)
     sign_align_kernel(const uint64_t* wc, const uint64_t* wg, const uint64_t* wgp, int64_t M,
                       int blocks_per_req, unsigned long long* out) {
+  using V = typename Vec16<T>::type;
+  constexpr int VN = Vec16<T>::n;
   const int r = blockIdx.x / blocks_per_req;
   const int blk = blockIdx.x % blocks_per_req;
-  const double* c = reinterpret_cast<const double*>(wc[r]);
-  const double* g = reinterpret_cast<const double*>(wg[r]);
-  const double* p = MODE == FS_ALIGN_DELTA_SIGN ? reinterpret_cast<const double*>(wgp[r]) : nullptr;
+  const T* c = reinterpret_cast<const T*>(wc[r]);
+  const T* g = reinterpret_cast<const T*>(wg[r]);
+  const T* p = MODE == FS_ALIGN_DELTA_SIGN ? reinterpret_cast<const T*>(wgp[r]) : nullptr;
   unsigned cnt = 0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(g) |
-                     reinterpret_cast<uintptr_t>(p)) & 15) == 0;
   const int64_t span = (M + blocks_per_req - 1) / blocks_per_req;
-  int64_t lo = (int64_t)blk * span;
+  const int64_t lo = (int64_t)blk * span;
   const int64_t hi = min(M, lo + span);
-  if (vec) {
-    // 16-byte aligned bulk of [lo, hi): lo is rounded to an even index
-    int64_t v0 = (lo + 1) & ~(int64_t)1;
-    int64_t v1 = hi & ~(int64_t)1;
-    if (v0 > v1) v0 = v1;
-    for (int64_t j = lo + threadIdx.x; j < v0; j += ALIGN_THREADS)
-      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
-    const double2* c2 = reinterpret_cast<const double2*>(c + v0);
-    const double2* g2 = reinterpret_cast<const double2*>(g + v0);
-    const double2* p2 = p ? reinterpret_cast<const double2*>(p + v0) : nullptr;
-    const int64_t n2 = (v1 - v0) / 2;
-    int64_t i = threadIdx.x;
-    for (; i + (ALIGN_UNROLL - 1) * ALIGN_THREADS < n2; i += ALIGN_UNROLL * ALIGN_THREADS) {
-      double2 cv[ALIGN_UNROLL], gv[ALIGN_UNROLL], pv[ALIGN_UNROLL];
-#pragma unroll
-      for (int u = 0; u < ALIGN_UNROLL; ++u) {
-        cv[u] = __ldcs(c2 + i + u * ALIGN_THREADS);
-        gv[u] = __ldg(g2 + i + u * ALIGN_THREADS);
-        if (MODE == FS_ALIGN_DELTA_SIGN) pv[u] = __ldg(p2 + i + u * ALIGN_THREADS);
-      }
-#pragma unroll
-      for (int u = 0; u < ALIGN_UNROLL; ++u) {
-        const double px = MODE == FS_ALIGN_DELTA_SIGN ? pv[u].x : 0.0;
-        const double py = MODE == FS_ALIGN_DELTA_SIGN ? pv[u].y : 0.0;
-        cnt += aligned1<MODE>(cv[u].x, gv[u].x, px);
-        cnt += aligned1<MODE>(cv[u].y, gv[u].y, py);
-      }
-    }
-    for (; i < n2; i += ALIGN_THREADS) {
-      const double2 cv = c2[i], gv = g2[i];
-      const double2 pv = p2 ? p2[i] : make_double2(0.0, 0.0);
-      cnt += aligned1<MODE>(cv.x, gv.x, pv.x);
-      cnt += aligned1<MODE>(cv.y, gv.y, pv.y);
-    }
-    for (int64_t j = v1 + threadIdx.x; j < hi; j += ALIGN_THREADS)
-      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
-  } else {
-    for (int64_t j = lo + threadIdx.x; j < hi; j += ALIGN_THREADS)
-      cnt += aligned1<MODE>(c[j], g[j], p ? p[j] : 0.0);
+  const T zero = T(0);
+  // 16-byte aligned bulk [v0, v1) of [lo, hi); scalar head/tail
+  const uintptr_t mis = (reinterpret_cast<uintptr_t>(c + lo) | reinterpret_cast<uintptr_t>(g + lo) |
+                         (p ? reinterpret_cast<uintptr_t>(p + lo) : 0)) & 15;
+  const bool same_phase = ((reinterpret_cast<uintptr_t>(c) ^ reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
+                          (!p || ((reinterpret_cast<uintptr_t>(c) ^ reinterpret_cast<uintptr_t>(p)) & 15) == 0);
+  int64_t v0 = hi, v1 = hi;
+  if (same_phase) {
+    const int64_t head = mis ? (int64_t)((16 - (reinterpret_cast<uintptr_t>(c + lo) & 15)) / sizeof(T)) : 0;
+    v0 = min(hi, lo + head);
+    v1 = v0 + (hi - v0) / VN * VN;
   }
+  for (int64_t j = lo + threadIdx.x; j < v0; j += ALIGN_THREADS)
+    cnt += aligned1<MODE, T>(c[j], g[j], p ? p[j] : zero);
+  const V* c2 = reinterpret_cast<const V*>(c + v0);
+  const V* g2 = reinterpret_cast<const V*>(g + v0);
+  const V* p2 = p ? reinterpret_cast<const V*>(p + v0) : nullptr;
+  const int64_t nv = (v1 - v0) / VN;
+  int64_t i = threadIdx.x;
+  for (; i + (ALIGN_UNROLL - 1) * ALIGN_THREADS < nv; i += ALIGN_UNROLL * ALIGN_THREADS) {
+    V cv[ALIGN_UNROLL], gv[ALIGN_UNROLL], pv[ALIGN_UNROLL];
+#pragma unroll
+    for (int u = 0; u < ALIGN_UNROLL; ++u) {
+      cv[u] = __ldcs(c2 + i + u * ALIGN_THREADS);
+      gv[u] = __ldg(g2 + i + u * ALIGN_THREADS);
+      if (MODE == FS_ALIGN_DELTA_SIGN) pv[u] = __ldg(p2 + i + u * ALIGN_THREADS); else pv[u] = V{};
+    }
+#pragma unroll
+    for (int u = 0; u < ALIGN_UNROLL; ++u) cnt += aligned_vec<MODE, T>(cv[u], gv[u], pv[u]);
+  }
+  for (; i < nv; i += ALIGN_THREADS) {
+    const V pv = p2 ? p2[i] : V{};
+    cnt += aligned_vec<MODE, T>(c2[i], g2[i], pv);
+  }
+  for (int64_t j = v1 + threadIdx.x; j < hi; j += ALIGN_THREADS)
+    cnt += aligned1<MODE, T>(c[j], g[j], p ? p[j] : zero);
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   __shared__ unsigned warp_sums[ALIGN_THREADS / 32];
   if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = cnt;
@@ -103,30 +117,41 @@ __global__ void sort_keys_kernel(const uint64_t* rows, int k, int n_keys, uint64
             ((uint64_t)__byte_perm((unsigned)bits, 0, 0x0123) << 32);
 }
 
+__global__ void sort_keys_f32_kernel(const uint64_t* rows, int k, int n_keys, uint64_t* keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k * n_keys) return;
+  const int row = i / n_keys, t = i % n_keys;
+  const unsigned bits = __float_as_uint(reinterpret_cast<const float*>(rows[row])[t]);
+  keys[i] = __byte_perm(bits, 0, 0x0123);
+}
+
 constexpr int AGG_THREADS = 128;
 constexpr int AGG_UNROLL = 8;
 
 // out[j] = ((rows[0][j] + rows[1][j]) + ...) / k : numpy's mean(axis=0) of
 // the stacked (k x M) updates adds rows in order, then true-divides by k.
+// (the float32 variant of the bf16 mode accumulates in float64 and rounds once)
+template <class T>
 __global__ void __launch_bounds__(AGG_THREADS)
-    aggregate_kernel(const uint64_t* rows, int k, int64_t M, double* out) {
-  extern __shared__ const double* sh_rows[];
+    aggregate_kernel(const uint64_t* rows, int k, int64_t M, T* out) {
+  extern __shared__ uint64_t sh_row_ptrs[];
+  const T** sh_rows = reinterpret_cast<const T**>(sh_row_ptrs);
   for (int i = threadIdx.x; i < k; i += AGG_THREADS)
-    sh_rows[i] = reinterpret_cast<const double*>(rows[i]);
+    sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
   __syncthreads();
   const int64_t j = (int64_t)blockIdx.x * AGG_THREADS + threadIdx.x;
   if (j >= M) return;
-  double acc = __ldcs(sh_rows[0] + j);
+  double acc = (double)__ldcs(sh_rows[0] + j);
   int i = 1;
   for (; i + AGG_UNROLL <= k; i += AGG_UNROLL) {
-    double v[AGG_UNROLL];
+    T v[AGG_UNROLL];
 #pragma unroll
     for (int u = 0; u < AGG_UNROLL; ++u) v[u] = __ldcs(sh_rows[i + u] + j);
 #pragma unroll
-    for (int u = 0; u < AGG_UNROLL; ++u) acc += v[u];
+    for (int u = 0; u < AGG_UNROLL; ++u) acc += (double)v[u];
   }
-  for (; i < k; ++i) acc += __ldcs(sh_rows[i] + j);
-  out[j] = acc / (double)k;
+  for (; i < k; ++i) acc += (double)__ldcs(sh_rows[i] + j);
+  out[j] = (T)(acc / (double)k);
 }
 
 // M == 1: a single stacked column reduces pairwise (np.sum semantics).
@@ -159,9 +184,9 @@ __global__ void aggregate_single_kernel(const uint64_t* rows, int k, double* out
 
 using namespace fs;
 
-extern "C" int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
-                                 int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
-                                 void* stream) {
+template <class T>
+static int sign_align_impl(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev, int32_t n_req,
+                           int64_t M, int32_t mode, int64_t* aligned_out, void* stream) {
   if (n_req < 0 || M < 0 || (mode != FS_ALIGN_WEIGHT_SIGN && mode != FS_ALIGN_DELTA_SIGN) ||
       (mode == FS_ALIGN_DELTA_SIGN && !wg_prev)) {
     set_error("fs_sign_align_f64: invalid arguments");
@@ -184,10 +209,20 @@ extern "C" int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const u
   const unsigned nblk = (unsigned)bpr * (unsigned)n_req;
   auto* out = reinterpret_cast<unsigned long long*>(aligned_out);
   if (mode == FS_ALIGN_WEIGHT_SIGN)
-    sign_align_kernel<FS_ALIGN_WEIGHT_SIGN><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
+    sign_align_kernel<FS_ALIGN_WEIGHT_SIGN, T><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
   else
-    sign_align_kernel<FS_ALIGN_DELTA_SIGN><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
+    sign_align_kernel<FS_ALIGN_DELTA_SIGN, T><<<nblk, ALIGN_THREADS, 0, st>>>(wc, wg, wg_prev, M, bpr, out);
   return check_launch("sign_align_kernel");
+}
+
+extern "C" int fs_sign_align_f64(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
+                                 int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out, void* stream) {
+  return sign_align_impl<double>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
+}
+
+extern "C" int fs_sign_align_f32(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg_prev,
+                                 int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out, void* stream) {
+  return sign_align_impl<float>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
 }
 
 extern "C" int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t n_keys,
@@ -200,6 +235,36 @@ extern "C" int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t 
   if (total == 0) return FS_OK;
   sort_keys_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(rows, k, n_keys, keys_out);
   return check_launch("sort_keys_kernel");
+}
+
+extern "C" int fs_gather_sort_keys_f32(const uint64_t* rows, int32_t k, int32_t n_keys,
+                                       uint64_t* keys_out, void* stream) {
+  if (k < 0 || n_keys < 0) {
+    set_error("fs_gather_sort_keys_f32: invalid sizes");
+    return FS_EINVAL;
+  }
+  const int total = k * n_keys;
+  if (total == 0) return FS_OK;
+  sort_keys_f32_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(rows, k, n_keys, keys_out);
+  return check_launch("sort_keys_f32_kernel");
+}
+
+extern "C" int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, void* stream) {
+  if (k < 1 || M < 0) {
+    set_error("fs_aggregate_f32: need k >= 1 updates");
+    return FS_EINVAL;
+  }
+  if (M == 0) return FS_OK;
+  const size_t smem = (size_t)k * sizeof(float*);
+  if (smem > 200 * 1024) {
+    set_error("fs_aggregate_f32: k=%d updates exceed the staged pointer table", k);
+    return FS_EINVAL;
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(aggregate_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
+  aggregate_kernel<float><<<blocks, AGG_THREADS, smem, (cudaStream_t)stream>>>(rows, k, M, out);
+  return check_launch("aggregate_kernel<float>");
 }
 
 extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out,
@@ -220,8 +285,8 @@ extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, doub
     return FS_EINVAL;
   }
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(aggregate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
-  aggregate_kernel<<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  aggregate_kernel<double><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
   return check_launch("aggregate_kernel");
 }

@@ -1,0 +1,591 @@
+// K5 (bf16 mixed-precision mode): batched per-client local SGD on the
+// 5th-generation tensor cores.
+//
+// Same contract as the fp64 trainer (client.train_local, client.py:98-172;
+// loss_and_grad, _core.pyx:140-219) with mixed precision: fp32 master
+// weights (the client's update row, updated in place), bf16 GEMM operands,
+// fp32 accumulation in TMEM, fp32 head/loss/SGD arithmetic.
+//
+// One persistent CTA per SM owns one client at a time (longest first).
+// Per SGD step the batch is processed in chunks of 64 rows; every layer
+// product is a tcgen05.mma (M=128, N<=256, K=16 slices) issued by one thread
+// with operands in shared memory and the accumulator in TMEM:
+//   forward   H_{l+1} = relu(H_l W_l + b_l) * mask     (A K-major, B MN-major)
+//   backward  G_l     = H_l^T D_{l+1}                  (A MN-major, B MN-major)
+//             D_l     = gate(D_{l+1} W_l^T, H_l)       (A K-major, B K-major)
+// All bf16 matrices live in shared memory as 8x8 core-matrix tiles, which
+// serve both K-major and MN-major operand roles (fs_tc.cuh), so no
+// transposes are ever materialised. Epilogues read TMEM with tcgen05.ld,
+// apply bias/relu/dropout or the gate, and write bf16 tiles back in place;
+// the weight-gradient epilogue applies W -= lr*G to the fp32 master row and
+// refreshes the bf16 weight tile. The sigmoid/BCE head (N=1) and the bias
+// gradients run on CUDA cores.
+#include <cstdio>
+
+#include "fs_common.cuh"
+#include "fs_tc.cuh"
+
+namespace fs {
+namespace bf16 {
+
+using namespace tc;
+
+constexpr int R = 64;           // batch rows per chunk (MMA M=128; rows >= 64 are ignored)
+constexpr int THREADS = 256;    // 8 warps: (lane quarter q = w & 3, column half h = w >> 2)
+constexpr int MAXL = 5;         // weight layers supported (<= 4 hidden)
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Geo {
+  int L;
+  int f[MAXL + 1];      // true dims
+  int fp[MAXL + 1];     // K-padded dims (fp[0] = roundup16(f0); hidden dims already % 16)
+  int woff[MAXL], boff[MAXL];
+  int M;                // parameters
+  int sum_hidden;
+  // shared-memory layout (bytes from the dynamic smem base)
+  uint32_t s_h[MAXL];   // activation tiles: s_h[0] = X [R x fp0], s_h[l] = H_l [R x f_l]
+  uint32_t s_w[MAXL];   // weight tiles W_l [fp_l x f_{l+1}] (hidden layers only)
+  uint32_t s_misc;      // fp32 scratch: z, dz, y, zpart[2][R], gw_head, gb
+  uint32_t smem_bytes;
+};
+
+struct Args {
+  Geo g;
+  int n_req, epochs, mask_mode;
+  float scale;
+  const __nv_bfloat16* feat;  // [rows x fp0] bf16, zero padded
+  const float* labels;        // [rows]
+  const int64_t* row_off;
+  const int32_t* n_rows;
+  const int32_t* batch;
+  const double* lr;           // [n_req x epochs]
+  const uint64_t* w_start;    // fp32 flat start parameters
+  float* w_out;               // fp32 flat, ldw floats per request
+  int64_t ldw;
+  const int32_t* perm;
+  const int64_t* perm_off;
+  const uint32_t* mask_bits;
+  const int64_t* mask_off;
+  const int32_t* start_step;
+  const int32_t* end_step;
+  const int32_t* order;
+  int32_t* status;
+  int* counter;
+  float* gacc;                // [grid x M] fp32 gradient accumulators (multi-chunk steps)
+};
+
+__device__ __forceinline__ float sigmoidf_stable(float z) {
+  if (z >= 0.f) return 1.f / (1.f + __expf(-z));
+  const float e = __expf(z);
+  return e / (1.f + e);
+}
+
+struct MaskSrc {
+  const uint32_t* bits;  // slot of this step (nullptr = no dropout)
+  int step_rows;         // rows of the whole batch (draw layout)
+  int row0;              // chunk offset inside the batch
+  float scale;
+  __device__ __forceinline__ uint32_t word(int64_t j) const { return __ldg(bits + (j >> 5)); }
+  // 16 keep bits for (row r of the chunk, units c..c+15) of hidden layer with
+  // draw base `base` and width `w`
+  __device__ __forceinline__ uint32_t keep16(int base, int r, int c, int w) const {
+    const int64_t j = (int64_t)step_rows * base + (int64_t)(row0 + r) * w + c;
+    const uint64_t lo = word(j);
+    const uint64_t both = ((j >> 5) == ((j + 15) >> 5)) ? lo : (lo | ((uint64_t)word(j + 15) << 32));
+    return (uint32_t)(both >> (j & 31)) & 0xFFFFu;
+  }
+};
+
+// Builds the bf16 tile of weight layer l from the fp32 master row.
+__device__ void load_weight_tile(const Geo& g, const float* W, int l, uint8_t* smem) {
+  const Tile t{smem_u32(smem + g.s_w[l]), g.fp[l]};
+  const int rows = g.fp[l], cols = g.f[l + 1];
+  const int chunks = rows * (cols / 8);
+  for (int i = threadIdx.x; i < chunks; i += THREADS) {
+    const int r = i / (cols / 8), c = (i % (cols / 8)) * 8;
+    uint32_t p[4] = {0, 0, 0, 0};
+    if (r < g.f[l]) {
+      const float* src = W + g.woff[l] + (int64_t)r * cols + c;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) p[k] = pack_bf16x2(src[2 * k], src[2 * k + 1]);
+    }
+    st_shared_v4(t.saddr + t.off(r, c), p[0], p[1], p[2], p[3]);
+  }
+}
+
+__device__ __forceinline__ void stage_sync() {
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+}
+
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  fence_after_sync();
+}
+
+__global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mma_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int s_item;
+  __shared__ int64_t s_rowidx[R];
+
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, h = warp >> 2;
+  float* misc = reinterpret_cast<float*>(smem + g.s_misc);
+  float* z_sh = misc;              // [R]
+  float* dz_sh = misc + R;         // [R]
+  float* y_sh = misc + 2 * R;      // [R]
+  float* zpart = misc + 3 * R;     // [2][R]
+  float* gwh = misc + 5 * R;       // [f_{L-1}] head weight grad (<= 256)
+  float* gbh = misc + 5 * R + 256; // [1]
+
+  if (warp == 0) tmem_alloc(&tmem_base_sh, TMEM_COLS);
+  if (tid == 0) {
+    mbar_init(&mma_bar, 1);
+    fence_mbar_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base_sh;
+  uint32_t phase = 0;
+  float* gacc = a.gacc + (int64_t)blockIdx.x * g.M;
+  const int L = g.L;
+  const int FL = g.f[L - 1];  // width feeding the head
+
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= a.n_req) break;
+    const int rq = a.order[item];
+    const int n = a.n_rows[rq], B = a.batch[rq];
+    const int spe = (n + B - 1) / B;
+    float* W = a.w_out + (int64_t)rq * a.ldw;
+    const float* W0 = reinterpret_cast<const float*>(a.w_start[rq]);
+    if (W0 != W)
+      for (int j = tid; j < g.M; j += THREADS) W[j] = W0[j];
+    __syncthreads();
+    for (int l = 0; l < L - 1; ++l) load_weight_tile(g, W, l, smem);
+    // padding columns of the input tile stay zero forever (gather writes only f0)
+    const int64_t slot_words = ((int64_t)B * g.sum_hidden + 31) / 32;
+
+    for (int step = a.start_step[rq]; step < a.end_step[rq]; ++step) {
+      const int e = step / spe, s = step % spe;
+      const int step_rows = min(B, n - s * B);
+      const float lr = (float)a.lr[(int64_t)rq * a.epochs + e];
+      const int32_t* perm_e = a.perm + a.perm_off[rq] + (int64_t)e * n;
+      MaskSrc mk;
+      mk.bits = a.mask_mode == FS_MASK_BITS ? a.mask_bits + a.mask_off[rq] + (int64_t)step * slot_words : nullptr;
+      mk.step_rows = step_rows;
+      mk.scale = a.scale;
+      const int nchunks = (step_rows + R - 1) / R;
+
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int row0 = ch * R;
+        const int rows = min(R, step_rows - row0);
+        const bool last_chunk = ch == nchunks - 1;
+        const bool first_chunk = ch == 0;
+        mk.row0 = row0;
+        // ---------------- gather the chunk's rows (bf16 features) and labels
+        if (tid < R) {
+          const int64_t row = tid < rows ? a.row_off[rq] + perm_e[s * B + row0 + tid] : -1;
+          s_rowidx[tid] = row;
+          y_sh[tid] = row >= 0 ? a.labels[row] : 0.f;
+        }
+        __syncthreads();
+        {
+          const Tile xt{smem_u32(smem + g.s_h[0]), R};
+          const int cpr = g.fp[0] / 8;  // 16-byte chunks per row
+          for (int i = tid; i < R * cpr; i += THREADS) {
+            const int r = i / cpr, c = (i % cpr) * 8;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r < rows) v = __ldg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * g.fp[0] + c));
+            st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
+          }
+        }
+        // ---------------- forward through the hidden layers
+        int base = 0;  // mask draw base of hidden layer l
+        for (int l = 0; l < L - 1; ++l) {
+          const int K = g.fp[l], N = g.f[l + 1];
+          stage_sync();
+          if (tid == 0) {
+            const Tile at{smem_u32(smem + g.s_h[l]), R};
+            const Tile bt{smem_u32(smem + g.s_w[l]), g.fp[l]};
+            const uint32_t id = idesc_bf16(128, N, false, true);
+            for (int ks = 0; ks < K / 16; ++ks) mma_bf16(tbase, at.kmajor(ks), bt.mnmajor(ks), id, ks > 0);
+            mma_commit(&mma_bar);
+          }
+          wait_mma(&mma_bar, phase);
+          // epilogue: rows q*32+lane (q < 2), columns [h*N/2, (h+1)*N/2)
+          const bool head_in = (l == L - 2);
+          float zp = 0.f;
+          if (q < 2) {
+            const int r = q * 32 + lane;
+            const Tile ot{smem_u32(smem + g.s_h[l + 1]), R};
+            const float* bias = W + g.boff[l];
+            const float* wh = W + g.woff[L - 1];
+            for (int c = h * (N / 2); c < (h + 1) * (N / 2); c += 16) {
+              float v[16];
+              tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+              const uint32_t keep = mk.bits ? mk.keep16(base, r, c, N) : 0xFFFFu;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                float x = v[i] + __ldg(bias + c + i);
+                x = x > 0.f ? x : 0.f;
+                if (mk.bits) x = ((keep >> i) & 1u) ? x * mk.scale : 0.f;
+                if (r >= rows) x = 0.f;
+                v[i] = x;
+              }
+              if (head_in) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) zp = fmaf(v[i], __ldg(wh + c + i), zp);
+              }
+              st_shared_v4(ot.saddr + ot.off(r, c), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                           pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+              st_shared_v4(ot.saddr + ot.off(r, c + 8), pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
+                           pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+            }
+            if (head_in) zpart[h * R + r] = zp;
+          }
+          base += N;
+        }
+        // ---------------- head: logits, dz = (sigmoid(z) - y) / step_rows
+        stage_sync();
+        if (tid < R) {
+          const float z = zpart[tid] + zpart[R + tid] + W[g.boff[L - 1]];
+          z_sh[tid] = z;
+          float d = 0.f;
+          if (tid < rows) {
+            d = (sigmoidf_stable(z) - y_sh[tid]) / (float)step_rows;
+            if (!isfinite(z)) atomicOr(a.status + rq, 1);
+          }
+          dz_sh[tid] = d;
+        }
+        __syncthreads();
+        // head weight/bias gradients (from the bf16 H_{L-1} tile, fp32 sums)
+        {
+          const Tile ht{smem_u32(smem + g.s_h[L - 1]), R};
+          for (int k = tid; k < FL; k += THREADS) {
+            float acc = 0.f;
+            const uint32_t colbase = ht.saddr + ht.off(0, k & ~7) + (uint32_t)((k & 7) * 2);
+            for (int r = 0; r < rows; ++r) {
+              uint16_t hv;
+              asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hv) : "r"(colbase + (uint32_t)((r >> 3) * 128 + (r & 7) * 16)));
+              acc = fmaf(__uint_as_float((uint32_t)hv << 16), dz_sh[r], acc);
+            }
+            gwh[k] = acc;
+          }
+          if (tid == THREADS - 1) {
+            float sacc = 0.f;
+            for (int r = 0; r < rows; ++r) sacc += dz_sh[r];
+            gbh[0] = sacc;
+          }
+        }
+        __syncthreads();
+        // D_{L-1} = gate(dz (x) w_head, H_{L-1}) written in place of H_{L-1}
+        {
+          const Tile ht{smem_u32(smem + g.s_h[L - 1]), R};
+          const float* wh = W + g.woff[L - 1];
+          const int cpr = FL / 8;
+          for (int i = tid; i < R * cpr; i += THREADS) {
+            const int r = i / cpr, c = (i % cpr) * 8;
+            const uint32_t ad = ht.saddr + ht.off(r, c);
+            uint32_t p[4];
+            ld_shared_v4(ad, p[0], p[1], p[2], p[3]);
+            const float dzr = dz_sh[r];
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float lo = bf16lo(p[k]) > 0.f ? dzr * __ldg(wh + c + 2 * k) : 0.f;
+              float hi = bf16hi(p[k]) > 0.f ? dzr * __ldg(wh + c + 2 * k + 1) : 0.f;
+              if (mk.bits) {
+                lo *= mk.scale;
+                hi *= mk.scale;
+              }
+              o[k] = pack_bf16x2(lo, hi);
+            }
+            st_shared_v4(ad, o[0], o[1], o[2], o[3]);
+          }
+        }
+        // head update (or accumulation for a multi-chunk step), after D used old w
+        __syncthreads();
+        {
+          float* wh = W + g.woff[L - 1];
+          float* ga = gacc + g.woff[L - 1];
+          for (int k = tid; k < FL; k += THREADS) {
+            const float gk = gwh[k] + (first_chunk ? 0.f : ga[k]);
+            if (last_chunk) wh[k] = wh[k] - lr * gk; else ga[k] = gk;
+          }
+          if (tid == THREADS - 1) {
+            const int bo = g.boff[L - 1];
+            const float gb = gbh[0] + (first_chunk ? 0.f : gacc[bo]);
+            if (last_chunk) W[bo] = W[bo] - lr * gb; else gacc[bo] = gb;
+          }
+        }
+        // ---------------- backward through the hidden layers
+        for (int l = L - 2; l >= 0; --l) {
+          const int K = g.fp[l];        // rows of W_l (padded)
+          const int N = g.f[l + 1];     // cols of W_l
+          const int mblocks = (K + 127) / 128;
+          const uint32_t dcol = (uint32_t)(mblocks * N);  // TMEM column of D_l
+          stage_sync();
+          if (tid == 0) {
+            const Tile ht{smem_u32(smem + g.s_h[l]), R};       // H_l (X for l = 0)
+            const Tile dt{smem_u32(smem + g.s_h[l + 1]), R};   // D_{l+1} (in place of H_{l+1})
+            const Tile wt{smem_u32(smem + g.s_w[l]), g.fp[l]};
+            const uint32_t idg = idesc_bf16(128, N, true, true);
+            for (int mb = 0; mb < mblocks; ++mb)
+              for (int ks = 0; ks < R / 16; ++ks)
+                mma_bf16(tbase + (uint32_t)(mb * N), ht.mnmajor(ks, mb), dt.mnmajor(ks), idg, ks > 0);
+            if (l > 0) {
+              const uint32_t idd = idesc_bf16(128, K, false, false);
+              for (int ks = 0; ks < N / 16; ++ks) mma_bf16(tbase + dcol, dt.kmajor(ks), wt.kmajor(ks), idd, ks > 0);
+            }
+            mma_commit(&mma_bar);
+          }
+          wait_mma(&mma_bar, phase);
+          // (a) D_l = gate(acc, H_l) in place of H_l  (rows q*32+lane, column half h)
+          if (l > 0 && q < 2) {
+            const int r = q * 32 + lane;
+            const Tile ht{smem_u32(smem + g.s_h[l]), R};
+            for (int c = h * (K / 2); c < (h + 1) * (K / 2); c += 16) {
+              float v[16];
+              tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + dcol + (uint32_t)c, v);
+              uint32_t hv[8];
+              ld_shared_v4(ht.saddr + ht.off(r, c), hv[0], hv[1], hv[2], hv[3]);
+              ld_shared_v4(ht.saddr + ht.off(r, c + 8), hv[4], hv[5], hv[6], hv[7]);
+              uint32_t o[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                float lo = bf16lo(hv[k]) > 0.f ? v[2 * k] : 0.f;
+                float hi = bf16hi(hv[k]) > 0.f ? v[2 * k + 1] : 0.f;
+                if (mk.bits) {
+                  lo *= mk.scale;
+                  hi *= mk.scale;
+                }
+                if (r >= rows) lo = hi = 0.f;
+                o[k] = pack_bf16x2(lo, hi);
+              }
+              st_shared_v4(ht.saddr + ht.off(r, c), o[0], o[1], o[2], o[3]);
+              st_shared_v4(ht.saddr + ht.off(r, c + 8), o[4], o[5], o[6], o[7]);
+            }
+          }
+          // (b) G_l -> W_l -= lr * G_l on the fp32 master row; refresh the bf16 tile
+          {
+            const Tile wt{smem_u32(smem + g.s_w[l]), g.fp[l]};
+            float* Wl = W + g.woff[l];
+            float* Gl = gacc + g.woff[l];
+            for (int mb = 0; mb < mblocks; ++mb) {
+              const int m = mb * 128 + q * 32 + lane;
+              for (int c = h * (N / 2); c < (h + 1) * (N / 2); c += 16) {
+                float v[16];
+                tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * N + c), v);
+                if (m < g.f[l]) {
+                  float* wp = Wl + (int64_t)m * N + c;
+                  float* gp = Gl + (int64_t)m * N + c;
+                  if (!first_chunk) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] += gp[i];
+                  }
+                  if (last_chunk) {
+                    float nw[16];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                      float4 w4 = *reinterpret_cast<float4*>(wp + i);
+                      w4.x -= lr * v[i];
+                      w4.y -= lr * v[i + 1];
+                      w4.z -= lr * v[i + 2];
+                      w4.w -= lr * v[i + 3];
+                      *reinterpret_cast<float4*>(wp + i) = w4;
+                      nw[i] = w4.x;
+                      nw[i + 1] = w4.y;
+                      nw[i + 2] = w4.z;
+                      nw[i + 3] = w4.w;
+                    }
+                    st_shared_v4(wt.saddr + wt.off(m, c), pack_bf16x2(nw[0], nw[1]), pack_bf16x2(nw[2], nw[3]),
+                                 pack_bf16x2(nw[4], nw[5]), pack_bf16x2(nw[6], nw[7]));
+                    st_shared_v4(wt.saddr + wt.off(m, c + 8), pack_bf16x2(nw[8], nw[9]),
+                                 pack_bf16x2(nw[10], nw[11]), pack_bf16x2(nw[12], nw[13]),
+                                 pack_bf16x2(nw[14], nw[15]));
+                  } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) gp[i] = v[i];
+                  }
+                }
+              }
+            }
+          }
+          // (c) bias b_l gradient: column sums of D_{l+1} over the chunk's rows
+          {
+            const Tile dt{smem_u32(smem + g.s_h[l + 1]), R};
+            float* bl = W + g.boff[l];
+            float* gb = gacc + g.boff[l];
+            for (int c = tid; c < N; c += THREADS) {
+              float acc = 0.f;
+              const uint32_t colbase = dt.saddr + dt.off(0, c & ~7) + (uint32_t)((c & 7) * 2);
+              for (int r = 0; r < rows; ++r) {
+                uint16_t dv;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=h"(dv) : "r"(colbase + (uint32_t)((r >> 3) * 128 + (r & 7) * 16)));
+                acc += __uint_as_float((uint32_t)dv << 16);
+              }
+              if (!first_chunk) acc += gb[c];
+              if (last_chunk) bl[c] = bl[c] - lr * acc; else gb[c] = acc;
+            }
+          }
+        }
+        __syncthreads();
+      }  // chunks
+    }    // steps
+    __syncthreads();
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, TMEM_COLS);
+}
+
+// features float64 [rows x d] -> bf16 [rows x dp] zero padded; labels -> fp32
+__global__ void prep_features_kernel(const double* X, const double* Y, int64_t rows, int d, int dp,
+                                     __nv_bfloat16* xb, float* yf) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * dp) return;
+  const int64_t r = i / dp;
+  const int c = (int)(i % dp);
+  xb[i] = __float2bfloat16_rn(c < d ? (float)X[r * d + c] : 0.f);
+  if (c == 0) yf[r] = (float)Y[r];
+}
+
+}  // namespace bf16
+
+using namespace bf16;
+
+static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
+  if (n_dims < 3 || n_dims > MAXL + 1) return FS_EINVAL;
+  Geo g{};
+  g.L = n_dims - 1;
+  for (int i = 0; i < n_dims; ++i) g.f[i] = dims[i];
+  if (g.f[g.L] != 1 || g.f[0] < 1 || g.f[0] > 256) return FS_EINVAL;
+  g.fp[0] = (g.f[0] + 15) / 16 * 16;
+  for (int l = 1; l < g.L; ++l) {
+    if (g.f[l] % 32 != 0 || g.f[l] < 32 || g.f[l] > 256) return FS_EINVAL;
+    g.fp[l] = g.f[l];
+  }
+  int off = 0;
+  for (int l = 0; l < g.L; ++l) {
+    g.woff[l] = off;
+    off += g.f[l] * g.f[l + 1];
+    g.boff[l] = off;
+    off += g.f[l + 1];
+  }
+  g.M = off;
+  g.sum_hidden = 0;
+  for (int l = 1; l < g.L; ++l) g.sum_hidden += g.f[l];
+  if (g.f[g.L - 1] > 256) return FS_EINVAL;
+  // TMEM budget of every backward stage: G blocks + D columns
+  for (int l = 0; l < g.L - 1; ++l) {
+    const int mblocks = (g.fp[l] + 127) / 128;
+    const int cols = mblocks * g.f[l + 1] + (l > 0 ? g.fp[l] : 0);
+    if (cols > (int)TMEM_COLS) return FS_EINVAL;
+  }
+  uint32_t s = 0;
+  for (int l = 0; l < g.L; ++l) {  // activation tiles (X, H_1..H_{L-1})
+    g.s_h[l] = s;
+    s += (uint32_t)(R * g.fp[l] * 2);
+  }
+  for (int l = 0; l < g.L - 1; ++l) {  // hidden weight tiles
+    g.s_w[l] = s;
+    s += (uint32_t)(g.fp[l] * g.f[l + 1] * 2);
+  }
+  g.s_misc = s;
+  s += (5 * R + 256 + 4) * 4;
+  // MMAs with M=128 over 64-row tiles read up to 16 KB past a tile; keep
+  // those reads inside the allocation
+  s += 16 * 1024;
+  g.smem_bytes = s;
+  if (s > 200 * 1024) return FS_EINVAL;
+  *out = g;
+  return FS_OK;
+}
+
+}  // namespace fs
+
+using namespace fs;
+
+extern "C" int fs_bf16_supported(const int32_t* dims, int32_t n_dims) {
+  Geo g;
+  return make_geo(dims, n_dims, &g) == FS_OK ? 1 : 0;
+}
+
+extern "C" int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
+                                     void* xb_out, float* y_out, void* stream) {
+  if (rows < 0 || d < 1 || dp < d || dp % 8) {
+    set_error("fs_prep_features_bf16: invalid sizes");
+    return FS_EINVAL;
+  }
+  if (rows == 0) return FS_OK;
+  const int64_t total = rows * dp;
+  prep_features_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      x, y, rows, d, dp, reinterpret_cast<__nv_bfloat16*>(xb_out), y_out);
+  return check_launch("prep_features_kernel");
+}
+
+extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
+  Geo g;
+  if (!d || make_geo(d->dims, d->n_dims, &g) != FS_OK || d->n_req < 1) return 0;
+  const int grid = d->grid > 0 ? d->grid : kNumSMs;
+  const int gg = grid < d->n_req ? grid : d->n_req;
+  return 256 + (size_t)gg * g.M * sizeof(float);
+}
+
+extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, const float* labels_f32,
+                             void* stream) {
+  Geo g;
+  if (!d || make_geo(d->dims, d->n_dims, &g) != FS_OK) {
+    set_error("fs_train_bf16: unsupported layer dims for the tensor-core trainer");
+    return FS_EINVAL;
+  }
+  if (d->n_req == 0) return FS_OK;
+  const size_t need = fs_train_bf16_workspace_bytes(d);
+  if (!d->workspace || d->workspace_bytes < need) {
+    set_error("fs_train_bf16: workspace %zu < required %zu", d->workspace_bytes, need);
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  Args a;
+  a.g = g;
+  a.n_req = d->n_req;
+  a.epochs = d->epochs;
+  a.mask_mode = d->mask_mode;
+  a.scale = (float)d->scale;
+  a.feat = reinterpret_cast<const __nv_bfloat16*>(features_bf16);
+  a.labels = labels_f32;
+  a.row_off = d->row_off;
+  a.n_rows = d->n_rows;
+  a.batch = d->batch;
+  a.lr = d->lr;
+  a.w_start = d->w_start;
+  a.w_out = reinterpret_cast<float*>(const_cast<double*>(d->w_out));
+  a.ldw = d->ldw;
+  a.perm = d->perm;
+  a.perm_off = d->perm_off;
+  a.mask_bits = d->mask_bits;
+  a.mask_off = d->mask_off;
+  a.start_step = d->start_step;
+  a.end_step = d->end_step;
+  a.order = d->order;
+  a.status = d->status;
+  a.counter = reinterpret_cast<int*>(d->workspace);
+  a.gacc = reinterpret_cast<float*>(reinterpret_cast<char*>(d->workspace) + 256);
+  if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
+  cudaFuncSetAttribute(train_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+  int grid = d->grid > 0 ? d->grid : kNumSMs;
+  if (grid > d->n_req) grid = d->n_req;
+  train_bf16_kernel<<<grid, THREADS, g.smem_bytes, st>>>(a);
+  return check_launch("train_bf16_kernel");
+}

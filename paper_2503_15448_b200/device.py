@@ -174,6 +174,19 @@ class DeviceShards:
     def __len__(self) -> int:
         return len(self.n_rows)
 
+    def bf16(self):
+        """(features bf16 [rows x round16(d)], labels fp32) for the tensor-core trainer."""
+        if getattr(self, "_bf16", None) is None:
+            rows = self.features.shape[0] if self.features.dim() == 2 else 0
+            dp = (self.dim + 15) // 16 * 16
+            xb = torch.empty((rows, dp), dtype=torch.bfloat16, device=self.rt.device)
+            yf = torch.empty(rows, dtype=torch.float32, device=self.rt.device)
+            self.rt.call(self.rt.lib.fs_prep_features_bf16(self.features.data_ptr(), self.labels.data_ptr(), rows,
+                                                           self.dim, dp, xb.data_ptr(), yf.data_ptr(), self.rt.stream),
+                         "fs_prep_features_bf16")
+            self._bf16 = (xb, yf)
+        return self._bf16
+
 
 # --------------------------------------------------------------- training
 @dataclass
@@ -215,21 +228,24 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
 def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.ndarray, lr: np.ndarray,
                 w_start: np.ndarray, batch: np.ndarray, epochs: int, dropout_rate: float,
                 start: np.ndarray | None = None, end: np.ndarray | None = None,
-                w_out: torch.Tensor | None = None, rt: Runtime | None = None):
+                w_out: torch.Tensor | None = None, rt: Runtime | None = None, precision: str = "fp64"):
     """Batched K2 -> K3 -> K5 over n requests given as arrays.
 
     clients [n] shard index, seeds [n] uint64 train seeds, lr [n x epochs],
     w_start [n] device pointers of the start parameters, batch [n]; optional
     start/end global step (end < 0 = all E*ceil(n_i/b_i) steps).
-    Returns (w_out [n x M] float64, status int32 [n]) on the device.
+    precision "fp64" runs the parity trainer (float64 rows); "bf16" runs the
+    tcgen05 mixed-precision trainer (float32 master rows, bf16 operands).
+    Returns (w_out [n x M], status int32 [n]) on the device.
     """
     rt = rt or Runtime.get()
     lib = rt.lib
     n = int(len(clients))
     dims = tuple(int(x) for x in spec_dims)
     M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
+    bf16 = precision == "bf16"
     if w_out is None:
-        w_out = torch.empty((n, M), dtype=torch.float64, device=rt.device)
+        w_out = torch.empty((n, M), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)
     status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
     if n == 0:
         return w_out, status
@@ -306,7 +322,9 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
     desc.order = order_p
     desc.status = status.data_ptr()
     desc.grid = TRAIN_GRID
-    need = lib.fs_train_workspace_bytes(ctypes.byref(desc))
+    need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
+    if need == 0:
+        raise ValueError(f"layer dims {dims} are not supported by the {precision} trainer")
     ws = rt.scratch("train", need)
     desc.workspace = ws.data_ptr()
     desc.workspace_bytes = ws.numel()
@@ -316,7 +334,11 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
         rows = (end - start - last) * batch + last * (n_rows - (spe - 1) * batch)
         work = float(rows.sum()) * mlp_flops_per_sample(dims)
     with rt.timed("train", work):
-        rt.call(lib.fs_train_f64(ctypes.byref(desc), stream), "fs_train_f64")
+        if bf16:
+            xb, yf = shards.bf16()
+            rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream), "fs_train_bf16")
+        else:
+            rt.call(lib.fs_train_f64(ctypes.byref(desc), stream), "fs_train_f64")
     # staging tensors may be released now: torch's caching allocator only
     # reuses their blocks for later work on this same stream
     return w_out, status
@@ -326,8 +348,9 @@ TRAIN_GRID = int(__import__("os").environ.get("FS_TRAIN_GRID", "0"))
 
 
 # --------------------------------------------------------------- alignment
-def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | None = None) -> torch.Tensor:
-    """K6: aligned counts [n] int64 (device)."""
+def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | None = None,
+                   dtype: torch.dtype = torch.float64) -> torch.Tensor:
+    """K6: aligned counts [n] int64 (device); dtype of the parameter vectors."""
     rt = rt or Runtime.get()
     n = len(wc_ptrs)
     out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
@@ -339,9 +362,11 @@ def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | 
         ptrs.append(np.asarray(wgp_ptrs, dtype=np.uint64).ravel())
     d = rt.h2d(np.concatenate(ptrs).view(np.int64))
     p = d.data_ptr()
-    with rt.timed("align", 8.0 * M * (n + (2 if m else 1))):
-        rt.call(rt.lib.fs_sign_align_f64(p, p + 8 * n, (p + 16 * n) if m else None, n, M, m,
-                                     out.data_ptr(), rt.stream), "fs_sign_align_f64")
+    esz = 4 if dtype == torch.float32 else 8
+    fn = rt.lib.fs_sign_align_f32 if esz == 4 else rt.lib.fs_sign_align_f64
+    with rt.timed("align", float(esz) * M * (n + (2 if m else 1))):
+        rt.call(fn(p, p + 8 * n, (p + 16 * n) if m else None, n, M, m, out.data_ptr(), rt.stream),
+                "fs_sign_align")
     return out[:n]
 
 
@@ -361,8 +386,8 @@ def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
     nk = min(_N_KEYS, M)
     d = rt.h2d(np.asarray([r.data_ptr() for r in rows], dtype=np.uint64).view(np.int64))
     keys = torch.empty(k * nk, dtype=torch.int64, device=rt.device)
-    rt.call(rt.lib.fs_gather_sort_keys_f64(d.data_ptr(), k, nk, keys.data_ptr(), rt.stream),
-            "fs_gather_sort_keys_f64")
+    fn = rt.lib.fs_gather_sort_keys_f32 if rows[0].dtype == torch.float32 else rt.lib.fs_gather_sort_keys_f64
+    rt.call(fn(d.data_ptr(), k, nk, keys.data_ptr(), rt.stream), "fs_gather_sort_keys")
     kh = keys.cpu().numpy().view(np.uint64).reshape(k, nk)
     order = list(np.lexsort([kh[:, t] for t in range(nk - 1, -1, -1)]))
     if nk == M:
@@ -388,9 +413,12 @@ def aggregate_rows(rows: list[torch.Tensor], M: int, rt: Runtime | None = None) 
     k = len(rows)
     order = canonical_order(rows, M, rt)
     d = rt.h2d(np.asarray([rows[i].data_ptr() for i in order], dtype=np.uint64).view(np.int64))
-    out = torch.empty(M, dtype=torch.float64, device=rt.device)
-    with rt.timed("aggregate", 8.0 * M * (k + 1)):
-        rt.call(rt.lib.fs_aggregate_f64(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate_f64")
+    dt = rows[0].dtype
+    out = torch.empty(M, dtype=dt, device=rt.device)
+    esz = out.element_size()
+    fn = rt.lib.fs_aggregate_f32 if dt == torch.float32 else rt.lib.fs_aggregate_f64
+    with rt.timed("aggregate", float(esz) * M * (k + 1)):
+        rt.call(fn(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate")
     return out
 
 

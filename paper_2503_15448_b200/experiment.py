@@ -41,7 +41,7 @@ def load_dataset(config: ExperimentConfig):
                          seed=derive_seed(config.seed, "data"))
 
 
-def build_world(config: ExperimentConfig, workers: int = 1) -> tuple[World, ParamVector]:
+def build_world(config: ExperimentConfig, workers: int = 1, precision: str = "fp64") -> tuple[World, ParamVector]:
     cfg = config.raw
     seed = config.seed
     ds = load_dataset(config)
@@ -91,6 +91,7 @@ def build_world(config: ExperimentConfig, workers: int = 1) -> tuple[World, Para
         fail_offsets=failure_offsets(config.num_clients, cycles, seed),
         checkpointing=ck["enabled"], recovery_s=ck["recovery_s"], step_overhead_s=cfg["step_overhead_s"],
         workers=workers, horizon_s=cfg["async_run"]["horizon_s"], cycle_cap=cfg["async_run"]["cycle_cap"],
+        precision=precision,
     )
     return world, init_params(world.spec, derive_seed(seed, "model-init"))
 

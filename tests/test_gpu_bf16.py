@@ -1,0 +1,150 @@
+"""bf16 mixed-precision (tcgen05) trainer: numerics against PyTorch fp32
+emulations and tolerance parity against the fp64 parity trainer."""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+UNSW = (42, 256, 128, 64, 1)
+
+
+def bf(t):
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+def emulate_step(dims, W, X, y, masks, scale, lr):
+    """PyTorch fp32 reference of one SGD step with the kernel's rounding points:
+    bf16 GEMM operands (activations, weights, gradients D), fp32 accumulation,
+    fp32 head/loss/update."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    L = len(dims) - 1
+    offs, o = [], 0
+    for a, b in zip(dims[:-1], dims[1:]):
+        offs.append((o, o + a * b))
+        o += a * b + b
+    Wl = [W[s:e].view(dims[i], dims[i + 1]) for i, (s, e) in enumerate(offs)]
+    bl = [W[e:e + dims[i + 1]] for i, (s, e) in enumerate(offs)]
+    rows = X.shape[0]
+    H = [bf(X)]
+    for l in range(L - 1):
+        v = torch.relu(H[l] @ bf(Wl[l]) + bl[l])
+        if masks is not None:
+            v = v * masks[l]
+        if l == L - 2:
+            z = v @ Wl[L - 1][:, 0] + bl[L - 1][0]
+        H.append(bf(v))
+    dz = (torch.sigmoid(z) - y) / rows
+    g = torch.zeros_like(W)
+    gW = [g[s:e].view(dims[i], dims[i + 1]) for i, (s, e) in enumerate(offs)]
+    gb = [g[e:e + dims[i + 1]] for i, (s, e) in enumerate(offs)]
+    gW[L - 1][:, 0] = H[L - 1].T @ dz
+    gb[L - 1][0] = dz.sum()
+    sc = scale if masks is not None else 1.0
+    D = bf(torch.where(H[L - 1] > 0, dz[:, None] * Wl[L - 1][:, 0][None, :] * sc, 0.0))
+    for l in range(L - 2, -1, -1):
+        gW[l][...] = H[l].T @ D
+        gb[l][...] = D.sum(0)
+        if l > 0:
+            D = bf(torch.where(H[l] > 0, (D @ bf(Wl[l]).T) * sc, 0.0))
+    return W - lr * g
+
+
+def _one_step(dims, rows, dropout, seed=5):
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, dropout_masks_device, init_params
+    from paper_2503_15448_b200.rng import derive_rng, derive_seed
+
+    spec = ModelSpec(input_dim=dims[0], hidden_dims=dims[1:-1], dropout_rate=dropout)
+    rng = np.random.default_rng(seed)
+    x = rng.normal(size=(rows, dims[0]))
+    y = rng.integers(0, 2, rows).astype(np.int8)
+    w0 = torch.tensor(init_params(spec, seed).values, dtype=torch.float32, device="cuda")
+    rt = D.Runtime.get()
+    shards = D.DeviceShards([x], [y], rt)
+    lr = 0.05
+    w_out, status = D.train_batch(spec.dims, shards, np.array([0]), np.array([seed], dtype=np.uint64),
+                                  np.array([[lr]]), np.array([w0.data_ptr()], dtype=np.uint64),
+                                  np.array([rows]), 1, dropout, rt=rt, precision="bf16")
+    torch.cuda.synchronize()
+    assert int(status[0]) == 0
+    perm = derive_rng(seed, "shuffle", 0).permutation(rows)
+    X = torch.tensor(x[perm], dtype=torch.float32, device="cuda")
+    Y = torch.tensor(y[perm], dtype=torch.float32, device="cuda")
+    masks = None
+    if dropout > 0:
+        masks = [m.to(torch.float32) for m in dropout_masks_device(spec, rows, derive_seed(seed, "mask", 0, 0))]
+    want = emulate_step(spec.dims, w0.clone(), X, Y, masks, 1.0 / (1.0 - dropout), lr)
+    return w0, w_out[0], want
+
+
+@pytest.mark.parametrize("rows,dropout", [(64, 0.3), (37, 0.3), (64, 0.0), (150, 0.3)])
+def test_bf16_single_step_matches_fp32_emulation(rows, dropout):
+    w0, got, want = _one_step(UNSW, rows, dropout)
+    delta_w = want - w0
+    err = (got - want).abs().max().item()
+    scale = delta_w.abs().max().item()
+    assert err <= 2e-3 * scale, (err, scale)
+    rel = ((got - want).norm() / delta_w.norm()).item()
+    assert rel < 1e-2, rel
+
+
+def test_bf16_local_training_tracks_fp64():
+    """Whole local trainings (5 epochs, dropout) stay within the bf16 budget
+    of the fp64 parity trainer: relative L2 error of the update delta."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=42, hidden_dims=(256, 128, 64), dropout_rate=0.3)
+    rng = np.random.default_rng(1)
+    sizes = [40, 171, 300, 64]
+    feats = [rng.normal(size=(n, 42)) + (rng.random() - 0.5) for n in sizes]
+    labs = [(rng.random(n) < 0.3).astype(np.int8) for n in sizes]
+    rt = D.Runtime.get()
+    shards = D.DeviceShards(feats, labs, rt)
+    w64 = torch.tensor(init_params(spec, 2).values, device="cuda")
+    w32 = w64.float()
+    k = len(sizes)
+    args = dict(clients=np.arange(k), seeds=np.arange(k, dtype=np.uint64) + 11, lr=np.full((k, 5), 0.05),
+                batch=np.array([64, 64, 128, 64]), epochs=5, dropout_rate=0.3, rt=rt)
+    out64, _ = D.train_batch(spec.dims, shards, w_start=np.full(k, w64.data_ptr(), dtype=np.uint64), **args)
+    out32, _ = D.train_batch(spec.dims, shards, w_start=np.full(k, w32.data_ptr(), dtype=np.uint64),
+                             precision="bf16", **args)
+    for i in range(k):
+        d64 = out64[i] - w64
+        d32 = out32[i].double() - w64
+        rel = ((d32 - d64).norm() / d64.norm()).item()
+        assert rel < 0.08, (i, rel)
+
+
+def test_bf16_engine_masks_match_fp64_outside_threshold_band():
+    """Teacher-forced selection parity: from the same global model, the bf16
+    trainer's accept decisions equal the fp64 ones except for clients whose
+    fp64 ratio lies within eps_r = 5e-3 of theta."""
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import execute_cycles, plan_cycle
+
+    cfg = {"num_clients": 48, "rounds": 2, "epochs": 2, "dataset": {"n": 30000, "d": 42},
+           "selection_mode": "delta_sign", "batch": {"policy": "dynamic"}, "seed": 3,
+           "profiles": {"capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
+                        "speed": {"distribution": "constant", "value": 50.0},
+                        "up_latency": {"distribution": "constant", "value": 1.0},
+                        "down_latency": {"distribution": "constant", "value": 1.0}}}
+    out = {}
+    theta = 0.65
+    for prec in ("fp64", "bf16"):
+        world, init = build_world(ExperimentConfig.from_dict(cfg), precision=prec)
+        plans = [plan_cycle(world, ci, 1, 1) for ci in range(world.num_clients)]
+        prev = type(init)(init.values * 0.98 + 0.001, init.spec_digest)
+        outs = execute_cycles(world, plans, [init] * len(plans), [prev] * len(plans))
+        out[prec] = [(o.accepted, o.relevance) for o in outs]
+    eps = 5e-3
+    flips = [i for i, (a, b) in enumerate(zip(out["fp64"], out["bf16"])) if a[0] != b[0]]
+    for i in flips:
+        assert abs(out["fp64"][i][1] - theta) <= eps, (i, out["fp64"][i], out["bf16"][i])
+    dr = [abs(a[1] - b[1]) for a, b in zip(out["fp64"], out["bf16"])]
+    assert max(dr) < 1e-2
