@@ -245,7 +245,12 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
     M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
     bf16 = precision == "bf16"
     if w_out is None:
-        w_out = torch.empty((n, M), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)
+        # rows padded to 128 bytes: 16-byte vector access to every client row
+        esz = 4 if bf16 else 8
+        ld = (M * esz + 127) // 128 * 128 // esz
+        w_out = torch.empty((n, ld), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)[:, :M]
+    if bf16 and (w_out.data_ptr() % 16 or (w_out.stride(0) * 4) % 16):
+        raise ValueError("bf16 trainer needs 16-byte aligned float32 rows")
     status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
     if n == 0:
         return w_out, status
