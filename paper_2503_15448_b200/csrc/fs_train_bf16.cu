@@ -46,6 +46,8 @@ struct Geo {
   uint32_t s_h[MAXL];   // activation tiles: s_h[0] = X [R x fp0], s_h[l] = H_l [R x f_l]
   uint32_t s_w[MAXL];   // weight tiles W_l [fp_l x f_{l+1}] (hidden layers only)
   uint32_t s_misc;      // fp32 scratch: z, dz, y, zpart[2][R], gw_head, gb
+  uint32_t s_bias;      // fp32 copies of the hidden-layer biases (sum_hidden floats)
+  int bias_off[MAXL];   // offset of b_l inside s_bias
   uint32_t smem_bytes;
 };
 
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
   float* zpart = misc + 3 * R;     // [2][R]
   float* gwh = misc + 5 * R;       // [f_{L-1}] head weight grad (<= 256)
   float* gbh = misc + 5 * R + 256; // [1]
+  float* bias_sh = reinterpret_cast<float*>(smem + g.s_bias);
 
   if (warp == 0) tmem_alloc(&tmem_base_sh, TMEM_COLS);
   if (tid == 0) {
@@ -169,10 +172,30 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
     const int spe = (n + B - 1) / B;
     float* W = a.w_out + (int64_t)rq * a.ldw;
     const float* W0 = reinterpret_cast<const float*>(a.w_start[rq]);
-    if (W0 != W)
-      for (int j = tid; j < g.M; j += THREADS) W[j] = W0[j];
+    if (W0 != W) {  // 16-byte vector copy of the start parameters (rows are 16 B aligned)
+      const int nv = g.M / 4;
+      const float4* s4 = reinterpret_cast<const float4*>(W0);
+      float4* d4 = reinterpret_cast<float4*>(W);
+      if ((reinterpret_cast<uintptr_t>(W0) & 15) == 0) {
+        for (int j = tid; j < nv; j += 4 * THREADS) {
+          float4 t[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j + u * THREADS < nv) t[u] = __ldg(s4 + j + u * THREADS);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j + u * THREADS < nv) d4[j + u * THREADS] = t[u];
+        }
+        for (int j = 4 * nv + tid; j < g.M; j += THREADS) W[j] = W0[j];
+      } else {
+        for (int j = tid; j < g.M; j += THREADS) W[j] = W0[j];
+      }
+    }
     __syncthreads();
-    for (int l = 0; l < L - 1; ++l) load_weight_tile(g, W, l, smem);
+    for (int l = 0; l < L - 1; ++l) {
+      load_weight_tile(g, W, l, smem);
+      for (int j = tid; j < g.f[l + 1]; j += THREADS) bias_sh[g.bias_off[l] + j] = W[g.boff[l] + j];
+    }
     // padding columns of the input tile stay zero forever (gather writes only f0)
     const int64_t slot_words = ((int64_t)B * g.sum_hidden + 31) / 32;
 
@@ -222,6 +245,17 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             for (int ks = 0; ks < K / 16; ++ks) mma_bf16(tbase, at.kmajor(ks), bt.mnmajor(ks), id, ks > 0);
             mma_commit(&mma_bar);
           }
+          // keep-bits of this thread's (row, column half) fetched while the MMA runs
+          uint32_t mw[5] = {0, 0, 0, 0, 0};
+          int mbit0 = 0;
+          if (mk.bits && q < 2) {
+            const int64_t j0 = (int64_t)mk.step_rows * base + (int64_t)(row0 + q * 32 + lane) * N + h * (N / 2);
+            const int64_t w0 = j0 >> 5, w1 = (j0 + N / 2 - 1) >> 5;
+            mbit0 = (int)(j0 & 31);
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+              if (w0 + i <= w1) mw[i] = __ldg(mk.bits + w0 + i);
+          }
           wait_mma(&mma_bar, phase);
           // epilogue: rows q*32+lane (q < 2), columns [h*N/2, (h+1)*N/2)
           const bool head_in = (l == L - 2);
@@ -229,15 +263,26 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           if (q < 2) {
             const int r = q * 32 + lane;
             const Tile ot{smem_u32(smem + g.s_h[l + 1]), R};
-            const float* bias = W + g.boff[l];
+            const float* bias = bias_sh + g.bias_off[l];
             const float* wh = W + g.woff[L - 1];
             for (int c = h * (N / 2); c < (h + 1) * (N / 2); c += 16) {
               float v[16];
               tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-              const uint32_t keep = mk.bits ? mk.keep16(base, r, c, N) : 0xFFFFu;
+              uint32_t keep = 0xFFFFu;
+              if (mk.bits) {
+                const int p = mbit0 + (c - h * (N / 2));
+                const int wi = p >> 5, sh = p & 31;
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                  if (i == wi) lo = mw[i];
+                  if (i == wi + 1) hi = mw[i];
+                }
+                keep = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh) & 0xFFFFu;
+              }
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                float x = v[i] + __ldg(bias + c + i);
+                float x = v[i] + bias[c + i];
                 x = x > 0.f ? x : 0.f;
                 if (mk.bits) x = ((keep >> i) & 1u) ? x * mk.scale : 0.f;
                 if (r >= rows) x = 0.f;
@@ -382,42 +427,61 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             const Tile wt{smem_u32(smem + g.s_w[l]), g.fp[l]};
             float* Wl = W + g.woff[l];
             float* Gl = gacc + g.woff[l];
+            const bool single = first_chunk && last_chunk;
             for (int mb = 0; mb < mblocks; ++mb) {
               const int m = mb * 128 + q * 32 + lane;
-              for (int c = h * (N / 2); c < (h + 1) * (N / 2); c += 16) {
-                float v[16];
-                tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * N + c), v);
-                if (m < g.f[l]) {
+              const bool valid = m < g.f[l];
+              const int cend = (h + 1) * (N / 2);
+              for (int c0 = h * (N / 2); c0 < cend; c0 += 64) {
+                const int cw = min(64, cend - c0);  // multiple of 16, warp-uniform
+                float4 wv[16];
+                if (single && valid) {  // issue the whole master slice before touching TMEM
+                  const float4* wp4 = reinterpret_cast<const float4*>(Wl + (int64_t)m * N + c0);
+#pragma unroll
+                  for (int i = 0; i < 16; ++i)
+                    if (4 * i < cw) wv[i] = wp4[i];
+                }
+#pragma unroll
+                for (int s16 = 0; s16 < 4; ++s16) {
+                  if (16 * s16 >= cw) break;
+                  const int c = c0 + 16 * s16;
+                  float v[16];
+                  tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * N + c), v);
+                  if (!valid) continue;
                   float* wp = Wl + (int64_t)m * N + c;
                   float* gp = Gl + (int64_t)m * N + c;
-                  if (!first_chunk) {
+                  if (!single) {
+                    if (!first_chunk) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] += gp[i];
-                  }
-                  if (last_chunk) {
-                    float nw[16];
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                      float4 w4 = *reinterpret_cast<float4*>(wp + i);
-                      w4.x -= lr * v[i];
-                      w4.y -= lr * v[i + 1];
-                      w4.z -= lr * v[i + 2];
-                      w4.w -= lr * v[i + 3];
-                      *reinterpret_cast<float4*>(wp + i) = w4;
-                      nw[i] = w4.x;
-                      nw[i + 1] = w4.y;
-                      nw[i + 2] = w4.z;
-                      nw[i + 3] = w4.w;
+                      for (int i = 0; i < 16; ++i) v[i] += gp[i];
                     }
-                    st_shared_v4(wt.saddr + wt.off(m, c), pack_bf16x2(nw[0], nw[1]), pack_bf16x2(nw[2], nw[3]),
-                                 pack_bf16x2(nw[4], nw[5]), pack_bf16x2(nw[6], nw[7]));
-                    st_shared_v4(wt.saddr + wt.off(m, c + 8), pack_bf16x2(nw[8], nw[9]),
-                                 pack_bf16x2(nw[10], nw[11]), pack_bf16x2(nw[12], nw[13]),
-                                 pack_bf16x2(nw[14], nw[15]));
-                  } else {
+                    if (!last_chunk) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) gp[i] = v[i];
+                      for (int i = 0; i < 16; ++i) gp[i] = v[i];
+                      continue;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) wv[4 * s16 + i] = reinterpret_cast<const float4*>(wp)[i];
                   }
+                  float nw[16];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    float4 w4 = wv[4 * s16 + i];
+                    w4.x -= lr * v[4 * i];
+                    w4.y -= lr * v[4 * i + 1];
+                    w4.z -= lr * v[4 * i + 2];
+                    w4.w -= lr * v[4 * i + 3];
+                    reinterpret_cast<float4*>(wp)[i] = w4;
+                    nw[4 * i] = w4.x;
+                    nw[4 * i + 1] = w4.y;
+                    nw[4 * i + 2] = w4.z;
+                    nw[4 * i + 3] = w4.w;
+                  }
+                  st_shared_v4(wt.saddr + wt.off(m, c), pack_bf16x2(nw[0], nw[1]), pack_bf16x2(nw[2], nw[3]),
+                               pack_bf16x2(nw[4], nw[5]), pack_bf16x2(nw[6], nw[7]));
+                  st_shared_v4(wt.saddr + wt.off(m, c + 8), pack_bf16x2(nw[8], nw[9]),
+                               pack_bf16x2(nw[10], nw[11]), pack_bf16x2(nw[12], nw[13]),
+                               pack_bf16x2(nw[14], nw[15]));
                 }
               }
             }
@@ -436,7 +500,13 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
                 acc += __uint_as_float((uint32_t)dv << 16);
               }
               if (!first_chunk) acc += gb[c];
-              if (last_chunk) bl[c] = bl[c] - lr * acc; else gb[c] = acc;
+              if (last_chunk) {
+                const float nb = bl[c] - lr * acc;
+                bl[c] = nb;
+                bias_sh[g.bias_off[l] + c] = nb;
+              } else {
+                gb[c] = acc;
+              }
             }
           }
         }
@@ -504,6 +574,15 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
   }
   g.s_misc = s;
   s += (5 * R + 256 + 4) * 4;
+  g.s_bias = s;
+  {
+    int bo = 0;
+    for (int l = 0; l < g.L - 1; ++l) {
+      g.bias_off[l] = bo;
+      bo += g.f[l + 1];
+    }
+    s += (uint32_t)((bo + 3) / 4 * 16);
+  }
   // MMAs with M=128 over 64-row tiles read up to 16 KB past a tile; keep
   // those reads inside the allocation
   s += 16 * 1024;

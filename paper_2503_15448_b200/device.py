@@ -394,20 +394,24 @@ def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
     fn = rt.lib.fs_gather_sort_keys_f32 if rows[0].dtype == torch.float32 else rt.lib.fs_gather_sort_keys_f64
     rt.call(fn(d.data_ptr(), k, nk, keys.data_ptr(), rt.stream), "fs_gather_sort_keys")
     kh = keys.cpu().numpy().view(np.uint64).reshape(k, nk)
-    order = list(np.lexsort([kh[:, t] for t in range(nk - 1, -1, -1)]))
+    order = np.lexsort([kh[:, t] for t in range(nk - 1, -1, -1)])
     if nk == M:
+        return [int(x) for x in order]
+    sk = kh[order]
+    tie = np.all(sk[1:] == sk[:-1], axis=1)  # row i+1 ties row i on the key prefix
+    if not tie.any():
         return [int(x) for x in order]
     out: list[int] = []
     i = 0
     while i < k:
         j = i + 1
-        while j < k and np.array_equal(kh[order[j]], kh[order[i]]):
+        while j < k and tie[j - 1]:
             j += 1
-        group = order[i:j]
+        group = [int(g) for g in order[i:j]]
         if len(group) > 1:
             full = {g: rows[g].cpu().numpy().tobytes() for g in group}
             group = sorted(group, key=lambda g: full[g])
-        out.extend(int(g) for g in group)
+        out.extend(group)
         i = j
     return out
 
