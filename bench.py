@@ -7,8 +7,10 @@ E=5 local epochs, capacity-driven batch sizes (dynamic 64..1024),
 gradient-sign (delta_sign) selection at theta=0.65, FedAvg, per-round
 evaluation on the 43,835-row test split. One bench "step" is one
 synchronous FL round over all 1024 clients (training, selection,
-aggregation, evaluation, event-log bookkeeping). fp64 parity mode: the
-event log is bit-identical to the reference's.
+aggregation, evaluation, event-log bookkeeping). Default precision is the
+bf16 tensor-core mode (fp32 master weights); the fp64 parity mode (event
+log bit-identical to the reference's) is measured in the same run and
+reported under "fp64_parity".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -178,21 +180,19 @@ def flush_l2(buf):
     buf.zero_()
 
 
-def run_b200(args, rank: int, world_size: int) -> None:
+def measure_rounds(world, initial, comm, steps: int, warmup: int, device_index: int):
+    """Time `steps` sync rounds (after `warmup`) with CUDA events on the launching
+    stream, L2 flushed between rounds, max over ranks. Returns a dict."""
     import torch
 
     from paper_2503_15448_b200 import device as D
     from paper_2503_15448_b200.server import FederationEngine, GlobalState
 
-    torch.cuda.set_device(rank % max(torch.cuda.device_count(), 1))
-    dist = None
-    if world_size > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl")
-    world, initial = build_c4_world(precision=args.precision)
     rt = D.Runtime.get()
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=rt.device)
+    dist = None
+    if comm is not None:
+        import torch.distributed as dist
 
     def barrier():
         torch.cuda.synchronize()
@@ -200,19 +200,18 @@ def run_b200(args, rank: int, world_size: int) -> None:
             dist.barrier()
             torch.cuda.synchronize()
 
-    # ---- device-resident timed run (value)
-    eng = FederationEngine(world)
+    eng = FederationEngine(world, comm=comm)
     state = GlobalState(round=0, w_g=initial)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         state = eng.run_sync_round(state)
     barrier()
     D.Runtime.timer = D.KernelTimer()
     calls0 = D.Runtime.abi_calls
     trainings0 = eng.trainings
     round_ms = []
-    with ClockSampler(rank % max(torch.cuda.device_count(), 1)) as clocks:
-        for _ in range(args.steps):
+    with ClockSampler(device_index) as clocks:
+        for _ in range(steps):
             flush_l2(l2_flush)
             barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -222,56 +221,120 @@ def run_b200(args, rank: int, world_size: int) -> None:
             barrier()
             round_ms.append(a.elapsed_time(b))
     timer, D.Runtime.timer = D.Runtime.timer, None
-    abi_calls = D.Runtime.abi_calls - calls0
-    trainings = eng.trainings - trainings0
     total_ms = float(np.sum(round_ms))
     if dist is not None:
         t = torch.tensor([total_ms], device=rt.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    ms_per_round = total_ms / args.steps
-    value = 1000.0 / ms_per_round
-    ksum = timer.summary()
+    return {"engine": eng, "state": state, "ms_per_round": total_ms / steps, "round_ms": round_ms,
+            "kernels": timer.summary(), "abi_calls": D.Runtime.abi_calls - calls0,
+            "trainings": eng.trainings - trainings0, "clocks": clocks.summary(), "barrier": barrier}
 
-    # ---- end-to-end through the public API with host buffers (e2e)
+
+def measure_e2e(world, eng, state, reps: int, barrier):
+    """Same metric through the public API with HOST inputs: every step re-uploads
+    the world's shards/test set from host numpy and reads w_g back."""
+    import torch
+
+    stream = torch.cuda.current_stream()
     e2e_ms = []
     h2d = d2h = 0
-    for i in range(max(2, args.steps // 2) + 1):
-        world._device = None   # drop the HBM copy: shards + test set re-uploaded from host
+    for i in range(reps + 1):
+        world._device = None
         barrier()
-        t0 = time.perf_counter()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         dev = world.device_state()
         state = eng.run_sync_round(state)
-        host_w = state.w_g.values  # D2H of the round's result
+        host_w = state.w_g.values
         b.record(stream)
         barrier()
         if i > 0:
             e2e_ms.append(a.elapsed_time(b))
         h2d = (dev.shards.features.numel() + dev.shards.labels.numel() + dev.test_x.numel()) * 8 + dev.test_y.numel()
-        d2h = host_w.nbytes + 1024 * 8 * 2  # w_g + aligned counts/status of 1024 clients
-    e2e_value = 1000.0 / float(np.mean(e2e_ms))
+        d2h = host_w.nbytes + world.num_clients * 8 * 2
+    return 1000.0 / float(np.mean(e2e_ms)), int(h2d), int(d2h)
 
+
+def hbm_microbench(M: int = 3193857, n_clients: int = 256):
+    """K6/K7 at the C5 (WIDE MLP) row length, float32 rows: achieved GB/s."""
+    import torch
+
+    from paper_2503_15448_b200 import device as D
+
+    rt = D.Runtime.get()
+    ld = (M + 31) // 32 * 32
+    W = torch.randn(n_clients, ld, device=rt.device, dtype=torch.float32)[:, :M]
+    wg = torch.randn(M, device=rt.device, dtype=torch.float32)
+    wp = torch.randn(M, device=rt.device, dtype=torch.float32)
+    ptr_c = W.data_ptr() + np.arange(n_clients, dtype=np.uint64) * np.uint64(ld * 4)
+    out = {}
+    for name in ("align", "aggregate"):
+        times = []
+        for it in range(6):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if name == "align":
+                D.align_requests(ptr_c, np.full(n_clients, wg.data_ptr(), dtype=np.uint64),
+                                 np.full(n_clients, wp.data_ptr(), dtype=np.uint64), M, "delta_sign", rt,
+                                 dtype=torch.float32)
+                nbytes = 4.0 * M * (n_clients + 2)
+            else:
+                d = rt.h2d(ptr_c.view(np.int64))
+                res = torch.empty(M, dtype=torch.float32, device=rt.device)
+                rt.call(rt.lib.fs_aggregate_f32(d.data_ptr(), n_clients, M, res.data_ptr(), rt.stream), "agg")
+                nbytes = 4.0 * M * (n_clients + 1)
+            b.record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(a.elapsed_time(b))
+        ms = float(np.mean(times))
+        out[name] = {"ms": ms, "bytes": nbytes, "achieved_gbs": nbytes / ms / 1e6}
+    return out
+
+
+def run_b200(args, rank: int, world_size: int) -> None:
+    import torch
+
+    from paper_2503_15448_b200.parallel import ShardComm
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
+    comm = ShardComm.from_env()
+    world, initial = build_c4_world(precision=args.precision)
+    m = measure_rounds(world, initial, comm, args.steps, args.warmup, local)
+    value = 1000.0 / m["ms_per_round"]
+    e2e_value, h2d, d2h = measure_e2e(world, m["engine"], m["state"], max(2, args.steps // 2), m["barrier"])
+    parity = None
+    if not args.no_parity:
+        w64, i64 = build_c4_world(precision="fp64")
+        p = measure_rounds(w64, i64, comm, max(2, args.steps // 2), 1, local)
+        parity = {"value": 1000.0 / p["ms_per_round"], "unit": "rounds/s", "ms_per_step": p["ms_per_round"],
+                  "train_kernel_ms": p["kernels"].get("train", {}).get("mean_ms"),
+                  "note": "fp64 parity mode: event log bit-identical to the reference (tests/test_gpu_parity.py)"}
     if rank != 0:
-        if dist is not None:
+        if comm is not None:
+            import torch.distributed as dist
+
             dist.destroy_process_group()
         return
-
-    # ---- roofline of the dominant kernel (the trainer)
+    ksum = m["kernels"]
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     tr = ksum.get("train", {})
-    achieved_tflops = tr["work_per_launch"] / (tr["mean_ms"] * 1e-3) / 1e12 if tr else None
-    roofline = {
-        "kernel": "fs::f64::train_kernel (K5, fp64 parity mode)",
-        "bound": "fp64",
-        "achieved": achieved_tflops, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved_tflops / FP64_NOMINAL_TFLOPS if achieved_tflops else None,
-        "peak_source": "nominal B200 FP64 37 TFLOP/s (MEASURED_PEAKS.json has no fp64 figure)",
-        "traffic": None,
-        "share_of_round": tr.get("total_ms", 0.0) / total_ms if tr else None,
-    }
+    achieved = tr["work_per_launch"] / (tr["mean_ms"] * 1e-3) / 1e12 if tr else None
+    if args.precision == "bf16":
+        peak, src = peaks.get("bf16_tflops", 1590.0), ("MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
+                                                      else "B200_PROFILING.md fallback 1.59 PFLOP/s")
+        roofline = {"kernel": "fs::bf16::train_bf16_kernel (K5, tcgen05/TMEM)", "bound": "tensor"}
+    else:
+        peak, src = FP64_NOMINAL_TFLOPS, "nominal B200 FP64 37 TFLOP/s (no measured fp64 peak)"
+        roofline = {"kernel": "fs::f64::train_kernel (K5, fp64 parity)", "bound": "fp64"}
+    roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if achieved else None, "peak_source": src,
+                     "traffic": None, "algorithmic_flops_per_launch": tr.get("work_per_launch"),
+                     "share_of_round": tr.get("total_ms", 0.0) / (m["ms_per_round"] * args.steps) if tr else None})
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     kernels = {}
     for name in ("align", "aggregate"):
@@ -280,8 +343,11 @@ def run_b200(args, rank: int, world_size: int) -> None:
             gbs = k["work_per_launch"] / (k["mean_ms"] * 1e-3) / 1e9
             kernels[name] = {"achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak, "mean_ms": k["mean_ms"],
                              "bytes_per_launch": k["work_per_launch"]}
-
-    # ---- CPU baseline (oracle port, bounded sample)
+    c5 = None
+    if not args.no_micro:
+        c5 = hbm_microbench()
+        for v in c5.values():
+            v["frac_hbm"] = v["achieved_gbs"] / hbm_peak
     cpu = None
     if world_size == 1 and not args.no_cpu:
         per_round, detail = oracle_round_sample(world, initial, args.cpu_sample)
@@ -289,32 +355,35 @@ def run_b200(args, rank: int, world_size: int) -> None:
                "sample": f"{args.cpu_sample} of 1024 client cycles of round 0 + FedAvg + full eval, "
                          f"extrapolated x1024/{args.cpu_sample}; oracle/fl_oracle.py numpy, 1 thread",
                "detail": detail}
-
     line = {
         "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world_size, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_round, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": m["ms_per_round"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "f64", "data": "synthetic",
         "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients (175,341 train rows, d=42), "
                                "MLP 42-256-128-64-1 dropout 0.3, E=5, dynamic batch 64..1024, delta_sign "
                                "theta=0.65, FedAvg, eval on 43,835 rows",
-                   "global_batch": None, "precision": "fp64 parity (digest-identical to reference)",
+                   "precision": ("bf16 GEMM operands, fp32 accumulate/master weights (tolerance-matched)"
+                                 if args.precision == "bf16" else "fp64 parity (digest-identical to reference)"),
                    "l2": "256 MiB buffer written between timed rounds (L2 flush)",
-                   "parallelism": f"clients sharded over {world_size} GPU(s)"},
-        "client_updates_per_s": value * trainings / args.steps,
-        "e2e": {"value": e2e_value, "unit": "rounds/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h),
-                "note": "public FederationEngine.run_sync_round with the world re-uploaded from host numpy "
-                        "each step and w_g read back"},
+                   "parallelism": f"1024 clients sharded over {world_size} GPU(s), 1 NCCL all-reduce/round"},
+        "client_updates_per_s": value * m["trainings"] / args.steps,
+        "e2e": {"value": e2e_value, "unit": "rounds/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "public FederationEngine.run_sync_round; shards + test set re-uploaded from host numpy "
+                        "each step, w_g read back"},
         "roofline": roofline,
         "hbm_kernels": kernels,
+        "hbm_kernels_c5": c5,
+        "fp64_parity": parity,
         "cpu_baseline": cpu,
-        "gpu_launches": int(abi_calls),
-        "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (CUB sort counts as one)",
-        "clocks": clocks.summary(),
+        "gpu_launches": int(m["abi_calls"]),
+        "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (a CUB sort counts as one)",
+        "clocks": m["clocks"],
         "kernel_ms": {k: v["mean_ms"] for k, v in ksum.items()},
     }
     print(json.dumps(line), flush=True)
-    if dist is not None:
+    if comm is not None:
+        import torch.distributed as dist
+
         dist.destroy_process_group()
 
 
@@ -327,7 +396,9 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--ref-sample", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
+    ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity-mode measurement")
+    ap.add_argument("--no-micro", action="store_true", help="skip the C5-shape HBM microbenchmark")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))

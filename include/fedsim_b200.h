@@ -131,6 +131,9 @@ int fs_train_f64(const fs_train_desc* desc, void* stream);
  * and desc->labels are ignored). Hidden widths must be multiples of 32 (<=256),
  * input width <= 256, at most 4 hidden layers.                              */
 int fs_bf16_supported(const int32_t* dims, int32_t n_dims);
+/* Diagnostic: accumulate per-phase SM cycles of the bf16 trainer into 32
+ * device counters (nullptr disables).                                     */
+void fs_bf16_set_profile(unsigned long long* counters);
 int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
                           void* xb_out, float* y_out, void* stream);
 size_t fs_train_bf16_workspace_bytes(const fs_train_desc* desc);
@@ -182,6 +185,15 @@ int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out, vo
 int fs_gather_sort_keys_f32(const uint64_t* rows, int32_t k, int32_t n_keys, uint64_t* keys_out,
                             void* stream);
 int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, void* stream);
+
+/* Client-sharded rounds (one GPU per rank): each rank sums its accepted
+ * updates (float64 accumulation, rows of float32 or float64 given by
+ * dtype_bytes), the ranks all-reduce [sum | counts] over NCCL, and every
+ * rank finishes out[j] = sum[j] / k in the parameter dtype, so the global
+ * model stays replicated without a broadcast.                            */
+int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
+                void* stream);
+int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out, void* stream);
 
 /* ---------------------------------------------------------------- K8 metrics
  * accuracy at `threshold` and rank AUC with midrank ties

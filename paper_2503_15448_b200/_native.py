@@ -84,6 +84,7 @@ _SIGNATURES = {
     "fs_train_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
     "fs_train_f64": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp]),
     "fs_bf16_supported": (ctypes.c_int, [_c_vp, _c_i32]),
+    "fs_bf16_set_profile": (None, [_c_vp]),
     "fs_prep_features_bf16": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp]),
     "fs_train_bf16_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
     "fs_train_bf16": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp, _c_vp, _c_vp]),
@@ -100,6 +101,8 @@ _SIGNATURES = {
     "fs_aggregate_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_gather_sort_keys_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
+    "fs_sum_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "fs_mean_finish": (ctypes.c_int, [_c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_eval_workspace_bytes": (_c_sz, [_c_i32]),
     "fs_eval_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_f64, _c_vp, _c_vp, _c_sz, _c_vp]),
 }

@@ -154,6 +154,37 @@ __global__ void __launch_bounds__(AGG_THREADS)
   out[j] = (T)(acc / (double)k);
 }
 
+// Partial FedAvg for client-sharded rounds: out[j] = sum_i rows[i][j] in
+// float64 (the rank's accepted updates in canonical order); the ranks'
+// partial sums are then all-reduced and finished by mean_finish_kernel.
+template <class T>
+__global__ void __launch_bounds__(AGG_THREADS)
+    sum_rows_kernel(const uint64_t* rows, int k, int64_t M, double* out) {
+  extern __shared__ uint64_t sh_row_ptrs2[];
+  const T** sh_rows = reinterpret_cast<const T**>(sh_row_ptrs2);
+  for (int i = threadIdx.x; i < k; i += AGG_THREADS) sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * AGG_THREADS + threadIdx.x;
+  if (j >= M) return;
+  double acc = 0.0;
+  int i = 0;
+  for (; i + AGG_UNROLL <= k; i += AGG_UNROLL) {
+    T v[AGG_UNROLL];
+#pragma unroll
+    for (int u = 0; u < AGG_UNROLL; ++u) v[u] = __ldcs(sh_rows[i + u] + j);
+#pragma unroll
+    for (int u = 0; u < AGG_UNROLL; ++u) acc += (double)v[u];
+  }
+  for (; i < k; ++i) acc += (double)__ldcs(sh_rows[i] + j);
+  out[j] = acc;
+}
+
+template <class T>
+__global__ void mean_finish_kernel(const double* sum, double k, int64_t M, T* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < M) out[j] = (T)(sum[j] / k);
+}
+
 // M == 1: a single stacked column reduces pairwise (np.sum semantics).
 __device__ double pairwise_rows(const uint64_t* rows, int lo, int n) {
   if (n < 8) {
@@ -289,4 +320,49 @@ extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, doub
   const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
   aggregate_kernel<double><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
   return check_launch("aggregate_kernel");
+}
+
+extern "C" int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
+                           void* stream) {
+  if (k < 0 || M < 0 || (dtype_bytes != 4 && dtype_bytes != 8)) {
+    set_error("fs_sum_rows: invalid arguments");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M == 0) return FS_OK;
+  if (k == 0) {
+    if (cudaMemsetAsync(out, 0, sizeof(double) * M, st) != cudaSuccess) return check_launch("memset sum");
+    return FS_OK;
+  }
+  const size_t smem = (size_t)k * sizeof(void*);
+  if (smem > 200 * 1024) {
+    set_error("fs_sum_rows: k=%d updates exceed the staged pointer table", k);
+    return FS_EINVAL;
+  }
+  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
+  if (dtype_bytes == 8) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(sum_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sum_rows_kernel<double><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(sum_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sum_rows_kernel<float><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  }
+  return check_launch("sum_rows_kernel");
+}
+
+extern "C" int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out,
+                              void* stream) {
+  if (k < 1 || M < 0 || (dtype_bytes != 4 && dtype_bytes != 8)) {
+    set_error("fs_mean_finish: invalid arguments");
+    return FS_EINVAL;
+  }
+  if (M == 0) return FS_OK;
+  const unsigned blocks = (unsigned)((M + 255) / 256);
+  if (dtype_bytes == 8)
+    mean_finish_kernel<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(sum, (double)k, M, (double*)out);
+  else
+    mean_finish_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(sum, (double)k, M, (float*)out);
+  return check_launch("mean_finish_kernel");
 }

@@ -74,7 +74,18 @@ struct Args {
   int32_t* status;
   int* counter;
   float* gacc;                // [grid x M] fp32 gradient accumulators (multi-chunk steps)
+  unsigned long long* prof;   // optional [32] phase cycle counters (thread 0 of every CTA)
 };
+
+// Phase profiler: thread 0 attributes elapsed SM cycles to phase k.
+#define FS_PROF(k)                                        \
+  do {                                                    \
+    if (a.prof && tid == 0) {                             \
+      const long long t1_ = clock64();                    \
+      s_prof[k] += (unsigned long long)(t1_ - prof_t0);   \
+      prof_t0 = t1_;                                      \
+    }                                                     \
+  } while (0)
 
 __device__ __forceinline__ float sigmoidf_stable(float z) {
   if (z >= 0.f) return 1.f / (1.f + __expf(-z));
@@ -134,6 +145,8 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_item;
   __shared__ int64_t s_rowidx[R];
+  __shared__ unsigned long long s_prof[32];
+  long long prof_t0 = clock64();
 
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -147,6 +160,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
   float* gbh = misc + 5 * R + 256; // [1]
   float* bias_sh = reinterpret_cast<float*>(smem + g.s_bias);
 
+  if (tid < 32) s_prof[tid] = 0;
   if (warp == 0) tmem_alloc(&tmem_base_sh, TMEM_COLS);
   if (tid == 0) {
     mbar_init(&mma_bar, 1);
@@ -223,6 +237,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           y_sh[tid] = row >= 0 ? a.labels[row] : 0.f;
         }
         __syncthreads();
+        FS_PROF(0);
         {
           const Tile xt{smem_u32(smem + g.s_h[0]), R};
           const int cpr = g.fp[0] / 8;  // 16-byte chunks per row
@@ -257,6 +272,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
               if (w0 + i <= w1) mw[i] = __ldg(mk.bits + w0 + i);
           }
           wait_mma(&mma_bar, phase);
+          FS_PROF(1 + l);
           // epilogue: rows q*32+lane (q < 2), columns [h*N/2, (h+1)*N/2)
           const bool head_in = (l == L - 2);
           float zp = 0.f;
@@ -299,6 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             }
             if (head_in) zpart[h * R + r] = zp;
           }
+          FS_PROF(5 + l);
           base += N;
         }
         // ---------------- head: logits, dz = (sigmoid(z) - y) / step_rows
@@ -314,6 +331,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           dz_sh[tid] = d;
         }
         __syncthreads();
+        FS_PROF(9);
         // head weight/bias gradients (from the bf16 H_{L-1} tile, fp32 sums)
         {
           const Tile ht{smem_u32(smem + g.s_h[L - 1]), R};
@@ -334,6 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           }
         }
         __syncthreads();
+        FS_PROF(10);
         // D_{L-1} = gate(dz (x) w_head, H_{L-1}) written in place of H_{L-1}
         {
           const Tile ht{smem_u32(smem + g.s_h[L - 1]), R};
@@ -361,6 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         }
         // head update (or accumulation for a multi-chunk step), after D used old w
         __syncthreads();
+        FS_PROF(11);
         {
           float* wh = W + g.woff[L - 1];
           float* ga = gacc + g.woff[L - 1];
@@ -396,6 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             mma_commit(&mma_bar);
           }
           wait_mma(&mma_bar, phase);
+          FS_PROF(12 + l);
           // (a) D_l = gate(acc, H_l) in place of H_l  (rows q*32+lane, column half h)
           if (l > 0 && q < 2) {
             const int r = q * 32 + lane;
@@ -422,6 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
               st_shared_v4(ht.saddr + ht.off(r, c + 8), o[4], o[5], o[6], o[7]);
             }
           }
+          FS_PROF(16 + l);
           // (b) G_l -> W_l -= lr * G_l on the fp32 master row; refresh the bf16 tile
           {
             const Tile wt{smem_u32(smem + g.s_w[l]), g.fp[l]};
@@ -486,6 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
               }
             }
           }
+          FS_PROF(20 + l);
           // (c) bias b_l gradient: column sums of D_{l+1} over the chunk's rows
           {
             const Tile dt{smem_u32(smem + g.s_h[l + 1]), R};
@@ -510,13 +533,16 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             }
           }
         }
+        FS_PROF(24);
         __syncthreads();
+        FS_PROF(25);
       }  // chunks
     }    // steps
     __syncthreads();
   }
   fence_before_sync();
   __syncthreads();
+  if (a.prof && tid < 32) atomicAdd(a.prof + tid, s_prof[tid]);
   if (warp == 0) tmem_dealloc(tbase, TMEM_COLS);
 }
 
@@ -596,6 +622,12 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
 
 using namespace fs;
 
+static unsigned long long* g_bf16_prof = nullptr;
+
+// Diagnostic: accumulate per-phase SM cycles of the bf16 trainer into a
+// device buffer of 32 counters (nullptr disables).
+extern "C" void fs_bf16_set_profile(unsigned long long* counters) { g_bf16_prof = counters; }
+
 extern "C" int fs_bf16_supported(const int32_t* dims, int32_t n_dims) {
   Geo g;
   return make_geo(dims, n_dims, &g) == FS_OK ? 1 : 0;
@@ -661,6 +693,7 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.status = d->status;
   a.counter = reinterpret_cast<int*>(d->workspace);
   a.gacc = reinterpret_cast<float*>(reinterpret_cast<char*>(d->workspace) + 256);
+  a.prof = g_bf16_prof;
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   cudaFuncSetAttribute(train_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   int grid = d->grid > 0 ? d->grid : kNumSMs;
