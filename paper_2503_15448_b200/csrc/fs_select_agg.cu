@@ -14,7 +14,7 @@ namespace fs {
 
 constexpr int ALIGN_THREADS = 256;
 constexpr int ALIGN_UNROLL = 4;                                    // double2 per thread per pass
-constexpr int ALIGN_TILE = ALIGN_THREADS * ALIGN_UNROLL * 2;        // doubles per CTA pass
+constexpr int ALIGN_BLOCK_BYTES = 128 * 1024;  // client-row bytes streamed per CTA
 
 template <class T>
 __device__ __forceinline__ int sgn(T x) { return (x > T(0)) - (x < T(0)); }
@@ -228,7 +228,10 @@ static int sign_align_impl(const uint64_t* wc, const uint64_t* wg, const uint64_
   if (cudaMemsetAsync(aligned_out, 0, sizeof(int64_t) * n_req, st) != cudaSuccess)
     return check_launch("memset aligned");
   if (M == 0) return FS_OK;
-  int bpr = (int)((M + ALIGN_TILE - 1) / ALIGN_TILE);
+  // ~128 KB of each client row per CTA (32 x 16-byte loads per thread): long
+  // enough to amortise the CTA reduction, short enough for >= 2 waves
+  const int64_t per_block = ALIGN_BLOCK_BYTES / (int64_t)sizeof(T);
+  int bpr = (int)((M + per_block - 1) / per_block);
   // keep >= 2 waves of 8 resident CTAs per SM even for few requests
   const int64_t want = (int64_t)kNumSMs * 8 * 2;
   if ((int64_t)bpr * n_req < want) {

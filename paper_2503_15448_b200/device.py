@@ -225,6 +225,159 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
         w_out=w_out, rt=rt)
 
 
+class TrainPlan:
+    """The data-independent half of a training launch: per-request metadata in
+    HBM plus the K2 permutations and K3 dropout keep-bits. It depends only on
+    (clients, train seeds, batch sizes, epochs), never on model values, so the
+    engines build the NEXT round's plan on a side stream while the current
+    round's aggregation, evaluation and event bookkeeping run."""
+
+    def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
+                 dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None):
+        rt = rt or Runtime.get()
+        self.rt = rt
+        lib = rt.lib
+        self.dims = tuple(int(x) for x in spec_dims)
+        self.shards = shards
+        self.epochs = int(epochs)
+        self.dropout_rate = float(dropout_rate)
+        cl = np.asarray(clients, dtype=np.int64)
+        n = len(cl)
+        self.n = n
+        self.clients = cl
+        self.seeds = np.asarray(seeds, dtype=np.uint64)
+        self.batch = np.asarray(batch, dtype=np.int64)
+        self.ready = None
+        if n == 0:
+            return
+        torch_stream = stream if stream is not None else torch.cuda.current_stream(rt.device)
+        s_handle = torch_stream.cuda_stream
+        sum_hidden = sum(self.dims[1:-1])
+        n_rows = shards.n_rows[cl].astype(np.int64)
+        spe = -(-n_rows // self.batch)
+        total = self.epochs * spe
+        start = np.zeros(n, dtype=np.int64) if start is None else np.asarray(start, dtype=np.int64)
+        end = total.copy() if end is None else np.where(np.asarray(end) < 0, total, end).astype(np.int64)
+        self.n_rows, self.spe, self.start, self.end = n_rows, spe, start, end
+        perm_len = self.epochs * n_rows
+        perm_off = np.zeros(n, dtype=np.int64)
+        np.cumsum(perm_len[:-1], out=perm_off[1:])
+        use_masks = self.dropout_rate > 0.0
+        slot = (self.batch * sum_hidden + 31) // 32
+        mask_len = total * slot if use_masks else np.zeros(n, dtype=np.int64)
+        mask_off = np.zeros(n, dtype=np.int64)
+        np.cumsum(mask_len[:-1], out=mask_off[1:])
+        # longest client first (LPT) so the critical path starts at t=0
+        order = np.argsort(-((end - start) * self.batch), kind="stable")
+        with torch.cuda.stream(torch_stream):
+            self.d_i64 = rt.h2d(np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)]))
+            self.d_i32 = rt.h2d(np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32))
+            self.perm = torch.empty(max(int(perm_len.sum()), 1), dtype=torch.int32, device=rt.device)
+            self.bits = (torch.empty(max(int(mask_len.sum()), 1), dtype=torch.int32, device=rt.device)
+                         if use_masks and self.epochs > 0 else None)
+        p64, p32 = self.d_i64.data_ptr(), self.d_i32.data_ptr()
+        self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
+        self.n_rows_p, self.batch_p, self.start_p, self.end_p, self.order_p = (p32 + 4 * n * k for k in range(5))
+        if self.epochs > 0:
+            rt.call(lib.fs_shuffle_perms(self.seeds_p, self.n_rows_p, self.perm_off_p, n, self.epochs,
+                                         int(n_rows.max()), self.perm.data_ptr(), s_handle), "fs_shuffle_perms")
+        self.scale = 1.0
+        if self.bits is not None:
+            keep = 1.0 - self.dropout_rate
+            self.scale = 1.0 / keep
+            rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n, self.epochs,
+                                        sum_hidden, keep, self.bits.data_ptr(), s_handle), "fs_dropout_bits")
+        if stream is not None:  # consumer stream waits on this event before the trainer reads the plan
+            self.ready = torch.cuda.Event()
+            self.ready.record(torch_stream)
+
+    def matches(self, clients, seeds, batch, epochs) -> bool:
+        return (self.epochs == epochs and np.array_equal(self.clients, clients)
+                and np.array_equal(self.seeds, seeds) and np.array_equal(self.batch, batch))
+
+    def consume(self, stream) -> None:
+        """Order `stream` after the plan's producer and keep its buffers alive for it."""
+        if self.ready is not None:
+            stream.wait_event(self.ready)
+            for t in (self.d_i64, self.d_i32, self.perm, self.bits):
+                if t is not None:
+                    t.record_stream(stream)
+            self.ready = None
+
+
+def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision: str = "fp64",
+                w_out: torch.Tensor | None = None):
+    """K5 over a prepared plan: lr [n x epochs], w_start [n] device pointers.
+    Returns (w_out [n x M], status int32 [n]) on the device."""
+    rt = plan.rt
+    lib = rt.lib
+    n = plan.n
+    dims = plan.dims
+    M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
+    bf16 = precision == "bf16"
+    if w_out is None:
+        # rows padded to 128 bytes: 16-byte vector access to every client row
+        esz = 4 if bf16 else 8
+        ld = (M * esz + 127) // 128 * 128 // esz
+        w_out = torch.empty((n, ld), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)[:, :M]
+    if bf16 and (w_out.data_ptr() % 16 or (w_out.stride(0) * 4) % 16):
+        raise ValueError("bf16 trainer needs 16-byte aligned float32 rows")
+    status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
+    if n == 0:
+        return w_out, status
+    stream = torch.cuda.current_stream(rt.device)
+    plan.consume(stream)
+    d_run = rt.h2d(np.asarray(w_start, dtype=np.uint64).view(np.int64))
+    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
+    desc = N.TrainDesc()
+    desc.n_dims = len(dims)
+    for i, v in enumerate(dims):
+        desc.dims[i] = v
+    desc.n_req = n
+    desc.epochs = plan.epochs
+    desc.max_batch = int(plan.batch.max())
+    desc.mask_mode = N.FS_MASK_BITS if plan.bits is not None else N.FS_MASK_NONE
+    desc.scale = plan.scale
+    desc.features = plan.shards.features.data_ptr()
+    desc.labels = plan.shards.labels.data_ptr()
+    desc.row_off = plan.row_off_p
+    desc.n_rows = plan.n_rows_p
+    desc.batch = plan.batch_p
+    desc.lr = d_lr.data_ptr()
+    desc.w_start = d_run.data_ptr()
+    desc.w_out = w_out.data_ptr()
+    desc.ldw = w_out.stride(0)
+    desc.perm = plan.perm.data_ptr()
+    desc.perm_off = plan.perm_off_p
+    desc.mask_bits = plan.bits.data_ptr() if plan.bits is not None else None
+    desc.mask_off = plan.mask_off_p
+    desc.start_step = plan.start_p
+    desc.end_step = plan.end_p
+    desc.order = plan.order_p
+    desc.status = status.data_ptr()
+    desc.grid = TRAIN_GRID
+    need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
+    if need == 0:
+        raise ValueError(f"layer dims {dims} are not supported by the {precision} trainer")
+    ws = rt.scratch("train", need)
+    desc.workspace = ws.data_ptr()
+    desc.workspace_bytes = ws.numel()
+    work = 0.0
+    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
+        s, e, spe, b, nr = plan.start, plan.end, plan.spe, plan.batch, plan.n_rows
+        last = e // spe - s // spe   # epoch-final (partial) steps in [start, end)
+        rows = (e - s - last) * b + last * (nr - (spe - 1) * b)
+        work = float(rows.sum()) * mlp_flops_per_sample(dims)
+    with rt.timed("train", work):
+        if bf16:
+            xb, yf = plan.shards.bf16()
+            rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream.cuda_stream),
+                    "fs_train_bf16")
+        else:
+            rt.call(lib.fs_train_f64(ctypes.byref(desc), stream.cuda_stream), "fs_train_f64")
+    return w_out, status
+
+
 def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.ndarray, lr: np.ndarray,
                 w_start: np.ndarray, batch: np.ndarray, epochs: int, dropout_rate: float,
                 start: np.ndarray | None = None, end: np.ndarray | None = None,
@@ -238,115 +391,8 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
     tcgen05 mixed-precision trainer (float32 master rows, bf16 operands).
     Returns (w_out [n x M], status int32 [n]) on the device.
     """
-    rt = rt or Runtime.get()
-    lib = rt.lib
-    n = int(len(clients))
-    dims = tuple(int(x) for x in spec_dims)
-    M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
-    bf16 = precision == "bf16"
-    if w_out is None:
-        # rows padded to 128 bytes: 16-byte vector access to every client row
-        esz = 4 if bf16 else 8
-        ld = (M * esz + 127) // 128 * 128 // esz
-        w_out = torch.empty((n, ld), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)[:, :M]
-    if bf16 and (w_out.data_ptr() % 16 or (w_out.stride(0) * 4) % 16):
-        raise ValueError("bf16 trainer needs 16-byte aligned float32 rows")
-    status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
-    if n == 0:
-        return w_out, status
-    sum_hidden = sum(dims[1:-1])
-    cl = np.asarray(clients, dtype=np.int64)
-    n_rows = shards.n_rows[cl].astype(np.int64)
-    batch = np.asarray(batch, dtype=np.int64)
-    spe = -(-n_rows // batch)
-    total = epochs * spe
-    start = np.zeros(n, dtype=np.int64) if start is None else np.asarray(start, dtype=np.int64)
-    end = total.copy() if end is None else np.where(np.asarray(end) < 0, total, end).astype(np.int64)
-    perm_len = epochs * n_rows
-    perm_off = np.zeros(n, dtype=np.int64)
-    np.cumsum(perm_len[:-1], out=perm_off[1:])
-    use_masks = dropout_rate > 0.0
-    slot = (batch * sum_hidden + 31) // 32
-    mask_len = total * slot if use_masks else np.zeros(n, dtype=np.int64)
-    mask_off = np.zeros(n, dtype=np.int64)
-    np.cumsum(mask_len[:-1], out=mask_off[1:])
-    # longest client first (LPT) so the critical path starts at t=0
-    order = np.argsort(-((end - start) * batch), kind="stable")
-
-    i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off,
-                          np.asarray(w_start, dtype=np.uint64).view(np.int64),
-                          np.asarray(seeds, dtype=np.uint64).view(np.int64)])
-    i32 = np.concatenate([n_rows, batch, start, end, order]).astype(np.int32)
-    d_i64 = rt.h2d(i64)
-    d_i32 = rt.h2d(i32)
-    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
-    p64 = d_i64.data_ptr()
-    p32 = d_i32.data_ptr()
-    row_off_p, perm_off_p, mask_off_p, wstart_p, seeds_p = (p64 + 8 * n * k for k in range(5))
-    n_rows_p, batch_p, start_p, end_p, order_p = (p32 + 4 * n * k for k in range(5))
-
-    perm = rt.scratch("perm", 4 * max(int(perm_len.sum()), 1))
-    stream = rt.stream
-    if epochs > 0:
-        rt.call(lib.fs_shuffle_perms(seeds_p, n_rows_p, perm_off_p, n, epochs,
-                                     int(n_rows.max()), perm.data_ptr(), stream), "fs_shuffle_perms")
-    mask_ptr = None
-    scale = 1.0
-    if use_masks and epochs > 0:
-        keep = 1.0 - dropout_rate
-        scale = 1.0 / keep
-        bits = rt.scratch("mask_bits", 4 * max(int(mask_len.sum()), 1))
-        rt.call(lib.fs_dropout_bits(seeds_p, n_rows_p, batch_p, mask_off_p, n, epochs, sum_hidden,
-                                    keep, bits.data_ptr(), stream), "fs_dropout_bits")
-        mask_ptr = bits.data_ptr()
-
-    desc = N.TrainDesc()
-    desc.n_dims = len(dims)
-    for i, v in enumerate(dims):
-        desc.dims[i] = v
-    desc.n_req = n
-    desc.epochs = epochs
-    desc.max_batch = int(batch.max())
-    desc.mask_mode = N.FS_MASK_BITS if mask_ptr else N.FS_MASK_NONE
-    desc.scale = scale
-    desc.features = shards.features.data_ptr()
-    desc.labels = shards.labels.data_ptr()
-    desc.row_off = row_off_p
-    desc.n_rows = n_rows_p
-    desc.batch = batch_p
-    desc.lr = d_lr.data_ptr()
-    desc.w_start = wstart_p
-    desc.w_out = w_out.data_ptr()
-    desc.ldw = w_out.stride(0)
-    desc.perm = perm.data_ptr()
-    desc.perm_off = perm_off_p
-    desc.mask_bits = mask_ptr
-    desc.mask_off = mask_off_p
-    desc.start_step = start_p
-    desc.end_step = end_p
-    desc.order = order_p
-    desc.status = status.data_ptr()
-    desc.grid = TRAIN_GRID
-    need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
-    if need == 0:
-        raise ValueError(f"layer dims {dims} are not supported by the {precision} trainer")
-    ws = rt.scratch("train", need)
-    desc.workspace = ws.data_ptr()
-    desc.workspace_bytes = ws.numel()
-    work = 0.0
-    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
-        last = end // spe - start // spe   # epoch-final (partial) steps in [start, end)
-        rows = (end - start - last) * batch + last * (n_rows - (spe - 1) * batch)
-        work = float(rows.sum()) * mlp_flops_per_sample(dims)
-    with rt.timed("train", work):
-        if bf16:
-            xb, yf = shards.bf16()
-            rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream), "fs_train_bf16")
-        else:
-            rt.call(lib.fs_train_f64(ctypes.byref(desc), stream), "fs_train_f64")
-    # staging tensors may be released now: torch's caching allocator only
-    # reuses their blocks for later work on this same stream
-    return w_out, status
+    plan = TrainPlan(spec_dims, shards, clients, seeds, batch, epochs, dropout_rate, start, end, rt)
+    return run_trainer(plan, lr, w_start, precision, w_out)
 
 
 TRAIN_GRID = int(__import__("os").environ.get("FS_TRAIN_GRID", "0"))
