@@ -425,28 +425,30 @@ def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | 
 _N_KEYS = 4
 
 
-def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
-    """Indices of ``rows`` sorted by ``values.tobytes()`` (server.py:84).
-
-    K9 gathers the leading elements as big-endian integer keys; rows tied on
-    that prefix fall back to a full-row byte comparison (rare).
-    """
-    k = len(rows)
+def canonical_order_ptrs(ptrs: np.ndarray, M: int, dtype: torch.dtype, rt: Runtime, row_of=None) -> np.ndarray:
+    """Order of parameter rows (device pointers) by ``values.tobytes()``
+    (server.py:84). K9 gathers the leading elements as big-endian integer
+    keys; rows tied on that prefix fall back to full-row byte comparison
+    (``row_of(i)`` -> tensor; rare)."""
+    ptrs = np.asarray(ptrs, dtype=np.uint64)
+    k = len(ptrs)
     if k <= 1:
-        return list(range(k))
+        return np.arange(k)
     nk = min(_N_KEYS, M)
-    d = rt.h2d(np.asarray([r.data_ptr() for r in rows], dtype=np.uint64).view(np.int64))
+    d = rt.h2d(ptrs.view(np.int64))
     keys = torch.empty(k * nk, dtype=torch.int64, device=rt.device)
-    fn = rt.lib.fs_gather_sort_keys_f32 if rows[0].dtype == torch.float32 else rt.lib.fs_gather_sort_keys_f64
+    fn = rt.lib.fs_gather_sort_keys_f32 if dtype == torch.float32 else rt.lib.fs_gather_sort_keys_f64
     rt.call(fn(d.data_ptr(), k, nk, keys.data_ptr(), rt.stream), "fs_gather_sort_keys")
     kh = keys.cpu().numpy().view(np.uint64).reshape(k, nk)
     order = np.lexsort([kh[:, t] for t in range(nk - 1, -1, -1)])
     if nk == M:
-        return [int(x) for x in order]
+        return order
     sk = kh[order]
     tie = np.all(sk[1:] == sk[:-1], axis=1)  # row i+1 ties row i on the key prefix
     if not tie.any():
-        return [int(x) for x in order]
+        return order
+    if row_of is None:
+        raise ValueError("rows tie on their leading bytes: a row accessor is needed to break the tie")
     out: list[int] = []
     i = 0
     while i < k:
@@ -455,26 +457,41 @@ def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
             j += 1
         group = [int(g) for g in order[i:j]]
         if len(group) > 1:
-            full = {g: rows[g].cpu().numpy().tobytes() for g in group}
+            full = {g: row_of(g).cpu().numpy().tobytes() for g in group}
             group = sorted(group, key=lambda g: full[g])
         out.extend(group)
         i = j
+    return np.asarray(out)
+
+
+def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
+    """Indices of ``rows`` (tensors) sorted by ``values.tobytes()``."""
+    if len(rows) <= 1:
+        return list(range(len(rows)))
+    ptrs = np.array([r.data_ptr() for r in rows], dtype=np.uint64)
+    return [int(i) for i in canonical_order_ptrs(ptrs, M, rows[0].dtype, rt, row_of=lambda i: rows[i])]
+
+
+def aggregate_ptrs(ptrs: np.ndarray, M: int, dtype: torch.dtype, rt: Runtime | None = None,
+                   row_of=None) -> torch.Tensor:
+    """K9 + K7 over raw row pointers: mean in canonical byte order."""
+    rt = rt or Runtime.get()
+    ptrs = np.asarray(ptrs, dtype=np.uint64)
+    k = len(ptrs)
+    order = canonical_order_ptrs(ptrs, M, dtype, rt, row_of)
+    d = rt.h2d(ptrs[order].view(np.int64))
+    out = torch.empty(M, dtype=dtype, device=rt.device)
+    esz = out.element_size()
+    fn = rt.lib.fs_aggregate_f32 if dtype == torch.float32 else rt.lib.fs_aggregate_f64
+    with rt.timed("aggregate", float(esz) * M * (k + 1)):
+        rt.call(fn(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate")
     return out
 
 
 def aggregate_rows(rows: list[torch.Tensor], M: int, rt: Runtime | None = None) -> torch.Tensor:
     """K9 + K7: mean of k device rows in canonical byte order (server.aggregate)."""
-    rt = rt or Runtime.get()
-    k = len(rows)
-    order = canonical_order(rows, M, rt)
-    d = rt.h2d(np.asarray([rows[i].data_ptr() for i in order], dtype=np.uint64).view(np.int64))
-    dt = rows[0].dtype
-    out = torch.empty(M, dtype=dt, device=rt.device)
-    esz = out.element_size()
-    fn = rt.lib.fs_aggregate_f32 if dt == torch.float32 else rt.lib.fs_aggregate_f64
-    with rt.timed("aggregate", float(esz) * M * (k + 1)):
-        rt.call(fn(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate")
-    return out
+    ptrs = np.array([r.data_ptr() for r in rows], dtype=np.uint64)
+    return aggregate_ptrs(ptrs, M, rows[0].dtype, rt, row_of=lambda i: rows[i])
 
 
 # --------------------------------------------------------------- eval
