@@ -85,6 +85,7 @@ _SIGNATURES = {
     "fs_train_f64": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp]),
     "fs_bf16_supported": (ctypes.c_int, [_c_vp, _c_i32]),
     "fs_bf16_set_profile": (None, [_c_vp]),
+    "fs_bf16_force_generic": (None, [ctypes.c_int]),
     "fs_prep_features_bf16": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp]),
     "fs_train_bf16_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
     "fs_train_bf16": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp, _c_vp, _c_vp]),

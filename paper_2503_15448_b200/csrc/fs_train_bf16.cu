@@ -48,6 +48,8 @@ struct Geo {
   uint32_t s_misc;      // fp32 scratch: z, dz, y, zpart[2][R], gw_head, gb
   uint32_t s_bias;      // fp32 copies of the hidden-layer biases (sum_hidden floats)
   int bias_off[MAXL];   // offset of b_l inside s_bias
+  uint32_t s_w2m;       // V2: fp32 master of W_2, column-major [f3][f2]
+  int v2;               // V2 eligible (3 hidden layers fitting the on-chip optimizer state)
   uint32_t smem_bytes;
 };
 
@@ -139,6 +141,193 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
   fence_after_sync();
 }
 
+
+// Column sums over the chunk's rows of a bf16 activation tile (bias gradients).
+__device__ __forceinline__ float tile_colsum(const Tile& t, int c, int rows) {
+  float acc = 0.f;
+  const uint32_t colbase = t.saddr + t.off(0, c & ~7) + (uint32_t)((c & 7) * 2);
+  for (int r = 0; r < rows; ++r) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(colbase + (uint32_t)((r >> 3) * 128 + (r & 7) * 16)));
+    acc += __uint_as_float((uint32_t)v << 16);
+  }
+  return acc;
+}
+
+// Row epilogue of a backward stage: D = gate(acc, H) * dropout * factor,
+// written as bf16 in place of H (rows q*32+lane for q < 2, column half h).
+__device__ __forceinline__ void gate_rows(const Tile& ht, uint32_t tacc, int K, int rows, bool dropout, float scale,
+                                          float factor, int q, int h, int lane) {
+  if (q >= 2) return;
+  const int r = q * 32 + lane;
+  for (int c = h * (K / 2); c < (h + 1) * (K / 2); c += 16) {
+    float v[16];
+    tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+    uint32_t hv[8];
+    ld_shared_v4(ht.saddr + ht.off(r, c), hv[0], hv[1], hv[2], hv[3]);
+    ld_shared_v4(ht.saddr + ht.off(r, c + 8), hv[4], hv[5], hv[6], hv[7]);
+    const float f = dropout ? factor * scale : factor;
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float lo = bf16lo(hv[k]) > 0.f ? v[2 * k] * f : 0.f;
+      float hi = bf16hi(hv[k]) > 0.f ? v[2 * k + 1] * f : 0.f;
+      if (r >= rows) lo = hi = 0.f;
+      o[k] = pack_bf16x2(lo, hi);
+    }
+    st_shared_v4(ht.saddr + ht.off(r, c), o[0], o[1], o[2], o[3]);
+    st_shared_v4(ht.saddr + ht.off(r, c + 8), o[4], o[5], o[6], o[7]);
+  }
+}
+
+// Backward through the 3 hidden layers with on-chip optimizer state (V2).
+// Layer indices: W_0 [f0 x f1] (HBM master), W_1 [f1 x f2] (TMEM master),
+// W_2 [f2 x f3] (smem master). D_3 (unscaled) is in the H_3 slot on entry.
+__device__ __forceinline__ void backward_v2(const Geo& g, const Args& a, uint8_t* smem, uint32_t tbase, uint32_t& phase,
+                                         uint64_t& mma_bar, float* W, float* bias_sh, float lr, int rows,
+                                         bool last_chunk, bool dropout, float scale, int tid, int q, int h,
+                                         int lane, unsigned long long* s_prof, long long& prof_t0) {
+  const int f0 = g.f[0], fp0 = g.fp[0], f1 = g.f[1], f2 = g.f[2], f3 = g.f[3];
+  const int mb1 = (f1 + 127) / 128;
+  const Tile xt{smem_u32(smem + g.s_h[0]), R};
+  const Tile h1{smem_u32(smem + g.s_h[1]), R};
+  const Tile h2{smem_u32(smem + g.s_h[2]), R};
+  const Tile h3{smem_u32(smem + g.s_h[3]), R};
+  const Tile w0t{smem_u32(smem + g.s_w[0]), fp0};
+  const Tile w1t{smem_u32(smem + g.s_w[1]), f1};
+  const Tile w2t{smem_u32(smem + g.s_w[2]), f2};
+  float* w2m = reinterpret_cast<float*>(smem + g.s_w2m);
+
+  // ---------------- stage 2: G2 = H2^T D3 (TMEM [0,f3)), D2 = D3 W2^T (TMEM [f3, f3+f2))
+  stage_sync();
+  if (tid == 0) {
+    const uint32_t idg = idesc_bf16(128, f3, true, true);
+    for (int ks = 0; ks < R / 16; ++ks) mma_bf16(tbase, h2.mnmajor(ks), h3.mnmajor(ks), idg, ks > 0);
+    const uint32_t idd = idesc_bf16(128, f2, false, false);
+    for (int ks = 0; ks < f3 / 16; ++ks) mma_bf16(tbase + (uint32_t)f3, h3.kmajor(ks), w2t.kmajor(ks), idd, ks > 0);
+    mma_commit(&mma_bar);
+  }
+  wait_mma(&mma_bar, phase);
+  FS_PROF(14);
+  // D2 carries the step size from here on: tiles hold -lr * dL/dH
+  gate_rows(h2, tbase + (uint32_t)f3, f2, rows, dropout, scale, -lr, q, h, lane);
+  FS_PROF(18);
+  {  // W2 -= lr * G2 on the shared-memory master (column-major: lane-consecutive rows)
+    const int m = q * 32 + lane;
+    for (int c = h * (f3 / 2); c < (h + 1) * (f3 / 2); c += 16) {
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+      if (m < f2) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float* p = w2m + (c + i) * f2 + m;
+          const float nw = *p - lr * v[i];
+          *p = nw;
+          v[i] = nw;
+        }
+        if (last_chunk) {
+          st_shared_v4(w2t.saddr + w2t.off(m, c), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                       pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+          st_shared_v4(w2t.saddr + w2t.off(m, c + 8), pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
+                       pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+        }
+      }
+    }
+  }
+  for (int c = tid; c < f3; c += THREADS) {  // b2 -= lr * colsum(D3)
+    const float nb = W[g.boff[2] + c] - lr * tile_colsum(h3, c, rows);
+    W[g.boff[2] + c] = nb;
+    if (last_chunk) bias_sh[g.bias_off[2] + c] = nb;
+  }
+  FS_PROF(22);
+
+  // ---------------- stage 1: W1_master += H1^T (-lr D2) in TMEM; D1 = (-lr D2) W1^T (TMEM [0,f1))
+  stage_sync();
+  if (tid == 0) {
+    const uint32_t idg = idesc_bf16(128, f2, true, true);
+    for (int mb = 0; mb < mb1; ++mb)
+      for (int ks = 0; ks < R / 16; ++ks)
+        mma_bf16(tbase + 256u + (uint32_t)(mb * f2), h1.mnmajor(ks, mb), h2.mnmajor(ks), idg, 1u);
+    const uint32_t idd = idesc_bf16(128, f1, false, false);
+    for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase, h2.kmajor(ks), w1t.kmajor(ks), idd, ks > 0);
+    mma_commit(&mma_bar);
+  }
+  wait_mma(&mma_bar, phase);
+  FS_PROF(13);
+  gate_rows(h1, tbase, f1, rows, dropout, scale, 1.f, q, h, lane);
+  FS_PROF(17);
+  if (last_chunk) {  // refresh the bf16 W1 tile from the TMEM master
+    for (int mb = 0; mb < mb1; ++mb) {
+      const int m = mb * 128 + q * 32 + lane;
+      for (int c = h * (f2 / 2); c < (h + 1) * (f2 / 2); c += 16) {
+        float v[16];
+        tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + 256u + (uint32_t)(mb * f2 + c), v);
+        if (m < f1) {
+          st_shared_v4(w1t.saddr + w1t.off(m, c), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                       pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+          st_shared_v4(w1t.saddr + w1t.off(m, c + 8), pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
+                       pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+        }
+      }
+    }
+  }
+  for (int c = tid; c < f2; c += THREADS) {  // b1 += colsum(-lr D2)
+    const float nb = W[g.boff[1] + c] + tile_colsum(h2, c, rows);
+    W[g.boff[1] + c] = nb;
+    if (last_chunk) bias_sh[g.bias_off[1] + c] = nb;
+  }
+  FS_PROF(21);
+
+  // ---------------- stage 0: G0^T = (-lr D1)^T X (TMEM [mb*fp0, ...)), W0 += G0^T^T in HBM
+  stage_sync();
+  if (tid == 0) {
+    const uint32_t idg = idesc_bf16(128, fp0, true, true);
+    for (int mb = 0; mb < mb1; ++mb)
+      for (int ks = 0; ks < R / 16; ++ks)
+        mma_bf16(tbase + (uint32_t)(mb * fp0), h1.mnmajor(ks, mb), xt.mnmajor(ks), idg, ks > 0);
+    mma_commit(&mma_bar);
+  }
+  wait_mma(&mma_bar, phase);
+  FS_PROF(12);
+  for (int mb = 0; mb < mb1; ++mb) {
+    const int m = mb * 128 + q * 32 + lane;  // output unit of layer 0
+    for (int ci = h; ci * 16 < fp0; ci += 2) {
+      const int c = ci * 16;
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * fp0 + c), v);
+      if (m < f1) {
+        float w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[i] = (c + i < f0) ? W[(c + i) * f1 + m] : 0.f;  // coalesced across lanes
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (c + i < f0) {
+            w[i] += v[i];
+            W[(c + i) * f1 + m] = w[i];
+            if (last_chunk) {
+              const __nv_bfloat16 b = __float2bfloat16_rn(w[i]);
+              const uint32_t ad = w0t.saddr + w0t.off(c + i, m & ~7) + (uint32_t)((m & 7) * 2);
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(ad), "h"(*reinterpret_cast<const uint16_t*>(&b)));
+            }
+          }
+        }
+      }
+    }
+  }
+  for (int c = tid; c < f1; c += THREADS) {  // b0 += colsum(-lr D1)
+    const float nb = W[g.boff[0] + c] + tile_colsum(h1, c, rows);
+    W[g.boff[0] + c] = nb;
+    if (last_chunk) bias_sh[g.bias_off[0] + c] = nb;
+  }
+  FS_PROF(20);
+}
+
+// V2 = on-chip optimizer state for 3-hidden-layer MLPs: the largest hidden
+// weight's fp32 master lives in TMEM columns [256, 512) and is updated by the
+// weight-gradient MMA itself (master += H^T (-lr D)); W_{L-2}'s master lives
+// in shared memory; W_0's master stays in HBM but is updated through the
+// transposed gradient G_0^T so every warp issues coalesced row segments.
+template <bool V2>
 __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mma_bar;
@@ -209,6 +398,21 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
     for (int l = 0; l < L - 1; ++l) {
       load_weight_tile(g, W, l, smem);
       for (int j = tid; j < g.f[l + 1]; j += THREADS) bias_sh[g.bias_off[l] + j] = W[g.boff[l] + j];
+    }
+    if constexpr (V2) {
+      // W_1 master -> TMEM [256, 512); W_2 master -> smem (column-major)
+      const int f1 = g.f[1], f2 = g.f[2], f3 = g.f[3];
+      for (int mb = 0; mb < (g.fp[1] + 127) / 128; ++mb) {
+        const int m = mb * 128 + q * 32 + lane;
+        for (int c = h * (f2 / 2); c < (h + 1) * (f2 / 2); c += 16) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = m < f1 ? W[g.woff[1] + m * f2 + c + i] : 0.f;
+          tmem_st16(tbase + ((uint32_t)(q * 32) << 16) + 256u + (uint32_t)(mb * f2 + c), v);
+        }
+      }
+      float* w2m = reinterpret_cast<float*>(smem + g.s_w2m);
+      for (int i = tid; i < f2 * f3; i += THREADS) w2m[(i % f3) * f2 + i / f3] = W[g.woff[2] + i];
     }
     // padding columns of the input tile stay zero forever (gather writes only f0)
     const int64_t slot_words = ((int64_t)B * g.sum_hidden + 31) / 32;
@@ -381,7 +585,18 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         // head update (or accumulation for a multi-chunk step), after D used old w
         __syncthreads();
         FS_PROF(11);
-        {
+        if constexpr (V2) {
+          float* wh = W + g.woff[L - 1];
+          float* ghs = misc + 5 * R + 260;  // [FL] head-gradient accumulator across chunks
+          for (int k = tid; k < FL; k += THREADS) {
+            const float gk = gwh[k] + (first_chunk ? 0.f : ghs[k]);
+            if (last_chunk) wh[k] = wh[k] - lr * gk; else ghs[k] = gk;
+          }
+          if (tid == THREADS - 1) {
+            const float gb = gbh[0] + (first_chunk ? 0.f : ghs[FL]);
+            if (last_chunk) W[g.boff[L - 1]] = W[g.boff[L - 1]] - lr * gb; else ghs[FL] = gb;
+          }
+        } else {
           float* wh = W + g.woff[L - 1];
           float* ga = gacc + g.woff[L - 1];
           for (int k = tid; k < FL; k += THREADS) {
@@ -394,6 +609,10 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
             if (last_chunk) W[bo] = W[bo] - lr * gb; else gacc[bo] = gb;
           }
         }
+        if constexpr (V2) {
+          backward_v2(g, a, smem, tbase, phase, mma_bar, W, bias_sh, lr, rows, last_chunk, mk.bits != nullptr,
+                      mk.scale, tid, q, h, lane, s_prof, prof_t0);
+        } else
         // ---------------- backward through the hidden layers
         for (int l = L - 2; l >= 0; --l) {
           const int K = g.fp[l];        // rows of W_l (padded)
@@ -538,6 +757,27 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         FS_PROF(25);
       }  // chunks
     }    // steps
+    if constexpr (V2) {  // write the on-chip masters back to the client's row
+      fence_before_sync();
+      __syncthreads();
+      fence_after_sync();
+      const int f1 = g.f[1], f2 = g.f[2], f3 = g.f[3];
+      for (int mb = 0; mb < (g.fp[1] + 127) / 128; ++mb) {
+        const int m = mb * 128 + q * 32 + lane;
+        for (int c = h * (f2 / 2); c < (h + 1) * (f2 / 2); c += 16) {
+          float v[16];
+          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + 256u + (uint32_t)(mb * f2 + c), v);
+          if (m < f1) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(W + g.woff[1] + m * f2 + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+        }
+      }
+      const float* w2m = reinterpret_cast<const float*>(smem + g.s_w2m);
+      for (int i = tid; i < f2 * f3; i += THREADS) W[g.woff[2] + i] = w2m[(i % f3) * f2 + i / f3];
+      fence_before_sync();
+    }
     __syncthreads();
   }
   fence_before_sync();
@@ -599,7 +839,7 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
     s += (uint32_t)(g.fp[l] * g.f[l + 1] * 2);
   }
   g.s_misc = s;
-  s += (5 * R + 256 + 4) * 4;
+  s += (5 * R + 256 + 4 + 260) * 4;  // z, dz, y, zpart[2], gw_head, gb_head, head-grad accumulator
   g.s_bias = s;
   {
     int bo = 0;
@@ -609,11 +849,28 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
     }
     s += (uint32_t)((bo + 3) / 4 * 16);
   }
-  // MMAs with M=128 over 64-row tiles read up to 16 KB past a tile; keep
-  // those reads inside the allocation
-  s += 16 * 1024;
+  // V2 (on-chip optimizer state): 3 hidden layers, W_1 master fits TMEM
+  // columns [256,512), W_2 master fits shared memory, and every transient
+  // accumulator fits TMEM columns [0,256)
+  g.v2 = 0;
+  if (g.L == 4) {
+    const int mb1 = (g.f[1] + 127) / 128;
+    const bool tm = mb1 * g.f[2] <= 256 && g.f[1] <= 256 && g.f[2] <= 128 && g.f[3] + g.f[2] <= 256 &&
+                    mb1 * g.fp[0] <= 256 && g.fp[0] <= 64;
+    const uint32_t w2m_bytes = (uint32_t)(g.f[2] * g.f[3] * 4);
+    if (tm && s + w2m_bytes <= 220 * 1024) {
+      g.v2 = 1;
+      g.s_w2m = s;
+      s += w2m_bytes;
+    }
+  }
+  if (!g.v2) {
+    // generic path: MMAs with M=128 over 64-row tiles read up to 16 KB past a
+    // tile; keep those reads inside the allocation
+    s += 16 * 1024;
+  }
   g.smem_bytes = s;
-  if (s > 200 * 1024) return FS_EINVAL;
+  if (s > 220 * 1024) return FS_EINVAL;
   *out = g;
   return FS_OK;
 }
@@ -623,6 +880,10 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
 using namespace fs;
 
 static unsigned long long* g_bf16_prof = nullptr;
+static int g_bf16_force_generic = 0;
+
+// Diagnostic: force the generic (HBM optimizer state) bf16 kernel.
+extern "C" void fs_bf16_force_generic(int on) { g_bf16_force_generic = on; }
 
 // Diagnostic: accumulate per-phase SM cycles of the bf16 trainer into a
 // device buffer of 32 counters (nullptr disables).
@@ -695,9 +956,18 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.gacc = reinterpret_cast<float*>(reinterpret_cast<char*>(d->workspace) + 256);
   a.prof = g_bf16_prof;
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
-  cudaFuncSetAttribute(train_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
-  train_bf16_kernel<<<grid, THREADS, g.smem_bytes, st>>>(a);
+  if (g.v2 && !g_bf16_force_generic) {
+    cudaFuncSetAttribute(train_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    train_bf16_kernel<true><<<grid, THREADS, g.smem_bytes, st>>>(a);
+  } else {
+    if (g.v2) {  // the generic kernel needs its over-read pad
+      a.g.smem_bytes += 16 * 1024;
+      g.smem_bytes += 16 * 1024;
+    }
+    cudaFuncSetAttribute(train_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    train_bf16_kernel<false><<<grid, THREADS, g.smem_bytes, st>>>(a);
+  }
   return check_launch("train_bf16_kernel");
 }
