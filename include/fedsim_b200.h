@@ -129,7 +129,7 @@ int fs_train_f64(const fs_train_desc* desc, void* stream);
  * ldw] buffer (fp32 master weights, bf16 GEMM operands, fp32 accumulate).
  * Features/labels come pre-converted by fs_prep_features_bf16 (desc->features
  * and desc->labels are ignored). Hidden widths must be multiples of 32 (<=256),
- * input width <= 256, at most 4 hidden layers.                              */
+ * input width <= 64, at most 4 hidden layers.                              */
 int fs_bf16_supported(const int32_t* dims, int32_t n_dims);
 /* Diagnostic: accumulate per-phase SM cycles of the bf16 trainer into 32
  * device counters (nullptr disables).                                     */

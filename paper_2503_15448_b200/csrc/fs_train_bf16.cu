@@ -34,6 +34,7 @@ constexpr int R = 64;           // batch rows per chunk (MMA M=128; rows >= 64 a
 constexpr int THREADS = 256;    // 8 warps: (lane quarter q = w & 3, column half h = w >> 2)
 constexpr int MAXL = 5;         // weight layers supported (<= 4 hidden)
 constexpr uint32_t TMEM_COLS = 512;
+constexpr int XPRE = 2;         // 16-byte feature chunks per thread per chunk (R * fp0/8 <= 512)
 
 struct Geo {
   int L;
@@ -155,14 +156,17 @@ __device__ __forceinline__ float tile_colsum(const Tile& t, int c, int rows) {
 }
 
 // Row epilogue of a backward stage: D = gate(acc, H) * dropout * factor,
-// written as bf16 in place of H (rows q*32+lane for q < 2, column half h).
+// written as bf16 in place of H. The accumulator comes from an M=64 MMA, whose
+// rows sit 16 per TMEM lane quarter (row q*16 + i at lane 32*q + i), so all 8
+// warps work: lanes 0-15 of warp (q, h) own row q*16+lane, column half h.
 __device__ __forceinline__ void gate_rows(const Tile& ht, uint32_t tacc, int K, int rows, bool dropout, float scale,
                                           float factor, int q, int h, int lane) {
-  if (q >= 2) return;
-  const int r = q * 32 + lane;
+  const int r = q * 16 + lane;
+  const bool own = lane < 16;
   for (int c = h * (K / 2); c < (h + 1) * (K / 2); c += 16) {
     float v[16];
     tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+    if (!own) continue;
     uint32_t hv[8];
     ld_shared_v4(ht.saddr + ht.off(r, c), hv[0], hv[1], hv[2], hv[3]);
     ld_shared_v4(ht.saddr + ht.off(r, c + 8), hv[4], hv[5], hv[6], hv[7]);
@@ -203,7 +207,7 @@ __device__ __forceinline__ void backward_v2(const Geo& g, const Args& a, uint8_t
   if (tid == 0) {
     const uint32_t idg = idesc_bf16(128, f3, true, true);
     for (int ks = 0; ks < R / 16; ++ks) mma_bf16(tbase, h2.mnmajor(ks), h3.mnmajor(ks), idg, ks > 0);
-    const uint32_t idd = idesc_bf16(128, f2, false, false);
+    const uint32_t idd = idesc_bf16(64, f2, false, false);
     for (int ks = 0; ks < f3 / 16; ++ks) mma_bf16(tbase + (uint32_t)f3, h3.kmajor(ks), w2t.kmajor(ks), idd, ks > 0);
     mma_commit(&mma_bar);
   }
@@ -248,7 +252,7 @@ __device__ __forceinline__ void backward_v2(const Geo& g, const Args& a, uint8_t
     for (int mb = 0; mb < mb1; ++mb)
       for (int ks = 0; ks < R / 16; ++ks)
         mma_bf16(tbase + 256u + (uint32_t)(mb * f2), h1.mnmajor(ks, mb), h2.mnmajor(ks), idg, 1u);
-    const uint32_t idd = idesc_bf16(128, f1, false, false);
+    const uint32_t idd = idesc_bf16(64, f1, false, false);
     for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase, h2.kmajor(ks), w1t.kmajor(ks), idd, ks > 0);
     mma_commit(&mma_bar);
   }
@@ -287,25 +291,41 @@ __device__ __forceinline__ void backward_v2(const Geo& g, const Args& a, uint8_t
         mma_bf16(tbase + (uint32_t)(mb * fp0), h1.mnmajor(ks, mb), xt.mnmajor(ks), idg, ks > 0);
     mma_commit(&mma_bar);
   }
+  // W0 master slices (coalesced across lanes) for both M-blocks, issued before
+  // the TMEM reads so their latency overlaps the gradient MMA drain
+  constexpr int MAXCI = 2;  // 16-column chunks per thread and M-block (fp0 <= 64)
+  float wpre[2][MAXCI][16];
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb) {
+    const int m = mb * 128 + q * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < MAXCI; ++j) {
+      const int c = (h + 2 * j) * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        wpre[mb][j][i] = (mb < mb1 && m < f1 && c + i < f0) ? W[(c + i) * f1 + m] : 0.f;
+    }
+  }
   wait_mma(&mma_bar, phase);
   FS_PROF(12);
-  for (int mb = 0; mb < mb1; ++mb) {
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb) {
+    if (mb >= mb1) break;
     const int m = mb * 128 + q * 32 + lane;  // output unit of layer 0
-    for (int ci = h; ci * 16 < fp0; ci += 2) {
-      const int c = ci * 16;
+#pragma unroll
+    for (int j = 0; j < MAXCI; ++j) {
+      const int c = (h + 2 * j) * 16;
+      if (c >= fp0) break;
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * fp0 + c), v);
       if (m < f1) {
-        float w[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) w[i] = (c + i < f0) ? W[(c + i) * f1 + m] : 0.f;  // coalesced across lanes
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if (c + i < f0) {
-            w[i] += v[i];
-            W[(c + i) * f1 + m] = w[i];
+            const float w = wpre[mb][j][i] + v[i];
+            W[(c + i) * f1 + m] = w;
             if (last_chunk) {
-              const __nv_bfloat16 b = __float2bfloat16_rn(w[i]);
+              const __nv_bfloat16 b = __float2bfloat16_rn(w);
               const uint32_t ad = w0t.saddr + w0t.off(c + i, m & ~7) + (uint32_t)((m & 7) * 2);
               asm volatile("st.shared.b16 [%0], %1;" ::"r"(ad), "h"(*reinterpret_cast<const uint16_t*>(&b)));
             }
@@ -334,6 +354,8 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_item;
   __shared__ int64_t s_rowidx[R];
+  __shared__ int64_t s_rowidx_next[R];
+  __shared__ float s_y_next[R];
   __shared__ unsigned long long s_prof[32];
   long long prof_t0 = clock64();
 
@@ -416,6 +438,8 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
     }
     // padding columns of the input tile stay zero forever (gather writes only f0)
     const int64_t slot_words = ((int64_t)B * g.sum_hidden + 31) / 32;
+    bool have_next = false;
+    uint4 xnext[XPRE];
 
     for (int step = a.start_step[rq]; step < a.end_step[rq]; ++step) {
       const int e = step / spe, s = step % spe;
@@ -434,8 +458,16 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         const bool last_chunk = ch == nchunks - 1;
         const bool first_chunk = ch == 0;
         mk.row0 = row0;
-        // ---------------- gather the chunk's rows (bf16 features) and labels
-        if (tid < R) {
+        // ---------------- gather the chunk's rows (bf16 features) and labels;
+        // after the first chunk of a client they were prefetched during the
+        // previous chunk's backward pass (registers xnext / smem *_next)
+        const int cpr = g.fp[0] / 8;  // 16-byte chunks per input row
+        if (have_next) {
+          if (tid < R) {
+            s_rowidx[tid] = s_rowidx_next[tid];
+            y_sh[tid] = s_y_next[tid];
+          }
+        } else if (tid < R) {
           const int64_t row = tid < rows ? a.row_off[rq] + perm_e[s * B + row0 + tid] : -1;
           s_rowidx[tid] = row;
           y_sh[tid] = row >= 0 ? a.labels[row] : 0.f;
@@ -444,14 +476,28 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         FS_PROF(0);
         {
           const Tile xt{smem_u32(smem + g.s_h[0]), R};
-          const int cpr = g.fp[0] / 8;  // 16-byte chunks per row
-          for (int i = tid; i < R * cpr; i += THREADS) {
-            const int r = i / cpr, c = (i % cpr) * 8;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (r < rows) v = __ldg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * g.fp[0] + c));
-            st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
+#pragma unroll
+          for (int u = 0; u < XPRE; ++u) {
+            const int i = tid + u * THREADS;
+            if (i < R * cpr) {
+              const int r = i / cpr, c = (i % cpr) * 8;
+              uint4 v = xnext[u];
+              if (!have_next) {
+                v = make_uint4(0, 0, 0, 0);
+                if (r < rows) v = __ldg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * g.fp[0] + c));
+              }
+              st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
+            }
           }
         }
+        have_next = false;
+        // next chunk of this client (same step or the next one)
+        int nstep = step, nch = ch + 1;
+        if (nch == nchunks) {
+          nstep = step + 1;
+          nch = 0;
+        }
+        const bool next_ok = nstep < a.end_step[rq];
         // ---------------- forward through the hidden layers
         int base = 0;  // mask draw base of hidden layer l
         for (int l = 0; l < L - 1; ++l) {
@@ -460,15 +506,15 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           if (tid == 0) {
             const Tile at{smem_u32(smem + g.s_h[l]), R};
             const Tile bt{smem_u32(smem + g.s_w[l]), g.fp[l]};
-            const uint32_t id = idesc_bf16(128, N, false, true);
+            const uint32_t id = idesc_bf16(64, N, false, true);
             for (int ks = 0; ks < K / 16; ++ks) mma_bf16(tbase, at.kmajor(ks), bt.mnmajor(ks), id, ks > 0);
             mma_commit(&mma_bar);
           }
           // keep-bits of this thread's (row, column half) fetched while the MMA runs
           uint32_t mw[5] = {0, 0, 0, 0, 0};
           int mbit0 = 0;
-          if (mk.bits && q < 2) {
-            const int64_t j0 = (int64_t)mk.step_rows * base + (int64_t)(row0 + q * 32 + lane) * N + h * (N / 2);
+          if (mk.bits && lane < 16) {
+            const int64_t j0 = (int64_t)mk.step_rows * base + (int64_t)(row0 + q * 16 + lane) * N + h * (N / 2);
             const int64_t w0 = j0 >> 5, w1 = (j0 + N / 2 - 1) >> 5;
             mbit0 = (int)(j0 & 31);
 #pragma unroll
@@ -477,17 +523,20 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
           }
           wait_mma(&mma_bar, phase);
           FS_PROF(1 + l);
-          // epilogue: rows q*32+lane (q < 2), columns [h*N/2, (h+1)*N/2)
+          // epilogue (M=64 accumulator layout): lanes 0-15 of warp (q, h) own
+          // row q*16+lane, columns [h*N/2, (h+1)*N/2); all 8 warps work
           const bool head_in = (l == L - 2);
           float zp = 0.f;
-          if (q < 2) {
-            const int r = q * 32 + lane;
+          {
+            const int r = q * 16 + lane;
+            const bool own = lane < 16;
             const Tile ot{smem_u32(smem + g.s_h[l + 1]), R};
             const float* bias = bias_sh + g.bias_off[l];
             const float* wh = W + g.woff[L - 1];
             for (int c = h * (N / 2); c < (h + 1) * (N / 2); c += 16) {
               float v[16];
               tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+              if (!own) continue;
               uint32_t keep = 0xFFFFu;
               if (mk.bits) {
                 const int p = mbit0 + (c - h * (N / 2));
@@ -517,10 +566,20 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
               st_shared_v4(ot.saddr + ot.off(r, c + 8), pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
                            pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
             }
-            if (head_in) zpart[h * R + r] = zp;
+            if (head_in && own) zpart[h * R + r] = zp;
           }
           FS_PROF(5 + l);
           base += N;
+        }
+        if (next_ok && tid < R) {  // prefetch A: next chunk's row ids and labels
+          const int ne = nstep / spe, ns = nstep % spe;
+          const int nrows_step = min(B, n - ns * B);
+          const int nr0 = nch * R;
+          const int64_t row = tid < min(R, nrows_step - nr0)
+                                  ? a.row_off[rq] + a.perm[a.perm_off[rq] + (int64_t)ne * n + ns * B + nr0 + tid]
+                                  : -1;
+          s_rowidx_next[tid] = row;
+          s_y_next[tid] = row >= 0 ? a.labels[row] : 0.f;
         }
         // ---------------- head: logits, dz = (sigmoid(z) - y) / step_rows
         stage_sync();
@@ -536,6 +595,18 @@ __global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
         }
         __syncthreads();
         FS_PROF(9);
+        if (next_ok) {  // prefetch B: next chunk's feature rows, held in registers
+#pragma unroll
+          for (int u = 0; u < XPRE; ++u) {
+            const int i = tid + u * THREADS;
+            xnext[u] = make_uint4(0, 0, 0, 0);
+            if (i < R * cpr) {
+              const int64_t row = s_rowidx_next[i / cpr];
+              if (row >= 0) xnext[u] = __ldg(reinterpret_cast<const uint4*>(a.feat + row * g.fp[0] + (i % cpr) * 8));
+            }
+          }
+          have_next = true;
+        }
         // head weight/bias gradients (from the bf16 H_{L-1} tile, fp32 sums)
         {
           const Tile ht{smem_u32(smem + g.s_h[L - 1]), R};
@@ -806,7 +877,7 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
   Geo g{};
   g.L = n_dims - 1;
   for (int i = 0; i < n_dims; ++i) g.f[i] = dims[i];
-  if (g.f[g.L] != 1 || g.f[0] < 1 || g.f[0] > 256) return FS_EINVAL;
+  if (g.f[g.L] != 1 || g.f[0] < 1 || g.f[0] > 64) return FS_EINVAL;  // input rows prefetched in registers
   g.fp[0] = (g.f[0] + 15) / 16 * 16;
   for (int l = 1; l < g.L; ++l) {
     if (g.f[l] % 32 != 0 || g.f[l] < 32 || g.f[l] > 256) return FS_EINVAL;
@@ -856,7 +927,7 @@ static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
   if (g.L == 4) {
     const int mb1 = (g.f[1] + 127) / 128;
     const bool tm = mb1 * g.f[2] <= 256 && g.f[1] <= 256 && g.f[2] <= 128 && g.f[3] + g.f[2] <= 256 &&
-                    mb1 * g.fp[0] <= 256 && g.fp[0] <= 64;
+                    mb1 * g.fp[0] <= 256 && g.fp[0] <= 64 && mb1 <= 2;
     const uint32_t w2m_bytes = (uint32_t)(g.f[2] * g.f[3] * 4);
     if (tm && s + w2m_bytes <= 220 * 1024) {
       g.v2 = 1;
