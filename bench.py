@@ -379,6 +379,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
         "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (a CUB sort counts as one)",
         "clocks": m["clocks"],
         "kernel_ms": {k: v["mean_ms"] for k, v in ksum.items()},
+        "round_ms": [round(x, 3) for x in m["round_ms"]],
     }
     print(json.dumps(line), flush=True)
     if comm is not None:
