@@ -10,6 +10,8 @@
 #include "fs_common.cuh"
 #include "fs_rng.cuh"
 
+#include <cmath>
+
 namespace fs {
 
 __global__ void train_seeds_kernel(uint64_t master, const int32_t* cid, const int32_t* cyc, int n,
@@ -50,7 +52,9 @@ constexpr int MASK_YSPLIT = 8;
 
 // Packs keep-bits of one stream: bit j = (random_j < keep). Each thread
 // jumps its own PCG64 copy ahead to its first word and steps sequentially.
-__device__ void mask_stream(const Pcg64& base, int64_t n_draws, double keep, uint32_t* out) {
+// random() = (x >> 11) * 2^-53 < keep  <=>  (x >> 11) < ceil(keep * 2^53),
+// so the comparison runs on integers (threshold computed exactly on host).
+__device__ void mask_stream(const Pcg64& base, int64_t n_draws, uint64_t thresh, uint32_t* out) {
   const int64_t words = (n_draws + 31) / 32;
   const int64_t wpt = (words + MASK_THREADS - 1) / MASK_THREADS;
   const int64_t w0 = threadIdx.x * wpt;
@@ -61,15 +65,19 @@ __device__ void mask_stream(const Pcg64& base, int64_t n_draws, double keep, uin
   for (int64_t w = w0; w < w1; ++w) {
     uint32_t bits = 0;
     const int64_t lim = min((int64_t)32, n_draws - w * 32);
-    for (int b = 0; b < lim; ++b)
-      if (g.next_double() < keep) bits |= (1u << b);
+    if (lim == 32) {
+#pragma unroll 8
+      for (int b = 0; b < 32; ++b) bits |= (uint32_t)((g.next64() >> 11) < thresh) << b;
+    } else {
+      for (int b = 0; b < lim; ++b) bits |= (uint32_t)((g.next64() >> 11) < thresh) << b;
+    }
     out[w] = bits;
   }
 }
 
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
-                        const int64_t* mask_off, int epochs, int sum_hidden, double keep,
+                        const int64_t* mask_off, int epochs, int sum_hidden, uint64_t thresh,
                         uint32_t* bits) {
   const int r = blockIdx.x;
   const int n = n_rows[r], B = batch[r];
@@ -80,13 +88,20 @@ __global__ void __launch_bounds__(MASK_THREADS)
     const int e = st / spe, s = st % spe;
     const int rows = min(B, n - s * B);
     const Pcg64 base = pcg_from_seed(derive_mask_seed(train_seed, (uint32_t)e, (uint32_t)s));
-    mask_stream(base, (int64_t)rows * sum_hidden, keep, bits + mask_off[r] + (int64_t)st * slot);
+    mask_stream(base, (int64_t)rows * sum_hidden, thresh, bits + mask_off[r] + (int64_t)st * slot);
   }
 }
 
 __global__ void __launch_bounds__(MASK_THREADS)
-    dropout_bits_seed_kernel(uint64_t mask_seed, int64_t n_draws, double keep, uint32_t* bits) {
-  mask_stream(pcg_from_seed(mask_seed), n_draws, keep, bits);
+    dropout_bits_seed_kernel(uint64_t mask_seed, int64_t n_draws, uint64_t thresh, uint32_t* bits) {
+  mask_stream(pcg_from_seed(mask_seed), n_draws, thresh, bits);
+}
+
+// ceil(keep * 2^53): keep-bit threshold on the 53-bit integer behind random()
+static uint64_t keep_threshold(double keep) {
+  if (!(keep > 0.0)) return 0;
+  if (keep >= 1.0) return 1ull << 53;
+  return (uint64_t)ceil(ldexp(keep, 53));
 }
 
 }  // namespace fs
@@ -153,7 +168,7 @@ extern "C" int fs_dropout_bits(const uint64_t* seeds, const int32_t* n_rows, con
   if (n_req == 0 || epochs == 0) return FS_OK;
   dim3 grid(n_req, MASK_YSPLIT);
   dropout_bits_kernel<<<grid, MASK_THREADS, 0, (cudaStream_t)stream>>>(
-      seeds, n_rows, batch, mask_off, epochs, sum_hidden, keep, bits_out);
+      seeds, n_rows, batch, mask_off, epochs, sum_hidden, keep_threshold(keep), bits_out);
   return check_launch("dropout_bits_kernel");
 }
 
@@ -164,7 +179,7 @@ extern "C" int fs_dropout_bits_seed(uint64_t mask_seed, int64_t n_draws, double 
     return FS_EINVAL;
   }
   if (n_draws == 0) return FS_OK;
-  dropout_bits_seed_kernel<<<1, MASK_THREADS, 0, (cudaStream_t)stream>>>(mask_seed, n_draws, keep,
-                                                                         bits_out);
+  dropout_bits_seed_kernel<<<1, MASK_THREADS, 0, (cudaStream_t)stream>>>(mask_seed, n_draws,
+                                                                         keep_threshold(keep), bits_out);
   return check_launch("dropout_bits_seed_kernel");
 }

@@ -233,7 +233,8 @@ class TrainPlan:
     round's aggregation, evaluation and event bookkeeping run."""
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
-                 dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None):
+                 dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
+                 pool: dict | None = None):
         rt = rt or Runtime.get()
         self.rt = rt
         lib = rt.lib
@@ -269,11 +270,26 @@ class TrainPlan:
         np.cumsum(mask_len[:-1], out=mask_off[1:])
         # longest client first (LPT) so the critical path starts at t=0
         order = np.argsort(-((end - start) * self.batch), kind="stable")
+        def buf(name, n_elems, dtype):
+            # `pool`: caller-owned buffers reused across plans (no per-round allocation)
+            if pool is None:
+                return torch.empty(n_elems, dtype=dtype, device=rt.device)
+            t = pool.get(name)
+            if t is None or t.numel() < n_elems:
+                t = torch.empty(int(n_elems * 1.25) + 1, dtype=dtype, device=rt.device)
+                pool[name] = t
+            return t[:n_elems]
+
+        self.pooled = pool is not None
         with torch.cuda.stream(torch_stream):
-            self.d_i64 = rt.h2d(np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)]))
-            self.d_i32 = rt.h2d(np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32))
-            self.perm = torch.empty(max(int(perm_len.sum()), 1), dtype=torch.int32, device=rt.device)
-            self.bits = (torch.empty(max(int(mask_len.sum()), 1), dtype=torch.int32, device=rt.device)
+            i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)])
+            i32 = np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32)
+            self.d_i64 = buf("i64", len(i64), torch.int64)
+            self.d_i32 = buf("i32", len(i32), torch.int32)
+            self.d_i64.copy_(torch.from_numpy(i64).pin_memory(), non_blocking=True)
+            self.d_i32.copy_(torch.from_numpy(i32).pin_memory(), non_blocking=True)
+            self.perm = buf("perm", max(int(perm_len.sum()), 1), torch.int32)
+            self.bits = (buf("bits", max(int(mask_len.sum()), 1), torch.int32)
                          if use_masks and self.epochs > 0 else None)
         p64, p32 = self.d_i64.data_ptr(), self.d_i32.data_ptr()
         self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
@@ -299,9 +315,10 @@ class TrainPlan:
         """Order `stream` after the plan's producer and keep its buffers alive for it."""
         if self.ready is not None:
             stream.wait_event(self.ready)
-            for t in (self.d_i64, self.d_i32, self.perm, self.bits):
-                if t is not None:
-                    t.record_stream(stream)
+            if not self.pooled:
+                for t in (self.d_i64, self.d_i32, self.perm, self.bits):
+                    if t is not None:
+                        t.record_stream(stream)
             self.ready = None
 
 
