@@ -34,6 +34,11 @@ constexpr int R = 64;           // batch rows per chunk (MMA M=128; rows >= 64 a
 constexpr int THREADS = 256;    // 8 warps: (lane quarter q = w & 3, column half h = w >> 2)
 constexpr int MAXL = 5;         // weight layers supported (<= 4 hidden)
 constexpr uint32_t TMEM_COLS = 512;
+#ifndef FS_BF16_MAXNREG
+// register cap: leaves ~1/3 of the register file for a co-resident kernel
+// (the next round's dropout-mask/shuffle prefetch soaks up idle issue slots)
+#define FS_BF16_MAXNREG 168
+#endif
 constexpr int XPRE = 2;         // 16-byte feature chunks per thread per chunk (R * fp0/8 <= 512)
 
 struct Geo {
@@ -348,7 +353,7 @@ __device__ __forceinline__ void backward_v2(const Geo& g, const Args& a, uint8_t
 // in shared memory; W_0's master stays in HBM but is updated through the
 // transposed gradient G_0^T so every warp issues coalesced row segments.
 template <bool V2>
-__global__ void __launch_bounds__(THREADS, 1) train_bf16_kernel(Args a) {
+__global__ void __maxnreg__(FS_BF16_MAXNREG) train_bf16_kernel(Args a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mma_bar;
   __shared__ uint32_t tmem_base_sh;
