@@ -278,9 +278,7 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             if name == "align":
-                D.align_requests(ptr_c, np.full(n_clients, wg.data_ptr(), dtype=np.uint64),
-                                 np.full(n_clients, wp.data_ptr(), dtype=np.uint64), M, "delta_sign", rt,
-                                 dtype=torch.float32)
+                D.align_shared(ptr_c, wg, wp, M, "delta_sign", rt)
                 nbytes = 4.0 * M * (n_clients + 2)
             else:
                 d = rt.h2d(ptr_c.view(np.int64))
@@ -338,7 +336,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
     parity = None
     if not args.no_parity:
         w64, i64 = build_c4_world(precision="fp64")
-        p = measure_rounds(w64, i64, comm, max(2, args.steps // 2), 1, local)
+        p = measure_rounds(w64, i64, comm, 3, 3, local)
         parity = {"value": 1000.0 / p["ms_per_round"], "unit": "rounds/s", "ms_per_step": p["ms_per_round"],
                   "train_kernel_ms": p["kernels"].get("train", {}).get("mean_ms"),
                   "note": "fp64 parity mode: event log bit-identical to the reference (tests/test_gpu_parity.py)"}

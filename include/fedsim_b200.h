@@ -174,6 +174,13 @@ int fs_sign_align_f32(const uint64_t* wc, const uint64_t* wg, const uint64_t* wg
                       int32_t n_req, int64_t M, int32_t mode, int64_t* aligned_out,
                       void* stream);
 
+/* Synchronous-round form: every request compares against the same wg (and
+ * wg_prev) vectors, given directly as device pointers (16-byte aligned);
+ * rows in wc must be 16-byte aligned. dtype_bytes = 8 (fp64) or 4 (fp32).  */
+int fs_sign_align_shared(const uint64_t* wc, const void* wg, const void* wg_prev, int32_t n_req,
+                         int64_t M, int32_t mode, int32_t dtype_bytes, int64_t* aligned_out,
+                         void* stream);
+
 /* ---------------------------------------------------------------- K7/K9 FedAvg
  * keys_out[i*n_keys + t] = bswap64(bits(rows[i][t])) — the leading bytes
  * of values.tobytes() as big-endian integers (server.py:84 sort key).     */

@@ -107,6 +107,67 @@ __global__ void __launch_bounds__(ALIGN_THREADS)
   }
 }
 
+// Same count when every request compares against the SAME reference vectors
+// (a synchronous round: all clients fetched one w_g / w_g_prev). A CTA takes
+// one slice of the parameter range for G clients: the shared vectors are read
+// once per slice and reused from registers, so HBM/L2 traffic is ~one stream
+// per client row. Requires 16-byte aligned rows (rows are padded to 128 B).
+template <int MODE, class T, int G>
+__global__ void __launch_bounds__(ALIGN_THREADS)
+    sign_align_shared_kernel(const uint64_t* wc, const T* __restrict__ g, const T* __restrict__ p, int n_req,
+                             int64_t M, int blocks_per_grp, unsigned long long* out) {
+  using V = typename Vec16<T>::type;
+  constexpr int VN = Vec16<T>::n;
+  const int grp = blockIdx.x / blocks_per_grp;
+  const int blk = blockIdx.x % blocks_per_grp;
+  const int r0 = grp * G;
+  const int nq = min(G, n_req - r0);
+  const T* c[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) c[q] = reinterpret_cast<const T*>(wc[r0 + (q < nq ? q : 0)]);
+  const int64_t nvec = M / VN;
+  const int64_t span = (nvec + blocks_per_grp - 1) / blocks_per_grp;
+  const int64_t v0 = (int64_t)blk * span, v1 = min(nvec, v0 + span);
+  unsigned cnt[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) cnt[q] = 0;
+  const V* g2 = reinterpret_cast<const V*>(g);
+  const V* p2 = reinterpret_cast<const V*>(p);
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += ALIGN_THREADS) {
+    const V gv = __ldg(g2 + i);
+    const V pv = MODE == FS_ALIGN_DELTA_SIGN ? __ldg(p2 + i) : V{};
+    V cv[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (q < nq) cv[q] = __ldcs(reinterpret_cast<const V*>(c[q]) + i);
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (q < nq) cnt[q] += aligned_vec<MODE, T>(cv[q], gv, pv);
+  }
+  if (blk == blocks_per_grp - 1) {  // scalar tail [nvec*VN, M)
+    const T zero = T(0);
+    for (int64_t j = nvec * VN + threadIdx.x; j < M; j += ALIGN_THREADS)
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+        if (q < nq) cnt[q] += aligned1<MODE, T>(c[q][j], g[j], MODE == FS_ALIGN_DELTA_SIGN ? p[j] : zero);
+  }
+  __shared__ unsigned warp_sums[G][ALIGN_THREADS / 32];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const unsigned v = __reduce_add_sync(0xffffffffu, cnt[q]);
+    if ((threadIdx.x & 31) == 0) warp_sums[q][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      unsigned v = threadIdx.x < ALIGN_THREADS / 32 ? warp_sums[q][threadIdx.x] : 0u;
+      v = __reduce_add_sync(0xffffffffu, v);
+      if (threadIdx.x == 0 && q < nq && v) atomicAdd(out + r0 + q, (unsigned long long)v);
+    }
+  }
+}
+
 __global__ void sort_keys_kernel(const uint64_t* rows, int k, int n_keys, uint64_t* keys) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= k * n_keys) return;
@@ -368,4 +429,46 @@ extern "C" int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t d
   else
     mean_finish_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(sum, (double)k, M, (float*)out);
   return check_launch("mean_finish_kernel");
+}
+
+template <class T>
+static int sign_align_shared_impl(const uint64_t* wc, const void* wg, const void* wgp, int32_t n_req, int64_t M,
+                                  int32_t mode, int64_t* aligned_out, void* stream) {
+  constexpr int G = 4;
+  if (n_req < 0 || M < 0 || !wg || (mode != FS_ALIGN_WEIGHT_SIGN && mode != FS_ALIGN_DELTA_SIGN) ||
+      (mode == FS_ALIGN_DELTA_SIGN && !wgp) || (reinterpret_cast<uintptr_t>(wg) & 15) ||
+      (wgp && (reinterpret_cast<uintptr_t>(wgp) & 15))) {
+    set_error("fs_sign_align_shared: invalid arguments (reference vectors must be 16-byte aligned)");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_req == 0) return FS_OK;
+  if (cudaMemsetAsync(aligned_out, 0, sizeof(int64_t) * n_req, st) != cudaSuccess)
+    return check_launch("memset aligned");
+  if (M == 0) return FS_OK;
+  const int groups = (n_req + G - 1) / G;
+  // ~64 KB of each of the G client rows per CTA, >= 2 waves of 8 CTAs per SM
+  int bpg = (int)((M * (int64_t)sizeof(T) + 65535) / 65536);
+  const int64_t want = (int64_t)kNumSMs * 16;
+  if ((int64_t)bpg * groups < want) bpg = (int)((want + groups - 1) / groups);
+  const int64_t cap = (M + 1023) / 1024;
+  if (bpg > cap) bpg = (int)(cap > 0 ? cap : 1);
+  const unsigned nblk = (unsigned)bpg * (unsigned)groups;
+  auto* out = reinterpret_cast<unsigned long long*>(aligned_out);
+  const T* g = reinterpret_cast<const T*>(wg);
+  const T* p = reinterpret_cast<const T*>(wgp);
+  if (mode == FS_ALIGN_WEIGHT_SIGN)
+    sign_align_shared_kernel<FS_ALIGN_WEIGHT_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out);
+  else
+    sign_align_shared_kernel<FS_ALIGN_DELTA_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out);
+  return check_launch("sign_align_shared_kernel");
+}
+
+extern "C" int fs_sign_align_shared(const uint64_t* wc, const void* wg, const void* wg_prev, int32_t n_req,
+                                    int64_t M, int32_t mode, int32_t dtype_bytes, int64_t* aligned_out,
+                                    void* stream) {
+  if (dtype_bytes == 8) return sign_align_shared_impl<double>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
+  if (dtype_bytes == 4) return sign_align_shared_impl<float>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
+  set_error("fs_sign_align_shared: dtype_bytes must be 4 or 8");
+  return FS_EINVAL;
 }

@@ -465,6 +465,27 @@ def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | 
     return out[:n]
 
 
+def align_shared(wc_ptrs, wg: torch.Tensor, wgp: torch.Tensor | None, M: int, mode: str,
+                 rt: Runtime | None = None) -> torch.Tensor:
+    """K6 for a synchronous round: all rows against the same (w_g, w_g_prev)."""
+    rt = rt or Runtime.get()
+    n = len(wc_ptrs)
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if n == 0:
+        return out[:0]
+    m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
+    ptrs = np.asarray(wc_ptrs, dtype=np.uint64).ravel()
+    if (wg.data_ptr() % 16) or (m and wgp.data_ptr() % 16) or np.any(ptrs % 16):
+        return align_requests(ptrs, np.full(n, wg.data_ptr(), dtype=np.uint64),
+                              np.full(n, wgp.data_ptr(), dtype=np.uint64) if m else None, M, mode, rt, wg.dtype)
+    d = rt.h2d(ptrs.view(np.int64))
+    esz = wg.element_size()
+    with rt.timed("align", float(esz) * M * (n + (2 if m else 1))):
+        rt.call(rt.lib.fs_sign_align_shared(d.data_ptr(), wg.data_ptr(), wgp.data_ptr() if m else None, n, M, m,
+                                            esz, out.data_ptr(), rt.stream), "fs_sign_align_shared")
+    return out[:n]
+
+
 # --------------------------------------------------------------- FedAvg
 _N_KEYS = 4
 

@@ -123,6 +123,28 @@ def test_sign_align_edge_cases():
         assert be.sign_align_count(a[1:], b[1:]) == int(np.count_nonzero(np.sign(a[1:]) == np.sign(b[1:])))
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("mode", ["weight_sign", "delta_sign"])
+def test_sign_align_shared_matches_numpy(dtype, mode):
+    from paper_2503_15448_b200 import device as D
+
+    rt = D.Runtime.get()
+    rng = np.random.default_rng(7)
+    for n, M in ((1, 1), (3, 5), (7, 1023), (13, 52225), (6, 100003)):
+        ld = (M + 31) // 32 * 32
+        W = torch.tensor(np.round(rng.normal(size=(n, ld)), 1), dtype=dtype, device="cuda")[:, :M]
+        g = torch.tensor(np.round(rng.normal(size=M), 1), dtype=dtype, device="cuda")
+        p = torch.tensor(np.round(rng.normal(size=M), 1), dtype=dtype, device="cuda")
+        rows = W.data_ptr() + np.arange(n, dtype=np.uint64) * np.uint64(ld * W.element_size())
+        got = D.align_shared(rows, g, p if mode == "delta_sign" else None, M, mode, rt).cpu().numpy()
+        Wn, gn, pn = W.cpu().double().numpy(), g.cpu().double().numpy(), p.cpu().double().numpy()
+        if mode == "weight_sign":
+            want = [(np.sign(Wn[i]) == np.sign(gn)).sum() for i in range(n)]
+        else:
+            want = [(np.sign(Wn[i] - gn) == np.sign(gn - pn)).sum() for i in range(n)]
+        assert list(got) == [int(x) for x in want], (n, M)
+
+
 def test_aggregate_bitwise(golden):
     from paper_2503_15448_b200.model import ParamVector
     from paper_2503_15448_b200.server import aggregate
