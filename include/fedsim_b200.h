@@ -186,6 +186,10 @@ int fs_sign_align_shared(const uint64_t* wc, const void* wg, const void* wg_prev
  * of values.tobytes() as big-endian integers (server.py:84 sort key).     */
 int fs_gather_sort_keys_f64(const uint64_t* rows, int32_t k, int32_t n_keys, uint64_t* keys_out,
                             void* stream);
+/* Device-side K9: sorted_rows = rows ordered by values.tobytes() (k <= 1024),
+ * no host round trip; feeds fs_aggregate_* / fs_sum_rows directly.        */
+int fs_canonical_order(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes,
+                       uint64_t* sorted_rows, void* stream);
 /* out[j] = (sum_{i=0..k-1} rows[i][j]) / k, summed sequentially in the given
  * row order (server.py:84-86: stack in sorted order, mean(axis=0)).        */
 int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out, void* stream);

@@ -102,6 +102,7 @@ _SIGNATURES = {
     "fs_gather_sort_keys_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_gather_sort_keys_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
+    "fs_canonical_order": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_sum_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_mean_finish": (ctypes.c_int, [_c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp]),

@@ -186,6 +186,83 @@ __global__ void sort_keys_f32_kernel(const uint64_t* rows, int k, int n_keys, ui
   keys[i] = __byte_perm(bits, 0, 0x0123);
 }
 
+// ---------------------------------------------------------------- K9 on device
+// Canonical order of k <= 1024 update rows by values.tobytes() without a host
+// round trip: a bitonic sort in shared memory whose comparator looks at the
+// leading 4 elements as big-endian integers (byte order of tobytes) and, on
+// a tie, keeps scanning the rows element by element. Writes the row pointers
+// in sorted order for the aggregation kernels.
+constexpr int SORT_MAX = 1024;
+constexpr int SORT_KEYS = 4;
+
+template <class T>
+__device__ __forceinline__ uint64_t be_key(T v);
+template <>
+__device__ __forceinline__ uint64_t be_key<double>(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return ((uint64_t)__byte_perm((unsigned)b, 0, 0x0123) << 32) | __byte_perm((unsigned)(b >> 32), 0, 0x0123);
+}
+template <>
+__device__ __forceinline__ uint64_t be_key<float>(float v) {
+  return __byte_perm(__float_as_uint(v), 0, 0x0123);
+}
+
+template <class T>
+__device__ bool row_less(const uint64_t* keys, const uint64_t* rows, int a, int b, int nk, int64_t M) {
+  for (int t = 0; t < nk; ++t) {
+    const uint64_t ka = keys[a * SORT_KEYS + t], kb = keys[b * SORT_KEYS + t];
+    if (ka != kb) return ka < kb;
+  }
+  const T* ra = reinterpret_cast<const T*>(rows[a]);
+  const T* rb = reinterpret_cast<const T*>(rows[b]);
+  for (int64_t j = nk; j < M; ++j) {
+    const uint64_t ka = be_key<T>(ra[j]), kb = be_key<T>(rb[j]);
+    if (ka != kb) return ka < kb;
+  }
+  return a < b;  // identical rows: any order gives the same sum
+}
+
+template <class T>
+__global__ void __launch_bounds__(SORT_MAX) canonical_order_kernel(const uint64_t* rows, int k, int64_t M,
+                                                                   uint64_t* sorted_rows) {
+  __shared__ uint64_t keys[SORT_MAX * SORT_KEYS];
+  __shared__ int idx[SORT_MAX];
+  const int nk = M < SORT_KEYS ? (int)M : SORT_KEYS;
+  int n2 = 1;
+  while (n2 < k) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    idx[i] = i;
+    if (i < k)
+      for (int t = 0; t < nk; ++t) keys[i * SORT_KEYS + t] = be_key<T>(reinterpret_cast<const T*>(rows[i])[t]);
+  }
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const int a = idx[i], b = idx[j];
+          const bool up = (i & size) == 0;
+          // padding entries (>= k) sort last
+          bool a_gt_b;
+          if (a >= k)
+            a_gt_b = (b < k) || (a > b);
+          else if (b >= k)
+            a_gt_b = false;
+          else
+            a_gt_b = row_less<T>(keys, rows, b, a, nk, M);
+          if (a_gt_b == up) {
+            idx[i] = b;
+            idx[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) sorted_rows[i] = rows[idx[i]];
+}
+
 constexpr int AGG_THREADS = 128;
 constexpr int AGG_UNROLL = 8;
 
@@ -471,4 +548,20 @@ extern "C" int fs_sign_align_shared(const uint64_t* wc, const void* wg, const vo
   if (dtype_bytes == 4) return sign_align_shared_impl<float>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
   set_error("fs_sign_align_shared: dtype_bytes must be 4 or 8");
   return FS_EINVAL;
+}
+
+extern "C" int fs_canonical_order(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes,
+                                  uint64_t* sorted_rows, void* stream) {
+  if (k < 0 || k > SORT_MAX || M < 1 || (dtype_bytes != 4 && dtype_bytes != 8)) {
+    set_error("fs_canonical_order: need 0 <= k <= %d rows of M >= 1 elements", SORT_MAX);
+    return FS_EINVAL;
+  }
+  if (k == 0) return FS_OK;
+  int threads = 32;
+  while (threads < k && threads < SORT_MAX) threads <<= 1;
+  if (dtype_bytes == 8)
+    canonical_order_kernel<double><<<1, threads, 0, (cudaStream_t)stream>>>(rows, k, M, sorted_rows);
+  else
+    canonical_order_kernel<float><<<1, threads, 0, (cudaStream_t)stream>>>(rows, k, M, sorted_rows);
+  return check_launch("canonical_order_kernel");
 }

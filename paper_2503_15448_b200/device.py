@@ -537,14 +537,24 @@ def canonical_order(rows: list[torch.Tensor], M: int, rt: Runtime) -> list[int]:
     return [int(i) for i in canonical_order_ptrs(ptrs, M, rows[0].dtype, rt, row_of=lambda i: rows[i])]
 
 
+SORT_ON_DEVICE_MAX = 1024
+
+
 def aggregate_ptrs(ptrs: np.ndarray, M: int, dtype: torch.dtype, rt: Runtime | None = None,
                    row_of=None) -> torch.Tensor:
-    """K9 + K7 over raw row pointers: mean in canonical byte order."""
+    """K9 + K7 over raw row pointers: mean in canonical byte order. Up to 1024
+    rows are ordered on the device (no host synchronisation)."""
     rt = rt or Runtime.get()
     ptrs = np.asarray(ptrs, dtype=np.uint64)
     k = len(ptrs)
-    order = canonical_order_ptrs(ptrs, M, dtype, rt, row_of)
-    d = rt.h2d(ptrs[order].view(np.int64))
+    esz = 4 if dtype == torch.float32 else 8
+    if 1 < k <= SORT_ON_DEVICE_MAX:
+        src = rt.h2d(ptrs.view(np.int64))
+        d = torch.empty(k, dtype=torch.int64, device=rt.device)
+        rt.call(rt.lib.fs_canonical_order(src.data_ptr(), k, M, esz, d.data_ptr(), rt.stream), "fs_canonical_order")
+    else:
+        order = canonical_order_ptrs(ptrs, M, dtype, rt, row_of)
+        d = rt.h2d(ptrs[order].view(np.int64))
     out = torch.empty(M, dtype=dtype, device=rt.device)
     esz = out.element_size()
     fn = rt.lib.fs_aggregate_f32 if dtype == torch.float32 else rt.lib.fs_aggregate_f64
