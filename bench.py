@@ -27,8 +27,13 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
-os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU legs are single-threaded (stated as cores=1)
+# CPU legs run the oracle single-threaded: the reference path is GIL-bound, and
+# a thread pool over clients (the reference's `workers`) plus BLAS threads was
+# measured 3.6x SLOWER on 8 cores (0.0154 vs 0.055 rounds/s); --ref-workers N
+# reproduces that variant.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 
 import numpy as np
 
@@ -117,7 +122,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU sides
-def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None):
+def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None, workers: int = 1):
     """Time the oracle (reference algorithm, numpy, 1 thread) on a bounded
     sample of one C4 sync round: `sample_clients` client cycles (training +
     delta_sign scoring), FedAvg of their updates, and one full evaluation.
@@ -130,7 +135,11 @@ def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 
     wp = w_prev if w_prev is not None else w0 * 0.999
     picks = [int(i) for i in np.linspace(0, n - 1, sample_clients).round()]
     t0 = time.perf_counter()
-    outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
+    if workers > 1:  # the reference's own fan-out: a thread pool over clients (server.py:412-415)
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            outs = list(pool.map(lambda ci: sim.cycle(ci, round_index, round_index, w0, wp), picks))
+    else:
+        outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
     t_train = time.perf_counter() - t0
     ups = [o["res"]["params"] for o in outs if o["accepted"]]
     t0 = time.perf_counter()
@@ -153,9 +162,10 @@ def run_reference(args, rank: int, world_size: int) -> None:
         return
     world, initial = build_c4_world()
     sample = args.ref_sample
+    threads = max(1, args.ref_workers)
     times = []
     for i in range(args.warmup + args.steps):
-        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0)
+        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0, workers=threads)
         if i >= args.warmup:
             times.append(per_round)
     sec = float(np.mean(times))
@@ -166,9 +176,11 @@ def run_reference(args, rank: int, world_size: int) -> None:
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients, MLP 42-256-128-64-1, E=5, "
                                "dynamic batch, delta_sign theta=0.65"},
-        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": cpu_threads_used(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": threads, "kind": "port",
                          "sample": f"{sample} of 1024 client cycles of round 0 + FedAvg + full eval per step, "
-                                   "extrapolated x1024/sample (oracle/fl_oracle.py, numpy, 1 thread)"},
+                                   f"extrapolated x1024/sample (oracle/fl_oracle.py, numpy, {threads} worker thread(s) "
+                                   "over clients like the reference's `workers`; 1 BLAS thread; more threads were slower)",
+                         "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "client_updates_per_s": value * 1024,
     }
@@ -426,6 +438,7 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--ref-workers", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
     ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity-mode measurement")
