@@ -115,8 +115,12 @@ class RunResult:
         return self.reports[-1].auc if self.reports else float("nan")
 
 
-def run_experiment(config: ExperimentConfig, world_and_initial=None) -> RunResult:
-    world, initial = world_and_initial if world_and_initial is not None else build_world(config)
+def run_experiment(config: ExperimentConfig, world_and_initial=None, workers: int = 1,
+                   precision: str = "fp64") -> RunResult:
+    """Build (or take) a world and run it; ``workers`` is accepted for API
+    compatibility (clients are batched on the device, results are identical)."""
+    world, initial = (world_and_initial if world_and_initial is not None
+                      else build_world(config, workers=workers, precision=precision))
     engine = FederationEngine(world)
     t0 = time.perf_counter()
     state = engine.run(initial)
