@@ -136,7 +136,7 @@ int fs_bf16_supported(const int32_t* dims, int32_t n_dims);
 void fs_bf16_set_profile(unsigned long long* counters);
 /* Diagnostic: 1 = always run the generic bf16 kernel (optimizer state in
  * HBM) instead of the on-chip-state kernel for 3-hidden-layer MLPs.       */
-void fs_bf16_force_generic(int on);
+void fs_bf16_force_generic(int mode); /* 0 auto, 1 generic, 2 row-major V2 */
 int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
                           void* xb_out, float* y_out, void* stream);
 size_t fs_train_bf16_workspace_bytes(const fs_train_desc* desc);

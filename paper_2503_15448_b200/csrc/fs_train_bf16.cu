@@ -20,86 +20,12 @@
 // the weight-gradient epilogue applies W -= lr*G to the fp32 master row and
 // refreshes the bf16 weight tile. The sigmoid/BCE head (N=1) and the bias
 // gradients run on CUDA cores.
-#include <cstdio>
-
-#include "fs_common.cuh"
-#include "fs_tc.cuh"
+#include "fs_bf16.cuh"
 
 namespace fs {
 namespace bf16 {
 
 using namespace tc;
-
-constexpr int R = 64;           // batch rows per chunk (MMA M=128; rows >= 64 are ignored)
-constexpr int THREADS = 256;    // 8 warps: (lane quarter q = w & 3, column half h = w >> 2)
-constexpr int MAXL = 5;         // weight layers supported (<= 4 hidden)
-constexpr uint32_t TMEM_COLS = 512;
-#ifndef FS_BF16_MAXNREG
-// register cap: leaves ~1/3 of the register file for a co-resident kernel
-// (the next round's dropout-mask/shuffle prefetch soaks up idle issue slots)
-#define FS_BF16_MAXNREG 168
-#endif
-constexpr int XPRE = 2;         // 16-byte feature chunks per thread per chunk (R * fp0/8 <= 512)
-
-struct Geo {
-  int L;
-  int f[MAXL + 1];      // true dims
-  int fp[MAXL + 1];     // K-padded dims (fp[0] = roundup16(f0); hidden dims already % 16)
-  int woff[MAXL], boff[MAXL];
-  int M;                // parameters
-  int sum_hidden;
-  // shared-memory layout (bytes from the dynamic smem base)
-  uint32_t s_h[MAXL];   // activation tiles: s_h[0] = X [R x fp0], s_h[l] = H_l [R x f_l]
-  uint32_t s_w[MAXL];   // weight tiles W_l [fp_l x f_{l+1}] (hidden layers only)
-  uint32_t s_misc;      // fp32 scratch: z, dz, y, zpart[2][R], gw_head, gb
-  uint32_t s_bias;      // fp32 copies of the hidden-layer biases (sum_hidden floats)
-  int bias_off[MAXL];   // offset of b_l inside s_bias
-  uint32_t s_w2m;       // V2: fp32 master of W_2, column-major [f3][f2]
-  int v2;               // V2 eligible (3 hidden layers fitting the on-chip optimizer state)
-  uint32_t smem_bytes;
-};
-
-struct Args {
-  Geo g;
-  int n_req, epochs, mask_mode;
-  float scale;
-  const __nv_bfloat16* feat;  // [rows x fp0] bf16, zero padded
-  const float* labels;        // [rows]
-  const int64_t* row_off;
-  const int32_t* n_rows;
-  const int32_t* batch;
-  const double* lr;           // [n_req x epochs]
-  const uint64_t* w_start;    // fp32 flat start parameters
-  float* w_out;               // fp32 flat, ldw floats per request
-  int64_t ldw;
-  const int32_t* perm;
-  const int64_t* perm_off;
-  const uint32_t* mask_bits;
-  const int64_t* mask_off;
-  const int32_t* start_step;
-  const int32_t* end_step;
-  const int32_t* order;
-  int32_t* status;
-  int* counter;
-  float* gacc;                // [grid x M] fp32 gradient accumulators (multi-chunk steps)
-  unsigned long long* prof;   // optional [32] phase cycle counters (thread 0 of every CTA)
-};
-
-// Phase profiler: thread 0 attributes elapsed SM cycles to phase k.
-#define FS_PROF(k)                                        \
-  do {                                                    \
-    if (a.prof && tid == 0) {                             \
-      const long long t1_ = clock64();                    \
-      s_prof[k] += (unsigned long long)(t1_ - prof_t0);   \
-      prof_t0 = t1_;                                      \
-    }                                                     \
-  } while (0)
-
-__device__ __forceinline__ float sigmoidf_stable(float z) {
-  if (z >= 0.f) return 1.f / (1.f + __expf(-z));
-  const float e = __expf(z);
-  return e / (1.f + e);
-}
 
 struct MaskSrc {
   const uint32_t* bits;  // slot of this step (nullptr = no dropout)
@@ -133,20 +59,6 @@ __device__ void load_weight_tile(const Geo& g, const float* W, int l, uint8_t* s
     st_shared_v4(t.saddr + t.off(r, c), p[0], p[1], p[2], p[3]);
   }
 }
-
-__device__ __forceinline__ void stage_sync() {
-  fence_async_smem();
-  fence_before_sync();
-  __syncthreads();
-  fence_after_sync();
-}
-
-__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
-  mbar_wait(bar, phase);
-  phase ^= 1u;
-  fence_after_sync();
-}
-
 
 // Column sums over the chunk's rows of a bf16 activation tile (bias gradients).
 __device__ __forceinline__ float tile_colsum(const Tile& t, int c, int rows) {
@@ -877,7 +789,7 @@ __global__ void prep_features_kernel(const double* X, const double* Y, int64_t r
 
 using namespace bf16;
 
-static int make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
+int bf16::make_geo(const int32_t* dims, int32_t n_dims, Geo* out) {
   if (n_dims < 3 || n_dims > MAXL + 1) return FS_EINVAL;
   Geo g{};
   g.L = n_dims - 1;
@@ -958,8 +870,10 @@ using namespace fs;
 static unsigned long long* g_bf16_prof = nullptr;
 static int g_bf16_force_generic = 0;
 
-// Diagnostic: force the generic (HBM optimizer state) bf16 kernel.
-extern "C" void fs_bf16_force_generic(int on) { g_bf16_force_generic = on; }
+// Diagnostic kernel selection: 0 = automatic (unit-major V3 where the layer
+// shape allows, else row-major V2, else generic), 1 = generic (HBM optimizer
+// state), 2 = row-major V2.
+extern "C" void fs_bf16_force_generic(int mode) { g_bf16_force_generic = mode; }
 
 // Diagnostic: accumulate per-phase SM cycles of the bf16 trainer into a
 // device buffer of 32 counters (nullptr disables).
@@ -1034,7 +948,8 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
-  if (g.v2 && !g_bf16_force_generic) {
+  if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
+  if (g.v2 && g_bf16_force_generic != 1) {
     cudaFuncSetAttribute(train_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
     train_bf16_kernel<true><<<grid, THREADS, g.smem_bytes, st>>>(a);
   } else {

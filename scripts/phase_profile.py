@@ -12,7 +12,7 @@ from paper_2503_15448_b200.server import FederationEngine, GlobalState  # noqa: 
 NAMES = {0: "gather", 1: "F0 mma", 2: "F1 mma", 3: "F2 mma", 5: "F0 epi", 6: "F1 epi", 7: "F2 epi+z",
          9: "head z/dz", 10: "head grads", 11: "D_L-1 + head upd", 12: "B0 mma", 13: "B1 mma", 14: "B2 mma",
          16: "B0 D-epi", 17: "B1 D-epi", 18: "B2 D-epi", 20: "B0 G-epi", 21: "B1 G-epi", 22: "B2 G-epi",
-         24: "bias grads (last stage)", 25: "chunk end barrier"}
+         24: "bias grads (last stage)", 25: "chunk end barrier", 26: "client setup: W0 + biases", 27: "client end sync", 28: "X tile stores", 29: "mask finish", 30: "client: write-back + claim", 31: "client setup: W1/W2"}
 world, init = bench.build_c4_world(precision="bf16")
 eng = FederationEngine(world)
 st = GlobalState(round=0, w_g=init)

@@ -81,9 +81,21 @@ def _one_step(dims, rows, dropout, seed=5):
     return w0, w_out[0], want
 
 
+@pytest.fixture(params=[0, 2], ids=["unit-major", "row-major"])
+def kernel_mode(request):
+    """Selects the bf16 trainer variant (fs_bf16_force_generic) for one test."""
+    from paper_2503_15448_b200 import _native as N
+
+    lib = N.load()
+    lib.fs_bf16_force_generic(request.param)
+    yield request.param
+    lib.fs_bf16_force_generic(0)
+
+
 @pytest.mark.parametrize("rows,dropout", [(64, 0.3), (37, 0.3), (64, 0.0), (150, 0.3)])
-def test_bf16_single_step_matches_fp32_emulation(rows, dropout):
-    w0, got, want = _one_step(UNSW, rows, dropout)
+@pytest.mark.parametrize("dims", [UNSW, (20, 128, 128, 64, 1)], ids=["unsw", "f1_128"])
+def test_bf16_single_step_matches_fp32_emulation(rows, dropout, dims, kernel_mode):
+    w0, got, want = _one_step(dims, rows, dropout)
     delta_w = want - w0
     err = (got - want).abs().max().item()
     scale = delta_w.abs().max().item()
@@ -92,7 +104,7 @@ def test_bf16_single_step_matches_fp32_emulation(rows, dropout):
     assert rel < 1e-2, rel
 
 
-def test_bf16_local_training_tracks_fp64():
+def test_bf16_local_training_tracks_fp64(kernel_mode):
     """Whole local trainings (5 epochs, dropout) stay within the bf16 budget
     of the fp64 parity trainer: relative L2 error of the update delta."""
     from paper_2503_15448_b200 import device as D
