@@ -140,6 +140,12 @@ void fs_bf16_force_generic(int mode); /* 0 auto, 1 generic, 2 row-major V2 */
 int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
                           void* xb_out, float* y_out, void* stream);
 size_t fs_train_bf16_workspace_bytes(const fs_train_desc* desc);
+/* K8 forward in bf16 mode (_core.pyx:109-137 with bf16 GEMM operands, fp32
+ * accumulation): probs_out[rows] (float64) of fs_prep_features_bf16 rows under
+ * fp32 parameters w. Layer shapes of the unit-major trainer only (3 hidden
+ * layers, f1 in {128, 256}, f2 = 128, f3 = 64, f0 <= 64); else FS_EINVAL. */
+int fs_forward_bf16(const int32_t* dims, int32_t n_dims, const float* w, const void* x_bf16, int32_t rows,
+                    double* probs_out, void* stream);
 int fs_train_bf16(const fs_train_desc* desc, const void* features_bf16, const float* labels_f32,
                   void* stream);
 

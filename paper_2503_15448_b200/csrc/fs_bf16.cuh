@@ -105,5 +105,6 @@ namespace bf16t {
 bool geo_ok(const bf16::Geo& g);
 uint32_t smem_bytes(const bf16::Geo& g);
 int launch(const bf16::Args& a, int grid, cudaStream_t st);
+int launch_eval(const bf16::Geo& g, const float* w, const void* xb, int n, double* probs, cudaStream_t st);
 }  // namespace bf16t
 }  // namespace fs

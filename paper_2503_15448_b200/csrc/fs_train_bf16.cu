@@ -782,7 +782,7 @@ __global__ void prep_features_kernel(const double* X, const double* Y, int64_t r
   const int64_t r = i / dp;
   const int c = (int)(i % dp);
   xb[i] = __float2bfloat16_rn(c < d ? (float)X[r * d + c] : 0.f);
-  if (c == 0) yf[r] = (float)Y[r];
+  if (c == 0 && yf) yf[r] = (float)Y[r];
 }
 
 }  // namespace bf16
@@ -895,6 +895,17 @@ extern "C" int fs_prep_features_bf16(const double* x, const double* y, int64_t r
   prep_features_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       x, y, rows, d, dp, reinterpret_cast<__nv_bfloat16*>(xb_out), y_out);
   return check_launch("prep_features_kernel");
+}
+
+extern "C" int fs_forward_bf16(const int32_t* dims, int32_t n_dims, const float* w, const void* x_bf16,
+                               int32_t rows, double* probs_out, void* stream) {
+  Geo g;
+  if (make_geo(dims, n_dims, &g) != FS_OK || !bf16t::geo_ok(g) || rows < 0) {
+    set_error("fs_forward_bf16: unsupported layer dims or rows");
+    return FS_EINVAL;
+  }
+  if (rows == 0) return FS_OK;
+  return bf16t::launch_eval(g, w, x_bf16, rows, probs_out, (cudaStream_t)stream);
 }
 
 extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {

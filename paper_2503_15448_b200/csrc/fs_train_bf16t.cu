@@ -777,6 +777,171 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
   if (warp == 0) tmem_dealloc(tbase, bf16::TMEM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// K8 forward (bf16 mode): class-1 probabilities of the test rows under the
+// fp32 global model, same unit-major tcgen05 forward as the trainer (bf16
+// operands, fp32 accumulation, fp32 head/sigmoid), one 64-row chunk per CTA
+// iteration. The fp64 parity mode keeps fs_forward_f64.
+struct EvalLay {
+  uint32_t x, h1, h2, w0, w1, w2, pad, fl, total;
+};
+__host__ __device__ inline EvalLay eval_lay(const Geo& g) {
+  EvalLay l;
+  uint32_t s = 0;
+  l.x = s;   s += (uint32_t)(R * g.fp[0] * 2);
+  l.h1 = s;  s += (uint32_t)(g.f[1] * R * 2);
+  l.h2 = s;  s += (uint32_t)(g.f[2] * R * 2);
+  l.w0 = s;  s += (uint32_t)(g.f[1] * g.fp[0] * 2);
+  l.w1 = s;  s += (uint32_t)(g.f[1] * g.f[2] * 2);
+  l.w2 = s;  s += (uint32_t)(g.f[2] * g.f[3] * 2);
+  l.pad = s; s += 16 * 1024;  // F2 (M = 128 over 64 units) reads past the W_2 tile
+  l.fl = s;  s += (uint32_t)((g.f[1] + g.f[2] + g.f[3] + g.f[3] + 1 + 2 * R) * 4);
+  l.total = s;
+  return l;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __restrict__ w,
+                                                       const __nv_bfloat16* __restrict__ xb, int n,
+                                                       double* __restrict__ probs) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mma_bar;
+  __shared__ uint32_t tmem_base_sh;
+  const EvalLay ly = eval_lay(g);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3;
+  const int f0 = g.f[0], fp0 = g.fp[0], f1 = g.f[1], f2 = g.f[2], f3 = g.f[3];
+  const int MB = f1 / 128;
+  float* fl = reinterpret_cast<float*>(smem + ly.fl);
+  float* bias = fl;                         // [f1 + f2 + f3]
+  float* wh = fl + f1 + f2 + f3;            // [f3 + 1]
+  float* zpart = wh + f3 + 1;               // [2][R]
+  const Tile xt{smem_u32(smem + ly.x), R};
+  const Tile h1t{smem_u32(smem + ly.h1), f1};
+  const Tile h2t{smem_u32(smem + ly.h2), f2};
+  const Tile w0t{smem_u32(smem + ly.w0), f1};
+  const Tile w1t{smem_u32(smem + ly.w1), f1};
+  const Tile w2t{smem_u32(smem + ly.w2), f2};
+
+  if (warp == 0) tmem_alloc(&tmem_base_sh, 128);
+  if (tid == 0) {
+    mbar_init(&mma_bar, 1);
+    fence_mbar_init();
+  }
+  // weights: bf16 tiles (unit-major W_0^T) and fp32 biases / head
+  for (int i = tid; i < f1 * (fp0 / 8); i += THREADS) {
+    const int m = i % f1, c0 = (i / f1) * 8;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = c0 + k < f0 ? w[(c0 + k) * f1 + m] : 0.f;
+    st_shared_v4(w0t.saddr + w0t.off(m, c0), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                 pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+  }
+  for (int i = tid; i < f1 * (f2 / 8); i += THREADS) {
+    const int m = i / (f2 / 8), c0 = (i % (f2 / 8)) * 8;
+    const float* src = w + g.woff[1] + (int64_t)m * f2 + c0;
+    st_shared_v4(w1t.saddr + w1t.off(m, c0), pack_bf16x2(src[0], src[1]), pack_bf16x2(src[2], src[3]),
+                 pack_bf16x2(src[4], src[5]), pack_bf16x2(src[6], src[7]));
+  }
+  for (int i = tid; i < f2 * (f3 / 8); i += THREADS) {
+    const int m = i / (f3 / 8), c0 = (i % (f3 / 8)) * 8;
+    const float* src = w + g.woff[2] + (int64_t)m * f3 + c0;
+    st_shared_v4(w2t.saddr + w2t.off(m, c0), pack_bf16x2(src[0], src[1]), pack_bf16x2(src[2], src[3]),
+                 pack_bf16x2(src[4], src[5]), pack_bf16x2(src[6], src[7]));
+  }
+  for (int c = tid; c < f1 + f2 + f3; c += THREADS) {
+    const int l = c < f1 ? 0 : (c < f1 + f2 ? 1 : 2);
+    const int o = l == 0 ? c : (l == 1 ? c - f1 : c - f1 - f2);
+    bias[c] = w[g.boff[l] + o];
+  }
+  for (int k = tid; k <= f3; k += THREADS) wh[k] = k < f3 ? w[g.woff[3] + k] : w[g.boff[3]];
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base_sh;
+  const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16);
+  uint32_t phase = 0;
+  const int cpr = fp0 / 8;
+  const int nchunks = (n + R - 1) / R;
+
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int r0 = ch * R;
+    const int rows = min(R, n - r0);
+    for (int i = tid; i < R * cpr; i += THREADS) {
+      const int r = i / cpr, c = (i % cpr) * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < rows) v = __ldg(reinterpret_cast<const uint4*>(xb + (int64_t)(r0 + r) * fp0 + c));
+      st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
+    }
+    // F0
+    stage_sync();
+    if (tid == 0) {
+      const uint32_t id = idesc_bf16(128, R, false, false);
+      for (int ks = 0; ks < fp0 / 16; ++ks)
+        for (int mb = 0; mb < MB; ++mb)
+          mma_bf16(tbase + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
+      mma_commit(&mma_bar);
+    }
+    wait_mma(&mma_bar, phase);
+    for (int it = warp; it < MB * 8; it += 8) {
+      const int hh = (it >> 2) & 1, mb = it >> 3;
+      const int m = mb * 128 + q * 32 + lane;
+      float v[32];
+      tmem_ld32(tq + (uint32_t)(mb * R + hh * 32), v);
+      const float b = bias[m];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + b, 0.f);
+      store_row32(h1t, m, hh * 32, v);
+    }
+    // F1
+    stage_sync();
+    if (tid == 0) {
+      const uint32_t id = idesc_bf16(128, R, true, true);
+      for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16(tbase, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
+      mma_commit(&mma_bar);
+    }
+    wait_mma(&mma_bar, phase);
+    {
+      const int hh = warp >> 2, m = q * 32 + lane;
+      float v[32];
+      tmem_ld32(tq + (uint32_t)(hh * 32), v);
+      const float b = bias[f1 + m];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + b, 0.f);
+      store_row32(h2t, m, hh * 32, v);
+    }
+    // F2 + head
+    stage_sync();
+    if (tid == 0) {
+      const uint32_t id = idesc_bf16(128, R, true, true);
+      for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
+      mma_commit(&mma_bar);
+    }
+    wait_mma(&mma_bar, phase);
+    if (q < f3 / 32) {
+      const int hh = warp >> 2, m = q * 32 + lane;
+      float v[32];
+      tmem_ld32(tq + (uint32_t)(hh * 32), v);
+      const float b = bias[f1 + f2 + m], wm = wh[m];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + b, 0.f) * wm;
+      zpart[q * R + hh * 32 + lane] = reduce_scatter32(v, lane);
+    }
+    __syncthreads();
+    if (tid < rows) probs[r0 + tid] = (double)bf16::sigmoidf_stable(zpart[tid] + zpart[R + tid] + wh[f3]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 128);
+}
+
+int launch_eval(const Geo& g, const float* w, const void* xb, int n, double* probs, cudaStream_t st) {
+  const uint32_t bytes = eval_lay(g).total;
+  cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const int chunks = (n + R - 1) / R;
+  const int grid = chunks < kNumSMs ? chunks : kNumSMs;
+  eval_kernel<<<grid, THREADS, bytes, st>>>(g, w, reinterpret_cast<const __nv_bfloat16*>(xb), n, probs);
+  return check_launch("bf16t::eval_kernel");
+}
+
 int launch(const Args& a, int grid, cudaStream_t st) {
   const uint32_t bytes = lay_of(a.g).total;
   cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

@@ -583,6 +583,23 @@ def forward_probs(spec_dims, w: torch.Tensor, x: torch.Tensor, dense_masks: torc
     return probs
 
 
+def eval_bf16_supported(spec_dims) -> bool:
+    """Layer shapes of the unit-major tensor-core kernels (fs_forward_bf16)."""
+    d = list(spec_dims)
+    return len(d) == 5 and d[1] in (128, 256) and d[2] == 128 and d[3] == 64 and d[0] <= 64 and d[4] == 1
+
+
+def forward_probs_bf16(spec_dims, w32: torch.Tensor, xb: torch.Tensor, rt: Runtime | None = None) -> torch.Tensor:
+    """K8 forward on the tensor cores: float64 probabilities of bf16 rows under fp32 parameters."""
+    rt = rt or Runtime.get()
+    dims_c, nd = dims_array(spec_dims)
+    rows = xb.shape[0]
+    probs = torch.empty(rows, dtype=torch.float64, device=rt.device)
+    rt.call(rt.lib.fs_forward_bf16(dims_c, nd, w32.data_ptr(), xb.data_ptr(), rows, probs.data_ptr(), rt.stream),
+            "fs_forward_bf16")
+    return probs
+
+
 def eval_counts(scores: torch.Tensor, labels_i8: torch.Tensor, threshold: float, rt: Runtime | None = None) -> torch.Tensor:
     """K8 metrics: device int64 [3] = (#correct, 2*U_pos, n_pos)."""
     rt = rt or Runtime.get()

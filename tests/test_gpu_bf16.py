@@ -160,3 +160,42 @@ def test_bf16_engine_masks_match_fp64_outside_threshold_band():
         assert abs(out["fp64"][i][1] - theta) <= eps, (i, out["fp64"][i], out["bf16"][i])
     dr = [abs(a[1] - b[1]) for a, b in zip(out["fp64"], out["bf16"])]
     assert max(dr) < 1e-2
+
+
+@pytest.mark.parametrize("rows", [1, 64, 1037])
+def test_bf16_eval_forward_tracks_fp64(rows):
+    """K8 tensor-core forward (bf16 mode) against the fp64 forward of the same
+    fp32 parameters: bf16-operand tolerance on probabilities, and the metrics
+    the engine reports from them."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=42, hidden_dims=(256, 128, 64), dropout_rate=0.3)
+    rng = np.random.default_rng(rows)
+    w = init_params(spec, 4).values
+    x = rng.normal(size=(rows, 42))
+    y = (rng.random(rows) < 0.4).astype(np.int8)
+    rt = D.Runtime.get()
+    xd = torch.tensor(x, device="cuda")
+    xb = torch.empty((rows, 48), dtype=torch.bfloat16, device="cuda")
+    rt.call(rt.lib.fs_prep_features_bf16(xd.data_ptr(), None, rows, 42, 48, xb.data_ptr(), None, rt.stream), "prep")
+    w32 = torch.tensor(w, dtype=torch.float32, device="cuda")
+    p64 = D.forward_probs(spec.dims, w32.double(), xd, None, rt).cpu().numpy()
+    p16 = D.forward_probs_bf16(spec.dims, w32, xb, rt).cpu().numpy()
+    # compare in logit space: bf16 operands give a relative logit error of
+    # ~2^-8 per layer, so the tolerance scales with |z|
+    z64 = np.log(np.clip(p64, 1e-12, 1 - 1e-12) / np.clip(1 - p64, 1e-12, 1))
+    z16 = np.log(np.clip(p16, 1e-12, 1 - 1e-12) / np.clip(1 - p16, 1e-12, 1))
+    ok = np.abs(z64) < 20  # beyond that both probabilities saturate
+    assert ok.any()
+    zerr = np.abs(z16 - z64)[ok] / (1.0 + np.abs(z64[ok]))
+    assert zerr.max() < 5e-2 and zerr.mean() < 1e-2, (zerr.max(), zerr.mean())
+    if rows > 100:
+        # labels that follow the model (10 % flipped), so the metrics are not
+        # decided by coin-flip probabilities sitting on the threshold
+        y = ((p64 > np.median(p64)) ^ (rng.random(rows) < 0.1)).astype(np.int8)
+        yd = torch.tensor(y, device="cuda")
+        thr = float(np.median(p64))
+        c64 = D.metrics_from_counts(D.eval_counts(torch.tensor(p64, device="cuda"), yd, thr, rt).cpu().numpy(), rows)
+        c16 = D.metrics_from_counts(D.eval_counts(torch.tensor(p16, device="cuda"), yd, thr, rt).cpu().numpy(), rows)
+        assert abs(c64[0] - c16[0]) < 0.02 and abs(c64[1] - c16[1]) < 0.01, (c64, c16)
