@@ -49,52 +49,123 @@ __global__ void shuffle_kernel(const uint64_t* seeds, const int32_t* n_rows, con
 
 constexpr int MASK_THREADS = 128;
 constexpr int MASK_YSPLIT = 8;
+constexpr int MASK_ILP = 4;  // independent PCG64 sub-streams per thread
 
-// Packs keep-bits of one stream: bit j = (random_j < keep). Each thread
-// jumps its own PCG64 copy ahead to its first word and steps sequentially.
-// random() = (x >> 11) * 2^-53 < keep  <=>  (x >> 11) < ceil(keep * 2^53),
-// so the comparison runs on integers (threshold computed exactly on host).
-__device__ void mask_stream(const Pcg64& base, int64_t n_draws, uint64_t thresh, uint32_t* out) {
-  const int64_t words = (n_draws + 31) / 32;
-  const int64_t wpt = (words + MASK_THREADS - 1) / MASK_THREADS;
-  const int64_t w0 = threadIdx.x * wpt;
-  const int64_t w1 = min(words, w0 + wpt);
-  if (w0 >= w1) return;
-  Pcg64 g = base;
-  g.advance((uint64_t)(w0 * 32));
-  for (int64_t w = w0; w < w1; ++w) {
-    uint32_t bits = 0;
-    const int64_t lim = min((int64_t)32, n_draws - w * 32);
-    if (lim == 32) {
-#pragma unroll 8
-      for (int b = 0; b < 32; ++b) bits |= (uint32_t)((g.next64() >> 11) < thresh) << b;
-    } else {
-      for (int b = 0; b < lim; ++b) bits |= (uint32_t)((g.next64() >> 11) < thresh) << b;
+// LCG jump by k steps, independent of the stream: state' = a*state + g*inc.
+struct LcgJump {
+  U128 a, g;
+};
+FS_HD LcgJump lcg_jump(uint64_t k) {
+  U128 acc_mult{0, 1}, acc_plus{0, 0};
+  U128 cur_mult = pcg_mult(), cur_plus{0, 1};
+  const U128 one{0, 1};
+  while (k) {
+    if (k & 1) {
+      acc_mult = u128_mul(acc_mult, cur_mult);
+      acc_plus = u128_add(u128_mul(acc_plus, cur_mult), cur_plus);
     }
-    out[w] = bits;
+    cur_plus = u128_mul(u128_add(cur_mult, one), cur_plus);
+    cur_mult = u128_mul(cur_mult, cur_mult);
+    k >>= 1;
+  }
+  return LcgJump{acc_mult, acc_plus};
+}
+__device__ __forceinline__ U128 lcg_apply(const LcgJump& j, U128 state, U128 inc) {
+  return u128_add(u128_mul(j.a, state), u128_mul(j.g, inc));
+}
+__device__ __forceinline__ uint64_t xsl_rr(U128 s) {
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// Packs keep-bits of one stream: bit j = (random_j < keep), with
+// random() = (x >> 11) * 2^-53 < keep  <=>  (x >> 11) < ceil(keep * 2^53)
+// (integer comparison, threshold computed exactly on host). Thread t owns
+// words t, t + T, t + 2T, ... (T = MASK_THREADS) and runs MASK_ILP of them
+// at once as independent LCG chains: word w starts 32w steps after `base`,
+// reached with precomputed jumps (jt: 32t steps, j1: 32T steps, jr: from the
+// end of a word to the thread's word MASK_ILP*T further on).
+__device__ void mask_stream(U128 base_state, U128 inc, int64_t n_draws, uint64_t thresh, uint32_t* out,
+                            const LcgJump& jt, const LcgJump& j1, const LcgJump& jr) {
+  const int64_t words = (n_draws + 31) / 32;
+  const int t = threadIdx.x;
+  if (t >= words) return;
+  const U128 mult = pcg_mult();
+  U128 s[MASK_ILP];
+  s[0] = lcg_apply(jt, base_state, inc);
+#pragma unroll
+  for (int u = 1; u < MASK_ILP; ++u) s[u] = lcg_apply(j1, s[u - 1], inc);
+  for (int64_t w = t; w < words; w += (int64_t)MASK_ILP * MASK_THREADS) {
+    uint32_t bits[MASK_ILP];
+#pragma unroll
+    for (int u = 0; u < MASK_ILP; ++u) bits[u] = 0;
+#pragma unroll 4
+    for (int b = 0; b < 32; ++b) {
+#pragma unroll
+      for (int u = 0; u < MASK_ILP; ++u) {
+        s[u] = u128_add(u128_mul(s[u], mult), inc);
+        bits[u] |= (uint32_t)((xsl_rr(s[u]) >> 11) < thresh) << b;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < MASK_ILP; ++u) {
+      const int64_t wu = w + (int64_t)u * MASK_THREADS;
+      if (wu < words) {
+        const int64_t lim = n_draws - wu * 32;
+        out[wu] = lim >= 32 ? bits[u] : (bits[u] & ((1u << lim) - 1u));
+      }
+      s[u] = lcg_apply(jr, s[u], inc);
+    }
   }
 }
 
+// grid (request, MASK_YSPLIT): block y handles steps y, y + YSPLIT, ... of its
+// request. Warp 0 derives up to 32 step streams at once (one lane each:
+// SeedSequence hashing + PCG64 seeding), then all threads fill their words.
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
                         const int64_t* mask_off, int epochs, int sum_hidden, uint64_t thresh,
                         uint32_t* bits) {
+  __shared__ U128 sh_state[32], sh_inc[32];
   const int r = blockIdx.x;
   const int n = n_rows[r], B = batch[r];
   const int spe = (n + B - 1) / B;
+  const int total = epochs * spe;
   const int64_t slot = ((int64_t)B * sum_hidden + 31) / 32;
   const uint64_t train_seed = seeds[r];
-  for (int st = blockIdx.y; st < epochs * spe; st += gridDim.y) {
-    const int e = st / spe, s = st % spe;
-    const int rows = min(B, n - s * B);
-    const Pcg64 base = pcg_from_seed(derive_mask_seed(train_seed, (uint32_t)e, (uint32_t)s));
-    mask_stream(base, (int64_t)rows * sum_hidden, thresh, bits + mask_off[r] + (int64_t)st * slot);
+  const LcgJump jt = lcg_jump(32ull * threadIdx.x);
+  const LcgJump j1 = lcg_jump(32ull * MASK_THREADS);
+  const LcgJump jr = lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32);
+  uint32_t* out_r = bits + mask_off[r];
+  for (int k0 = 0;; k0 += 32) {
+    const int st0 = blockIdx.y + k0 * MASK_YSPLIT;
+    if (st0 >= total) break;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int st = st0 + threadIdx.x * MASK_YSPLIT;
+      if (st < total) {
+        const Pcg64 g = pcg_from_seed(derive_mask_seed(train_seed, (uint32_t)(st / spe), (uint32_t)(st % spe)));
+        sh_state[threadIdx.x] = g.state;
+        sh_inc[threadIdx.x] = g.inc;
+      }
+    }
+    __syncthreads();
+    for (int j = 0; j < 32; ++j) {
+      const int st = st0 + j * MASK_YSPLIT;
+      if (st >= total) break;
+      const int rows = min(B, n - (st % spe) * B);
+      mask_stream(sh_state[j], sh_inc[j], (int64_t)rows * sum_hidden, thresh, out_r + (int64_t)st * slot, jt, j1,
+                  jr);
+    }
   }
 }
 
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_seed_kernel(uint64_t mask_seed, int64_t n_draws, uint64_t thresh, uint32_t* bits) {
-  mask_stream(pcg_from_seed(mask_seed), n_draws, thresh, bits);
+  const Pcg64 g = pcg_from_seed(mask_seed);
+  mask_stream(g.state, g.inc, n_draws, thresh, bits, lcg_jump(32ull * threadIdx.x), lcg_jump(32ull * MASK_THREADS),
+              lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32));
 }
 
 // ceil(keep * 2^53): keep-bit threshold on the 53-bit integer behind random()
