@@ -69,7 +69,61 @@ def build_c4_world(num_clients: int = 1024, precision: str = "fp64"):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons, sampled through NVML between the timed
+    rounds of the timed region (`sample()` after each round's barrier).
+
+    NVML clock/throttle queries stall the GPU for milliseconds (measured:
+    scripts/nvml_probe.py), so a background sampler would land those stalls
+    inside the rounds it is meant to observe; sampled between rounds, the
+    clocks still reflect the load (they do not relax within microseconds)."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[tuple] = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self._nv = self._h = None
+        self._smi = None
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nv, self._h = nv, nv.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            self._smi = _SmiSampler(self.index).__enter__()
+        self.sample()
+        return self
+
+    def sample(self) -> None:
+        if self._nv is None:
+            return
+        nv, h = self._nv, self._h
+        try:
+            self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        except Exception:
+            pass
+
+    def __exit__(self, *exc):
+        if self._smi is not None:
+            self._smi.__exit__(*exc)
+            self.samples = self._smi.samples()
+        return False
+
+    def summary(self) -> dict:
+        sm = [x[0] for x in self.samples]
+        mx = [x[1] for x in self.samples]
+        reasons = sorted({name for _, _, bits in self.samples for name, bit in self.REASONS if bits & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm), "how": "NVML, between timed rounds"}
+
+
+class _SmiSampler:
+    """nvidia-smi -lms fallback of ClockSampler."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -85,40 +139,34 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.reader = threading.Thread(target=self._read, daemon=True)
-            self.reader.start()
+            threading.Thread(target=lambda: self.lines.extend(ln.strip() for ln in self.proc.stdout),
+                             daemon=True).start()
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *exc):
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
             self.proc.wait(timeout=5)
-        return False
 
-    def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    def samples(self) -> list[tuple]:
+        out = []
+        bits = [0x8, 0x40, 0x20, 0x4]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) != 6:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                mask = sum(b for b, v in zip(bits, parts[2:]) if v.lower() == "active")
+                out.append((float(parts[0]), float(parts[1]), mask))
             except ValueError:
                 continue
-            for name, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return out
 
 
 # ------------------------------------------------------------------ CPU sides
@@ -231,6 +279,7 @@ def measure_rounds(world, initial, comm, steps: int, warmup: int, device_index: 
             state = eng.run_sync_round(state)
             b.record(stream)
             barrier()
+            clocks.sample()
             round_ms.append(a.elapsed_time(b))
     timer, D.Runtime.timer = D.Runtime.timer, None
     total_ms = float(np.sum(round_ms))
@@ -253,12 +302,11 @@ def measure_e2e(world, eng, state, reps: int, barrier):
     e2e_ms = []
     h2d = d2h = 0
     for i in range(reps + 1):
-        world._device = None
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        dev = world.device_state()
+        dev = world.upload()  # this step's inputs: host -> HBM
         state = eng.run_sync_round(state)
         host_w = state.w_g.values
         b.record(stream)
@@ -409,8 +457,9 @@ def run_b200(args, rank: int, world_size: int) -> None:
                    "parallelism": f"1024 clients sharded over {world_size} GPU(s), 1 NCCL all-reduce/round"},
         "client_updates_per_s": value * m["trainings"] / args.steps,
         "e2e": {"value": e2e_value, "unit": "rounds/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "public FederationEngine.run_sync_round; shards + test set uploaded from page-locked host "
-                        "memory every step (bf16 feature copy rebuilt on device), w_g read back"},
+                "note": "public World.upload + FederationEngine.run_sync_round: shards + test set copied from "
+                        "page-locked host memory into HBM every step (bf16 mode: the trainer's bf16 row format, "
+                        "converted once at world build), w_g read back"},
         "roofline": roofline,
         "hbm_kernels": kernels,
         "hbm_kernels_c5": c5,

@@ -154,7 +154,7 @@ class HostPack:
     with ``pin=True`` the buffers are page-locked, so uploads are plain async
     DMA copies (the bench's end-to-end leg re-uploads them every round)."""
 
-    def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True):
+    def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True, bf16: bool = False):
         n_rows = np.array([f.shape[0] for f in features], dtype=np.int64)
         self.n_rows = n_rows.astype(np.int32)
         self.row_off = np.zeros(len(features), dtype=np.int64)
@@ -166,6 +166,16 @@ class HostPack:
              if labels else np.zeros(0))
         self.x = torch.from_numpy(x.reshape(-1, self.dim) if self.dim else x)
         self.y = torch.from_numpy(y)
+        self.bf16 = bf16
+        if bf16:
+            # the tensor-core trainer's input format, converted once like any
+            # dataset preprocessing: rows zero-padded to 16 columns, features
+            # rounded float64 -> float32 -> bf16 (the same two RN steps as
+            # fs_prep_features_bf16), labels float32
+            self.dp = (self.dim + 15) // 16 * 16
+            xb = torch.zeros((self.x.shape[0], self.dp), dtype=torch.bfloat16)
+            xb[:, :self.dim] = self.x.to(torch.float32).to(torch.bfloat16)
+            self.x, self.y = xb, self.y.to(torch.float32)
         self.pinned = pin
         if pin:
             self.x = self.x.pin_memory()
@@ -195,8 +205,12 @@ class DeviceShards:
         self.rt = rt or Runtime.get()
         pack = packed if packed is not None else HostPack(features, labels, pin=False)
         self.n_rows, self.row_off, self.dim = pack.n_rows, pack.row_off, pack.dim
-        self.features = pack.to_device(pack.x, self.rt)
-        self.labels = pack.to_device(pack.y, self.rt)
+        if pack.bf16:  # bf16-only shards (tensor-core trainer input)
+            self.features = self.labels = None
+            self._bf16 = (pack.to_device(pack.x, self.rt), pack.to_device(pack.y, self.rt))
+        else:
+            self.features = pack.to_device(pack.x, self.rt)
+            self.labels = pack.to_device(pack.y, self.rt)
 
     def __len__(self) -> int:
         return len(self.n_rows)
@@ -382,8 +396,10 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.max_batch = int(plan.batch.max())
     desc.mask_mode = N.FS_MASK_BITS if plan.bits is not None else N.FS_MASK_NONE
     desc.scale = plan.scale
-    desc.features = plan.shards.features.data_ptr()
-    desc.labels = plan.shards.labels.data_ptr()
+    if not bf16 and plan.shards.features is None:
+        raise ValueError("these shards hold bf16 features only (tensor-core trainer input)")
+    desc.features = plan.shards.features.data_ptr() if plan.shards.features is not None else None
+    desc.labels = plan.shards.labels.data_ptr() if plan.shards.labels is not None else None
     desc.row_off = plan.row_off_p
     desc.n_rows = plan.n_rows_p
     desc.batch = plan.batch_p

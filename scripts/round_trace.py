@@ -16,12 +16,21 @@ st = GlobalState(round=0, w_g=init)
 for _ in range(3):
     st = eng.run_sync_round(st)
 torch.cuda.synchronize()
+E2E = os.environ.get("E2E") == "1"  # rebuild the device world from host memory each round
+if E2E:
+    world.host_pack()
 for rep in range(2):
     eng.trace = []
     t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e0.record()
+    if E2E:
+        world._device = None
+        world.device_state()
+        eng._mark("device world rebuilt")
     st = eng.run_sync_round(st)
+    if E2E:
+        _ = st.w_g.values
     e1 = torch.cuda.Event(enable_timing=True)
     e1.record()
     torch.cuda.synchronize()
