@@ -54,6 +54,7 @@ C4_SYNC = {
     "lr": 0.05, "lr_decay": 0.9,
 }
 METRIC = "FL rounds/sec (1024 UNSW-shaped clients, C4 sync_filtered)"
+N_DELTA = 1  # FS_ALIGN_DELTA_SIGN
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA-core and DMMA) nominal; no measured fp64 peak exists
 
@@ -318,8 +319,10 @@ def measure_e2e(world, eng, state, reps: int, barrier):
     return 1000.0 / float(np.mean(e2e_ms)), int(h2d), int(d2h)
 
 
-def hbm_microbench(M: int = 3193857, n_clients: int = 256):
-    """K6/K7 at the C5 (WIDE MLP) row length, float32 rows: achieved GB/s."""
+def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = None, reps: int = 10):
+    """K6/K7 standalone (default: the C5 WIDE-MLP row length), float32 rows,
+    `n_agg` of the rows aggregated: achieved GB/s. Arguments are staged on the
+    device first; `reps` back-to-back launches are timed between two events."""
     import torch
 
     from paper_2503_15448_b200 import device as D
@@ -330,27 +333,43 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256):
     wg = torch.randn(M, device=rt.device, dtype=torch.float32)
     wp = torch.randn(M, device=rt.device, dtype=torch.float32)
     ptr_c = W.data_ptr() + np.arange(n_clients, dtype=np.uint64) * np.uint64(ld * 4)
+    k = n_agg or n_clients
+    d_all = rt.h2d(ptr_c.view(np.int64))
+    d_agg = rt.h2d(ptr_c[:k].view(np.int64))
+    counts = torch.empty(n_clients, dtype=torch.int64, device=rt.device)
+    res = torch.empty(M, dtype=torch.float32, device=rt.device)
+    stream = torch.cuda.current_stream()
+    launch = {
+        "align": (lambda: rt.call(rt.lib.fs_sign_align_shared(d_all.data_ptr(), wg.data_ptr(), wp.data_ptr(),
+                                                              n_clients, M, N_DELTA, 4, counts.data_ptr(),
+                                                              rt.stream), "align"),
+                  4.0 * M * (n_clients + 2)),
+        "aggregate": (lambda: rt.call(rt.lib.fs_aggregate_f32(d_agg.data_ptr(), k, M, res.data_ptr(), rt.stream),
+                                      "agg"), 4.0 * M * (k + 1)),
+    }
+    flush = torch.zeros(64 << 20, dtype=torch.float32, device=rt.device)
     out = {}
-    for name in ("align", "aggregate"):
-        times = []
-        for it in range(6):
-            torch.cuda.synchronize()
+    for name, (fn, nbytes) in launch.items():
+        fn()
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(reps):
+            # reading 256 MiB leaves L2 cold but clean (a write-flush would leave
+            # dirty lines whose write-back lands in the timed kernel); the spin
+            # keeps the GPU busy while the host queues the launch, so the
+            # events bracket the kernel alone
+            flush.sum()
+            torch.cuda._sleep(400_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            if name == "align":
-                D.align_shared(ptr_c, wg, wp, M, "delta_sign", rt)
-                nbytes = 4.0 * M * (n_clients + 2)
-            else:
-                d = rt.h2d(ptr_c.view(np.int64))
-                res = torch.empty(M, dtype=torch.float32, device=rt.device)
-                rt.call(rt.lib.fs_aggregate_f32(d.data_ptr(), n_clients, M, res.data_ptr(), rt.stream), "agg")
-                nbytes = 4.0 * M * (n_clients + 1)
-            b.record()
-            torch.cuda.synchronize()
-            if it >= 2:
-                times.append(a.elapsed_time(b))
-        ms = float(np.mean(times))
-        out[name] = {"ms": ms, "bytes": nbytes, "achieved_gbs": nbytes / ms / 1e6}
+            a.record(stream)
+            fn()
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+        out[name] = {"ms": ms, "bytes": nbytes, "achieved_gbs": nbytes / ms / 1e6, "M": M,
+                     "rows": n_clients if name == "align" else k,
+                     "how": f"median of {reps} launches, each queued behind a 256 MiB read (cold, clean L2)"}
     return out
 
 

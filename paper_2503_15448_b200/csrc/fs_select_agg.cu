@@ -9,6 +9,7 @@
 // 16-byte loads, many independent loads in flight per thread, integer
 // counts reduced with warp shuffles and one atomic per CTA.
 #include "fs_common.cuh"
+#include "fs_tc.cuh"
 
 namespace fs {
 
@@ -263,58 +264,127 @@ __global__ void __launch_bounds__(SORT_MAX) canonical_order_kernel(const uint64_
   for (int i = threadIdx.x; i < k; i += blockDim.x) sorted_rows[i] = rows[idx[i]];
 }
 
+// ---------------------------------------------------------------- K7
+// Ordered FedAvg column sums, out[j] = acc + rows[0][j] + rows[1][j] + ... in
+// row order in float64, acc starting at -0.0 (-0.0 + x == x for every x):
+// bitwise the reduction numpy's mean(axis=0) performs from the first row
+// (server.py:84-86). The order is sequential per column, so parallelism is
+// across columns only, and a thread's chain of loads must not stall on HBM
+// latency: each CTA owns a 1 KB strip of every row and streams it with TMA
+// bulk copies (cp.async.bulk, issued by warp 0, one lane per row) into a ring of AGG_STAGES x
+// AGG_ROWS x 1 KB in shared memory (64 KB in flight per CTA, 3 CTAs per SM),
+// completion tracked by mbarrier transaction counts; the 128 threads sum
+// their 2 (float) or 1 (double) columns out of shared memory in row order.
+// Rows whose pointers are not all 16-byte aligned, and a ragged last strip,
+// take the scalar path (same order).
 constexpr int AGG_THREADS = 128;
-constexpr int AGG_UNROLL = 8;
+constexpr int AGG_STRIP = 1024;  // bytes of each row per CTA
+constexpr int AGG_ROWS = 16;     // rows per stage
+constexpr int AGG_STAGES = 4;
+constexpr int AGG_RING = AGG_STAGES * AGG_ROWS * AGG_STRIP;
 
-// out[j] = ((rows[0][j] + rows[1][j]) + ...) / k : numpy's mean(axis=0) of
-// the stacked (k x M) updates adds rows in order, then true-divides by k.
-// (the float32 variant of the bf16 mode accumulates in float64 and rounds once)
-template <class T>
-__global__ void __launch_bounds__(AGG_THREADS)
-    aggregate_kernel(const uint64_t* rows, int k, int64_t M, T* out) {
-  extern __shared__ uint64_t sh_row_ptrs[];
-  const T** sh_rows = reinterpret_cast<const T**>(sh_row_ptrs);
-  for (int i = threadIdx.x; i < k; i += AGG_THREADS)
-    sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
-  __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * AGG_THREADS + threadIdx.x;
-  if (j >= M) return;
-  double acc = (double)__ldcs(sh_rows[0] + j);
-  int i = 1;
-  for (; i + AGG_UNROLL <= k; i += AGG_UNROLL) {
-    T v[AGG_UNROLL];
-#pragma unroll
-    for (int u = 0; u < AGG_UNROLL; ++u) v[u] = __ldcs(sh_rows[i + u] + j);
-#pragma unroll
-    for (int u = 0; u < AGG_UNROLL; ++u) acc += (double)v[u];
-  }
-  for (; i < k; ++i) acc += (double)__ldcs(sh_rows[i] + j);
-  out[j] = (T)(acc / (double)k);
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
 }
 
-// Partial FedAvg for client-sharded rounds: out[j] = sum_i rows[i][j] in
-// float64 (the rank's accepted updates in canonical order); the ranks'
-// partial sums are then all-reduced and finished by mean_finish_kernel.
 template <class T>
+__device__ __forceinline__ double ordered_column_sum(const T* const* rows, int k, int64_t j) {
+  double acc = -0.0;
+  for (int i = 0; i < k; ++i) acc += (double)__ldcs(rows[i] + j);
+  return acc;
+}
+
+// MEAN: out[j] = (ordered sum) / k as T (server.aggregate).
+// !MEAN: out[j] = ordered sum as float64 (a rank's partial FedAvg sum; the
+// ranks' sums are all-reduced and finished by mean_finish_kernel).
+template <class T, bool MEAN, class OUT>
 __global__ void __launch_bounds__(AGG_THREADS)
-    sum_rows_kernel(const uint64_t* rows, int k, int64_t M, double* out) {
-  extern __shared__ uint64_t sh_row_ptrs2[];
-  const T** sh_rows = reinterpret_cast<const T**>(sh_row_ptrs2);
-  for (int i = threadIdx.x; i < k; i += AGG_THREADS) sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
-  __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * AGG_THREADS + threadIdx.x;
-  if (j >= M) return;
-  double acc = 0.0;
-  int i = 0;
-  for (; i + AGG_UNROLL <= k; i += AGG_UNROLL) {
-    T v[AGG_UNROLL];
-#pragma unroll
-    for (int u = 0; u < AGG_UNROLL; ++u) v[u] = __ldcs(sh_rows[i + u] + j);
-#pragma unroll
-    for (int u = 0; u < AGG_UNROLL; ++u) acc += (double)v[u];
+    ordered_rows_kernel(const uint64_t* rows, int k, int64_t M, OUT* out) {
+  constexpr int CPT = AGG_STRIP / (int)sizeof(T) / AGG_THREADS;  // columns per thread
+  constexpr int64_t STRIP_COLS = AGG_STRIP / (int64_t)sizeof(T);
+  extern __shared__ __align__(128) uint8_t agg_smem[];
+  uint8_t* ring = agg_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(agg_smem + AGG_RING);
+  const T** sh_rows = reinterpret_cast<const T**>(full + AGG_STAGES);
+  const int tid = threadIdx.x;
+  uint64_t mis = 0;
+  for (int i = tid; i < k; i += AGG_THREADS) {
+    sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
+    mis |= rows[i] & 15;
   }
-  for (; i < k; ++i) acc += (double)__ldcs(sh_rows[i] + j);
-  out[j] = acc;
+  if (tid == 0) {
+    for (int s = 0; s < AGG_STAGES; ++s) tc::mbar_init(&full[s], 1);
+    tc::fence_mbar_init();
+  }
+  const bool vec_ok = !__syncthreads_or(mis != 0);
+  const int64_t col0 = (int64_t)blockIdx.x * STRIP_COLS;
+  const int64_t ncols = min(STRIP_COLS, M - col0);
+  auto emit = [&](int64_t j, double s) {
+    if (MEAN) out[j] = (OUT)(s / (double)k);
+    else out[j] = (OUT)(s + 0.0);  // an all -0.0 column sums to +0.0
+  };
+  if (!vec_ok || ncols != STRIP_COLS) {
+    for (int64_t c = tid; c < ncols; c += AGG_THREADS) emit(col0 + c, ordered_column_sum<T>(sh_rows, k, col0 + c));
+    return;
+  }
+  const int nb = (k + AGG_ROWS - 1) / AGG_ROWS;
+  // warp 0 refills a stage: lane 0 posts the byte count, lane r copies row r
+  auto issue = [&](int b) {
+    const int s = b % AGG_STAGES;
+    const int nr = min(AGG_ROWS, k - b * AGG_ROWS);
+    const int lane = tid & 31;
+    if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nr * AGG_STRIP));
+    __syncwarp();
+    if (lane < nr)
+      bulk_g2s(ring + (s * AGG_ROWS + lane) * AGG_STRIP, sh_rows[b * AGG_ROWS + lane] + col0, AGG_STRIP, &full[s]);
+  };
+  if (tid < 32)
+    for (int b = 0; b < min(AGG_STAGES, nb); ++b) issue(b);
+  {
+    double acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[c] = -0.0;
+    for (int b = 0; b < nb; ++b) {
+      const int s = b % AGG_STAGES;
+      tc::mbar_wait(&full[s], (uint32_t)((b / AGG_STAGES) & 1));
+      const int nr = min(AGG_ROWS, k - b * AGG_ROWS);
+      const T* st = reinterpret_cast<const T*>(ring + s * AGG_ROWS * AGG_STRIP) + tid * CPT;
+      for (int r = 0; r < nr; ++r) {
+        const T* e = st + r * STRIP_COLS;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[c] += (double)e[c];
+      }
+      __syncthreads();  // stage s fully read
+      if (tid < 32 && b + AGG_STAGES < nb) {
+        tc::fence_async_smem();
+        issue(b + AGG_STAGES);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) emit(col0 + tid * CPT + c, acc[c]);
+  }
+}
+
+template <class T, bool MEAN, class OUT>
+static int launch_ordered_rows(const uint64_t* rows, int k, int64_t M, OUT* out, cudaStream_t st, const char* what) {
+  const size_t smem = AGG_RING + AGG_STAGES * sizeof(uint64_t) + (size_t)k * sizeof(void*);
+  if (smem > 220 * 1024) {
+    set_error("%s: k=%d updates exceed the staged pointer table", what, k);
+    return FS_EINVAL;
+  }
+  auto kern = ordered_rows_kernel<T, MEAN, OUT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t strips = (M * (int64_t)sizeof(T) + AGG_STRIP - 1) / AGG_STRIP;
+  kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  return check_launch(what);
 }
 
 template <class T>
@@ -427,16 +497,7 @@ extern "C" int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, floa
     return FS_EINVAL;
   }
   if (M == 0) return FS_OK;
-  const size_t smem = (size_t)k * sizeof(float*);
-  if (smem > 200 * 1024) {
-    set_error("fs_aggregate_f32: k=%d updates exceed the staged pointer table", k);
-    return FS_EINVAL;
-  }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(aggregate_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
-  aggregate_kernel<float><<<blocks, AGG_THREADS, smem, (cudaStream_t)stream>>>(rows, k, M, out);
-  return check_launch("aggregate_kernel<float>");
+  return launch_ordered_rows<float, true, float>(rows, k, M, out, (cudaStream_t)stream, "fs_aggregate_f32");
 }
 
 extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, double* out,
@@ -451,16 +512,7 @@ extern "C" int fs_aggregate_f64(const uint64_t* rows, int32_t k, int64_t M, doub
     aggregate_single_kernel<<<1, 32, 0, st>>>(rows, k, out);
     return check_launch("aggregate_single_kernel");
   }
-  const size_t smem = (size_t)k * sizeof(double*);
-  if (smem > 200 * 1024) {
-    set_error("fs_aggregate_f64: k=%d updates exceed the staged pointer table", k);
-    return FS_EINVAL;
-  }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(aggregate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
-  aggregate_kernel<double><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
-  return check_launch("aggregate_kernel");
+  return launch_ordered_rows<double, true, double>(rows, k, M, out, st, "fs_aggregate_f64");
 }
 
 extern "C" int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
@@ -475,22 +527,8 @@ extern "C" int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t d
     if (cudaMemsetAsync(out, 0, sizeof(double) * M, st) != cudaSuccess) return check_launch("memset sum");
     return FS_OK;
   }
-  const size_t smem = (size_t)k * sizeof(void*);
-  if (smem > 200 * 1024) {
-    set_error("fs_sum_rows: k=%d updates exceed the staged pointer table", k);
-    return FS_EINVAL;
-  }
-  const unsigned blocks = (unsigned)((M + AGG_THREADS - 1) / AGG_THREADS);
-  if (dtype_bytes == 8) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(sum_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sum_rows_kernel<double><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(sum_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sum_rows_kernel<float><<<blocks, AGG_THREADS, smem, st>>>(rows, k, M, out);
-  }
-  return check_launch("sum_rows_kernel");
+  if (dtype_bytes == 8) return launch_ordered_rows<double, false, double>(rows, k, M, out, st, "fs_sum_rows");
+  return launch_ordered_rows<float, false, double>(rows, k, M, out, st, "fs_sum_rows");
 }
 
 extern "C" int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out,
