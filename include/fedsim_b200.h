@@ -211,6 +211,13 @@ int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, voi
  * dtype_bytes), the ranks all-reduce [sum | counts] over NCCL, and every
  * rank finishes out[j] = sum[j] / k in the parameter dtype, so the global
  * model stays replicated without a broadcast.                            */
+/* Many FedAvg means in one launch pair (an async run's aggregations between
+ * two training flushes): job j = mean of rows[job_off[j]..job_off[j+1]) in
+ * canonical byte order -> job_out[j] (device pointers; 1 <= rows per job <=
+ * max_k <= 1024; sorted_scratch holds job_off[n_jobs] pointers).         */
+int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k, int64_t M,
+                      int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out, void* stream);
+
 int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
                 void* stream);
 int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out, void* stream);
@@ -222,6 +229,82 @@ int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes,
 size_t fs_eval_workspace_bytes(int32_t n);
 int fs_eval_metrics(const double* scores, const int8_t* labels, int32_t n, double threshold,
                     int64_t* counts_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- f2 async event engine
+ * Host-side (all pointers HOST memory; no CUDA): the event loop of
+ * FederationEngine.run_async (server.py:485-637; simnet.py:18-103 clock).
+ * It never touches parameters. fs_async_run processes events until a
+ * train_done needs the outcome of a not-yet-trained cycle, then returns
+ * FS_ASYNC_NEED_EVAL with every pending cycle listed (eval_*: deferred id,
+ * client index, cycle, fetched model version); the caller trains + scores
+ * them and calls fs_async_provide, then fs_async_run again. Aggregations are
+ * returned as jobs (new version <- mean of the member cycles' updates, in
+ * server.aggregate's canonical order), to be launched before the next
+ * training batch; window reports likewise. The yield's arrays stay valid
+ * until the next fs_async_run. The processed-event log is read with
+ * fs_async_log (columnar; kind codes as in paper_2503_15448_b200/server.py). */
+#define FS_ASYNC_NEED_EVAL 1
+
+typedef struct fs_async_engine fs_async_engine;
+
+typedef struct {
+  int32_t n_clients, max_cycles, rounds, k_min;
+  int64_t budget;                /* rounds * n_clients accepted updates */
+  double buffer_timeout_s, agg_cost_per_update_s;
+  double horizon_s;              /* < 0: none */
+  double recovery_s, transfer_s0;
+  const int32_t* cid;            /* [n_clients] client ids */
+  const int32_t* steps;          /* [n_clients] SGD steps per training */
+  const double *down, *up;       /* [n_clients] latencies */
+  int32_t plan_per_cycle;        /* 1: plan arrays are [n_clients x max_cycles]; 0: [n_clients] */
+  const uint8_t *trains, *failed, *recovered;
+  const double *fail_off, *span;
+  const int32_t* n_captures;     /* checkpoint events per cycle (leading capture offsets) */
+  const int32_t* cap_ptr;        /* [n_clients + 1] CSR into cap_off */
+  const double* cap_off;
+  int64_t w_counts0[4];          /* open window at start: accepted, rejected, failures, steps */
+} fs_async_world;
+
+typedef struct {
+  int32_t n_eval;
+  const int32_t *eval_id, *eval_ci, *eval_cycle, *eval_version;
+  int32_t n_jobs;
+  const int32_t* job_version;    /* version created by job j */
+  const int64_t* job_off;        /* [n_jobs + 1] CSR into job_member (deferred ids) */
+  const int32_t* job_member;
+  int32_t n_reports;
+  const int64_t* rep_i;          /* [n_reports x 9]: window, version, updates, aggregations,
+                                    accepted, rejected, failures, steps, 0 */
+  const double* rep_d;           /* [n_reports x 2]: t_s, cumulative transfer_s */
+  const int64_t* rep_off;        /* [n_reports + 1] CSR into rep_stale */
+  const int32_t* rep_stale;
+  double now_s;
+  int64_t seq;
+  int32_t agg_count;
+  int64_t trainings;
+  int32_t stopped;
+  double transfer_s;
+  int64_t w_counts[4];           /* open window: accepted, rejected, failures, steps */
+} fs_async_yield;
+
+typedef struct {
+  int64_t n;
+  const int8_t* kind;
+  const double* t;
+  const int32_t *ci, *cycle;
+  const int64_t *a, *b;
+  const double* x;
+  const int64_t* l;              /* aggregate records: offset into list_cid / list_stale */
+  int64_t n_list;
+  const int32_t *list_cid, *list_stale;
+} fs_async_logview;
+
+fs_async_engine* fs_async_create(const fs_async_world* world);
+void fs_async_destroy(fs_async_engine* engine);
+int fs_async_run(fs_async_engine* engine, fs_async_yield* out);
+int fs_async_provide(fs_async_engine* engine, int32_t n, const uint8_t* accepted_host,
+                     const double* relevance_host);
+int fs_async_log(const fs_async_engine* engine, fs_async_logview* out);
 
 #ifdef __cplusplus
 }

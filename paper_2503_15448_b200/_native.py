@@ -105,13 +105,17 @@ _SIGNATURES = {
     "fs_gather_sort_keys_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_canonical_order": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
+    "fs_aggregate_jobs": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp]),
     "fs_sum_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_mean_finish": (ctypes.c_int, [_c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_eval_workspace_bytes": (_c_sz, [_c_i32]),
     "fs_eval_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_f64, _c_vp, _c_vp, _c_sz, _c_vp]),
 }
 
-EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+# host event engine (bound with its ctypes structs in async_loop.py)
+ASYNC_ENGINE_SYMBOLS = ("fs_async_create", "fs_async_destroy", "fs_async_run", "fs_async_provide", "fs_async_log")
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES) + ASYNC_ENGINE_SYMBOLS
 
 _lib = None
 _lock = threading.Lock()

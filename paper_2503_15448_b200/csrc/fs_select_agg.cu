@@ -225,7 +225,14 @@ __device__ bool row_less(const uint64_t* keys, const uint64_t* rows, int a, int 
 
 template <class T>
 __global__ void __launch_bounds__(SORT_MAX) canonical_order_kernel(const uint64_t* rows, int k, int64_t M,
-                                                                   uint64_t* sorted_rows) {
+                                                                   uint64_t* sorted_rows,
+                                                                   const int64_t* job_off = nullptr) {
+  if (job_off) {  // one CTA per aggregation job: rows[job_off[j], job_off[j+1])
+    const int64_t o = job_off[blockIdx.x];
+    rows += o;
+    sorted_rows += o;
+    k = (int)(job_off[blockIdx.x + 1] - o);
+  }
   __shared__ uint64_t keys[SORT_MAX * SORT_KEYS];
   __shared__ int idx[SORT_MAX];
   const int nk = M < SORT_KEYS ? (int)M : SORT_KEYS;
@@ -307,7 +314,14 @@ __device__ __forceinline__ double ordered_column_sum(const T* const* rows, int k
 // ranks' sums are all-reduced and finished by mean_finish_kernel).
 template <class T, bool MEAN, class OUT>
 __global__ void __launch_bounds__(AGG_THREADS)
-    ordered_rows_kernel(const uint64_t* rows, int k, int64_t M, OUT* out) {
+    ordered_rows_kernel(const uint64_t* rows, int k, int64_t M, OUT* out, const int64_t* job_off = nullptr,
+                        const uint64_t* job_out = nullptr) {
+  if (job_off) {  // blockIdx.y = aggregation job: rows[job_off[j], job_off[j+1]) -> job_out[j]
+    const int64_t o = job_off[blockIdx.y];
+    rows += o;
+    k = (int)(job_off[blockIdx.y + 1] - o);
+    out = reinterpret_cast<OUT*>(job_out[blockIdx.y]);
+  }
   constexpr int CPT = AGG_STRIP / (int)sizeof(T) / AGG_THREADS;  // columns per thread
   constexpr int64_t STRIP_COLS = AGG_STRIP / (int64_t)sizeof(T);
   extern __shared__ __align__(128) uint8_t agg_smem[];
@@ -383,7 +397,7 @@ static int launch_ordered_rows(const uint64_t* rows, int k, int64_t M, OUT* out,
   auto kern = ordered_rows_kernel<T, MEAN, OUT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t strips = (M * (int64_t)sizeof(T) + AGG_STRIP - 1) / AGG_STRIP;
-  kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out);
+  kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out, nullptr, nullptr);
   return check_launch(what);
 }
 
@@ -603,3 +617,43 @@ extern "C" int fs_canonical_order(const uint64_t* rows, int32_t k, int64_t M, in
     canonical_order_kernel<float><<<1, threads, 0, (cudaStream_t)stream>>>(rows, k, M, sorted_rows);
   return check_launch("canonical_order_kernel");
 }
+
+// Many independent FedAvg means in one launch pair (the aggregations an
+// asynchronous run queues between two training flushes): job j averages the
+// rows rows[job_off[j] .. job_off[j+1]) in canonical byte order into
+// job_out[j]. K9 orders every job's rows (one CTA per job) into
+// sorted_scratch, then K7 runs with one grid row per job.
+extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k,
+                                 int64_t M, int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out,
+                                 void* stream) {
+  if (n_jobs < 0 || max_k < 1 || max_k > SORT_MAX || M < 1 || (dtype_bytes != 4 && dtype_bytes != 8) ||
+      n_jobs > 65535) {
+    set_error("fs_aggregate_jobs: need 0 <= n_jobs <= 65535 jobs of 1..%d rows, M >= 1", SORT_MAX);
+    return FS_EINVAL;
+  }
+  if (n_jobs == 0) return FS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int threads = 32;
+  while (threads < max_k && threads < SORT_MAX) threads <<= 1;
+  const int esz = dtype_bytes;
+  if (esz == 8)
+    canonical_order_kernel<double><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+  else
+    canonical_order_kernel<float><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+  int rc = check_launch("canonical_order_kernel (jobs)");
+  if (rc != FS_OK) return rc;
+  const size_t smem = AGG_RING + AGG_STAGES * sizeof(uint64_t) + (size_t)max_k * sizeof(void*);
+  const int64_t strips = (M * (int64_t)esz + AGG_STRIP - 1) / AGG_STRIP;
+  const dim3 grid((unsigned)strips, (unsigned)n_jobs);
+  if (esz == 8) {
+    auto kern = ordered_rows_kernel<double, true, double>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
+  } else {
+    auto kern = ordered_rows_kernel<float, true, float>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
+  }
+  return check_launch("ordered_rows_kernel (jobs)");
+}
+

@@ -135,6 +135,52 @@ class _Null:
 _NULL_CTX = _Null()
 
 
+class Stage:
+    """Page-locked host bump arena + device mirror for per-launch metadata.
+
+    ``put`` packs a small array into the host arena and returns the device
+    address it will have; ``commit`` issues ONE async copy of everything put
+    since the last commit (instead of a pin_memory + copy per array). The
+    caller ``reset``s the arena only after a host synchronisation that
+    covers the previous copies (the async engine resets once per flush)."""
+
+    def __init__(self, rt: "Runtime", nbytes: int = 1 << 20):
+        self.rt = rt
+        self._old: list = []
+        self._alloc(nbytes)
+
+    def _alloc(self, n: int) -> None:
+        self.host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        self.hnp = self.host.numpy()
+        self.dev = torch.empty(n, dtype=torch.uint8, device=self.rt.device)
+        self.dbase = self.dev.data_ptr()
+        self.off = self.done = 0
+
+    def reset(self) -> None:
+        self.off = self.done = 0
+        self._old.clear()
+
+    def put(self, arr: np.ndarray) -> int:
+        b = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
+        n = b.size
+        start = (self.off + 15) & ~15
+        if start + n > self.hnp.size:
+            self.commit()
+            self._old.append((self.host, self.dev))  # in flight: keep until reset
+            self._alloc(max(2 * self.hnp.size, 2 * n))
+            start = 0
+        self.hnp[start:start + n] = b
+        self.off = start + n
+        return self.dbase + start
+
+    def commit(self, stream=None) -> None:
+        if self.off > self.done:
+            s = stream if stream is not None else torch.cuda.current_stream(self.rt.device)
+            with torch.cuda.stream(s):
+                self.dev[self.done:self.off].copy_(self.host[self.done:self.off], non_blocking=True)
+            self.done = self.off
+
+
 def mlp_flops_per_sample(dims) -> int:
     """Algorithmic fwd+bwd FLOPs per sample: 4*sum f_l f_l+1 over
     all layers for forward + weight gradients, plus 2*sum over layers l>=1 for
@@ -275,9 +321,10 @@ class TrainPlan:
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
                  dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
-                 pool: dict | None = None):
+                 pool: dict | None = None, stage: "Stage | None" = None):
         rt = rt or Runtime.get()
         self.rt = rt
+        self.stage = stage
         lib = rt.lib
         self.dims = tuple(int(x) for x in spec_dims)
         self.shards = shards
@@ -325,14 +372,19 @@ class TrainPlan:
         with torch.cuda.stream(torch_stream):
             i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)])
             i32 = np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32)
-            self.d_i64 = buf("i64", len(i64), torch.int64)
-            self.d_i32 = buf("i32", len(i32), torch.int32)
-            self.d_i64.copy_(torch.from_numpy(i64).pin_memory(), non_blocking=True)
-            self.d_i32.copy_(torch.from_numpy(i32).pin_memory(), non_blocking=True)
+            if stage is not None:
+                self.d_i64 = self.d_i32 = None
+                p64, p32 = stage.put(i64), stage.put(i32)
+                stage.commit(torch_stream)
+            else:
+                self.d_i64 = buf("i64", len(i64), torch.int64)
+                self.d_i32 = buf("i32", len(i32), torch.int32)
+                self.d_i64.copy_(torch.from_numpy(i64).pin_memory(), non_blocking=True)
+                self.d_i32.copy_(torch.from_numpy(i32).pin_memory(), non_blocking=True)
+                p64, p32 = self.d_i64.data_ptr(), self.d_i32.data_ptr()
             self.perm = buf("perm", max(int(perm_len.sum()), 1), torch.int32)
             self.bits = (buf("bits", max(int(mask_len.sum()), 1), torch.int32)
                          if use_masks and self.epochs > 0 else None)
-        p64, p32 = self.d_i64.data_ptr(), self.d_i32.data_ptr()
         self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
         self.n_rows_p, self.batch_p, self.start_p, self.end_p, self.order_p = (p32 + 4 * n * k for k in range(5))
         if self.epochs > 0:
@@ -364,7 +416,7 @@ class TrainPlan:
 
 
 def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision: str = "fp64",
-                w_out: torch.Tensor | None = None):
+                w_out: torch.Tensor | None = None, status: torch.Tensor | None = None):
     """K5 over a prepared plan: lr [n x epochs], w_start [n] device pointers.
     Returns (w_out [n x M], status int32 [n]) on the device."""
     rt = plan.rt
@@ -380,13 +432,20 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         w_out = torch.empty((n, ld), dtype=torch.float32 if bf16 else torch.float64, device=rt.device)[:, :M]
     if bf16 and (w_out.data_ptr() % 16 or (w_out.stride(0) * 4) % 16):
         raise ValueError("bf16 trainer needs 16-byte aligned float32 rows")
-    status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
+    if status is None:
+        status = torch.zeros(max(n, 1), dtype=torch.int32, device=rt.device)[:n]
     if n == 0:
         return w_out, status
     stream = torch.cuda.current_stream(rt.device)
     plan.consume(stream)
-    d_run = rt.h2d(np.asarray(w_start, dtype=np.uint64).view(np.int64))
-    d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
+    if plan.stage is not None:
+        run_p = plan.stage.put(np.asarray(w_start, dtype=np.uint64))
+        lr_p = plan.stage.put(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
+        plan.stage.commit(stream)
+    else:
+        d_run = rt.h2d(np.asarray(w_start, dtype=np.uint64).view(np.int64))
+        d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
+        run_p, lr_p = d_run.data_ptr(), d_lr.data_ptr()
     desc = N.TrainDesc()
     desc.n_dims = len(dims)
     for i, v in enumerate(dims):
@@ -403,8 +462,8 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.row_off = plan.row_off_p
     desc.n_rows = plan.n_rows_p
     desc.batch = plan.batch_p
-    desc.lr = d_lr.data_ptr()
-    desc.w_start = d_run.data_ptr()
+    desc.lr = lr_p
+    desc.w_start = run_p
     desc.w_out = w_out.data_ptr()
     desc.ldw = w_out.stride(0)
     desc.perm = plan.perm.data_ptr()
@@ -460,19 +519,25 @@ TRAIN_GRID = int(__import__("os").environ.get("FS_TRAIN_GRID", "0"))
 
 # --------------------------------------------------------------- alignment
 def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | None = None,
-                   dtype: torch.dtype = torch.float64) -> torch.Tensor:
+                   dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
+                   stage: Stage | None = None) -> torch.Tensor:
     """K6: aligned counts [n] int64 (device); dtype of the parameter vectors."""
     rt = rt or Runtime.get()
     n = len(wc_ptrs)
-    out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
     if n == 0:
         return out[:0]
     m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
     ptrs = [np.asarray(wc_ptrs, dtype=np.uint64).ravel(), np.asarray(wg_ptrs, dtype=np.uint64).ravel()]
     if m == N.FS_ALIGN_DELTA_SIGN:
         ptrs.append(np.asarray(wgp_ptrs, dtype=np.uint64).ravel())
-    d = rt.h2d(np.concatenate(ptrs).view(np.int64))
-    p = d.data_ptr()
+    if stage is not None:
+        p = stage.put(np.concatenate(ptrs))
+        stage.commit()
+    else:
+        d = rt.h2d(np.concatenate(ptrs).view(np.int64))
+        p = d.data_ptr()
     esz = 4 if dtype == torch.float32 else 8
     fn = rt.lib.fs_sign_align_f32 if esz == 4 else rt.lib.fs_sign_align_f64
     with rt.timed("align", float(esz) * M * (n + (2 if m else 1))):
@@ -576,6 +641,30 @@ def aggregate_ptrs(ptrs: np.ndarray, M: int, dtype: torch.dtype, rt: Runtime | N
     fn = rt.lib.fs_aggregate_f32 if dtype == torch.float32 else rt.lib.fs_aggregate_f64
     with rt.timed("aggregate", float(esz) * M * (k + 1)):
         rt.call(fn(d.data_ptr(), k, M, out.data_ptr(), rt.stream), "fs_aggregate")
+    return out
+
+
+def aggregate_jobs(jobs: list[np.ndarray], M: int, dtype: torch.dtype, rt: Runtime, stage: Stage) -> torch.Tensor:
+    """K9 + K7 for many independent means in one launch pair: job j = mean of
+    the rows at device pointers jobs[j] in canonical order. Returns [n_jobs x
+    ld] (rows padded to 128 bytes; row j is job j's mean)."""
+    n = len(jobs)
+    sizes = np.array([len(j) for j in jobs], dtype=np.int64)
+    esz = 4 if dtype == torch.float32 else 8
+    ld = (M * esz + 127) // 128 * 128 // esz
+    out = torch.empty((n, ld), dtype=dtype, device=rt.device)
+    if n == 0:
+        return out
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(sizes, out=off[1:])
+    rows = np.concatenate([np.asarray(j, dtype=np.uint64) for j in jobs])
+    outp = out.data_ptr() + np.arange(n, dtype=np.uint64) * np.uint64(ld * esz)
+    p_rows, p_off, p_out = stage.put(rows), stage.put(off), stage.put(outp)
+    stage.commit()
+    scratch = rt.scratch("agg_jobs_sorted", 8 * len(rows))
+    with rt.timed("aggregate", float(esz) * M * float((sizes + 1).sum()) / n):
+        rt.call(rt.lib.fs_aggregate_jobs(p_rows, p_off, n, int(sizes.max()), M, esz, scratch.data_ptr(), p_out,
+                                         rt.stream), "fs_aggregate_jobs")
     return out
 
 
