@@ -47,6 +47,8 @@ enum fs_align_mode { FS_ALIGN_WEIGHT_SIGN = 0, FS_ALIGN_DELTA_SIGN = 1 };
 
 const char* fs_last_error(void);
 int fs_abi_version(void);
+/* stream-ordered device-to-device copy (engine-owned model versions -> caller tensors) */
+int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 
 /* ---------------------------------------------------------------- K1 seeds
  * derive_seed(master, *path) with integer label words (rng.py:42-44).
@@ -244,6 +246,7 @@ int fs_eval_metrics(const double* scores, const int8_t* labels, int32_t n, doubl
  * until the next fs_async_run. The processed-event log is read with
  * fs_async_log (columnar; kind codes as in paper_2503_15448_b200/server.py). */
 #define FS_ASYNC_NEED_EVAL 1
+#define FS_ASYNC_REPORT 2   /* device mode: window reports ready (rep_w = versions to evaluate) */
 
 typedef struct fs_async_engine fs_async_engine;
 
@@ -285,6 +288,11 @@ typedef struct {
   int32_t stopped;
   double transfer_s;
   int64_t w_counts[4];           /* open window: accepted, rejected, failures, steps */
+  /* device mode (fs_async_attach_device) */
+  const uint64_t* rep_w;         /* [n_reports] device pointers of the report versions */
+  uint64_t w_g, w_g_prev;        /* current / previous global model (device; 0 = none) */
+  int64_t flushes, launches;     /* training flushes and kernel-launching calls so far */
+  int32_t diverged_client, diverged_cycle;  /* set with FS_EDIVERGED */
 } fs_async_yield;
 
 typedef struct {
@@ -299,7 +307,34 @@ typedef struct {
   const int32_t *list_cid, *list_stale;
 } fs_async_logview;
 
+/* Device mode: the engine does the parameter work itself on `stream` --
+ * per deferred flush one staged metadata copy, K2 + K3 + K5 + K6 and one
+ * device->host read of the counts; aggregation jobs go to fs_aggregate_jobs.
+ * fs_async_run then returns only FS_ASYNC_REPORT (evaluate rep_w, call
+ * again), FS_EDIVERGED or 0 (done). Model versions and trained rows are
+ * stream-ordered allocations owned by the engine (freed by destroy). */
+typedef struct {
+  int32_t n_dims;
+  int32_t dims[FS_MAX_LAYERS + 1];
+  int32_t epochs;
+  int32_t bf16;                  /* 1: tcgen05 trainer (float32 rows); 0: fp64 parity trainer */
+  double dropout_rate;
+  int32_t align_mode;            /* FS_ALIGN_* */
+  double theta;
+  uint64_t master_seed;
+  double base_lr, lr_decay;
+  int32_t grid;                  /* trainer CTAs (0 = auto) */
+  const void *features, *labels; /* fp64 shards (fp64) or fs_prep_features_bf16 rows + float32 labels */
+  const int64_t* row_off_host;   /* [n_clients] */
+  const int32_t* n_rows_host;    /* [n_clients] */
+  const int32_t* batch_host;     /* [n_clients] */
+  const void* w0;                /* version 0 (caller-owned, device) */
+  const void* w0_prev;           /* w_g_prev at start (caller-owned; NULL = none) */
+  void* stream;
+} fs_async_device;
+
 fs_async_engine* fs_async_create(const fs_async_world* world);
+int fs_async_attach_device(fs_async_engine* engine, const fs_async_device* dev);
 void fs_async_destroy(fs_async_engine* engine);
 int fs_async_run(fs_async_engine* engine, fs_async_yield* out);
 int fs_async_provide(fs_async_engine* engine, int32_t n, const uint8_t* accepted_host,

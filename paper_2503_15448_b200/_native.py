@@ -75,6 +75,7 @@ class TrainDesc(ctypes.Structure):
 _SIGNATURES = {
     "fs_last_error": (ctypes.c_char_p, []),
     "fs_abi_version": (ctypes.c_int, []),
+    "fs_memcpy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_derive_seed_host": (ctypes.c_int, [_c_u64, ctypes.POINTER(ctypes.c_uint32), _c_i32, ctypes.POINTER(_c_u64)]),
     "fs_train_seeds_host": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),
@@ -113,7 +114,8 @@ _SIGNATURES = {
 }
 
 # host event engine (bound with its ctypes structs in async_loop.py)
-ASYNC_ENGINE_SYMBOLS = ("fs_async_create", "fs_async_destroy", "fs_async_run", "fs_async_provide", "fs_async_log")
+ASYNC_ENGINE_SYMBOLS = ("fs_async_create", "fs_async_destroy", "fs_async_run", "fs_async_provide", "fs_async_log",
+                        "fs_async_attach_device")
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES) + ASYNC_ENGINE_SYMBOLS
 

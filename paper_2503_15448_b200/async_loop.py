@@ -32,6 +32,7 @@ _P64 = ctypes.POINTER(ctypes.c_int64)
 _PF = ctypes.POINTER(ctypes.c_double)
 
 NEED_EVAL = 1
+REPORT = 2
 
 KIND_NAMES = ("broadcast_arrive", "client_fail", "train_done", "upload_arrive", "client_recover", "checkpoint",
               "buffer_timeout", "aggregate", "run_end")
@@ -55,7 +56,19 @@ class AsyncYield(ctypes.Structure):
                 ("n_jobs", _i32), ("job_version", _P32), ("job_off", _P64), ("job_member", _P32),
                 ("n_reports", _i32), ("rep_i", _P64), ("rep_d", _PF), ("rep_off", _P64), ("rep_stale", _P32),
                 ("now_s", _f64), ("seq", _i64), ("agg_count", _i32), ("trainings", _i64), ("stopped", _i32),
-                ("transfer_s", _f64), ("w_counts", _i64 * 4)]
+                ("transfer_s", _f64), ("w_counts", _i64 * 4),
+                ("rep_w", ctypes.POINTER(ctypes.c_uint64)), ("w_g", ctypes.c_uint64), ("w_g_prev", ctypes.c_uint64),
+                ("flushes", _i64), ("launches", _i64), ("diverged_client", _i32), ("diverged_cycle", _i32)]
+
+
+class AsyncDevice(ctypes.Structure):
+    """Mirror of fs_async_device (include/fedsim_b200.h)."""
+
+    _fields_ = [("n_dims", _i32), ("dims", _i32 * (N.FS_MAX_LAYERS + 1)), ("epochs", _i32), ("bf16", _i32),
+                ("dropout_rate", _f64), ("align_mode", _i32), ("theta", _f64), ("master_seed", ctypes.c_uint64),
+                ("base_lr", _f64), ("lr_decay", _f64), ("grid", _i32), ("features", _vp), ("labels", _vp),
+                ("row_off_host", _vp), ("n_rows_host", _vp), ("batch_host", _vp), ("w0", _vp), ("w0_prev", _vp),
+                ("stream", _vp)]
 
 
 class AsyncLogView(ctypes.Structure):
@@ -70,6 +83,7 @@ _SIGS = {
     "fs_async_run": (ctypes.c_int, [_vp, ctypes.POINTER(AsyncYield)]),
     "fs_async_provide": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "fs_async_log": (ctypes.c_int, [_vp, ctypes.POINTER(AsyncLogView)]),
+    "fs_async_attach_device": (ctypes.c_int, [_vp, ctypes.POINTER(AsyncDevice)]),
 }
 
 
@@ -178,11 +192,24 @@ class AsyncLoop:
             raise ValueError("fs_async_create: invalid async world")
         self.y = AsyncYield()
 
+    def attach_device(self, dev: AsyncDevice, keep=()) -> None:
+        """Device mode: the engine trains, scores and aggregates on the GPU itself."""
+        self._dev_struct, self._dev_keep = dev, list(keep)
+        N.check(self.lib.fs_async_attach_device(self.handle, ctypes.byref(dev)), "fs_async_attach_device")
+
     def run(self) -> int:
         rc = self.lib.fs_async_run(self.handle, ctypes.byref(self.y))
+        if rc == N.FS_EDIVERGED:
+            from .model import TrainingDivergedError
+
+            raise TrainingDivergedError(self.lib.fs_last_error().decode(errors="replace"))
         if rc < 0:
-            raise ValueError(f"fs_async_run failed ({rc})")
+            N.check(rc, "fs_async_run")
         return rc
+
+    def report_versions(self) -> list[int]:
+        y = self.y
+        return [int(y.rep_w[i]) for i in range(y.n_reports)]
 
     def pending(self):
         y = self.y

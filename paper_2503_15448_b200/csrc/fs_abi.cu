@@ -29,3 +29,14 @@ int check_launch(const char* what) {
 extern "C" const char* fs_last_error(void) { return fs::g_err; }
 
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
+
+extern "C" int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return FS_OK;
+  if (!dst || !src) {
+    fs::set_error("fs_memcpy_d2d: null pointer");
+    return FS_EINVAL;
+  }
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+    return fs::check_launch("fs_memcpy_d2d");
+  return FS_OK;
+}

@@ -1,0 +1,836 @@
+// Host event engine of the buffered asynchronous federation (f2).
+//
+// Behavioural contract: FederationEngine.run_async, pkg/src/fedsim/server.py
+// :485-637 (handle 530-624, flush 516-528, AsyncBuffer 58-69), on the
+// discrete-event clock of simnet.py:18-103 -- events delivered in (time,
+// insertion counter) order, one log record per handled event. The Python
+// mirror is paper_2503_15448_b200/server.py (run_async); this engine runs the
+// same state machine over plain arrays and never touches parameters.
+//
+// Training is deferred exactly as in the Python engine: a cycle records the
+// model version it fetched at broadcast_arrive; the first train_done whose
+// cycle has no outcome yet suspends the engine (fs_async_run returns
+// FS_ASYNC_NEED_EVAL) with every not-yet-evaluated cycle listed; the caller
+// trains + scores that batch on the GPU and hands the accept flags back with
+// fs_async_provide. Aggregations never suspend: each one is queued as a job
+// (new version <- mean of the listed cycles' updates) for the caller to
+// launch, in order, before the next training batch. Window reports are
+// queued the same way. The processed-event log is kept columnar.
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <queue>
+#include <vector>
+
+#include "fs_common.cuh"
+#include "../../include/fedsim_b200.h"
+
+namespace {
+
+enum Kind : int8_t {
+  K_BROADCAST = 0, K_FAIL = 1, K_DONE = 2, K_UPLOAD = 3, K_RECOVER = 4, K_CHECKPOINT = 5,
+  K_TIMEOUT = 6, K_AGGREGATE = 7, K_RUN_END = 8
+};
+
+struct Ev {
+  double t;
+  int64_t seq;
+  int8_t kind;
+  int32_t ci, cycle;
+  int64_t a, b;  // kind-specific payload
+};
+struct EvLater {
+  bool operator()(const Ev& x, const Ev& y) const { return x.t > y.t || (x.t == y.t && x.seq > y.seq); }
+};
+
+struct Deferred {
+  int32_t ci, cycle, version;
+  int8_t evaluated, accepted;
+  double relevance;  // NaN = None
+};
+
+}  // namespace
+
+struct fs_async_engine {
+  // ---- world (copied)
+  int32_t N, C, rounds, k_min;
+  int64_t budget;
+  double timeout_s, agg_cost, horizon, recovery_s;
+  bool plan_per_cycle;
+  std::vector<int32_t> cid, steps;
+  std::vector<double> down, up;
+  std::vector<uint8_t> trains, failed, recovered;
+  std::vector<double> fail_off, span;
+  std::vector<int32_t> n_captures, cap_ptr;
+  std::vector<double> cap_off;
+  // ---- state
+  std::priority_queue<Ev, std::vector<Ev>, EvLater> heap;
+  int64_t seq = 0;
+  double now = 0.0;
+  bool stopped = false, started = false, finished = false, in_hand = false;
+  Ev hand{};
+  int32_t agg_count = 0, aggs_reported = 0;
+  int64_t applied = 0;
+  double server_free = 0.0, transfer = 0.0;
+  int64_t buf_epoch = 0;
+  std::vector<std::pair<int32_t, int32_t>> pending;               // (deferred id, fetched)
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> batches;  // aggregate event payloads
+  std::vector<int32_t> cycles;                                    // cycles started per client
+  std::vector<int32_t> active;                                    // deferred id per client (-1)
+  std::vector<Deferred> deferred;
+  std::vector<int32_t> unevaluated;
+  std::vector<int32_t> window_stale;
+  int64_t w_acc = 0, w_rej = 0, w_fail = 0, w_steps = 0, trainings = 0;
+  int32_t phase = 0;  // 0 = first run with horizon, 1 = after the horizon/cycle-cap run_end
+  // ---- outputs since the last yield
+  std::vector<int32_t> ev_id, ev_ci, ev_cycle, ev_version;
+  std::vector<int32_t> job_version, job_member;
+  std::vector<int64_t> job_off{0};
+  std::vector<int64_t> rep_i;
+  std::vector<double> rep_d;
+  std::vector<int64_t> rep_off{0};
+  std::vector<int32_t> rep_stale;
+  // ---- columnar log
+  std::vector<int8_t> lk;
+  std::vector<double> lt, lx;
+  std::vector<int32_t> lci, lcy;
+  std::vector<int64_t> la, lb, ll;
+  std::vector<int32_t> list_cid, list_stale;
+
+  size_t plan_ix(int32_t ci, int32_t cycle) const { return plan_per_cycle ? (size_t)ci * C + cycle : (size_t)ci; }
+
+  void schedule(double t, int8_t kind, int32_t ci, int32_t cycle, int64_t a = 0, int64_t b = 0) {
+    heap.push(Ev{t, seq++, kind, ci, cycle, a, b});
+  }
+  void log(const Ev& e, int64_t a, int64_t b, double x, int64_t l = -1) {
+    lk.push_back(e.kind); lt.push_back(e.t); lci.push_back(e.ci); lcy.push_back(e.cycle);
+    la.push_back(a); lb.push_back(b); lx.push_back(x); ll.push_back(l);
+  }
+
+  void start_cycle(int32_t ci, double t_request) {  // server.py start_cycle
+    const int32_t cyc = cycles[ci];
+    if (cyc >= C) return;
+    cycles[ci] += 1;
+    const double depart = std::max(t_request, server_free);
+    schedule(depart + down[ci], K_BROADCAST, ci, cyc);
+    transfer += down[ci];
+  }
+
+  void flush(double t_now, int trigger) {
+    batches.push_back(pending);
+    const int64_t count = (int64_t)pending.size();
+    pending.clear();
+    buf_epoch += 1;
+    const double start = std::max(t_now, server_free);
+    const double cost = agg_cost * (double)count;
+    const double done = start + cost;
+    server_free = done;
+    // a = batch slot, b = (trigger << 32) | window; round = agg_count at flush
+    const int64_t window = applied / N;
+    Ev e{done, seq++, K_AGGREGATE, trigger, agg_count, (int64_t)batches.size() - 1, window};
+    heap.push(e);
+  }
+
+  void report(int64_t window, double t_s) {
+    const int64_t ri[9] = {window, agg_count, N, agg_count - aggs_reported, w_acc, w_rej, w_fail, w_steps, 0};
+    rep_i.insert(rep_i.end(), ri, ri + 9);
+    rep_d.push_back(t_s);
+    rep_d.push_back(transfer);
+    rep_stale.insert(rep_stale.end(), window_stale.begin(), window_stale.end());
+    rep_off.push_back((int64_t)rep_stale.size());
+    w_acc = w_rej = w_fail = w_steps = 0;
+  }
+
+  // returns false when the event must wait for an evaluation
+  bool handle(const Ev& e) {
+    switch (e.kind) {
+      case K_BROADCAST: {
+        const int32_t ci = e.ci, cyc = e.cycle;
+        const size_t p = plan_ix(ci, cyc);
+        for (int32_t q = 0; q < n_captures[p]; ++q)
+          schedule(e.t + cap_off[cap_ptr[ci] + q], K_CHECKPOINT, ci, cyc);
+        if (failed[p]) {
+          schedule(e.t + fail_off[p], K_FAIL, ci, cyc, recovered[p]);
+          if (recovered[p]) schedule(e.t + fail_off[p] + recovery_s, K_RECOVER, ci, cyc);
+        }
+        if (!trains[p]) {
+          w_fail += 1;
+          start_cycle(ci, e.t + span[p]);
+        } else {
+          const int32_t id = (int32_t)deferred.size();
+          deferred.push_back(Deferred{ci, cyc, agg_count, 0, 0, NAN});
+          unevaluated.push_back(id);
+          schedule(e.t + span[p], K_DONE, ci, cyc, id);
+          if (failed[p]) w_fail += 1;
+          active[ci] = id;
+        }
+        log(e, 0, 0, 0.0);
+        return true;
+      }
+      case K_DONE: {
+        const int32_t id = (int32_t)e.a;
+        Deferred& d = deferred[id];
+        if (!d.evaluated) return false;
+        trainings += 1;
+        w_steps += steps[e.ci];
+        if (d.accepted) {
+          w_acc += 1;
+          schedule(e.t + up[e.ci], K_UPLOAD, e.ci, e.cycle, id, d.version);
+          transfer += up[e.ci];
+        } else {
+          w_rej += 1;
+          start_cycle(e.ci, e.t);
+        }
+        log(e, d.accepted, 0, d.relevance);
+        return true;
+      }
+      case K_UPLOAD: {
+        pending.emplace_back((int32_t)e.a, (int32_t)e.b);
+        if (pending.size() == 1) schedule(e.t + timeout_s, K_TIMEOUT, -1, -1, buf_epoch, 1);
+        if ((int64_t)pending.size() >= k_min) flush(e.t, 0);
+        start_cycle(e.ci, e.t);
+        log(e, agg_count - e.b, 0, 0.0);
+        return true;
+      }
+      case K_TIMEOUT: {
+        if (e.a != buf_epoch) return true;  // stale timer: no record
+        if (!pending.empty()) flush(e.t, 1);
+        log(e, e.a, e.b, 0.0);
+        return true;
+      }
+      case K_AGGREGATE: {
+        const auto& batch = batches[e.a];
+        const int64_t l0 = (int64_t)list_cid.size();
+        for (const auto& m : batch) {
+          list_cid.push_back(cid[deferred[m.first].ci]);
+          list_stale.push_back(agg_count - m.second);
+          window_stale.push_back(agg_count - m.second);
+        }
+        // job: version agg_count+1 = mean of the batch's updates (server.py:590-594)
+        for (const auto& m : batch) job_member.push_back(m.first);
+        job_version.push_back(agg_count + 1);
+        job_off.push_back((int64_t)job_member.size());
+        agg_count += 1;
+        const int64_t before = applied;
+        applied += (int64_t)batch.size();
+        // record: a = round, b = window, x = cost, ci = trigger, cycle = count, l = list offset
+        Ev rec = e;
+        rec.cycle = (int32_t)batch.size();
+        log(rec, e.cycle, e.b, agg_cost * (double)batch.size(), l0);
+        const int64_t w_hi = std::min<int64_t>(applied / N, rounds);
+        for (int64_t w = before / N; w < w_hi; ++w) {
+          report(w, e.t);
+          aggs_reported = agg_count;
+          window_stale.clear();
+        }
+        if (applied >= budget) schedule(e.t, K_RUN_END, -1, -1, 0);
+        return true;
+      }
+      case K_RUN_END:
+        stopped = true;
+        log(e, e.a, 0, 0.0);
+        return true;
+      default:  // client_fail, client_recover, checkpoint
+        log(e, e.a, 0, 0.0);
+        return true;
+    }
+  }
+
+  void clear_outputs() {
+    ev_id.clear(); ev_ci.clear(); ev_cycle.clear(); ev_version.clear();
+    job_version.clear(); job_member.clear(); job_off.assign(1, 0);
+    rep_i.clear(); rep_d.clear(); rep_off.assign(1, 0); rep_stale.clear();
+  }
+
+  // Timeline.run(handler, horizon): deliver until empty / stopped / beyond the
+  // horizon. Returns 1 when an event waits for an evaluation, 2 (device mode)
+  // when window reports are ready.
+  int drain(double limit) {
+    if (in_hand) {
+      if (!handle(hand)) return 1;
+      in_hand = false;
+      if (dx && !rep_d.empty()) return 2;
+    }
+    while (!heap.empty() && !stopped && heap.top().t <= limit) {
+      Ev e = heap.top();
+      heap.pop();
+      now = e.t;
+      if (!handle(e)) {
+        hand = e;
+        in_hand = true;
+        return 1;
+      }
+      if (dx && !rep_d.empty()) return 2;
+    }
+    return 0;
+  }
+
+  int step() {
+    if (!started) {
+      started = true;
+      for (int32_t ci = 0; ci < N; ++ci) start_cycle(ci, 0.0);
+    }
+    if (phase == 0) {
+      const double limit = horizon >= 0.0 ? horizon : INFINITY;
+      if (int r = drain(limit)) return r;
+      if (horizon >= 0.0 && !stopped && now < horizon) now = horizon;
+      if (!stopped) {
+        const int64_t reason = (horizon >= 0.0 && now >= horizon) ? 1 : 2;
+        schedule(now, K_RUN_END, -1, -1, reason);
+      }
+      phase = 1;
+    }
+    if (!stopped) {
+      if (int r = drain(INFINITY)) return r;
+    }
+    finished = true;
+    return 0;
+  }
+
+  struct DeviceExec* dx = nullptr;
+  int run();
+
+  int yield_eval() {
+    for (int32_t id : unevaluated) {
+      ev_id.push_back(id);
+      ev_ci.push_back(deferred[id].ci);
+      ev_cycle.push_back(deferred[id].cycle);
+      ev_version.push_back(deferred[id].version);
+    }
+    return FS_ASYNC_NEED_EVAL;
+  }
+
+  void provide(int32_t n, const uint8_t* accepted, const double* relevance) {
+    for (int32_t i = 0; i < n; ++i) {
+      Deferred& d = deferred[unevaluated[i]];
+      d.evaluated = 1;
+      d.accepted = accepted[i] ? 1 : 0;
+      d.relevance = relevance[i];
+    }
+    unevaluated.clear();
+  }
+};
+
+// ------------------------------------------------------------------ device mode
+// The engine's own executor: the per-flush work of server.DeviceAsyncExecutor
+// (TrainPlan + run_trainer + align + one host read) without a Python round trip.
+namespace {
+
+struct DevBlock {
+  void* ptr;
+  int64_t refs;
+};
+
+}  // namespace
+
+struct DeviceExec {
+  fs_async_device d;
+  cudaStream_t st;
+  int64_t M = 0, ldw = 0, esz = 8;
+  int32_t sum_hidden = 0;
+  std::vector<int64_t> row_off;
+  std::vector<int32_t> n_rows, batch;
+  // pinned staging + device mirror (one copy per flush)
+  uint8_t* h_stage = nullptr;
+  uint8_t* d_stage = nullptr;
+  size_t stage_cap = 0, stage_off = 0, stage_done = 0;  // [stage_done, stage_off) not yet copied
+  // pooled device buffers
+  void* d_perm = nullptr; size_t perm_cap = 0;
+  void* d_bits = nullptr; size_t bits_cap = 0;
+  void* d_ws = nullptr; size_t ws_cap = 0;
+  void* d_sorted = nullptr; size_t sorted_cap = 0;
+  int64_t* d_res = nullptr; size_t res_cap = 0;
+  int64_t* h_res = nullptr;
+  // model versions and trained rows (stream-ordered allocations)
+  std::vector<DevBlock> blocks;                 // block id -> allocation + live references
+  std::vector<std::pair<uint64_t, int64_t>> version;  // version -> (ptr, block id; -1 = caller-owned)
+  std::vector<uint64_t> row_ptr;                // deferred id -> trained row (accepted only)
+  std::vector<int64_t> row_block;
+  std::vector<uint64_t> rep_w;
+  int64_t flushes = 0, launches = 0;
+  int32_t div_client = -1, div_cycle = -1;
+
+  ~DeviceExec() {
+    for (auto& b : blocks)
+      if (b.ptr) cudaFreeAsync(b.ptr, st);
+    if (d_perm) cudaFreeAsync(d_perm, st);
+    if (d_bits) cudaFreeAsync(d_bits, st);
+    if (d_ws) cudaFreeAsync(d_ws, st);
+    if (d_sorted) cudaFreeAsync(d_sorted, st);
+    if (d_res) cudaFreeAsync(d_res, st);
+    if (d_stage) cudaFreeAsync(d_stage, st);
+    cudaStreamSynchronize(st);
+    if (h_stage) cudaFreeHost(h_stage);
+    if (h_res) cudaFreeHost(h_res);
+  }
+
+  static int cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return FS_OK;
+    fs::set_error("async device: %s: %s", what, cudaGetErrorString(e));
+    return FS_ECUDA;
+  }
+  int grow(void** p, size_t* cap, size_t need, const char* what) {
+    if (need <= *cap) return FS_OK;
+    if (*p) cudaFreeAsync(*p, st);
+    size_t n = need + need / 4 + 256;
+    *p = nullptr;
+    *cap = 0;
+    if (int rc = cuda(cudaMallocAsync(p, n, st), what)) return rc;
+    *cap = n;
+    return FS_OK;
+  }
+  int alloc_block(size_t bytes, int64_t refs, int64_t* id, void** out) {
+    void* p = nullptr;
+    if (int rc = cuda(cudaMallocAsync(&p, bytes, st), "row block")) return rc;
+    blocks.push_back(DevBlock{p, refs});
+    *id = (int64_t)blocks.size() - 1;
+    *out = p;
+    return FS_OK;
+  }
+  void unref(int64_t b) {
+    if (b < 0) return;
+    if (--blocks[b].refs == 0) {
+      cudaFreeAsync(blocks[b].ptr, st);
+      blocks[b].ptr = nullptr;
+    }
+  }
+  // staging: pack on the host, one H2D per commit
+  uint64_t put(const void* src, size_t bytes) {
+    stage_off = (stage_off + 15) & ~(size_t)15;
+    const uint64_t dptr = (uint64_t)(d_stage + stage_off);
+    memcpy(h_stage + stage_off, src, bytes);
+    stage_off += bytes;
+    return dptr;
+  }
+  // room for `more` bytes; growing waits for the stream (earlier regions were
+  // copied by then) and restarts the arena
+  int stage_reserve(size_t more) {
+    if (((stage_off + 15) & ~(size_t)15) + more <= stage_cap) return FS_OK;
+    if (int rc = cuda(cudaStreamSynchronize(st), "staging grow")) return rc;
+    if (h_stage) cudaFreeHost(h_stage);
+    if (d_stage) cudaFreeAsync(d_stage, st);
+    h_stage = nullptr;
+    d_stage = nullptr;
+    stage_cap = stage_off = stage_done = 0;
+    const size_t n = 2 * more + 4096;
+    if (int rc = cuda(cudaHostAlloc((void**)&h_stage, n, cudaHostAllocDefault), "pinned staging")) return rc;
+    if (int rc = cuda(cudaMallocAsync((void**)&d_stage, n, st), "device staging")) return rc;
+    stage_cap = n;
+    return FS_OK;
+  }
+  int commit() {
+    if (stage_off == stage_done) return FS_OK;
+    const size_t lo = stage_done;
+    stage_done = stage_off;
+    return cuda(cudaMemcpyAsync(d_stage + lo, h_stage + lo, stage_off - lo, cudaMemcpyHostToDevice, st),
+                "stage copy");
+  }
+  // after a host synchronisation every staged copy has run: reuse the arena
+  void stage_reset() { stage_off = stage_done = 0; }
+
+  int init(const fs_async_device* dev, int32_t n_clients) {
+    d = *dev;
+    st = (cudaStream_t)dev->stream;
+    M = 0;
+    for (int l = 0; l + 1 < d.n_dims; ++l) M += (int64_t)(d.dims[l] + 1) * d.dims[l + 1];
+    for (int l = 1; l + 1 < d.n_dims; ++l) sum_hidden += d.dims[l];
+    esz = d.bf16 ? 4 : 8;
+    ldw = (M * esz + 127) / 128 * 128 / esz;
+    row_off.assign(dev->row_off_host, dev->row_off_host + n_clients);
+    n_rows.assign(dev->n_rows_host, dev->n_rows_host + n_clients);
+    batch.assign(dev->batch_host, dev->batch_host + n_clients);
+    version.push_back({(uint64_t)dev->w0, -1});
+    cudaMemPool_t pool;
+    int device = 0;
+    cudaGetDevice(&device);
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // keep freed blocks cached across synchronisations
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    if (int rc = cuda(cudaHostAlloc((void**)&h_res, 1 << 20, cudaHostAllocDefault), "pinned results")) return rc;
+    return stage_reserve(1 << 19);
+  }
+
+  uint64_t prev_of(int32_t v) const {
+    return v > 0 ? version[v - 1].first : (uint64_t)d.w0_prev;
+  }
+
+  // aggregation jobs queued by the event loop, one launch pair
+  int launch_jobs(fs_async_engine* e) {
+    const int32_t nj = (int32_t)e->job_version.size();
+    if (nj == 0) return FS_OK;
+    const int64_t nrows = e->job_off[nj];
+    int32_t max_k = 1;
+    for (int32_t j = 0; j < nj; ++j) max_k = std::max<int32_t>(max_k, (int32_t)(e->job_off[j + 1] - e->job_off[j]));
+    int64_t blk;
+    void* base;
+    if (int rc = alloc_block((size_t)nj * ldw * esz, nj, &blk, &base)) return rc;
+    std::vector<uint64_t> rows(nrows), outs(nj);
+    for (int64_t i = 0; i < nrows; ++i) rows[i] = row_ptr[e->job_member[i]];
+    for (int32_t j = 0; j < nj; ++j) {
+      outs[j] = (uint64_t)base + (uint64_t)j * ldw * esz;
+      if ((int32_t)version.size() != e->job_version[j]) {
+        fs::set_error("async device: versions out of order");
+        return FS_EINVAL;
+      }
+      version.push_back({outs[j], blk});
+    }
+    if (int rc = stage_reserve(16 * (size_t)(2 * nrows + 2 * nj + 8))) return rc;
+    const uint64_t p_rows = put(rows.data(), 8 * nrows);
+    const uint64_t p_off = put(e->job_off.data(), 8 * (nj + 1));
+    const uint64_t p_out = put(outs.data(), 8 * nj);
+    if (int rc = commit()) return rc;
+    if (int rc = grow(&d_sorted, &sorted_cap, 8 * nrows, "sorted rows")) return rc;
+    launches += 1;
+    if (int rc = fs_aggregate_jobs((const uint64_t*)p_rows, (const int64_t*)p_off, nj, max_k, M, (int32_t)esz,
+                                   (uint64_t*)d_sorted, (const uint64_t*)p_out, st))
+      return rc;
+    for (int64_t i = 0; i < nrows; ++i) unref(row_block[e->job_member[i]]);
+    e->job_version.clear();
+    e->job_member.clear();
+    e->job_off.assign(1, 0);
+    return FS_OK;
+  }
+
+  // one deferred flush: train + score every pending cycle, hand outcomes back
+  int flush(fs_async_engine* e) {
+    if (int rc = launch_jobs(e)) return rc;
+    const std::vector<int32_t> ids = e->unevaluated;
+    const int32_t k = (int32_t)ids.size();
+    const int32_t E = d.epochs;
+    std::vector<int32_t> ci(k), cyc(k), ver(k);
+    for (int32_t i = 0; i < k; ++i) {
+      const Deferred& q = e->deferred[ids[i]];
+      ci[i] = q.ci; cyc[i] = q.cycle; ver[i] = q.version;
+    }
+    // ---- TrainPlan (device.TrainPlan): offsets, seeds, LPT order
+    std::vector<int64_t> i64(4 * (size_t)k);
+    std::vector<int32_t> i32(5 * (size_t)k), cid(k);
+    std::vector<uint64_t> seeds(k), wst(k);
+    std::vector<double> lr((size_t)k * std::max(E, 1));
+    int64_t perm_total = 0, mask_total = 0, max_rows = 1, max_b = 1;
+    std::vector<int64_t> work(k);
+    for (int32_t i = 0; i < k; ++i) cid[i] = e->cid[ci[i]];
+    fs_train_seeds_host(d.master_seed, cid.data(), cyc.data(), k, seeds.data());
+    for (int32_t i = 0; i < k; ++i) {
+      const int64_t nr = n_rows[ci[i]], b = batch[ci[i]];
+      const int64_t spe = (nr + b - 1) / b, total = (int64_t)E * spe;
+      i64[i] = row_off[ci[i]];
+      i64[k + i] = perm_total;
+      i64[2 * k + i] = mask_total;
+      i64[3 * k + i] = (int64_t)seeds[i];
+      perm_total += (int64_t)E * nr;
+      if (d.dropout_rate > 0.0) mask_total += total * ((b * sum_hidden + 31) / 32);
+      i32[i] = (int32_t)nr;
+      i32[k + i] = (int32_t)b;
+      i32[2 * k + i] = 0;
+      i32[3 * k + i] = (int32_t)total;
+      work[i] = total * b;
+      max_rows = std::max(max_rows, nr);
+      max_b = std::max(max_b, b);
+      const int32_t r = std::min(cyc[i], e->rounds - 1);
+      const double l = d.base_lr * std::pow(d.lr_decay, (double)r);  // lr_schedule (model.py:224-230)
+      for (int32_t ep = 0; ep < std::max(E, 1); ++ep) lr[(size_t)i * std::max(E, 1) + ep] = l;
+      wst[i] = version[ver[i]].first;
+    }
+    std::vector<int32_t> order(k);
+    for (int32_t i = 0; i < k; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+    for (int32_t i = 0; i < k; ++i) i32[4 * k + i] = order[i];
+    // ---- rows + alignment requests
+    int64_t blk;
+    void* wout;
+    if (int rc = alloc_block((size_t)k * ldw * esz, 1, &blk, &wout)) return rc;
+    std::vector<uint64_t> pc, pg, pp;
+    std::vector<int32_t> scored_ix;
+    for (int32_t i = 0; i < k; ++i) {
+      const uint64_t prev = prev_of(ver[i]);
+      if (d.align_mode == FS_ALIGN_DELTA_SIGN && prev == 0) continue;  // no movement history: accept
+      scored_ix.push_back(i);
+      pc.push_back((uint64_t)wout + (uint64_t)i * ldw * esz);
+      pg.push_back(wst[i]);
+      pp.push_back(prev);
+    }
+    const int32_t ns = (int32_t)scored_ix.size();
+    if (int rc = stage_reserve(64 * (size_t)k * (8 + std::max(E, 1)) + 4096)) return rc;
+    const uint64_t p64 = put(i64.data(), 8 * i64.size());
+    const uint64_t p32 = put(i32.data(), 4 * i32.size());
+    const uint64_t plr = put(lr.data(), 8 * lr.size());
+    const uint64_t pws = put(wst.data(), 8 * (size_t)k);
+    uint64_t palign = 0;
+    if (ns) {
+      std::vector<uint64_t> ap(pc);
+      ap.insert(ap.end(), pg.begin(), pg.end());
+      ap.insert(ap.end(), pp.begin(), pp.end());
+      palign = put(ap.data(), 8 * ap.size());
+    }
+    if (int rc = commit()) return rc;
+    // ---- K2 shuffles, K3 keep bits
+    if (int rc = grow(&d_perm, &perm_cap, 4 * (size_t)std::max<int64_t>(perm_total, 1), "perm")) return rc;
+    const uint64_t row_off_p = p64, perm_off_p = p64 + 8 * k, mask_off_p = p64 + 16 * k, seeds_p = p64 + 24 * k;
+    const uint64_t n_rows_p = p32, batch_p = p32 + 4 * k, start_p = p32 + 8 * k, end_p = p32 + 12 * k,
+                   order_p = p32 + 16 * k;
+    if (E > 0) {
+      launches += 1;
+      if (int rc = fs_shuffle_perms((const uint64_t*)seeds_p, (const int32_t*)n_rows_p, (const int64_t*)perm_off_p,
+                                    k, E, (int32_t)max_rows, (int32_t*)d_perm, st))
+        return rc;
+    }
+    const bool masks = d.dropout_rate > 0.0 && E > 0;
+    if (masks) {
+      if (int rc = grow(&d_bits, &bits_cap, 4 * (size_t)std::max<int64_t>(mask_total, 1), "bits")) return rc;
+      launches += 1;
+      if (int rc = fs_dropout_bits((const uint64_t*)seeds_p, (const int32_t*)n_rows_p, (const int32_t*)batch_p,
+                                   (const int64_t*)mask_off_p, k, E, sum_hidden, 1.0 - d.dropout_rate,
+                                   (uint32_t*)d_bits, st))
+        return rc;
+    }
+    // ---- K5
+    if (int rc = grow((void**)&d_res, &res_cap, 8 * (size_t)(2 * k + 2), "results")) return rc;
+    int32_t* status = (int32_t*)(d_res + k);
+    if (int rc = cuda(cudaMemsetAsync(status, 0, 4 * (size_t)k, st), "status")) return rc;
+    fs_train_desc t;
+    memset(&t, 0, sizeof(t));
+    t.n_dims = d.n_dims;
+    for (int l = 0; l < d.n_dims; ++l) t.dims[l] = d.dims[l];
+    t.n_req = k;
+    t.epochs = E;
+    t.max_batch = (int32_t)max_b;
+    t.mask_mode = masks ? FS_MASK_BITS : FS_MASK_NONE;
+    t.scale = masks ? 1.0 / (1.0 - d.dropout_rate) : 1.0;
+    t.features = (const double*)d.features;
+    t.labels = (const double*)d.labels;
+    t.row_off = (const int64_t*)row_off_p;
+    t.n_rows = (const int32_t*)n_rows_p;
+    t.batch = (const int32_t*)batch_p;
+    t.lr = (const double*)plr;
+    t.w_start = (const uint64_t*)pws;
+    t.w_out = (double*)wout;
+    t.ldw = ldw;
+    t.perm = (const int32_t*)d_perm;
+    t.perm_off = (const int64_t*)perm_off_p;
+    t.mask_bits = masks ? (const uint32_t*)d_bits : nullptr;
+    t.mask_off = (const int64_t*)mask_off_p;
+    t.start_step = (const int32_t*)start_p;
+    t.end_step = (const int32_t*)end_p;
+    t.order = (const int32_t*)order_p;
+    t.status = status;
+    t.grid = d.grid;
+    const size_t need = d.bf16 ? fs_train_bf16_workspace_bytes(&t) : fs_train_workspace_bytes(&t);
+    if (need == 0) {
+      fs::set_error("async device: layer dims not supported by the trainer");
+      return FS_EINVAL;
+    }
+    if (int rc = grow(&d_ws, &ws_cap, need, "trainer workspace")) return rc;
+    t.workspace = d_ws;
+    t.workspace_bytes = ws_cap;
+    launches += 1;
+    if (int rc = d.bf16 ? fs_train_bf16(&t, d.features, (const float*)d.labels, st) : fs_train_f64(&t, st))
+      return rc;
+    // ---- K6
+    if (ns) {
+      launches += 1;
+      const uint64_t* a = (const uint64_t*)palign;
+      const int rc = d.bf16 ? fs_sign_align_f32(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st)
+                            : fs_sign_align_f64(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st);
+      if (rc) return rc;
+    }
+    if (int rc = cuda(cudaMemcpyAsync(h_res, d_res, 8 * (size_t)k + 4 * (size_t)k, cudaMemcpyDeviceToHost, st),
+                      "results D2H"))
+      return rc;
+    if (int rc = cuda(cudaStreamSynchronize(st), "flush")) return rc;
+    stage_reset();
+    flushes += 1;
+    const int32_t* h_status = (const int32_t*)(h_res + k);
+    for (int32_t i = 0; i < k; ++i)
+      if (h_status[i]) {  // lowest pending index, as the serial reference would meet it
+        div_client = e->cid[ci[i]];
+        div_cycle = cyc[i];
+        fs::set_error("loss became non-finite training client %d cycle %d", div_client, div_cycle);
+        return FS_EDIVERGED;
+      }
+    // ---- outcomes (selection.filter_update: ratio >= theta, inclusive)
+    std::vector<uint8_t> acc(k, 1);
+    std::vector<double> rel(k, NAN);
+    for (int32_t s = 0; s < ns; ++s) {
+      const int32_t i = scored_ix[s];
+      const double r = (double)h_res[s] / (double)M;
+      rel[i] = r;
+      acc[i] = r >= d.theta;
+    }
+    int64_t n_acc = 0;
+    if ((int64_t)row_ptr.size() < (int64_t)e->deferred.size()) {
+      row_ptr.resize(e->deferred.size() * 2 + 16, 0);
+      row_block.resize(e->deferred.size() * 2 + 16, -1);
+    }
+    for (int32_t i = 0; i < k; ++i)
+      if (acc[i]) {
+        row_ptr[ids[i]] = (uint64_t)wout + (uint64_t)i * ldw * esz;
+        row_block[ids[i]] = blk;
+        ++n_acc;
+      }
+    blocks[blk].refs = n_acc;
+    if (n_acc == 0) {  // nothing to aggregate from this flush
+      cudaFreeAsync(blocks[blk].ptr, st);
+      blocks[blk].ptr = nullptr;
+    }
+    e->provide(k, acc.data(), rel.data());
+    // every deferred cycle is trained: later ones fetch the newest version
+    const int32_t latest = (int32_t)version.size() - 1;
+    for (int32_t v = 0; v < latest - 1; ++v)
+      if (version[v].second >= 0) {
+        unref(version[v].second);
+        version[v].second = -2;  // released
+      }
+    return FS_OK;
+  }
+};
+
+int fs_async_engine::run() {
+  clear_outputs();
+  if (finished) return 0;
+  for (;;) {
+    const int r = step();
+    if (r == 1) {
+      if (!dx) return yield_eval();
+      if (int rc = dx->flush(this)) return rc;
+      continue;
+    }
+    if (r == 2) {  // device mode: reports need their versions to exist
+      if (int rc = dx->launch_jobs(this)) return rc;
+      dx->rep_w.clear();
+      for (size_t i = 0; i < rep_i.size() / 9; ++i) dx->rep_w.push_back(dx->version[rep_i[9 * i + 1]].first);
+      return FS_ASYNC_REPORT;
+    }
+    if (dx)
+      if (int rc = dx->launch_jobs(this)) return rc;
+    return 0;
+  }
+}
+
+extern "C" {
+
+fs_async_engine* fs_async_create(const fs_async_world* w) {
+  if (!w || w->n_clients < 1 || w->max_cycles < 0 || w->k_min < 1) return nullptr;
+  auto* e = new fs_async_engine();
+  const int32_t N = w->n_clients;
+  e->N = N;
+  e->C = w->max_cycles;
+  e->rounds = w->rounds;
+  e->k_min = w->k_min;
+  e->budget = w->budget;
+  e->timeout_s = w->buffer_timeout_s;
+  e->agg_cost = w->agg_cost_per_update_s;
+  e->horizon = w->horizon_s;
+  e->recovery_s = w->recovery_s;
+  e->plan_per_cycle = w->plan_per_cycle != 0;
+  e->transfer = w->transfer_s0;
+  e->cid.assign(w->cid, w->cid + N);
+  e->steps.assign(w->steps, w->steps + N);
+  e->down.assign(w->down, w->down + N);
+  e->up.assign(w->up, w->up + N);
+  const size_t P = e->plan_per_cycle ? (size_t)N * (size_t)w->max_cycles : (size_t)N;
+  e->trains.assign(w->trains, w->trains + P);
+  e->failed.assign(w->failed, w->failed + P);
+  e->recovered.assign(w->recovered, w->recovered + P);
+  e->fail_off.assign(w->fail_off, w->fail_off + P);
+  e->span.assign(w->span, w->span + P);
+  e->n_captures.assign(w->n_captures, w->n_captures + P);
+  e->cap_ptr.assign(w->cap_ptr, w->cap_ptr + N + 1);
+  e->cap_off.assign(w->cap_off, w->cap_off + w->cap_ptr[N]);
+  e->w_acc = w->w_counts0[0];
+  e->w_rej = w->w_counts0[1];
+  e->w_fail = w->w_counts0[2];
+  e->w_steps = w->w_counts0[3];
+  e->cycles.assign(N, 0);
+  e->active.assign(N, -1);
+  return e;
+}
+
+void fs_async_destroy(fs_async_engine* e) {
+  if (e) delete e->dx;
+  delete e;
+}
+
+int fs_async_attach_device(fs_async_engine* e, const fs_async_device* dev) {
+  if (!e || !dev || !dev->w0 || e->started || e->dx) {
+    fs::set_error("fs_async_attach_device: invalid engine/device or engine already running");
+    return FS_EINVAL;
+  }
+  auto* x = new DeviceExec();
+  const int rc = x->init(dev, e->N);
+  if (rc) {
+    delete x;
+    return rc;
+  }
+  e->dx = x;
+  return FS_OK;
+}
+
+int fs_async_run(fs_async_engine* e, fs_async_yield* y) {
+  if (!e || !y) return FS_EINVAL;
+  const int rc = e->run();
+  memset(y, 0, sizeof(*y));
+  y->n_eval = (int32_t)e->ev_id.size();
+  y->eval_id = e->ev_id.data();
+  y->eval_ci = e->ev_ci.data();
+  y->eval_cycle = e->ev_cycle.data();
+  y->eval_version = e->ev_version.data();
+  y->n_jobs = (int32_t)e->job_version.size();
+  y->job_version = e->job_version.data();
+  y->job_off = e->job_off.data();
+  y->job_member = e->job_member.data();
+  y->n_reports = (int32_t)e->rep_d.size() / 2;
+  y->rep_i = e->rep_i.data();
+  y->rep_d = e->rep_d.data();
+  y->rep_off = e->rep_off.data();
+  y->rep_stale = e->rep_stale.data();
+  y->now_s = e->now;
+  y->seq = e->seq;
+  y->agg_count = e->agg_count;
+  y->trainings = e->trainings;
+  y->stopped = e->stopped ? 1 : 0;
+  y->transfer_s = e->transfer;
+  y->w_counts[0] = e->w_acc;
+  y->w_counts[1] = e->w_rej;
+  y->w_counts[2] = e->w_fail;
+  y->w_counts[3] = e->w_steps;
+  if (DeviceExec* x = e->dx) {
+    y->rep_w = x->rep_w.data();
+    const size_t nv = x->version.size();
+    y->w_g = x->version[nv - 1].first;
+    y->w_g_prev = nv > 1 ? x->version[nv - 2].first : (uint64_t)x->d.w0_prev;
+    y->flushes = x->flushes;
+    y->launches = x->launches;
+    y->diverged_client = x->div_client;
+    y->diverged_cycle = x->div_cycle;
+  }
+  return rc;
+}
+
+int fs_async_provide(fs_async_engine* e, int32_t n, const uint8_t* accepted, const double* relevance) {
+  if (!e || n != (int32_t)e->unevaluated.size()) return FS_EINVAL;
+  e->provide(n, accepted, relevance);
+  return FS_OK;
+}
+
+int fs_async_log(const fs_async_engine* e, fs_async_logview* v) {
+  if (!e || !v) return FS_EINVAL;
+  v->n = (int64_t)e->lk.size();
+  v->kind = e->lk.data();
+  v->t = e->lt.data();
+  v->ci = e->lci.data();
+  v->cycle = e->lcy.data();
+  v->a = e->la.data();
+  v->b = e->lb.data();
+  v->x = e->lx.data();
+  v->l = e->ll.data();
+  v->n_list = (int64_t)e->list_cid.size();
+  v->list_cid = e->list_cid.data();
+  v->list_stale = e->list_stale.data();
+  return FS_OK;
+}
+
+}  // extern "C"

@@ -295,3 +295,55 @@ def test_engine_matches_oracle_at_unsw_shape():
     wg = sim.run(init.values)
     assert eng.timeline.digest() == sim.digest()
     assert rel_err(st.w_g.values, wg) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["async_fail_lost", "async_weight", "async_delta_dyn"])
+@pytest.mark.parametrize("engine", ["device", "native", "python"])
+def test_async_engines_agree(golden, monkeypatch, name, engine):
+    """The C++ event loop with its C++ device executor ("device", default),
+    with the Python executor ("native") and the Python event loop
+    ("python") replay the reference digest and the same global model bitwise."""
+    from paper_2503_15448_b200 import server
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    monkeypatch.setattr(server, "_ASYNC_ENGINE", engine)
+    run = golden("runs.json")[name]
+    world, init = build_world(ExperimentConfig.from_dict(run["config"]))
+    eng = server.FederationEngine(world)
+    state = eng.run(init)
+    assert eng.timeline.digest() == run["digest"]
+    want = golden("runs_wg.npz")[name]
+    assert rel_err(state.w_g.values, want) < 1e-12
+    assert [r.accepted for r in eng.reports] == [r["accepted"] for r in run["reports"]]
+    assert [r.transfer_s for r in eng.reports] == pytest.approx([r["transfer_s"] for r in run["reports"]], abs=0)
+    assert len(state.history) == sum(1 for r in eng.timeline.log if r["kind"] == "aggregate")
+
+
+def test_async_engines_agree_bf16():
+    """bf16 mode: the three async engines make the same decisions and produce
+    the same float32 global model bitwise (same kernels, same order)."""
+    from paper_2503_15448_b200 import server
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    cfg = {"num_clients": 48, "rounds": 2, "epochs": 1, "dataset": {"n": 20000, "d": 42},
+           "mode": "async_filtered", "selection_mode": "delta_sign", "batch": {"policy": "dynamic"}, "seed": 6,
+           "profiles": {"speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
+                        "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
+                        "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
+                        "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}}}
+    out = {}
+    saved = server._ASYNC_ENGINE
+    try:
+        for engine in ("device", "native", "python"):
+            server._ASYNC_ENGINE = engine
+            world, init = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+            eng = server.FederationEngine(world)
+            st = eng.run(init)
+            out[engine] = (eng.timeline.digest(), st.w_g.values.copy())
+    finally:
+        server._ASYNC_ENGINE = saved
+    assert out["device"][0] == out["native"][0] == out["python"][0]
+    assert np.array_equal(out["device"][1], out["native"][1])
+    assert np.array_equal(out["device"][1], out["python"][1])
