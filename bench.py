@@ -374,8 +374,10 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = N
 
 
 def measure_async(precision: str, windows: int = 2):
-    """C4 `async_filtered` (the reference's buffered asynchronous engine, deferred
-    batched training): windows of 1024 applied updates per second."""
+    """C4 `async_filtered` (the reference's buffered asynchronous engine: C++
+    event loop driving the device executor, deferred batched training): windows
+    of 1024 applied updates per second. One untimed warm-up run first (module
+    load, memory pools), then the timed run, CUDA events on the launching stream."""
     import torch
 
     from paper_2503_15448_b200.config import ExperimentConfig
@@ -386,18 +388,23 @@ def measure_async(precision: str, windows: int = 2):
     cfg.update({"mode": "async_filtered", "rounds": windows})
     world, init = build_world(ExperimentConfig.from_dict(cfg), precision=precision)
     world.device_state()
+    FederationEngine(world).run(init)  # warm-up
     torch.cuda.synchronize()
     eng = FederationEngine(world)
+    stream = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    a.record(stream)
     eng.run(init)
-    b.record()
+    b.record(stream)
     torch.cuda.synchronize()
     sec = a.elapsed_time(b) / 1e3
     return {"value": windows / sec, "unit": "rounds/s (windows of 1024 applied updates)",
             "client_updates_per_s": eng.trainings / sec, "trainings": eng.trainings,
             "device_batches": eng.device_batches, "events": len(eng.timeline.log), "windows": windows,
-            "precision": precision}
+            "precision": precision, "gpu_launches": getattr(eng, "async_launches", None),
+            "host_s": dict(zip(("prep", "wait", "post"), getattr(eng, "async_host_s", (None,) * 3))),
+            "engine": "C++ event loop + C++ device executor (FS_ASYNC_ENGINE=device)",
+            "digest": eng.timeline.digest()}
 
 
 def run_b200(args, rank: int, world_size: int) -> None:

@@ -293,6 +293,7 @@ typedef struct {
   uint64_t w_g, w_g_prev;        /* current / previous global model (device; 0 = none) */
   int64_t flushes, launches;     /* training flushes and kernel-launching calls so far */
   int32_t diverged_client, diverged_cycle;  /* set with FS_EDIVERGED */
+  double host_s[3];              /* diagnostics: host seconds preparing flushes, waiting on them, after them */
 } fs_async_yield;
 
 typedef struct {

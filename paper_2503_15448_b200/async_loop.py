@@ -58,7 +58,8 @@ class AsyncYield(ctypes.Structure):
                 ("now_s", _f64), ("seq", _i64), ("agg_count", _i32), ("trainings", _i64), ("stopped", _i32),
                 ("transfer_s", _f64), ("w_counts", _i64 * 4),
                 ("rep_w", ctypes.POINTER(ctypes.c_uint64)), ("w_g", ctypes.c_uint64), ("w_g_prev", ctypes.c_uint64),
-                ("flushes", _i64), ("launches", _i64), ("diverged_client", _i32), ("diverged_cycle", _i32)]
+                ("flushes", _i64), ("launches", _i64), ("diverged_client", _i32), ("diverged_cycle", _i32),
+                ("host_s", _f64 * 3)]
 
 
 class AsyncDevice(ctypes.Structure):

@@ -1,3 +1,5 @@
+#include <mutex>
+#include <unordered_map>
 // C-ABI plumbing: thread-local error messages and launch checks.
 #include <cstdarg>
 #include <cstdio>
@@ -29,6 +31,18 @@ int check_launch(const char* what) {
 extern "C" const char* fs_last_error(void) { return fs::g_err; }
 
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
+
+namespace fs {
+void ensure_smem_impl(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> set_to;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = set_to.find(fn);
+  if (it != set_to.end() && it->second >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_to[fn] = bytes;
+}
+}  // namespace fs
 
 extern "C" int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return FS_OK;

@@ -20,6 +20,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <queue>
 #include <vector>
@@ -351,6 +352,27 @@ struct DeviceExec {
   std::vector<uint64_t> rep_w;
   int64_t flushes = 0, launches = 0;
   int32_t div_client = -1, div_cycle = -1;
+  double t_prep = 0, t_wait = 0, t_post = 0;  // host seconds: before the sync, in it, after it
+  // K2/K3 lookahead: every client owns two plan slots (shuffles + keep bits);
+  // after a flush trains cycle c of a client from slot p, its cycle c+1 is
+  // generated into slot 1-p on a side stream while the trainer runs, so the
+  // next flush's trainer starts without waiting for K2/K3.
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_copy = nullptr, side_done = nullptr;
+  bool side_used = false;
+  int32_t E = 0, C = 0;
+  std::vector<int64_t> perm_pre, mask_pre;   // per-client slot offsets
+  int64_t perm_sum = 0, mask_sum = 0;
+  int32_t* d_perm_all = nullptr;
+  uint32_t* d_bits_all = nullptr;
+  std::vector<int32_t> gen_cycle;            // [client][slot] cycle held (-1 none)
+  std::vector<int32_t> cid_of;
+  int64_t misses = 0;
+  int64_t perm_at(int32_t ci, int32_t p) const { return p * perm_sum + perm_pre[ci]; }
+  int64_t mask_at(int32_t ci, int32_t p) const { return p * mask_sum + mask_pre[ci]; }
+  static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
 
   ~DeviceExec() {
     for (auto& b : blocks)
@@ -361,6 +383,14 @@ struct DeviceExec {
     if (d_sorted) cudaFreeAsync(d_sorted, st);
     if (d_res) cudaFreeAsync(d_res, st);
     if (d_stage) cudaFreeAsync(d_stage, st);
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+    }
+    if (side_copy) cudaEventDestroy(side_copy);
+    if (side_done) cudaEventDestroy(side_done);
+    if (d_perm_all) cudaFreeAsync(d_perm_all, st);
+    if (d_bits_all) cudaFreeAsync(d_bits_all, st);
     cudaStreamSynchronize(st);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_res) cudaFreeHost(h_res);
@@ -409,6 +439,8 @@ struct DeviceExec {
   int stage_reserve(size_t more) {
     if (((stage_off + 15) & ~(size_t)15) + more <= stage_cap) return FS_OK;
     if (int rc = cuda(cudaStreamSynchronize(st), "staging grow")) return rc;
+    if (side)
+      if (int rc = cuda(cudaStreamSynchronize(side), "staging grow")) return rc;
     if (h_stage) cudaFreeHost(h_stage);
     if (d_stage) cudaFreeAsync(d_stage, st);
     h_stage = nullptr;
@@ -420,17 +452,25 @@ struct DeviceExec {
     stage_cap = n;
     return FS_OK;
   }
-  int commit() {
+  int commit(cudaStream_t s = nullptr) {
     if (stage_off == stage_done) return FS_OK;
+    // the side stream's kernels may still read staged arguments of an earlier
+    // lookahead: main-stream copies into the arena wait for them
+    if ((!s || s == st) && side_used)
+      if (int rc = cuda(cudaStreamWaitEvent(st, side_done, 0), "event")) return rc;
     const size_t lo = stage_done;
     stage_done = stage_off;
-    return cuda(cudaMemcpyAsync(d_stage + lo, h_stage + lo, stage_off - lo, cudaMemcpyHostToDevice, st),
+    return cuda(cudaMemcpyAsync(d_stage + lo, h_stage + lo, stage_off - lo, cudaMemcpyHostToDevice, s ? s : st),
                 "stage copy");
   }
   // after a host synchronisation every staged copy has run: reuse the arena
-  void stage_reset() { stage_off = stage_done = 0; }
+  void stage_reset() {
+    if (side_used) cudaEventSynchronize(side_copy);  // the side stream's staged copy ran too
+    stage_off = stage_done = 0;
+  }
 
-  int init(const fs_async_device* dev, int32_t n_clients) {
+  int init(const fs_async_device* dev, const fs_async_engine* e) {
+    const int32_t n_clients = e->N;
     d = *dev;
     st = (cudaStream_t)dev->stream;
     M = 0;
@@ -450,7 +490,80 @@ struct DeviceExec {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     if (int rc = cuda(cudaHostAlloc((void**)&h_res, 1 << 20, cudaHostAllocDefault), "pinned results")) return rc;
-    return stage_reserve(1 << 19);
+    if (int rc = stage_reserve(1 << 19)) return rc;
+    // lookahead plan slots
+    E = d.epochs;
+    C = e->C;
+    cid_of = e->cid;
+    perm_pre.resize(n_clients);
+    mask_pre.resize(n_clients);
+    for (int32_t i = 0; i < n_clients; ++i) {
+      const int64_t nr = n_rows[i], b = batch[i];
+      const int64_t spe = (nr + b - 1) / b;
+      perm_pre[i] = perm_sum;
+      mask_pre[i] = mask_sum;
+      perm_sum += (int64_t)E * nr;
+      if (d.dropout_rate > 0.0) mask_sum += (int64_t)E * spe * ((b * sum_hidden + 31) / 32);
+    }
+    gen_cycle.assign(2 * (size_t)n_clients, -1);
+    if (int rc = cuda(cudaMallocAsync((void**)&d_perm_all, 8 * (size_t)std::max<int64_t>(perm_sum, 1), st), "perm slots"))
+      return rc;
+    if (mask_sum > 0)
+      if (int rc = cuda(cudaMallocAsync((void**)&d_bits_all, 8 * (size_t)mask_sum, st), "mask slots")) return rc;
+    if (int rc = cuda(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream")) return rc;
+    if (int rc = cuda(cudaEventCreateWithFlags(&side_copy, cudaEventDisableTiming), "event")) return rc;
+    if (int rc = cuda(cudaEventCreateWithFlags(&side_done, cudaEventDisableTiming), "event")) return rc;
+    // the side stream may only touch the slots once they are allocated
+    if (int rc = cuda(cudaEventRecord(side_done, st), "event")) return rc;
+    if (int rc = cuda(cudaStreamWaitEvent(side, side_done, 0), "event")) return rc;
+    // cycle 0 of every client, in bulk, while the caller still prepares
+    std::vector<int32_t> all(n_clients), zero(n_clients, 0), slot(n_clients, 0);
+    for (int32_t i = 0; i < n_clients; ++i) all[i] = i;
+    if (C > 0)
+      if (int rc = generate(all.data(), zero.data(), slot.data(), n_clients, side)) return rc;
+    return FS_OK;
+  }
+
+  // K2 shuffles + K3 keep bits of (client ci[j], cycle cyc[j]) into slot par[j],
+  // on stream s (the main stream for misses, the side stream for lookahead)
+  int generate(const int32_t* ci, const int32_t* cyc, const int32_t* par, int32_t n, cudaStream_t s) {
+    if (n == 0 || E == 0) return FS_OK;
+    std::vector<uint64_t> seeds(n);
+    std::vector<int32_t> cid(n), i32(2 * (size_t)n);
+    std::vector<int64_t> i64(2 * (size_t)n);
+    int64_t max_rows = 1;
+    for (int32_t j = 0; j < n; ++j) cid[j] = cid_of[ci[j]];
+    fs_train_seeds_host(d.master_seed, cid.data(), cyc, n, seeds.data());
+    for (int32_t j = 0; j < n; ++j) {
+      i32[j] = n_rows[ci[j]];
+      i32[n + j] = batch[ci[j]];
+      i64[j] = perm_at(ci[j], par[j]);
+      i64[n + j] = mask_at(ci[j], par[j]);
+      max_rows = std::max<int64_t>(max_rows, n_rows[ci[j]]);
+      gen_cycle[2 * (size_t)ci[j] + par[j]] = cyc[j];
+    }
+    if (int rc = stage_reserve(16 * (size_t)n + 64 + 8 * (size_t)n * 3)) return rc;
+    const uint64_t p_seed = put(seeds.data(), 8 * (size_t)n);
+    const uint64_t p64 = put(i64.data(), 8 * i64.size());
+    const uint64_t p32 = put(i32.data(), 4 * i32.size());
+    if (int rc = commit(s)) return rc;
+    if (s == side) {
+      side_used = true;
+      if (int rc = cuda(cudaEventRecord(side_copy, side), "event")) return rc;
+    }
+    launches += 1;
+    if (int rc = fs_shuffle_perms((const uint64_t*)p_seed, (const int32_t*)p32, (const int64_t*)p64, n, E,
+                                  (int32_t)max_rows, d_perm_all, s))
+      return rc;
+    if (d.dropout_rate > 0.0) {
+      launches += 1;
+      if (int rc = fs_dropout_bits((const uint64_t*)p_seed, (const int32_t*)p32, (const int32_t*)(p32 + 4 * n),
+                                   (const int64_t*)(p64 + 8 * n), n, E, sum_hidden, 1.0 - d.dropout_rate,
+                                   d_bits_all, s))
+        return rc;
+    }
+    if (s == side) return cuda(cudaEventRecord(side_done, side), "event");
+    return FS_OK;
   }
 
   uint64_t prev_of(int32_t v) const {
@@ -496,6 +609,7 @@ struct DeviceExec {
 
   // one deferred flush: train + score every pending cycle, hand outcomes back
   int flush(fs_async_engine* e) {
+    const double t0 = now_s();
     if (int rc = launch_jobs(e)) return rc;
     const std::vector<int32_t> ids = e->unevaluated;
     const int32_t k = (int32_t)ids.size();
@@ -505,37 +619,50 @@ struct DeviceExec {
       const Deferred& q = e->deferred[ids[i]];
       ci[i] = q.ci; cyc[i] = q.cycle; ver[i] = q.version;
     }
-    // ---- TrainPlan (device.TrainPlan): offsets, seeds, LPT order
-    std::vector<int64_t> i64(4 * (size_t)k);
-    std::vector<int32_t> i32(5 * (size_t)k), cid(k);
-    std::vector<uint64_t> seeds(k), wst(k);
+    // ---- TrainPlan (device.TrainPlan): slots, offsets, LPT order
+    std::vector<int64_t> i64(3 * (size_t)k);
+    std::vector<int32_t> i32(5 * (size_t)k), slot(k);
+    std::vector<uint64_t> wst(k);
     std::vector<double> lr((size_t)k * std::max(E, 1));
-    int64_t perm_total = 0, mask_total = 0, max_rows = 1, max_b = 1;
+    int64_t max_b = 1;
     std::vector<int64_t> work(k);
-    for (int32_t i = 0; i < k; ++i) cid[i] = e->cid[ci[i]];
-    fs_train_seeds_host(d.master_seed, cid.data(), cyc.data(), k, seeds.data());
+    std::vector<int32_t> miss_ci, miss_cyc, miss_slot;
+    for (int32_t i = 0; i < k; ++i) {
+      const int32_t c = ci[i];
+      if (gen_cycle[2 * (size_t)c] == cyc[i]) slot[i] = 0;
+      else if (gen_cycle[2 * (size_t)c + 1] == cyc[i]) slot[i] = 1;
+      else {  // not generated ahead (first use after a skipped cycle): now, on the main stream
+        slot[i] = gen_cycle[2 * (size_t)c] < gen_cycle[2 * (size_t)c + 1] ? 0 : 1;
+        miss_ci.push_back(c);
+        miss_cyc.push_back(cyc[i]);
+        miss_slot.push_back(slot[i]);
+      }
+    }
+    if (side_used)  // lookahead of earlier flushes: ordered before this trainer (and any miss writes)
+      if (int rc = cuda(cudaStreamWaitEvent(st, side_done, 0), "event")) return rc;
+    if (!miss_ci.empty()) {
+      misses += (int64_t)miss_ci.size();
+      if (int rc = generate(miss_ci.data(), miss_cyc.data(), miss_slot.data(), (int32_t)miss_ci.size(), st))
+        return rc;
+    }
     for (int32_t i = 0; i < k; ++i) {
       const int64_t nr = n_rows[ci[i]], b = batch[ci[i]];
       const int64_t spe = (nr + b - 1) / b, total = (int64_t)E * spe;
       i64[i] = row_off[ci[i]];
-      i64[k + i] = perm_total;
-      i64[2 * k + i] = mask_total;
-      i64[3 * k + i] = (int64_t)seeds[i];
-      perm_total += (int64_t)E * nr;
-      if (d.dropout_rate > 0.0) mask_total += total * ((b * sum_hidden + 31) / 32);
+      i64[k + i] = perm_at(ci[i], slot[i]);
+      i64[2 * k + i] = mask_at(ci[i], slot[i]);
       i32[i] = (int32_t)nr;
       i32[k + i] = (int32_t)b;
       i32[2 * k + i] = 0;
       i32[3 * k + i] = (int32_t)total;
       work[i] = total * b;
-      max_rows = std::max(max_rows, nr);
       max_b = std::max(max_b, b);
       const int32_t r = std::min(cyc[i], e->rounds - 1);
       const double l = d.base_lr * std::pow(d.lr_decay, (double)r);  // lr_schedule (model.py:224-230)
       for (int32_t ep = 0; ep < std::max(E, 1); ++ep) lr[(size_t)i * std::max(E, 1) + ep] = l;
       wst[i] = version[ver[i]].first;
     }
-    std::vector<int32_t> order(k);
+    std::vector<int32_t> order(k);  // longest client first (LPT)
     for (int32_t i = 0; i < k; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
     for (int32_t i = 0; i < k; ++i) i32[4 * k + i] = order[i];
@@ -567,26 +694,10 @@ struct DeviceExec {
       palign = put(ap.data(), 8 * ap.size());
     }
     if (int rc = commit()) return rc;
-    // ---- K2 shuffles, K3 keep bits
-    if (int rc = grow(&d_perm, &perm_cap, 4 * (size_t)std::max<int64_t>(perm_total, 1), "perm")) return rc;
-    const uint64_t row_off_p = p64, perm_off_p = p64 + 8 * k, mask_off_p = p64 + 16 * k, seeds_p = p64 + 24 * k;
+    const uint64_t row_off_p = p64, perm_off_p = p64 + 8 * k, mask_off_p = p64 + 16 * k;
     const uint64_t n_rows_p = p32, batch_p = p32 + 4 * k, start_p = p32 + 8 * k, end_p = p32 + 12 * k,
                    order_p = p32 + 16 * k;
-    if (E > 0) {
-      launches += 1;
-      if (int rc = fs_shuffle_perms((const uint64_t*)seeds_p, (const int32_t*)n_rows_p, (const int64_t*)perm_off_p,
-                                    k, E, (int32_t)max_rows, (int32_t*)d_perm, st))
-        return rc;
-    }
     const bool masks = d.dropout_rate > 0.0 && E > 0;
-    if (masks) {
-      if (int rc = grow(&d_bits, &bits_cap, 4 * (size_t)std::max<int64_t>(mask_total, 1), "bits")) return rc;
-      launches += 1;
-      if (int rc = fs_dropout_bits((const uint64_t*)seeds_p, (const int32_t*)n_rows_p, (const int32_t*)batch_p,
-                                   (const int64_t*)mask_off_p, k, E, sum_hidden, 1.0 - d.dropout_rate,
-                                   (uint32_t*)d_bits, st))
-        return rc;
-    }
     // ---- K5
     if (int rc = grow((void**)&d_res, &res_cap, 8 * (size_t)(2 * k + 2), "results")) return rc;
     int32_t* status = (int32_t*)(d_res + k);
@@ -609,9 +720,9 @@ struct DeviceExec {
     t.w_start = (const uint64_t*)pws;
     t.w_out = (double*)wout;
     t.ldw = ldw;
-    t.perm = (const int32_t*)d_perm;
+    t.perm = (const int32_t*)d_perm_all;
     t.perm_off = (const int64_t*)perm_off_p;
-    t.mask_bits = masks ? (const uint32_t*)d_bits : nullptr;
+    t.mask_bits = masks ? (const uint32_t*)d_bits_all : nullptr;
     t.mask_off = (const int64_t*)mask_off_p;
     t.start_step = (const int32_t*)start_p;
     t.end_step = (const int32_t*)end_p;
@@ -629,6 +740,18 @@ struct DeviceExec {
     launches += 1;
     if (int rc = d.bf16 ? fs_train_bf16(&t, d.features, (const float*)d.labels, st) : fs_train_f64(&t, st))
       return rc;
+    // ---- lookahead: K2/K3 of every trained client's next cycle, on the side stream
+    {
+      std::vector<int32_t> nci, ncy, nsl;
+      for (int32_t i = 0; i < k; ++i)
+        if (cyc[i] + 1 < C) {
+          nci.push_back(ci[i]);
+          ncy.push_back(cyc[i] + 1);
+          nsl.push_back(1 - slot[i]);
+        }
+      if (!nci.empty())
+        if (int rc = generate(nci.data(), ncy.data(), nsl.data(), (int32_t)nci.size(), side)) return rc;
+    }
     // ---- K6
     if (ns) {
       launches += 1;
@@ -640,7 +763,11 @@ struct DeviceExec {
     if (int rc = cuda(cudaMemcpyAsync(h_res, d_res, 8 * (size_t)k + 4 * (size_t)k, cudaMemcpyDeviceToHost, st),
                       "results D2H"))
       return rc;
+    const double t1 = now_s();
     if (int rc = cuda(cudaStreamSynchronize(st), "flush")) return rc;
+    const double t2 = now_s();
+    t_prep += t1 - t0;
+    t_wait += t2 - t1;
     stage_reset();
     flushes += 1;
     const int32_t* h_status = (const int32_t*)(h_res + k);
@@ -677,6 +804,7 @@ struct DeviceExec {
       blocks[blk].ptr = nullptr;
     }
     e->provide(k, acc.data(), rel.data());
+    t_post += now_s() - t2;
     // every deferred cycle is trained: later ones fetch the newest version
     const int32_t latest = (int32_t)version.size() - 1;
     for (int32_t v = 0; v < latest - 1; ++v)
@@ -760,7 +888,7 @@ int fs_async_attach_device(fs_async_engine* e, const fs_async_device* dev) {
     return FS_EINVAL;
   }
   auto* x = new DeviceExec();
-  const int rc = x->init(dev, e->N);
+  const int rc = x->init(dev, e);
   if (rc) {
     delete x;
     return rc;
@@ -806,6 +934,9 @@ int fs_async_run(fs_async_engine* e, fs_async_yield* y) {
     y->launches = x->launches;
     y->diverged_client = x->div_client;
     y->diverged_cycle = x->div_cycle;
+    y->host_s[0] = x->t_prep;
+    y->host_s[1] = x->t_wait;
+    y->host_s[2] = x->t_post;
   }
   return rc;
 }

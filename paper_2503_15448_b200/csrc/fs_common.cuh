@@ -51,4 +51,12 @@ inline int make_layout(const int32_t* dims, int32_t n_dims, MlpLayout* out) {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
+// the attribute call costs microseconds of host time, paid per launch before.
+void ensure_smem_impl(const void* fn, int bytes);
+template <class K>
+inline void ensure_smem(K* kern, int bytes) {
+  ensure_smem_impl(reinterpret_cast<const void*>(kern), bytes);
+}
+
 }  // namespace fs

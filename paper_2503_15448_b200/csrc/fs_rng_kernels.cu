@@ -223,7 +223,7 @@ extern "C" int fs_shuffle_perms(const uint64_t* seeds, const int32_t* n_rows,
   const size_t smem = (size_t)max_rows * sizeof(int32_t);
   const int use_smem = smem <= 200 * 1024;
   if (use_smem && smem > 48 * 1024)
-    cudaFuncSetAttribute(shuffle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(shuffle_kernel, (int)smem);
   shuffle_kernel<<<n_req * epochs, 128, use_smem ? smem : 0, (cudaStream_t)stream>>>(
       seeds, n_rows, perm_off, epochs, perm_out, use_smem);
   return check_launch("shuffle_kernel");

@@ -395,7 +395,7 @@ static int launch_ordered_rows(const uint64_t* rows, int k, int64_t M, OUT* out,
     return FS_EINVAL;
   }
   auto kern = ordered_rows_kernel<T, MEAN, OUT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(kern, (int)smem);
   const int64_t strips = (M * (int64_t)sizeof(T) + AGG_STRIP - 1) / AGG_STRIP;
   kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out, nullptr, nullptr);
   return check_launch(what);
@@ -647,11 +647,11 @@ extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, i
   const dim3 grid((unsigned)strips, (unsigned)n_jobs);
   if (esz == 8) {
     auto kern = ordered_rows_kernel<double, true, double>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(kern, (int)smem);
     kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
   } else {
     auto kern = ordered_rows_kernel<float, true, float>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(kern, (int)smem);
     kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
   }
   return check_launch("ordered_rows_kernel (jobs)");

@@ -961,14 +961,14 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
   if (g.v2 && g_bf16_force_generic != 1) {
-    cudaFuncSetAttribute(train_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    ensure_smem(train_bf16_kernel<true>, (int)g.smem_bytes);
     train_bf16_kernel<true><<<grid, THREADS, g.smem_bytes, st>>>(a);
   } else {
     if (g.v2) {  // the generic kernel needs its over-read pad
       a.g.smem_bytes += 16 * 1024;
       g.smem_bytes += 16 * 1024;
     }
-    cudaFuncSetAttribute(train_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    ensure_smem(train_bf16_kernel<false>, (int)g.smem_bytes);
     train_bf16_kernel<false><<<grid, THREADS, g.smem_bytes, st>>>(a);
   }
   return check_launch("train_bf16_kernel");

@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
 
 int launch_eval(const Geo& g, const float* w, const void* xb, int n, double* probs, cudaStream_t st) {
   const uint32_t bytes = eval_lay(g).total;
-  cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  ensure_smem(eval_kernel, (int)bytes);
   const int chunks = (n + R - 1) / R;
   const int grid = chunks < kNumSMs ? chunks : kNumSMs;
   eval_kernel<<<grid, THREADS, bytes, st>>>(g, w, reinterpret_cast<const __nv_bfloat16*>(xb), n, probs);
@@ -944,7 +944,7 @@ int launch_eval(const Geo& g, const float* w, const void* xb, int n, double* pro
 
 int launch(const Args& a, int grid, cudaStream_t st) {
   const uint32_t bytes = lay_of(a.g).total;
-  cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  ensure_smem(train_kernel, (int)bytes);
   train_kernel<<<grid, THREADS, bytes, st>>>(a);
   return check_launch("bf16t::train_kernel");
 }

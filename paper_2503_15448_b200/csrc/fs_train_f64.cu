@@ -621,7 +621,7 @@ extern "C" int fs_train_f64(const fs_train_desc* d, void* stream) {
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   const size_t smem = train_smem_bytes(d->max_batch);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(train_kernel, (int)smem);
   train_kernel<<<train_grid(d), THREADS, smem, st>>>(a);
   return check_launch("train_kernel");
 }
@@ -654,7 +654,7 @@ extern "C" int fs_loss_and_grad_f64(const int32_t* dims, int32_t n_dims, const d
     return FS_EINVAL;
   }
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(grad_kernel, (int)smem);
   grad_kernel<<<1, THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("grad_kernel");
 }

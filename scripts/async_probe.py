@@ -25,3 +25,4 @@ torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 print(f"{prec}: {rounds} windows in {dt:.2f} s -> {rounds / dt:.3f} rounds/s, trainings {eng.trainings}, "
       f"flushes {eng.device_batches}, events {len(eng.timeline.log)}, digest {eng.timeline.digest()}")
+print("host s (prep, wait, post):", getattr(eng, "async_host_s", None))

@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples (SASS page) to CUDA source lines.
 
-usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-mangled-name> <lib.so> [top]
+usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-mangled-name> <lib.so> [top] [demangled substring]
 Needs -lineinfo builds; maps SASS offsets through nvdisasm --print-line-info.
 """
 import csv
@@ -17,11 +17,22 @@ top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr = rows[1]
-ix = {h: i for i, h in enumerate(hdr)}
+# one section per profiled kernel: ["Kernel Name", name], header, rows...
+# section filter: demangled-name substring (argv[5]); default the mangled name
+kname_plain = sys.argv[5] if len(sys.argv) > 5 else kname
 samples = []
-for r in rows[2:]:
-    if len(r) < len(hdr):
+take = False
+hdr = ix = None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        take = len(r) > 1 and kname_plain in r[1]
+        hdr = None
+        continue
+    if r and r[0] == "Address":
+        hdr = r
+        ix = {h: i for i, h in enumerate(hdr)}
+        continue
+    if not take or hdr is None or len(r) < len(hdr):
         continue
     samples.append((int(r[ix["Address"]], 16), int(r[ix["Warp Stall Sampling (All Samples)"]])))
 base = min(a for a, _ in samples)
