@@ -220,6 +220,15 @@ int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, voi
 int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k, int64_t M,
                       int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out, void* stream);
 
+/* filter_update on the device for a synchronous round (selection.py:77-85):
+ * accepted rows (aligned[i] / M >= theta; all rows when scored == 0) in
+ * client order -> rows_out, job_off = {0, k}, job_out[0] = out: the single
+ * job of fs_aggregate_jobs, so FedAvg follows K6 with no host round trip.
+ * Rows are base + i * stride_bytes.                                         */
+int fs_select_rows(const int64_t* aligned, int32_t n, int64_t M, double theta, int32_t scored, uint64_t base,
+                   int64_t stride_bytes, uint64_t* rows_out, int64_t* job_off, uint64_t* job_out, uint64_t out,
+                   void* stream);
+
 int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
                 void* stream);
 int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out, void* stream);

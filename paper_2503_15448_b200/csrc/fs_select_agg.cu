@@ -657,3 +657,56 @@ extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, i
   return check_launch("ordered_rows_kernel (jobs)");
 }
 
+// ---------------------------------------------------------------- selection on device
+// filter_update (selection.py:77-85) for a synchronous round without a host
+// round trip: accept[i] = aligned[i] / M >= theta (float64, inclusive), or
+// every client when the round is unscored (delta_sign without movement
+// history, server.py:283-284). The accepted rows (client order) become the
+// single job of fs_aggregate_jobs: rows_out[0..k), job_off = {0, k},
+// job_out[0] = out. One CTA, block-wide prefix sum.
+__global__ void __launch_bounds__(1024) select_rows_kernel(const int64_t* aligned, int n, int64_t M, double theta,
+                                                           int scored, uint64_t base, int64_t stride,
+                                                           uint64_t* rows_out, int64_t* job_off, uint64_t* job_out,
+                                                           uint64_t out) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < n; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const int acc = i < n && (!scored || (double)aligned[i] / (double)M >= theta);
+    const unsigned ball = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) warp_tot[warp] = __popc(ball);
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    before += __popc(ball & ((1u << lane) - 1u));
+    if (acc) rows_out[before] = base + (uint64_t)i * (uint64_t)stride;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
+      carry += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    job_off[0] = 0;
+    job_off[1] = carry;
+    job_out[0] = out;
+  }
+}
+
+extern "C" int fs_select_rows(const int64_t* aligned, int32_t n, int64_t M, double theta, int32_t scored,
+                              uint64_t base, int64_t stride_bytes, uint64_t* rows_out, int64_t* job_off,
+                              uint64_t* job_out, uint64_t out, void* stream) {
+  if (n < 0 || M < 1 || (scored && !aligned)) {
+    set_error("fs_select_rows: invalid arguments");
+    return FS_EINVAL;
+  }
+  select_rows_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(aligned, n, M, theta, scored, base, stride_bytes,
+                                                           rows_out, job_off, job_out, out);
+  return check_launch("select_rows_kernel");
+}
+
