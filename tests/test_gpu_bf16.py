@@ -93,7 +93,7 @@ def kernel_mode(request):
 
 
 @pytest.mark.parametrize("rows,dropout", [(64, 0.3), (37, 0.3), (64, 0.0), (150, 0.3)])
-@pytest.mark.parametrize("dims", [UNSW, (20, 128, 128, 64, 1)], ids=["unsw", "f1_128"])
+@pytest.mark.parametrize("dims", [UNSW, (20, 128, 128, 64, 1), (64, 256, 128, 64, 1)], ids=["unsw", "f1_128", "road"])
 def test_bf16_single_step_matches_fp32_emulation(rows, dropout, dims, kernel_mode):
     w0, got, want = _one_step(dims, rows, dropout)
     delta_w = want - w0

@@ -347,3 +347,28 @@ def test_async_engines_agree_bf16():
     assert out["device"][0] == out["native"][0] == out["python"][0]
     assert np.array_equal(out["device"][1], out["native"][1])
     assert np.array_equal(out["device"][1], out["python"][1])
+
+
+@pytest.mark.parametrize("mode", ["sync_filtered", "async_filtered"])
+def test_engine_matches_oracle_at_road_shape(mode):
+    """C3's shape (ROAD CAN windows: d = 64, 256 samples per client, b = 64,
+    delta_sign) in fp64 parity mode: digest and global model vs the oracle."""
+    from oracle.fl_oracle import OracleFederation
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    cfg = {"num_clients": 16, "rounds": 2, "epochs": 1, "mode": mode, "selection_mode": "delta_sign", "seed": 7,
+           "dataset": {"kind": "synthetic", "d": 64, "samples_per_client": 256, "anomaly_frac": 0.1,
+                       "separation": 2.0, "test_frac": 0.2},
+           "batch": {"policy": "fixed", "size": 64},
+           "profiles": {"speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
+                        "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
+                        "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}}}
+    world, init = build_world(ExperimentConfig.from_dict(cfg))
+    eng = FederationEngine(world)
+    st = eng.run(init)
+    sim = OracleFederation(world)
+    wg = sim.run(init.values)
+    assert eng.timeline.digest() == sim.digest()
+    assert rel_err(st.w_g.values, wg) < 1e-12
