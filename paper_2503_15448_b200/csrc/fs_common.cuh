@@ -51,6 +51,10 @@ inline int make_layout(const int32_t* dims, int32_t n_dims, MlpLayout* out) {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// wide-layer bf16 trainer (fs_train_wide.cu), reached through fs_train_bf16
+size_t wide_workspace_bytes(const fs_train_desc* d);
+int wide_train(const fs_train_desc* d, const void* features_bf16, const float* labels, cudaStream_t st);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
 // the attribute call costs microseconds of host time, paid per launch before.
 void ensure_smem_impl(const void* fn, int bytes);

@@ -879,9 +879,14 @@ extern "C" void fs_bf16_force_generic(int mode) { g_bf16_force_generic = mode; }
 // device buffer of 32 counters (nullptr disables).
 extern "C" void fs_bf16_set_profile(unsigned long long* counters) { g_bf16_prof = counters; }
 
+// 1 = on-chip tensor-core trainers, 2 = wide lockstep trainer (fs_train_wide.cu), 0 = neither
 extern "C" int fs_bf16_supported(const int32_t* dims, int32_t n_dims) {
   Geo g;
-  return make_geo(dims, n_dims, &g) == FS_OK ? 1 : 0;
+  if (make_geo(dims, n_dims, &g) == FS_OK) return 1;
+  MlpLayout lay;
+  if (n_dims >= 3 && n_dims <= FS_MAX_LAYERS + 1 && make_layout(dims, n_dims, &lay) == FS_OK && dims[0] <= 4096)
+    return 2;
+  return 0;
 }
 
 extern "C" int fs_prep_features_bf16(const double* x, const double* y, int64_t rows, int32_t d, int32_t dp,
@@ -910,7 +915,8 @@ extern "C" int fs_forward_bf16(const int32_t* dims, int32_t n_dims, const float*
 
 extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
   Geo g;
-  if (!d || make_geo(d->dims, d->n_dims, &g) != FS_OK || d->n_req < 1) return 0;
+  if (!d || d->n_req < 1) return 0;
+  if (make_geo(d->dims, d->n_dims, &g) != FS_OK) return fs_bf16_supported(d->dims, d->n_dims) == 2 ? wide_workspace_bytes(d) : 0;
   const int grid = d->grid > 0 ? d->grid : kNumSMs;
   const int gg = grid < d->n_req ? grid : d->n_req;
   return 256 + (size_t)gg * g.M * sizeof(float);
@@ -919,6 +925,8 @@ extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
 extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, const float* labels_f32,
                              void* stream) {
   Geo g;
+  if (d && make_geo(d->dims, d->n_dims, &g) != FS_OK && fs_bf16_supported(d->dims, d->n_dims) == 2)
+    return wide_train(d, features_bf16, labels_f32, (cudaStream_t)stream);
   if (!d || make_geo(d->dims, d->n_dims, &g) != FS_OK) {
     set_error("fs_train_bf16: unsupported layer dims for the tensor-core trainer");
     return FS_EINVAL;
