@@ -407,6 +407,52 @@ def measure_async(precision: str, windows: int = 2):
             "digest": eng.timeline.digest()}
 
 
+C5_SHARE = {
+    "num_clients": 1024, "rounds": 3, "epochs": 5, "mode": "sync_filtered", "selection_mode": "delta_sign",
+    "theta": 0.65, "seed": 1,
+    "dataset": {"kind": "synthetic", "n": 219176 // 8, "d": 42, "anomaly_frac": 0.3, "separation": 4.0,
+                "test_frac": 0.2},
+    "partition": {"alpha": 5.0},
+    "model": {"hidden_dims": [1024, 1024, 1024, 1024], "dropout_rate": 0.3},
+    "batch": {"policy": "fixed", "size": 64},
+    "profiles": C4_SYNC["profiles"],
+}
+
+
+def measure_c5_share(precision: str, rounds: int = 2):
+    """BASELINE configs[4] (WIDE MLP 42-1024x4-1, 8192 clients over 8 GPUs):
+    the 1024-client share one GPU owns, ~21 rows per client (data scaled 1/8),
+    sync_filtered rounds timed with CUDA events after one warm-up round."""
+    import torch
+
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine, GlobalState
+
+    world, init = build_world(ExperimentConfig.from_dict(C5_SHARE), precision=precision)
+    eng = FederationEngine(world)
+    st = eng.run_sync_round(GlobalState(round=0, w_g=init))
+    torch.cuda.synchronize()
+    D.Runtime.timer = D.KernelTimer()
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(rounds):
+        st = eng.run_sync_round(st)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ks, D.Runtime.timer = D.Runtime.timer.summary(), None
+    ms = a.elapsed_time(b) / rounds
+    tr = ks.get("train", {})
+    return {"workload": "C5 share: 1024 clients, WIDE MLP 42-1024x4-1 dropout 0.3, b=64, E=5, alpha=5, delta_sign",
+            "rounds_per_s": 1000.0 / ms, "client_updates_per_s": 1024 * 1000.0 / ms, "ms_per_round": ms,
+            "train_ms": tr.get("mean_ms"),
+            "train_tflops": (tr["work_per_launch"] / (tr["mean_ms"] * 1e-3) / 1e12) if tr else None,
+            "trainer": "fs_train_wide.cu (lockstep batched bf16 GEMMs + fused epilogues)" if precision == "bf16"
+            else "fp64 parity trainer"}
+
+
 def run_b200(args, rank: int, world_size: int) -> None:
     import torch
 
@@ -439,7 +485,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
     if args.precision == "bf16":
         peak, src = peaks.get("bf16_tflops", 1590.0), ("MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
                                                       else "B200_PROFILING.md fallback 1.59 PFLOP/s")
-        roofline = {"kernel": "fs::bf16::train_bf16_kernel (K5, tcgen05/TMEM)", "bound": "tensor"}
+        roofline = {"kernel": "fs::bf16t::train_kernel (K5 unit-major, tcgen05/TMEM)", "bound": "tensor"}
     else:
         peak, src = FP64_NOMINAL_TFLOPS, "nominal B200 FP64 37 TFLOP/s (no measured fp64 peak)"
         roofline = {"kernel": "fs::f64::train_kernel (K5, fp64 parity)", "bound": "fp64"}
@@ -455,14 +501,18 @@ def run_b200(args, rank: int, world_size: int) -> None:
             gbs = k["work_per_launch"] / (k["mean_ms"] * 1e-3) / 1e9
             kernels[name] = {"achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak, "mean_ms": k["mean_ms"],
                              "bytes_per_launch": k["work_per_launch"]}
-    c5 = None
+    c5 = c4_micro = None
     if not args.no_micro:
         c5 = hbm_microbench()
-        for v in c5.values():
+        c4_micro = hbm_microbench(52225, 1024, 400)
+        for v in list(c5.values()) + list(c4_micro.values()):
             v["frac_hbm"] = v["achieved_gbs"] / hbm_peak
     async_c4 = None
     if world_size == 1 and not args.no_async:
         async_c4 = measure_async(args.precision)
+    c5_share = None
+    if world_size == 1 and not args.no_c5:
+        c5_share = measure_c5_share(args.precision)
     cpu = None
     if world_size == 1 and not args.no_cpu:
         per_round, detail = oracle_round_sample(world, initial, args.cpu_sample)
@@ -487,10 +537,13 @@ def run_b200(args, rank: int, world_size: int) -> None:
                         "page-locked host memory into HBM every step (bf16 mode: the trainer's bf16 row format, "
                         "converted once at world build), w_g read back"},
         "roofline": roofline,
-        "hbm_kernels": kernels,
-        "hbm_kernels_c5": c5,
+        "hbm_kernels": {"c4_standalone": c4_micro, "c5_standalone": c5, "c4_in_round": kernels,
+                        "note": "standalone: each launch timed alone behind a 256 MiB read (cold, clean L2); "
+                                "in_round: CUDA events around the launch inside the timed rounds, where the "
+                                "next round's K2/K3 prefetch shares the SMs (overlap by design)"},
         "fp64_parity": parity,
         "async_c4": async_c4,
+        "c5_share_1gpu": c5_share,
         "cpu_baseline": cpu,
         "gpu_launches": int(m["abi_calls"]),
         "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (a CUB sort counts as one)",
@@ -519,6 +572,7 @@ def main() -> None:
     ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity-mode measurement")
     ap.add_argument("--no-micro", action="store_true", help="skip the C5-shape HBM microbenchmark")
     ap.add_argument("--no-async", action="store_true", help="skip the C4 async-engine measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5-share (WIDE MLP) measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
