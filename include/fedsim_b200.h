@@ -86,6 +86,13 @@ int fs_dropout_bits(const uint64_t* seeds, const int32_t* n_rows, const int32_t*
 
 /* Keep-bits of one stream: default_rng(SeedSequence(mask_seed)) drawing
  * n_draws doubles (model.dropout_masks).                                  */
+/* K3 overlapped with its own round's trainer: one CTA per (request, step),
+ * step-major in `order`, each step published by a release store of `tag`
+ * (non-zero, fresh per launch) into flags[r * max_steps + step].         */
+int fs_dropout_bits_flagged(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
+                            const int64_t* mask_off, const int32_t* order, int32_t n_req, int32_t epochs,
+                            int32_t max_steps, int32_t sum_hidden, double keep, uint32_t* bits_out, int32_t* flags,
+                            int32_t tag, void* stream);
 int fs_dropout_bits_seed(uint64_t mask_seed, int64_t n_draws, double keep, uint32_t* bits_out,
                          void* stream);
 
@@ -121,6 +128,12 @@ typedef struct fs_train_desc {
   void* workspace;
   size_t workspace_bytes;
   int32_t grid;                /* CTAs; 0 = auto                                */
+  /* bf16 unit-major trainer only: keep bits still being produced by
+   * fs_dropout_bits_flagged on another stream; step s of request r is read
+   * after mask_flags[r * max_steps + s] == mask_tag (NULL: bits complete)  */
+  const int32_t* mask_flags;
+  int32_t mask_tag;
+  int32_t max_steps;
 } fs_train_desc;
 
 size_t fs_train_workspace_bytes(const fs_train_desc* desc);

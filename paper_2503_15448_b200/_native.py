@@ -69,6 +69,9 @@ class TrainDesc(ctypes.Structure):
         ("workspace", _c_vp),
         ("workspace_bytes", _c_sz),
         ("grid", _c_i32),
+        ("mask_flags", _c_vp),
+        ("mask_tag", _c_i32),
+        ("max_steps", _c_i32),
     ]
 
 
@@ -81,6 +84,8 @@ _SIGNATURES = {
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),
     "fs_shuffle_perms": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_dropout_bits": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i32, _c_f64, _c_vp, _c_vp]),
+    "fs_dropout_bits_flagged": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i32, _c_i32,
+                                               _c_f64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_dropout_bits_seed": (ctypes.c_int, [_c_u64, _c_i64, _c_f64, _c_vp, _c_vp]),
     "fs_train_workspace_bytes": (_c_sz, [ctypes.POINTER(TrainDesc)]),
     "fs_train_f64": (ctypes.c_int, [ctypes.POINTER(TrainDesc), _c_vp]),

@@ -62,6 +62,8 @@ struct Args {
   const int32_t* order;
   int32_t* status;
   int* counter;
+  const int32_t* mask_flags;  // per (request, step) readiness of the keep bits (nullptr: complete)
+  int32_t mask_tag, max_steps;
   float* gacc;                // [grid x M] fp32 gradient accumulators (multi-chunk steps)
   unsigned long long* prof;   // optional [32] phase cycle counters (thread 0 of every CTA)
 };

@@ -86,12 +86,56 @@ __device__ __forceinline__ uint64_t xsl_rr(U128 s) {
 // at once as independent LCG chains: word w starts 32w steps after `base`,
 // reached with precomputed jumps (jt: 32t steps, j1: 32T steps, jr: from the
 // end of a word to the thread's word MASK_ILP*T further on).
+// One PCG64 step on 32-bit limbs: state = state * MULT + inc (mod 2^128),
+// the 128-bit additions as add.cc/addc carry chains (the C++ form spends its
+// ALU slots on compare-and-select carries; K3 is ALU-pipe bound).
+__device__ __forceinline__ void lcg128_step(uint64_t& hi, uint64_t& lo, uint64_t inc_hi, uint64_t inc_lo) {
+  constexpr uint64_t M_LO = 0x4385DF649FCCF645ull, M_HI = 0x2360ED051FC65DA4ull;
+  const uint64_t p_lo = lo * M_LO;
+  const uint64_t p_hi = __umul64hi(lo, M_LO) + lo * M_HI + hi * M_LO;
+  uint32_t r0, r1, r2, r3;
+  asm("add.cc.u32 %0, %4, %8;\n\t"
+      "addc.cc.u32 %1, %5, %9;\n\t"
+      "addc.cc.u32 %2, %6, %10;\n\t"
+      "addc.u32 %3, %7, %11;"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+      : "r"((uint32_t)p_lo), "r"((uint32_t)(p_lo >> 32)), "r"((uint32_t)p_hi), "r"((uint32_t)(p_hi >> 32)),
+        "r"((uint32_t)inc_lo), "r"((uint32_t)(inc_lo >> 32)), "r"((uint32_t)inc_hi), "r"((uint32_t)(inc_hi >> 32)));
+  lo = ((uint64_t)r1 << 32) | r0;
+  hi = ((uint64_t)r3 << 32) | r2;
+}
+
+// keep bit of the draw at the current state: XSL-RR output x, random() =
+// (x >> 11) * 2^-53 < keep  <=>  x < thresh << 11 (thresh < 2^53). The 64-bit
+// rotation is two 32-bit funnel shifts.
+__device__ __forceinline__ uint32_t keep_of(uint64_t hi, uint64_t lo, uint32_t t_hi, uint32_t t_lo) {
+  const uint64_t x = hi ^ lo;
+  const uint32_t rot = (uint32_t)(hi >> 58);
+  uint32_t a = (uint32_t)x, b = (uint32_t)(x >> 32);
+  if (rot & 32) {
+    const uint32_t t = a;
+    a = b;
+    b = t;
+  }
+  const uint32_t o_lo = __funnelshift_r(a, b, rot);
+  const uint32_t o_hi = __funnelshift_r(b, a, rot);
+  return (o_hi < t_hi || (o_hi == t_hi && o_lo < t_lo)) ? 1u : 0u;
+}
+
+// Packs keep-bits of one stream: bit j = (random_j < keep), with
+// random() = (x >> 11) * 2^-53 < keep  <=>  (x >> 11) < ceil(keep * 2^53)
+// (integer comparison, threshold computed exactly on host). Thread t owns
+// words t, t + T, t + 2T, ... (T = MASK_THREADS) and runs MASK_ILP of them
+// at once as independent LCG chains: word w starts 32w steps after `base`,
+// reached with precomputed jumps (jt: 32t steps, j1: 32T steps, jr: from the
+// end of a word to the thread's word MASK_ILP*T further on).
 __device__ void mask_stream(U128 base_state, U128 inc, int64_t n_draws, uint64_t thresh, uint32_t* out,
                             const LcgJump& jt, const LcgJump& j1, const LcgJump& jr) {
   const int64_t words = (n_draws + 31) / 32;
   const int t = threadIdx.x;
   if (t >= words) return;
-  const U128 mult = pcg_mult();
+  const uint64_t tq = thresh << 11;
+  const uint32_t t_hi = (uint32_t)(tq >> 32), t_lo = (uint32_t)tq;
   U128 s[MASK_ILP];
   s[0] = lcg_apply(jt, base_state, inc);
 #pragma unroll
@@ -104,8 +148,9 @@ __device__ void mask_stream(U128 base_state, U128 inc, int64_t n_draws, uint64_t
     for (int b = 0; b < 32; ++b) {
 #pragma unroll
       for (int u = 0; u < MASK_ILP; ++u) {
-        s[u] = u128_add(u128_mul(s[u], mult), inc);
-        bits[u] |= (uint32_t)((xsl_rr(s[u]) >> 11) < thresh) << b;
+        lcg128_step(s[u].hi, s[u].lo, inc.hi, inc.lo);
+        // shift in from the top: after 32 draws bit j holds draw j
+        bits[u] = __funnelshift_r(bits[u], keep_of(s[u].hi, s[u].lo, t_hi, t_lo), 1);
       }
     }
 #pragma unroll
@@ -166,6 +211,45 @@ __global__ void __launch_bounds__(MASK_THREADS)
   const Pcg64 g = pcg_from_seed(mask_seed);
   mask_stream(g.state, g.inc, n_draws, thresh, bits, lcg_jump(32ull * threadIdx.x), lcg_jump(32ull * MASK_THREADS),
               lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32));
+}
+
+// K3, flagged: the keep bits of one (request, step) per CTA, dispatched
+// step-major in the trainer's client order (block b -> step b / n, client
+// order[b % n]), each step published with a release store of `tag` into
+// flags[r * max_steps + step]. The trainer of the same round runs
+// concurrently and waits per step on the flag (fs_train_desc.mask_flags), so
+// the mask generation overlaps its own round's trainer instead of the
+// previous round's tail. Per-thread LCG jumps come from constant memory.
+__constant__ LcgJump c_jt[MASK_THREADS];
+__constant__ LcgJump c_j1, c_jr;
+
+__global__ void __launch_bounds__(MASK_THREADS)
+    dropout_bits_step_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
+                             const int64_t* mask_off, const int32_t* order, int n_req, int epochs, int max_steps,
+                             int sum_hidden, uint64_t thresh, uint32_t* bits, int32_t* flags, int32_t tag) {
+  __shared__ U128 sh_state, sh_inc;
+  const int b = blockIdx.x;
+  const int st = b / n_req;
+  const int r = order[b % n_req];
+  const int n = n_rows[r], B = batch[r];
+  const int spe = (n + B - 1) / B;
+  if (st >= epochs * spe) return;
+  if (threadIdx.x == 0) {
+    const Pcg64 g = pcg_from_seed(derive_mask_seed(seeds[r], (uint32_t)(st / spe), (uint32_t)(st % spe)));
+    sh_state = g.state;
+    sh_inc = g.inc;
+  }
+  __syncthreads();
+  const int64_t slot = ((int64_t)B * sum_hidden + 31) / 32;
+  const int rows = min(B, n - (st % spe) * B);
+  mask_stream(sh_state, sh_inc, (int64_t)rows * sum_hidden, thresh, bits + mask_off[r] + (int64_t)st * slot,
+              c_jt[threadIdx.x], c_j1, c_jr);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + (int64_t)r * max_steps + st), "r"(tag)
+                 : "memory");
+  }
 }
 
 // ceil(keep * 2^53): keep-bit threshold on the 53-bit integer behind random()
@@ -254,3 +338,34 @@ extern "C" int fs_dropout_bits_seed(uint64_t mask_seed, int64_t n_draws, double 
                                                                          keep_threshold(keep), bits_out);
   return check_launch("dropout_bits_seed_kernel");
 }
+
+extern "C" int fs_dropout_bits_flagged(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
+                                       const int64_t* mask_off, const int32_t* order, int32_t n_req, int32_t epochs,
+                                       int32_t max_steps, int32_t sum_hidden, double keep, uint32_t* bits_out,
+                                       int32_t* flags, int32_t tag, void* stream) {
+  if (n_req < 0 || epochs < 0 || sum_hidden < 1 || max_steps < 0 || !flags || tag == 0) {
+    set_error("fs_dropout_bits_flagged: invalid arguments");
+    return FS_EINVAL;
+  }
+  if (n_req == 0 || epochs == 0 || max_steps == 0) return FS_OK;
+  static bool jumps_ready = false;  // per-thread LCG jump constants (stream independent)
+  if (!jumps_ready) {
+    LcgJump jt[MASK_THREADS];
+    for (int t = 0; t < MASK_THREADS; ++t) jt[t] = lcg_jump(32ull * t);
+    const LcgJump j1 = lcg_jump(32ull * MASK_THREADS), jr = lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32);
+    if (cudaMemcpyToSymbol(c_jt, jt, sizeof(jt)) != cudaSuccess || cudaMemcpyToSymbol(c_j1, &j1, sizeof(j1)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_jr, &jr, sizeof(jr)) != cudaSuccess)
+      return check_launch("fs_dropout_bits_flagged: jump table");
+    jumps_ready = true;
+  }
+  const int64_t blocks = (int64_t)n_req * max_steps;
+  if (blocks > 0x7FFFFFFF) {
+    set_error("fs_dropout_bits_flagged: too many (request, step) blocks");
+    return FS_EINVAL;
+  }
+  dropout_bits_step_kernel<<<(unsigned)blocks, MASK_THREADS, 0, (cudaStream_t)stream>>>(
+      seeds, n_rows, batch, mask_off, order, n_req, epochs, max_steps, sum_hidden, keep_threshold(keep), bits_out,
+      flags, tag);
+  return check_launch("dropout_bits_step_kernel");
+}
+

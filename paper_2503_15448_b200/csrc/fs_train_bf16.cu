@@ -964,10 +964,17 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.counter = reinterpret_cast<int*>(d->workspace);
   a.gacc = reinterpret_cast<float*>(reinterpret_cast<char*>(d->workspace) + 256);
   a.prof = g_bf16_prof;
+  a.mask_flags = d->mask_mode == FS_MASK_BITS ? d->mask_flags : nullptr;
+  a.mask_tag = d->mask_tag;
+  a.max_steps = d->max_steps;
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
+  if (a.mask_flags) {
+    set_error("fs_train_bf16: flagged keep bits need the unit-major kernel's layer shapes");
+    return FS_EINVAL;
+  }
   if (g.v2 && g_bf16_force_generic != 1) {
     ensure_smem(train_bf16_kernel<true>, (int)g.smem_bytes);
     train_bf16_kernel<true><<<grid, THREADS, g.smem_bytes, st>>>(a);

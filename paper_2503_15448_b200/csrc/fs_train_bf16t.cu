@@ -119,12 +119,27 @@ __device__ __forceinline__ uint32_t rows_valid(int rows, int rb) {
   return k >= 32 ? 0xFFFFFFFFu : (k > 0 ? (1u << k) - 1u : 0u);
 }
 
-// Read-only load pinned where it is written (volatile: the compiler may not
-// sink it towards its use, which would expose the latency it is meant to hide).
+// Load pinned where it is written (volatile: the compiler may not sink it
+// towards its use, which would expose the latency it is meant to hide).
+// L2-coherent (.cg): with flagged keep bits the words of a later step may be
+// written by the concurrent K3 after an earlier step's read cached the line.
 __device__ __forceinline__ uint32_t ldg_early(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
+}
+
+// Wait until K3 has published the keep bits of (request, step).
+__device__ __forceinline__ void wait_mask_step(const int32_t* flag, int32_t tag) {
+  if (!flag) return;
+  int32_t v;
+  uint32_t spins = 0;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v == tag) break;
+    __nanosleep(128);
+    if (++spins > (1u << 24)) __trap();  // a missing producer must not hang the GPU
+  }
 }
 
 // Raw keep-bit words of this warp's four forward items (F0 block 0, F0
@@ -420,7 +435,10 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         FS_PROF(28);
         const int hh_w = warp >> 2;  // row half of this warp's forward items
         uint32_t kw[4];
-        if (!have_next) mask_issue(mrn, mbits, step_rows, row0, rows, f1, f2, f3, MB, q, hh_w, lane);
+        if (!have_next) {
+          if (mbits && a.mask_flags) wait_mask_step(a.mask_flags + (int64_t)rq * a.max_steps + step, a.mask_tag);
+          mask_issue(mrn, mbits, step_rows, row0, rows, f1, f2, f3, MB, q, hh_w, lane);
+        }
         mask_finish(mrn, mbits != nullptr, step_rows, rows, f1, f2, f3, MB, q, hh_w, lane, kw);
         FS_PROF(29);
         have_next = false;
@@ -555,6 +573,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           const int ns = nstep % spe;
           const int nsr = min(B, n - ns * B);
           const int nr0 = nch * R;
+          if (mask_c && a.mask_flags && nch == 0)
+            wait_mask_step(a.mask_flags + (int64_t)rq * a.max_steps + nstep, a.mask_tag);
           mask_issue(mrn, mask_c ? mask_c + (int64_t)nstep * slot_words : nullptr, nsr, nr0, min(R, nsr - nr0), f1,
                      f2, f3, MB, q, warp >> 2, lane);
         }

@@ -321,10 +321,12 @@ class TrainPlan:
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
                  dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
-                 pool: dict | None = None, stage: "Stage | None" = None):
+                 pool: dict | None = None, stage: "Stage | None" = None, defer_masks: bool = False):
         rt = rt or Runtime.get()
         self.rt = rt
         self.stage = stage
+        self.mask_flags = None   # set when K3 runs later, concurrently with the trainer (launch_masks)
+        self.mask_tag = 0
         lib = rt.lib
         self.dims = tuple(int(x) for x in spec_dims)
         self.shards = shards
@@ -391,14 +393,39 @@ class TrainPlan:
             rt.call(lib.fs_shuffle_perms(self.seeds_p, self.n_rows_p, self.perm_off_p, n, self.epochs,
                                          int(n_rows.max()), self.perm.data_ptr(), s_handle), "fs_shuffle_perms")
         self.scale = 1.0
+        self.max_steps = int(end.max()) if n else 0
+        self.sum_hidden = sum_hidden
         if self.bits is not None:
             keep = 1.0 - self.dropout_rate
             self.scale = 1.0 / keep
-            rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n, self.epochs,
-                                        sum_hidden, keep, self.bits.data_ptr(), s_handle), "fs_dropout_bits")
+            if defer_masks:
+                # K3 is launched with the trainer (launch_masks); steps are
+                # published through per-(request, step) flags
+                flags = pool.get("flags") if pool is not None else None
+                need = n * self.max_steps
+                if flags is None or flags.numel() < need:
+                    flags = torch.zeros(int(need * 1.25) + 1, dtype=torch.int32, device=rt.device)
+                    if pool is not None:
+                        pool["flags"] = flags
+                self.mask_flags = flags
+            else:
+                rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n,
+                                            self.epochs, sum_hidden, keep, self.bits.data_ptr(), s_handle),
+                        "fs_dropout_bits")
         if stream is not None:  # consumer stream waits on this event before the trainer reads the plan
             self.ready = torch.cuda.Event()
             self.ready.record(torch_stream)
+
+    def launch_masks(self, stream, tag: int) -> None:
+        """K3 for a deferred-mask plan on `stream`, concurrent with the trainer
+        that consumes it step by step (fs_dropout_bits_flagged)."""
+        if self.mask_flags is None:
+            return
+        self.mask_tag = int(tag)
+        self.rt.call(self.rt.lib.fs_dropout_bits_flagged(
+            self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, self.order_p, self.n, self.epochs,
+            self.max_steps, self.sum_hidden, 1.0 - self.dropout_rate, self.bits.data_ptr(),
+            self.mask_flags.data_ptr(), self.mask_tag, stream.cuda_stream), "fs_dropout_bits_flagged")
 
     def matches(self, clients, seeds, batch, epochs) -> bool:
         return (self.epochs == epochs and np.array_equal(self.clients, clients)
@@ -475,6 +502,12 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.order = plan.order_p
     desc.status = status.data_ptr()
     desc.grid = TRAIN_GRID
+    if plan.mask_flags is not None:
+        if not plan.mask_tag:
+            raise ValueError("deferred keep bits: launch_masks() must run before the trainer")
+        desc.mask_flags = plan.mask_flags.data_ptr()
+        desc.mask_tag = plan.mask_tag
+        desc.max_steps = plan.max_steps
     need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
     if need == 0:
         raise ValueError(f"layer dims {dims} are not supported by the {precision} trainer")
