@@ -134,7 +134,23 @@ typedef struct fs_train_desc {
   const int32_t* mask_flags;
   int32_t mask_tag;
   int32_t max_steps;
+  /* bf16 unit-major trainer only: per-client completion records. When
+   * done != NULL, each client's CTA counts the sign alignment of its trained
+   * row against (w_start[r], w_prev[r]) (align_mode FS_ALIGN_*, -1 = none)
+   * and then publishes {aligned, status, tag = done_tag} to the
+   * fs_client_done record at done[r] (typically mapped host memory), so a
+   * host can consume clients as they finish instead of the whole launch.  */
+  const uint64_t* done;
+  const uint64_t* w_prev;
+  int32_t align_mode;
+  int32_t done_tag;
 } fs_train_desc;
+
+typedef struct {
+  int64_t aligned;
+  int32_t status;
+  volatile int32_t tag;
+} fs_client_done;
 
 size_t fs_train_workspace_bytes(const fs_train_desc* desc);
 int fs_train_f64(const fs_train_desc* desc, void* stream);

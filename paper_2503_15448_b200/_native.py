@@ -72,6 +72,10 @@ class TrainDesc(ctypes.Structure):
         ("mask_flags", _c_vp),
         ("mask_tag", _c_i32),
         ("max_steps", _c_i32),
+        ("done", _c_vp),
+        ("w_prev", _c_vp),
+        ("align_mode", _c_i32),
+        ("done_tag", _c_i32),
     ]
 
 

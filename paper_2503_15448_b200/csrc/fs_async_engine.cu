@@ -20,7 +20,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <queue>
 #include <vector>
@@ -368,6 +370,28 @@ struct DeviceExec {
   std::vector<int32_t> gen_cycle;            // [client][slot] cycle held (-1 none)
   std::vector<int32_t> cid_of;
   int64_t misses = 0;
+  // ---- per-client completion mode (bf16 unit-major trainer): every flush
+  // launches its new cycles as one trainer kernel on a stream of its own; a
+  // client's CTA publishes {aligned, status} to a mapped host record the
+  // moment its row is written, and the event loop waits only for the cycle it
+  // needs, not for the launch's longest client.
+  bool percycle = false;
+  static constexpr int kRecChunk = 1 << 16;
+  std::vector<fs_client_done*> rec_host;      // chunks of mapped records, by deferred id
+  std::vector<uint64_t> rec_dev;
+  std::vector<uint8_t> launched;
+  std::vector<int32_t> vref;                  // launched-not-collected cycles reading a version
+  struct Batch {
+    cudaStream_t s;
+    std::vector<int32_t> ids;
+    int32_t left;
+  };
+  std::vector<Batch> inflight;
+  std::vector<cudaStream_t> stream_pool;
+  size_t next_stream = 0;
+  std::vector<std::pair<void*, cudaEvent_t>> deferred_free;  // freed once the event completes
+  int32_t low_version = 0;                    // versions below are released
+  double t_poll = 0;
   int64_t perm_at(int32_t ci, int32_t p) const { return p * perm_sum + perm_pre[ci]; }
   int64_t mask_at(int32_t ci, int32_t p) const { return p * mask_sum + mask_pre[ci]; }
   static double now_s() {
@@ -375,6 +399,16 @@ struct DeviceExec {
   }
 
   ~DeviceExec() {
+    for (cudaStream_t ps : stream_pool) {
+      cudaStreamSynchronize(ps);
+      cudaStreamDestroy(ps);
+    }
+    for (auto& f : deferred_free) {
+      cudaEventSynchronize(f.second);
+      cudaFree(f.first);
+      cudaEventDestroy(f.second);
+    }
+    for (auto* h : rec_host) cudaFreeHost(h);
     for (auto& b : blocks)
       if (b.ptr) cudaFreeAsync(b.ptr, st);
     if (d_perm) cudaFreeAsync(d_perm, st);
@@ -516,6 +550,13 @@ struct DeviceExec {
     // the side stream may only touch the slots once they are allocated
     if (int rc = cuda(cudaEventRecord(side_done, st), "event")) return rc;
     if (int rc = cuda(cudaStreamWaitEvent(side, side_done, 0), "event")) return rc;
+    percycle = d.bf16 && d.n_dims == 5 && (d.dims[1] == 128 || d.dims[1] == 256) && d.dims[2] == 128 &&
+               d.dims[3] == 64 && d.dims[0] <= 64 && !getenv("FS_ASYNC_BATCH_WAIT");
+    if (percycle) {
+      stream_pool.resize(8);
+      for (auto& ps : stream_pool)
+        if (int rc = cuda(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "pool stream")) return rc;
+    }
     // cycle 0 of every client, in bulk, while the caller still prepares
     std::vector<int32_t> all(n_clients), zero(n_clients, 0), slot(n_clients, 0);
     for (int32_t i = 0; i < n_clients; ++i) all[i] = i;
@@ -542,14 +583,30 @@ struct DeviceExec {
       max_rows = std::max<int64_t>(max_rows, n_rows[ci[j]]);
       gen_cycle[2 * (size_t)ci[j] + par[j]] = cyc[j];
     }
-    if (int rc = stage_reserve(16 * (size_t)n + 64 + 8 * (size_t)n * 3)) return rc;
-    const uint64_t p_seed = put(seeds.data(), 8 * (size_t)n);
-    const uint64_t p64 = put(i64.data(), 8 * i64.size());
-    const uint64_t p32 = put(i32.data(), 4 * i32.size());
-    if (int rc = commit(s)) return rc;
-    if (s == side) {
-      side_used = true;
-      if (int rc = cuda(cudaEventRecord(side_copy, side), "event")) return rc;
+    uint64_t p_seed, p64, p32;
+    void* tmp = nullptr;
+    if (percycle) {  // no per-flush host sync in this mode: a stream-ordered temporary
+      const size_t b_seed = 8 * (size_t)n, b64 = 8 * i64.size(), b32 = 4 * i32.size();
+      std::vector<uint8_t> h(b_seed + b64 + b32);
+      memcpy(h.data(), seeds.data(), b_seed);
+      memcpy(h.data() + b_seed, i64.data(), b64);
+      memcpy(h.data() + b_seed + b64, i32.data(), b32);
+      if (int rc = cuda(cudaMallocAsync(&tmp, h.size(), s), "plan args")) return rc;
+      if (int rc = cuda(cudaMemcpyAsync(tmp, h.data(), h.size(), cudaMemcpyHostToDevice, s), "plan args")) return rc;
+      p_seed = (uint64_t)tmp;
+      p64 = p_seed + b_seed;
+      p32 = p64 + b64;
+      if (s == side) side_used = true;
+    } else {
+      if (int rc = stage_reserve(16 * (size_t)n + 64 + 8 * (size_t)n * 3)) return rc;
+      p_seed = put(seeds.data(), 8 * (size_t)n);
+      p64 = put(i64.data(), 8 * i64.size());
+      p32 = put(i32.data(), 4 * i32.size());
+      if (int rc = commit(s)) return rc;
+      if (s == side) {
+        side_used = true;
+        if (int rc = cuda(cudaEventRecord(side_copy, side), "event")) return rc;
+      }
     }
     launches += 1;
     if (int rc = fs_shuffle_perms((const uint64_t*)p_seed, (const int32_t*)p32, (const int64_t*)p64, n, E,
@@ -562,6 +619,7 @@ struct DeviceExec {
                                    d_bits_all, s))
         return rc;
     }
+    if (tmp) cudaFreeAsync(tmp, s);
     if (s == side) return cuda(cudaEventRecord(side_done, side), "event");
     return FS_OK;
   }
@@ -590,17 +648,36 @@ struct DeviceExec {
       }
       version.push_back({outs[j], blk});
     }
-    if (int rc = stage_reserve(16 * (size_t)(2 * nrows + 2 * nj + 8))) return rc;
-    const uint64_t p_rows = put(rows.data(), 8 * nrows);
-    const uint64_t p_off = put(e->job_off.data(), 8 * (nj + 1));
-    const uint64_t p_out = put(outs.data(), 8 * nj);
-    if (int rc = commit()) return rc;
+    uint64_t p_rows, p_off, p_out;
+    void* tmp = nullptr;
+    if (percycle) {  // no per-flush host sync in this mode: a stream-ordered temporary
+      std::vector<uint64_t> h(nrows + nj + 1 + nj);
+      memcpy(h.data(), rows.data(), 8 * nrows);
+      memcpy(h.data() + nrows, e->job_off.data(), 8 * (nj + 1));
+      memcpy(h.data() + nrows + nj + 1, outs.data(), 8 * nj);
+      if (int rc = cuda(cudaMallocAsync(&tmp, 8 * h.size(), st), "jobs args")) return rc;
+      if (int rc = cuda(cudaMemcpyAsync(tmp, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st), "jobs args"))
+        return rc;
+      p_rows = (uint64_t)tmp;
+      p_off = p_rows + 8 * nrows;
+      p_out = p_off + 8 * (nj + 1);
+    } else {
+      if (int rc = stage_reserve(16 * (size_t)(2 * nrows + 2 * nj + 8))) return rc;
+      p_rows = put(rows.data(), 8 * nrows);
+      p_off = put(e->job_off.data(), 8 * (nj + 1));
+      p_out = put(outs.data(), 8 * nj);
+      if (int rc = commit()) return rc;
+    }
     if (int rc = grow(&d_sorted, &sorted_cap, 8 * nrows, "sorted rows")) return rc;
     launches += 1;
     if (int rc = fs_aggregate_jobs((const uint64_t*)p_rows, (const int64_t*)p_off, nj, max_k, M, (int32_t)esz,
                                    (uint64_t*)d_sorted, (const uint64_t*)p_out, st))
       return rc;
-    for (int64_t i = 0; i < nrows; ++i) unref(row_block[e->job_member[i]]);
+    if (tmp) cudaFreeAsync(tmp, st);
+    for (int64_t i = 0; i < nrows; ++i) {
+      if (percycle) drop_row(e->job_member[i]);
+      else unref(row_block[e->job_member[i]]);
+    }
     e->job_version.clear();
     e->job_member.clear();
     e->job_off.assign(1, 0);
@@ -814,6 +891,329 @@ struct DeviceExec {
       }
     return FS_OK;
   }
+
+  // ================================================================ per-client completion mode
+  fs_client_done* rec(int32_t id, uint64_t* dev_addr) {
+    const size_t c = (size_t)id / kRecChunk, o = (size_t)id % kRecChunk;
+    while (rec_host.size() <= c) {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, sizeof(fs_client_done) * kRecChunk, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+      memset(h, 0, sizeof(fs_client_done) * kRecChunk);
+      void* dv = nullptr;
+      cudaHostGetDevicePointer(&dv, h, 0);
+      rec_host.push_back((fs_client_done*)h);
+      rec_dev.push_back((uint64_t)dv);
+    }
+    if (dev_addr) *dev_addr = rec_dev[c] + o * sizeof(fs_client_done);
+    return rec_host[c] + o;
+  }
+
+  void free_after(void* p, cudaStream_t s) {  // device memory read by work queued on s
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s);
+    deferred_free.push_back({p, ev});
+  }
+  void reap() {
+    size_t w = 0;
+    for (size_t i = 0; i < deferred_free.size(); ++i) {
+      if (cudaEventQuery(deferred_free[i].second) == cudaSuccess) {
+        cudaFreeAsync(deferred_free[i].first, st);
+        cudaEventDestroy(deferred_free[i].second);
+      } else {
+        deferred_free[w++] = deferred_free[i];
+      }
+    }
+    deferred_free.resize(w);
+  }
+
+  // free model versions no launched cycle reads and no later cycle can fetch
+  void release_versions(const fs_async_engine* e) {
+    const int32_t latest = (int32_t)version.size() - 1;
+    if ((int32_t)vref.size() < latest + 1) vref.resize(latest + 1, 0);
+    // every deferred cycle not collected yet (launched or not) reads its
+    // fetched version and the one before it
+    int32_t keep = latest - 1;
+    for (int32_t id : e->unevaluated) keep = std::min(keep, std::max(e->deferred[id].version - 1, 0));
+    while (low_version < keep && vref[low_version] == 0) {
+      if (version[low_version].second >= 0) {
+        unref(version[low_version].second);
+        version[low_version].second = -2;
+      }
+      ++low_version;
+    }
+  }
+
+  // one trainer launch for every pending cycle not launched yet, on its own stream
+  int launch_batch(fs_async_engine* e) {
+    if ((int64_t)launched.size() < (int64_t)e->deferred.size()) {
+      const size_t n = e->deferred.size() * 2 + 16;
+      row_ptr.resize(n, 0);
+      row_block.resize(n, -1);
+      launched.resize(n, 0);
+    }
+    std::vector<int32_t> ids;
+    for (int32_t id : e->unevaluated)
+      if (!launched[id]) ids.push_back(id);
+    const int32_t k = (int32_t)ids.size();
+    if (k == 0) return FS_OK;
+    // an idle stream, so this launch never queues behind an older long one
+    cudaStream_t bs = nullptr;
+    for (size_t q = 0; q < stream_pool.size() && !bs; ++q) {
+      cudaStream_t cand = stream_pool[(next_stream + q) % stream_pool.size()];
+      if (cudaStreamQuery(cand) == cudaSuccess) bs = cand;
+    }
+    if (!bs) {
+      if (stream_pool.size() < 64) {
+        if (int rc = cuda(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking), "pool stream")) return rc;
+        stream_pool.push_back(bs);
+      } else {
+        bs = stream_pool[next_stream % stream_pool.size()];
+      }
+    }
+    ++next_stream;
+    std::vector<int32_t> ci(k), cyc(k), ver(k), slot(k);
+    for (int32_t i = 0; i < k; ++i) {
+      const Deferred& q = e->deferred[ids[i]];
+      ci[i] = q.ci; cyc[i] = q.cycle; ver[i] = q.version;
+    }
+    // K2/K3 slots (lookahead on the side stream, misses generated on the batch stream)
+    std::vector<int32_t> miss_ci, miss_cyc, miss_slot;
+    for (int32_t i = 0; i < k; ++i) {
+      const int32_t c = ci[i];
+      if (gen_cycle[2 * (size_t)c] == cyc[i]) slot[i] = 0;
+      else if (gen_cycle[2 * (size_t)c + 1] == cyc[i]) slot[i] = 1;
+      else {
+        slot[i] = gen_cycle[2 * (size_t)c] < gen_cycle[2 * (size_t)c + 1] ? 0 : 1;
+        miss_ci.push_back(c); miss_cyc.push_back(cyc[i]); miss_slot.push_back(slot[i]);
+      }
+    }
+    if (side_used)
+      if (int rc = cuda(cudaStreamWaitEvent(bs, side_done, 0), "event")) return rc;
+    // versions written by aggregation jobs on the main stream
+    cudaEvent_t main_ev;
+    cudaEventCreateWithFlags(&main_ev, cudaEventDisableTiming);
+    cudaEventRecord(main_ev, st);
+    cudaStreamWaitEvent(bs, main_ev, 0);
+    cudaEventDestroy(main_ev);
+    if (!miss_ci.empty()) {
+      misses += (int64_t)miss_ci.size();
+      // generate() stages through the shared arena; copies go on the batch stream
+      if (int rc = generate(miss_ci.data(), miss_cyc.data(), miss_slot.data(), (int32_t)miss_ci.size(), bs))
+        return rc;
+    }
+    const int32_t E = d.epochs;
+    const int32_t EL = std::max(E, 1);
+    std::vector<int64_t> i64(3 * (size_t)k);
+    std::vector<int32_t> i32(5 * (size_t)k);
+    std::vector<double> lr((size_t)k * EL);
+    std::vector<uint64_t> wst(k), wpv(k), dn(k);
+    std::vector<int64_t> work(k);
+    int64_t max_b = 1;
+    for (int32_t i = 0; i < k; ++i) {
+      const int64_t nr = n_rows[ci[i]], b = batch[ci[i]];
+      const int64_t spe = (nr + b - 1) / b, total = (int64_t)E * spe;
+      i64[i] = row_off[ci[i]];
+      i64[k + i] = perm_at(ci[i], slot[i]);
+      i64[2 * k + i] = mask_at(ci[i], slot[i]);
+      i32[i] = (int32_t)nr;
+      i32[k + i] = (int32_t)b;
+      i32[2 * k + i] = 0;
+      i32[3 * k + i] = (int32_t)total;
+      work[i] = total * b;
+      max_b = std::max(max_b, b);
+      const int32_t r = std::min(cyc[i], e->rounds - 1);
+      const double l = d.base_lr * std::pow(d.lr_decay, (double)r);  // lr_schedule (model.py:224-230)
+      for (int32_t ep = 0; ep < EL; ++ep) lr[(size_t)i * EL + ep] = l;
+      wst[i] = version[ver[i]].first;
+      wpv[i] = prev_of(ver[i]);
+      if (!rec(ids[i], &dn[i])) return cuda(cudaErrorMemoryAllocation, "completion records");
+      if ((int32_t)vref.size() <= ver[i]) vref.resize(ver[i] + 1, 0);
+      vref[ver[i]] += 1;
+      if (ver[i] > 0) vref[ver[i] - 1] += 1;
+    }
+    std::vector<int32_t> order(k);
+    for (int32_t i = 0; i < k; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+    for (int32_t i = 0; i < k; ++i) i32[4 * k + i] = order[i];
+    // one stream-ordered allocation: metadata | trainer workspace | rows
+    const size_t meta = ((8 * i64.size() + 4 * i32.size() + 8 * lr.size() + 8 * 3 * (size_t)k) + 255) / 256 * 256;
+    fs_train_desc t;
+    memset(&t, 0, sizeof(t));
+    t.n_dims = d.n_dims;
+    for (int l = 0; l < d.n_dims; ++l) t.dims[l] = d.dims[l];
+    t.n_req = k;
+    t.epochs = E;
+    t.max_batch = (int32_t)max_b;
+    t.grid = d.grid;
+    const size_t wsb = (fs_train_bf16_workspace_bytes(&t) + 255) / 256 * 256;
+    const size_t rows_b = (size_t)k * ldw * esz;
+    const size_t status_b = (4 * (size_t)k + 255) / 256 * 256;
+    uint8_t* mem = nullptr;
+    if (int rc = cuda(cudaMallocAsync((void**)&mem, meta + wsb + status_b + rows_b, bs), "batch memory")) return rc;
+    std::vector<uint8_t> h(meta);
+    size_t o = 0;
+    auto put_h = [&](const void* src, size_t n) {
+      const size_t at = o;
+      memcpy(h.data() + o, src, n);
+      o += n;
+      return (uint64_t)(mem + at);
+    };
+    const uint64_t p64 = put_h(i64.data(), 8 * i64.size());
+    const uint64_t plr = put_h(lr.data(), 8 * lr.size());
+    const uint64_t pws = put_h(wst.data(), 8 * (size_t)k);
+    const uint64_t ppv = put_h(wpv.data(), 8 * (size_t)k);
+    const uint64_t pdn = put_h(dn.data(), 8 * (size_t)k);
+    const uint64_t p32 = put_h(i32.data(), 4 * i32.size());
+    if (int rc = cuda(cudaMemcpyAsync(mem, h.data(), meta, cudaMemcpyHostToDevice, bs), "batch metadata")) return rc;
+    int32_t* status = (int32_t*)(mem + meta + wsb);
+    if (int rc = cuda(cudaMemsetAsync(status, 0, 4 * (size_t)k, bs), "status")) return rc;
+    uint8_t* rows = mem + meta + wsb + status_b;
+    const bool masks = d.dropout_rate > 0.0 && E > 0;
+    t.mask_mode = masks ? FS_MASK_BITS : FS_MASK_NONE;
+    t.scale = masks ? 1.0 / (1.0 - d.dropout_rate) : 1.0;
+    t.row_off = (const int64_t*)p64;
+    t.perm_off = (const int64_t*)(p64 + 8 * k);
+    t.mask_off = (const int64_t*)(p64 + 16 * k);
+    t.n_rows = (const int32_t*)p32;
+    t.batch = (const int32_t*)(p32 + 4 * k);
+    t.start_step = (const int32_t*)(p32 + 8 * k);
+    t.end_step = (const int32_t*)(p32 + 12 * k);
+    t.order = (const int32_t*)(p32 + 16 * k);
+    t.lr = (const double*)plr;
+    t.w_start = (const uint64_t*)pws;
+    t.w_out = (double*)rows;
+    t.ldw = ldw;
+    t.perm = (const int32_t*)d_perm_all;
+    t.mask_bits = masks ? (const uint32_t*)d_bits_all : nullptr;
+    t.status = status;
+    t.workspace = mem + meta;
+    t.workspace_bytes = wsb;
+    t.done = (const uint64_t*)pdn;
+    t.w_prev = (const uint64_t*)ppv;
+    t.align_mode = d.align_mode;
+    t.done_tag = 1;
+    launches += 1;
+    if (int rc = fs_train_bf16(&t, d.features, (const float*)d.labels, bs)) return rc;
+    // rows stay until aggregated (accepted) or collected (rejected); one block per batch
+    blocks.push_back(DevBlock{nullptr, k});
+    const int64_t blk = (int64_t)blocks.size() - 1;
+    for (int32_t i = 0; i < k; ++i) {
+      row_ptr[ids[i]] = (uint64_t)rows + (uint64_t)i * ldw * esz;
+      row_block[ids[i]] = blk;
+      launched[ids[i]] = 1;
+    }
+    cudaEvent_t end_ev;
+    cudaEventCreateWithFlags(&end_ev, cudaEventDisableTiming);
+    cudaEventRecord(end_ev, bs);
+    batch_mem.push_back({blk, mem, end_ev});
+    // lookahead: K2/K3 of every launched client's next cycle
+    std::vector<int32_t> nci, ncy, nsl;
+    for (int32_t i = 0; i < k; ++i)
+      if (cyc[i] + 1 < C) {
+        nci.push_back(ci[i]);
+        ncy.push_back(cyc[i] + 1);
+        nsl.push_back(1 - slot[i]);
+      }
+    if (!nci.empty())
+      if (int rc = generate(nci.data(), ncy.data(), nsl.data(), (int32_t)nci.size(), side)) return rc;
+    inflight.push_back(Batch{bs, ids, k});
+    flushes += 1;
+    return FS_OK;
+  }
+
+  struct BatchMem {
+    int64_t blk;
+    uint8_t* mem;
+    cudaEvent_t end;  // recorded right behind the batch's trainer kernel
+  };
+  std::vector<BatchMem> batch_mem;
+
+  void drop_row(int32_t id) {  // the row of a collected cycle is no longer needed
+    const int64_t b = row_block[id];
+    if (b < 0) return;
+    row_block[id] = -1;
+    if (--blocks[b].refs == 0)
+      for (size_t i = 0; i < batch_mem.size(); ++i)
+        if (batch_mem[i].blk == b) {
+          // after the aggregations queued on the main stream and the batch's own kernel
+          // (whose CTAs still claim work items from the workspace after their last client)
+          cudaStreamWaitEvent(st, batch_mem[i].end, 0);
+          cudaEventDestroy(batch_mem[i].end);
+          cudaFreeAsync(batch_mem[i].mem, st);
+          batch_mem.erase(batch_mem.begin() + i);
+          break;
+        }
+  }
+
+  // collect every finished client of the in-flight launches
+  int poll(fs_async_engine* e) {
+    for (size_t bi = 0; bi < inflight.size();) {
+      Batch& b = inflight[bi];
+      for (int32_t& id : b.ids) {
+        if (id < 0) continue;
+        fs_client_done* r = rec(id, nullptr);
+        if (r->tag == 0) continue;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        Deferred& q = e->deferred[id];
+        if (r->status) {
+          div_client = e->cid[q.ci];
+          div_cycle = q.cycle;
+          fs::set_error("loss became non-finite training client %d cycle %d", div_client, div_cycle);
+          return FS_EDIVERGED;
+        }
+        const uint64_t prev = prev_of(q.version);
+        const bool scored = !(d.align_mode == FS_ALIGN_DELTA_SIGN && prev == 0);
+        q.evaluated = 1;
+        if (scored) {
+          const double ratio = (double)r->aligned / (double)M;  // filter_update: ratio >= theta
+          q.relevance = ratio;
+          q.accepted = ratio >= d.theta;
+        } else {
+          q.relevance = NAN;
+          q.accepted = 1;
+        }
+        vref[q.version] -= 1;
+        if (q.version > 0) vref[q.version - 1] -= 1;
+        if (!q.accepted) drop_row(id);
+        auto it = std::find(e->unevaluated.begin(), e->unevaluated.end(), id);
+        if (it != e->unevaluated.end()) e->unevaluated.erase(it);
+        id = -1;
+        --b.left;
+      }
+      if (b.left == 0) inflight.erase(inflight.begin() + bi);
+      else ++bi;
+    }
+    return FS_OK;
+  }
+
+  int flush_percycle(fs_async_engine* e) {
+    const double t0 = now_s();
+    const int32_t X = (int32_t)e->hand.a;  // the train_done waiting for its outcome
+    if (int rc = launch_jobs(e)) return rc;
+    if (int rc = launch_batch(e)) return rc;  // every pending cycle not launched yet (X among them if new)
+    const double t1 = now_s();
+    uint32_t spins = 0;
+    while (!e->deferred[X].evaluated) {
+      if (int rc = poll(e)) return rc;
+      if (e->deferred[X].evaluated) break;
+      if ((++spins & 255) == 0) {  // a faulted launch never publishes: surface its error
+        for (const Batch& b : inflight) {
+          const cudaError_t err = cudaStreamQuery(b.s);
+          if (err != cudaSuccess && err != cudaErrorNotReady) return cuda(err, "in-flight trainer");
+        }
+        if (now_s() - t1 > 60.0) {
+          fs::set_error("async device: client %d did not complete within 60 s", X);
+          return FS_ECUDA;
+        }
+      }
+    }
+    const double t2 = now_s();
+    t_prep += t1 - t0;
+    t_wait += t2 - t1;
+    release_versions(e);
+    return FS_OK;
+  }
 };
 
 int fs_async_engine::run() {
@@ -823,7 +1223,7 @@ int fs_async_engine::run() {
     const int r = step();
     if (r == 1) {
       if (!dx) return yield_eval();
-      if (int rc = dx->flush(this)) return rc;
+      if (int rc = dx->percycle ? dx->flush_percycle(this) : dx->flush(this)) return rc;
       continue;
     }
     if (r == 2) {  // device mode: reports need their versions to exist

@@ -64,6 +64,13 @@ struct Args {
   int* counter;
   const int32_t* mask_flags;  // per (request, step) readiness of the keep bits (nullptr: complete)
   int32_t mask_tag, max_steps;
+  // per-client completion (async engine): after a client's row is written the
+  // CTA counts its sign alignment against (w_start, w_prev) and publishes
+  // {aligned, status, tag} to done[r] (mapped host memory); nullptr: off
+  const uint64_t* done;       // [n_req] device pointers of fs_client_done records
+  const uint64_t* w_prev;     // [n_req] previous global (delta_sign) or 0
+  int32_t align_mode;         // FS_ALIGN_*, or -1: no count
+  int32_t done_tag;
   float* gacc;                // [grid x M] fp32 gradient accumulators (multi-chunk steps)
   unsigned long long* prof;   // optional [32] phase cycle counters (thread 0 of every CTA)
 };

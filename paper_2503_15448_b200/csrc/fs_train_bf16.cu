@@ -967,12 +967,16 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.mask_flags = d->mask_mode == FS_MASK_BITS ? d->mask_flags : nullptr;
   a.mask_tag = d->mask_tag;
   a.max_steps = d->max_steps;
+  a.done = d->done;
+  a.w_prev = d->w_prev;
+  a.align_mode = d->done ? d->align_mode : -1;
+  a.done_tag = d->done_tag;
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
-  if (a.mask_flags) {
-    set_error("fs_train_bf16: flagged keep bits need the unit-major kernel's layer shapes");
+  if (a.mask_flags || a.done) {
+    set_error("fs_train_bf16: flagged keep bits / completion records need the unit-major kernel's layer shapes");
     return FS_EINVAL;
   }
   if (g.v2 && g_bf16_force_generic != 1) {

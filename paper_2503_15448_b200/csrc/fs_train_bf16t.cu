@@ -234,6 +234,38 @@ __device__ __forceinline__ float gate_seg(const Tile& t, int m, int c0, uint32_t
   return s;
 }
 
+__device__ __forceinline__ int sgn_f(float x) { return (x > 0.f) - (x < 0.f); }
+__device__ __forceinline__ int sgn_d(float a, float b) { return (a > b) - (a < b); }
+
+// K6 for one freshly trained row (selection.calculate_relevance,
+// selection.py:53-74), then {aligned, status, tag} into the client's record
+// (system-scope release: the record usually lives in mapped host memory and
+// the trained row must be visible to kernels the host launches next).
+__device__ __noinline__ void client_done(int M, int mode, const float* W, const float* g, const float* p,
+                                         const int32_t* status, uint64_t rec_addr, int32_t tag, int tid) {
+  __shared__ unsigned long long s_cnt[THREADS / 32];
+  unsigned cnt = 0;
+  if (mode == FS_ALIGN_DELTA_SIGN && !p) mode = -1;  // no movement history: unscored (server.py:283-284)
+  if (mode >= 0) {
+    for (int j = tid; j < M; j += THREADS) {
+      const float c = __ldcg(W + j), gv = __ldg(g + j);
+      cnt += mode == FS_ALIGN_WEIGHT_SIGN ? (sgn_f(c) == sgn_f(gv)) : (sgn_d(c, gv) == sgn_d(gv, __ldg(p + j)));
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((tid & 31) == 0) s_cnt[tid >> 5] = cnt;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < THREADS / 32; ++w) t += s_cnt[w];
+    fs_client_done* rec = reinterpret_cast<fs_client_done*>(rec_addr);
+    rec->aligned = (int64_t)t;
+    rec->status = __ldcg(status);
+    __threadfence_system();
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(&rec->tag), "r"(tag) : "memory");
+  }
+}
+
 // 184 registers x 256 threads leaves room for one 256-thread block of the next
 // round's K3 (70 registers) on the same SM
 #ifndef FS_BF16T_MAXNREG
@@ -786,6 +818,13 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     }
     for (int k = tid; k <= f3; k += THREADS) {
       if (k < f3) W[g.woff[3] + k] = wh[k]; else W[g.boff[3]] = wh[f3];
+    }
+    if (a.done) {  // per-client completion: fused K6 count + release of the record
+      __threadfence();
+      __syncthreads();
+      client_done(g.M, a.align_mode, W, Ws,
+                  a.align_mode == FS_ALIGN_DELTA_SIGN ? reinterpret_cast<const float*>(a.w_prev[rq]) : nullptr,
+                  a.status + rq, a.done[rq], a.done_tag, tid);
     }
     fence_before_sync();
     __syncthreads();
