@@ -179,6 +179,12 @@ int fs_forward_bf16(const int32_t* dims, int32_t n_dims, const float* w, const v
                     double* probs_out, void* stream);
 int fs_train_bf16(const fs_train_desc* desc, const void* features_bf16, const float* labels_f32,
                   void* stream);
+/* K8 forward in bf16 mode for shapes beyond the on-chip kernels (the wide
+ * MLP): cuBLAS bf16 GEMMs, fp32 accumulation, fused relu/bias epilogues,
+ * fp32 head; probs_out[rows] (float64) of fs_prep_features_bf16 rows.     */
+size_t fs_forward_wide_workspace_bytes(const int32_t* dims, int32_t n_dims, int32_t rows);
+int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float* w, const void* x_bf16, int32_t rows,
+                    double* probs_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* backend.loss_and_grad (_core.pyx:140-219 / numpy_backend.py:60-104):
  * one batch x[rows x dims[0]], labels y[rows], optional dense pre-scaled masks

@@ -105,6 +105,8 @@ _SIGNATURES = {
         [_c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp],
     ),
     "fs_forward_workspace_bytes": (_c_sz, [_c_vp, _c_i32, _c_i32]),
+    "fs_forward_wide_workspace_bytes": (_c_sz, [_c_vp, _c_i32, _c_i32]),
+    "fs_forward_wide": (ctypes.c_int, [_c_vp, _c_i32, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_forward_bf16": (ctypes.c_int, [_c_vp, _c_i32, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),
     "fs_forward_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_sign_align_f64": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),

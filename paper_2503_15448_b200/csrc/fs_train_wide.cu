@@ -100,8 +100,16 @@ __global__ void init_master_kernel(const uint64_t* w_start, const int* reqs, int
   const int r = reqs[a];
   const float* src = reinterpret_cast<const float*>(w_start[r]);
   float* dst = w_out + (int64_t)r * ldw;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)
-    dst[j] = src[j];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const int64_t m4 = M / 4;
+    for (int64_t j = t0; j < m4; j += stride)
+      reinterpret_cast<float4*>(dst)[j] = __ldcs(reinterpret_cast<const float4*>(src) + j);
+    for (int64_t j = m4 * 4 + t0; j < M; j += stride) dst[j] = src[j];
+  } else {
+    for (int64_t j = t0; j < M; j += stride) dst[j] = src[j];
+  }
 }
 
 struct ConvArgs {
@@ -115,22 +123,37 @@ struct ConvArgs {
 };
 
 // bf16 copies of every hidden weight matrix of the listed clients (W_0 rows
-// padded to dp with zeros, matching the zero-padded feature columns)
+// padded to dp with zeros, matching the zero-padded feature columns): one
+// 16-byte read and one 8-byte write per 4 parameters (fout % 4 == 0).
 __global__ void convert_kernel(ConvArgs c, const StepRow* rows, int n) {
   const int a = blockIdx.y;
   if (a >= n) return;
   const StepRow sr = rows[a];
   const float* m = c.w_out + (int64_t)sr.req * c.ldw;
   __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(c.slots + (size_t)sr.slot * c.slot_bytes);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int l = 0; l < c.lay.L - 1; ++l) {
     const int fin = c.lay.f[l], fout = c.lay.f[l + 1];
-    const int rows_l = l == 0 ? c.dp : fin;
-    const int64_t total = (int64_t)rows_l * fout;
     const float* src = m + c.lay.woff[l];
     __nv_bfloat16* dst = wb + c.wb_off[l];
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t rr = j / fout;
-      dst[j] = __float2bfloat16_rn(rr < fin ? src[j] : 0.f);
+    const int64_t real = (int64_t)fin * fout;
+    const int64_t total = (int64_t)(l == 0 ? c.dp : fin) * fout;
+    const bool vec = (fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(dst) & 7) == 0);
+    if (vec) {
+      for (int64_t j4 = t0; j4 < total / 4; j4 += stride) {
+        const int64_t j = j4 * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < real) v = __ldcs(reinterpret_cast<const float4*>(src + j));
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 packed;
+        packed.x = *reinterpret_cast<uint32_t*>(&lo);
+        packed.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(dst + j) = packed;
+      }
+    } else {
+      for (int64_t j = t0; j < total; j += stride) dst[j] = __float2bfloat16_rn(j < real ? src[j] : 0.f);
     }
   }
 }
@@ -432,7 +455,7 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
       init_master_kernel<<<grid, 256, 0, st>>>(d->w_start, reinterpret_cast<const int*>(stage + rb), gn, L.M, w_out,
                                                d->ldw);
       if (int rc = check_launch("wide init")) return rc;
-      convert_kernel<<<dim3(64, (unsigned)gn), 256, 0, st>>>(ca, reinterpret_cast<const StepRow*>(stage), gn);
+      convert_kernel<<<dim3(128, (unsigned)gn), 256, 0, st>>>(ca, reinterpret_cast<const StepRow*>(stage), gn);
       if (int rc = check_launch("wide convert")) return rc;
     }
     int t_end = 0;
@@ -574,11 +597,125 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
         }
       }
       // bf16 copies of the updated masters for the next step
-      convert_kernel<<<dim3(64, (unsigned)A), 256, 0, st>>>(ca, d_rows, A);
+      convert_kernel<<<dim3(128, (unsigned)A), 256, 0, st>>>(ca, d_rows, A);
       if (int rc = check_launch("wide convert")) return rc;
     }
   }
   return FS_OK;
 }
 
+
+// ------------------------------------------------------------------ eval forward (wide layers)
+namespace wide {
+
+__global__ void to_bf16_kernel(const float* src, int64_t rows_src, int64_t rows_dst, int cols, __nv_bfloat16* dst) {
+  const int64_t total = rows_dst * cols;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = __float2bfloat16_rn(j / cols < rows_src ? src[j] : 0.f);
+}
+
+// H = bf16(relu(Z + b)); the last hidden layer also accumulates the logits
+// from the fp32 values (z[r] += sum_u v * w_h[u]), as the trainers do
+__global__ void eval_epilogue_kernel(const float* Z, const float* b, int N, int rows, __nv_bfloat16* H,
+                                     const float* wh, float* z) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  float v = 0.f;
+  if (u < N) {
+    v = fmaxf(Z[(int64_t)r * N + u] + b[u], 0.f);
+    H[(int64_t)r * N + u] = __float2bfloat16_rn(v);
+  }
+  if (wh) {
+    float p = u < N ? v * wh[u] : 0.f;
+    for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(z + r, p);
+  }
+}
+
+__global__ void eval_probs_kernel(const float* z, const float* bh, int rows, double* probs) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float zz = z[r] + bh[0];
+  probs[r] = (double)(zz >= 0.f ? 1.f / (1.f + __expf(-zz)) : __expf(zz) / (1.f + __expf(zz)));
+}
+
+}  // namespace wide
 }  // namespace fs
+
+using namespace fs;
+
+extern "C" size_t fs_forward_wide_workspace_bytes(const int32_t* dims, int32_t n_dims, int32_t rows) {
+  MlpLayout L;
+  if (make_layout(dims, n_dims, &L) != FS_OK || rows < 0) return 0;
+  const int dp = (L.f[0] + 15) / 16 * 16;
+  const size_t wb = ((size_t)L.M + (size_t)(dp - L.f[0]) * L.f[1]) * 2;
+  const size_t act = (size_t)rows * std::max(L.max_hidden, dp) * 2;
+  return (wb + 255) / 256 * 256 + 2 * ((act + 255) / 256 * 256) +
+         (((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256) + ((size_t)rows * 4 + 256);
+}
+
+// K8 forward for layer shapes beyond the on-chip kernels (bf16 operands,
+// fp32 accumulation, fp32 head): probs_out[rows] of fs_prep_features_bf16 rows.
+extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float* w, const void* x_bf16, int32_t rows,
+                               double* probs_out, void* workspace, size_t workspace_bytes, void* stream) {
+  MlpLayout L;
+  if (make_layout(dims, n_dims, &L) != FS_OK || rows < 0 || L.L < 2) {
+    set_error("fs_forward_wide: invalid dims or rows");
+    return FS_EINVAL;
+  }
+  if (rows == 0) return FS_OK;
+  const size_t need = fs_forward_wide_workspace_bytes(dims, n_dims, rows);
+  if (!workspace || workspace_bytes < need) {
+    set_error("fs_forward_wide: workspace %zu < required %zu", workspace_bytes, need);
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cublasHandle_t h = wide::blas();
+  if (!h) {
+    set_error("fs_forward_wide: cublasCreate failed");
+    return FS_ECUDA;
+  }
+  if (int rc = wide::blas_ok(cublasSetStream(h, st), "cublasSetStream")) return rc;
+  const int dp = (L.f[0] + 15) / 16 * 16;
+  uint8_t* p = reinterpret_cast<uint8_t*>(workspace);
+  const size_t wb_bytes = ((size_t)L.M + (size_t)(dp - L.f[0]) * L.f[1]) * 2;
+  __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(p);
+  p += (wb_bytes + 255) / 256 * 256;
+  const size_t act = (size_t)rows * std::max(L.max_hidden, dp) * 2;
+  __nv_bfloat16* hbuf[2] = {reinterpret_cast<__nv_bfloat16*>(p),
+                            reinterpret_cast<__nv_bfloat16*>(p + (act + 255) / 256 * 256)};
+  p += 2 * ((act + 255) / 256 * 256);
+  float* Z = reinterpret_cast<float*>(p);
+  p += ((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256;
+  float* z = reinterpret_cast<float*>(p);
+  if (cudaMemsetAsync(z, 0, (size_t)rows * 4, st) != cudaSuccess) return check_launch("fs_forward_wide memset");
+  const float one = 1.f, zero = 0.f;
+  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(x_bf16);
+  int fin_pad = dp;
+  int64_t wofs = 0;
+  for (int l = 0; l < L.L - 1; ++l) {
+    const int fin = L.f[l], fout = L.f[l + 1];
+    const int kin = l == 0 ? dp : fin;
+    __nv_bfloat16* wl = wb + wofs;
+    wide::to_bf16_kernel<<<256, 256, 0, st>>>(w + L.woff[l], fin, kin, fout, wl);
+    if (int rc = check_launch("fs_forward_wide convert")) return rc;
+    wofs += (int64_t)kin * fout;
+    // col-major: Z'(fout x rows) = W'(fout x kin) * H'(kin x rows)
+    if (int rc = wide::blas_ok(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, fout, rows, kin, &one, wl, CUDA_R_16BF, fout,
+                                            in, CUDA_R_16BF, kin, &zero, Z, CUDA_R_32F, fout, CUBLAS_COMPUTE_32F,
+                                            CUBLAS_GEMM_DEFAULT),
+                               "forward GEMM"))
+      return rc;
+    __nv_bfloat16* out = hbuf[l & 1];
+    const bool last = l == L.L - 2;
+    wide::eval_epilogue_kernel<<<dim3((fout + 255) / 256, (unsigned)rows), 256, 0, st>>>(
+        Z, w + L.boff[l], fout, rows, out, last ? w + L.woff[L.L - 1] : nullptr, z);
+    if (int rc = check_launch("fs_forward_wide epilogue")) return rc;
+    in = out;
+    fin_pad = fout;
+  }
+  (void)fin_pad;
+  wide::eval_probs_kernel<<<(rows + 255) / 256, 256, 0, st>>>(z, w + L.boff[L.L - 1], rows, probs_out);
+  return check_launch("fs_forward_wide probs");
+}
+

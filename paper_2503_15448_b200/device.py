@@ -727,6 +727,18 @@ def eval_bf16_supported(spec_dims) -> bool:
     return len(d) == 5 and d[1] in (128, 256) and d[2] == 128 and d[3] == 64 and d[0] <= 64 and d[4] == 1
 
 
+def forward_probs_wide(spec_dims, w32: torch.Tensor, xb: torch.Tensor, rt: Runtime | None = None) -> torch.Tensor:
+    """K8 forward, bf16 mode, layer shapes beyond the on-chip kernels (fs_forward_wide)."""
+    rt = rt or Runtime.get()
+    dims_c, nd = dims_array(spec_dims)
+    rows = xb.shape[0]
+    probs = torch.empty(rows, dtype=torch.float64, device=rt.device)
+    ws = rt.scratch("forward_wide", rt.lib.fs_forward_wide_workspace_bytes(dims_c, nd, rows))
+    rt.call(rt.lib.fs_forward_wide(dims_c, nd, w32.data_ptr(), xb.data_ptr(), rows, probs.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), rt.stream), "fs_forward_wide")
+    return probs
+
+
 def forward_probs_bf16(spec_dims, w32: torch.Tensor, xb: torch.Tensor, rt: Runtime | None = None) -> torch.Tensor:
     """K8 forward on the tensor cores: float64 probabilities of bf16 rows under fp32 parameters."""
     rt = rt or Runtime.get()

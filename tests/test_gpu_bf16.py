@@ -264,3 +264,26 @@ def test_wide_local_training_tracks_fp64():
                                 precision="bf16", **one)
         # batching must not mix clients: only summation-order noise (a mixing bug is O(1))
         assert ((solo[0] - out32[i]).norm() / (out32[i] - w32).norm()).item() < 5e-2
+
+
+@pytest.mark.parametrize("dims", [WIDE, (30, 512, 384, 1)], ids=["wide", "w512_384"])
+def test_wide_eval_forward_tracks_fp64(dims):
+    """fs_forward_wide (bf16 operands, fp32 accumulation) vs the fp64 forward."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=dims[0], hidden_dims=dims[1:-1], dropout_rate=0.0)
+    rng = np.random.default_rng(4)
+    rows = 777
+    x = rng.normal(size=(rows, dims[0]))
+    rt = D.Runtime.get()
+    w32 = torch.tensor(init_params(spec, 3).values, dtype=torch.float32, device="cuda")
+    xd = torch.tensor(x, device="cuda")
+    dp = (dims[0] + 15) // 16 * 16
+    xb = torch.empty((rows, dp), dtype=torch.bfloat16, device="cuda")
+    rt.call(rt.lib.fs_prep_features_bf16(xd.data_ptr(), None, rows, dims[0], dp, xb.data_ptr(), None, rt.stream),
+            "prep")
+    p64 = D.forward_probs(spec.dims, w32.double(), xd, None, rt).cpu().numpy()
+    p16 = D.forward_probs_wide(spec.dims, w32, xb, rt).cpu().numpy()
+    assert np.max(np.abs(p16 - p64)) < 2e-2
+    assert np.mean(np.abs(p16 - p64)) < 3e-3
