@@ -47,6 +47,9 @@ enum fs_align_mode { FS_ALIGN_WEIGHT_SIGN = 0, FS_ALIGN_DELTA_SIGN = 1 };
 
 const char* fs_last_error(void);
 int fs_abi_version(void);
+/* dst[0..n) = value (device, stream-ordered): per-request launch arguments
+ * that are one value for a whole round (start model pointer, step size bits) */
+int fs_fill_u64(uint64_t* dst, uint64_t value, int64_t n, void* stream);
 /* stream-ordered device-to-device copy (engine-owned model versions -> caller tensors) */
 int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 
@@ -248,6 +251,11 @@ int fs_aggregate_f32(const uint64_t* rows, int32_t k, int64_t M, float* out, voi
  * dtype_bytes), the ranks all-reduce [sum | counts] over NCCL, and every
  * rank finishes out[j] = sum[j] / k in the parameter dtype, so the global
  * model stays replicated without a broadcast.                            */
+/* K6 for rows at base + i * stride_bytes, i < n_req (a trainer launch's
+ * output block), against one shared (w_g, w_g_prev): no pointer array.     */
+int fs_sign_align_rows(uint64_t base, int64_t stride_bytes, const void* wg, const void* wg_prev, int32_t n_req,
+                       int64_t M, int32_t mode, int32_t dtype_bytes, int64_t* aligned_out, void* stream);
+
 /* Many FedAvg means in one launch pair (an async run's aggregations between
  * two training flushes): job j = mean of rows[job_off[j]..job_off[j+1]) in
  * canonical byte order -> job_out[j] (device pointers; 1 <= rows per job <=

@@ -83,6 +83,7 @@ _SIGNATURES = {
     "fs_last_error": (ctypes.c_char_p, []),
     "fs_abi_version": (ctypes.c_int, []),
     "fs_memcpy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
+    "fs_fill_u64": (ctypes.c_int, [_c_vp, _c_u64, _c_i64, _c_vp]),
     "fs_derive_seed_host": (ctypes.c_int, [_c_u64, ctypes.POINTER(ctypes.c_uint32), _c_i32, ctypes.POINTER(_c_u64)]),
     "fs_train_seeds_host": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),
@@ -111,6 +112,7 @@ _SIGNATURES = {
     "fs_forward_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_sign_align_f64": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_sign_align_f32": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "fs_sign_align_rows": (ctypes.c_int, [_c_u64, _c_i64, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_sign_align_shared": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_gather_sort_keys_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f32": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),

@@ -44,6 +44,26 @@ void ensure_smem_impl(const void* fn, int bytes) {
 }
 }  // namespace fs
 
+namespace {
+__global__ void fill_u64_kernel(uint64_t* dst, uint64_t v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+}  // namespace
+
+// dst[0..n) = value (8-byte words; a double's bits or a device pointer): the
+// per-request launch arguments that are one value for a whole round
+extern "C" int fs_fill_u64(uint64_t* dst, uint64_t value, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && !dst)) {
+    fs::set_error("fs_fill_u64: invalid arguments");
+    return FS_EINVAL;
+  }
+  if (n == 0) return FS_OK;
+  const int blocks = (int)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
+  fill_u64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dst, value, n);
+  return fs::check_launch("fill_u64_kernel");
+}
+
 extern "C" int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return FS_OK;
   if (!dst || !src) {

@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(ALIGN_THREADS)
 template <int MODE, class T, int G>
 __global__ void __launch_bounds__(ALIGN_THREADS)
     sign_align_shared_kernel(const uint64_t* wc, const T* __restrict__ g, const T* __restrict__ p, int n_req,
-                             int64_t M, int blocks_per_grp, unsigned long long* out) {
+                             int64_t M, int blocks_per_grp, unsigned long long* out, uint64_t base = 0,
+                             int64_t stride = 0) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   const int grp = blockIdx.x / blocks_per_grp;
@@ -125,7 +126,10 @@ __global__ void __launch_bounds__(ALIGN_THREADS)
   const int nq = min(G, n_req - r0);
   const T* c[G];
 #pragma unroll
-  for (int q = 0; q < G; ++q) c[q] = reinterpret_cast<const T*>(wc[r0 + (q < nq ? q : 0)]);
+  for (int q = 0; q < G; ++q) {
+    const int r = r0 + (q < nq ? q : 0);
+    c[q] = reinterpret_cast<const T*>(wc ? wc[r] : base + (uint64_t)r * (uint64_t)stride);
+  }
   const int64_t nvec = M / VN;
   const int64_t span = (nvec + blocks_per_grp - 1) / blocks_per_grp;
   const int64_t v0 = (int64_t)blk * span, v1 = min(nvec, v0 + span);
@@ -562,7 +566,8 @@ extern "C" int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t d
 
 template <class T>
 static int sign_align_shared_impl(const uint64_t* wc, const void* wg, const void* wgp, int32_t n_req, int64_t M,
-                                  int32_t mode, int64_t* aligned_out, void* stream) {
+                                  int32_t mode, int64_t* aligned_out, void* stream, uint64_t base = 0,
+                                  int64_t stride = 0) {
   constexpr int G = 4;
   if (n_req < 0 || M < 0 || !wg || (mode != FS_ALIGN_WEIGHT_SIGN && mode != FS_ALIGN_DELTA_SIGN) ||
       (mode == FS_ALIGN_DELTA_SIGN && !wgp) || (reinterpret_cast<uintptr_t>(wg) & 15) ||
@@ -587,9 +592,11 @@ static int sign_align_shared_impl(const uint64_t* wc, const void* wg, const void
   const T* g = reinterpret_cast<const T*>(wg);
   const T* p = reinterpret_cast<const T*>(wgp);
   if (mode == FS_ALIGN_WEIGHT_SIGN)
-    sign_align_shared_kernel<FS_ALIGN_WEIGHT_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out);
+    sign_align_shared_kernel<FS_ALIGN_WEIGHT_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out,
+                                                                                     base, stride);
   else
-    sign_align_shared_kernel<FS_ALIGN_DELTA_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out);
+    sign_align_shared_kernel<FS_ALIGN_DELTA_SIGN, T, G><<<nblk, ALIGN_THREADS, 0, st>>>(wc, g, p, n_req, M, bpg, out,
+                                                                                    base, stride);
   return check_launch("sign_align_shared_kernel");
 }
 
@@ -599,6 +606,23 @@ extern "C" int fs_sign_align_shared(const uint64_t* wc, const void* wg, const vo
   if (dtype_bytes == 8) return sign_align_shared_impl<double>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
   if (dtype_bytes == 4) return sign_align_shared_impl<float>(wc, wg, wg_prev, n_req, M, mode, aligned_out, stream);
   set_error("fs_sign_align_shared: dtype_bytes must be 4 or 8");
+  return FS_EINVAL;
+}
+
+// Same count for rows at base + i * stride_bytes (a launch's output block):
+// no pointer array, so a round needs no host-to-device copy for it.
+extern "C" int fs_sign_align_rows(uint64_t base, int64_t stride_bytes, const void* wg, const void* wg_prev,
+                                  int32_t n_req, int64_t M, int32_t mode, int32_t dtype_bytes, int64_t* aligned_out,
+                                  void* stream) {
+  if ((base & 15) || (stride_bytes & 15)) {
+    set_error("fs_sign_align_rows: rows must be 16-byte aligned");
+    return FS_EINVAL;
+  }
+  if (dtype_bytes == 8)
+    return sign_align_shared_impl<double>(nullptr, wg, wg_prev, n_req, M, mode, aligned_out, stream, base, stride_bytes);
+  if (dtype_bytes == 4)
+    return sign_align_shared_impl<float>(nullptr, wg, wg_prev, n_req, M, mode, aligned_out, stream, base, stride_bytes);
+  set_error("fs_sign_align_rows: dtype_bytes must be 4 or 8");
   return FS_EINVAL;
 }
 

@@ -371,6 +371,7 @@ class TrainPlan:
             return t[:n_elems]
 
         self.pooled = pool is not None
+        self._pool = pool
         with torch.cuda.stream(torch_stream):
             i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)])
             i32 = np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32)
@@ -381,8 +382,23 @@ class TrainPlan:
             else:
                 self.d_i64 = buf("i64", len(i64), torch.int64)
                 self.d_i32 = buf("i32", len(i32), torch.int32)
-                self.d_i64.copy_(torch.from_numpy(i64).pin_memory(), non_blocking=True)
-                self.d_i32.copy_(torch.from_numpy(i32).pin_memory(), non_blocking=True)
+                if pool is not None:
+                    # page-locked landing buffers kept in the pool: a fresh
+                    # pin_memory() per plan can hit cudaHostAlloc, which waits
+                    # for the whole device (a host stall in the middle of a round)
+                    h64 = pool.get("h_i64")
+                    if h64 is None or h64.numel() < len(i64):
+                        h64 = pool["h_i64"] = torch.empty(int(len(i64) * 1.25) + 1, dtype=torch.int64).pin_memory()
+                    h32 = pool.get("h_i32")
+                    if h32 is None or h32.numel() < len(i32):
+                        h32 = pool["h_i32"] = torch.empty(int(len(i32) * 1.25) + 1, dtype=torch.int32).pin_memory()
+                    h64.numpy()[:len(i64)] = i64
+                    h32.numpy()[:len(i32)] = i32
+                    self.d_i64.copy_(h64[:len(i64)], non_blocking=True)
+                    self.d_i32.copy_(h32[:len(i32)], non_blocking=True)
+                else:
+                    self.d_i64.copy_(torch.from_numpy(i64).pin_memory(), non_blocking=True)
+                    self.d_i32.copy_(torch.from_numpy(i32).pin_memory(), non_blocking=True)
                 p64, p32 = self.d_i64.data_ptr(), self.d_i32.data_ptr()
             self.perm = buf("perm", max(int(perm_len.sum()), 1), torch.int32)
             self.bits = (buf("bits", max(int(mask_len.sum()), 1), torch.int32)
@@ -415,6 +431,14 @@ class TrainPlan:
         if stream is not None:  # consumer stream waits on this event before the trainer reads the plan
             self.ready = torch.cuda.Event()
             self.ready.record(torch_stream)
+
+    def pool_buf(self, name: str, n_elems: int, dtype) -> torch.Tensor:
+        """A pooled device buffer owned by this plan's pool (stream-ordered reuse)."""
+        t = self._pool.get(name)
+        if t is None or t.numel() < n_elems or t.dtype != dtype:
+            t = torch.empty(int(n_elems * 1.25) + 1, dtype=dtype, device=self.rt.device)
+            self._pool[name] = t
+        return t[:n_elems]
 
     def launch_masks(self, stream, tag: int) -> None:
         """K3 for a deferred-mask plan on `stream`, concurrent with the trainer
@@ -465,13 +489,25 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         return w_out, status
     stream = torch.cuda.current_stream(rt.device)
     plan.consume(stream)
-    if plan.stage is not None:
+    if np.ndim(lr) == 0 and np.ndim(w_start) == 0 and plan.pooled:
+        # one step size and one start model for the whole launch (a sync round):
+        # filled on the device into the plan's pooled buffers, no host staging
+        d_run = plan.pool_buf("run", n, torch.int64)
+        d_lr = plan.pool_buf("lr", n * max(plan.epochs, 1), torch.float64)
+        rt.call(lib.fs_fill_u64(d_run.data_ptr(), int(w_start), n, stream.cuda_stream), "fs_fill_u64")
+        rt.call(lib.fs_fill_u64(d_lr.data_ptr(), int(np.float64(lr).view(np.uint64)), d_lr.numel(),
+                                stream.cuda_stream), "fs_fill_u64")
+        run_p, lr_p = d_run.data_ptr(), d_lr.data_ptr()
+    elif plan.stage is not None:
         run_p = plan.stage.put(np.asarray(w_start, dtype=np.uint64))
         lr_p = plan.stage.put(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
         plan.stage.commit(stream)
     else:
-        d_run = rt.h2d(np.asarray(w_start, dtype=np.uint64).view(np.int64))
-        d_lr = rt.h2d(np.ascontiguousarray(lr, dtype=np.float64).reshape(n, -1))
+        w_arr = np.broadcast_to(np.asarray(w_start, dtype=np.uint64), (n,))
+        lr_arr = np.broadcast_to(np.asarray(lr, dtype=np.float64).reshape(-1, 1) if np.ndim(lr) == 1 else
+                                 np.asarray(lr, dtype=np.float64), (n, max(plan.epochs, 1)))
+        d_run = rt.h2d(np.ascontiguousarray(w_arr).view(np.int64))
+        d_lr = rt.h2d(np.ascontiguousarray(lr_arr))
         run_p, lr_p = d_run.data_ptr(), d_lr.data_ptr()
     desc = N.TrainDesc()
     desc.n_dims = len(dims)
@@ -576,6 +612,26 @@ def align_requests(wc_ptrs, wg_ptrs, wgp_ptrs, M: int, mode: str, rt: Runtime | 
     with rt.timed("align", float(esz) * M * (n + (2 if m else 1))):
         rt.call(fn(p, p + 8 * n, (p + 16 * n) if m else None, n, M, m, out.data_ptr(), rt.stream),
                 "fs_sign_align")
+    return out[:n]
+
+
+def align_rows(w_c: torch.Tensor, wg: torch.Tensor, wgp: torch.Tensor | None, M: int, mode: str,
+               rt: Runtime | None = None) -> torch.Tensor:
+    """K6 for every row of a trainer output block against one (w_g, w_g_prev)."""
+    rt = rt or Runtime.get()
+    n = w_c.shape[0]
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if n == 0:
+        return out[:0]
+    m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
+    esz = wg.element_size()
+    stride = w_c.stride(0) * w_c.element_size()
+    if (wg.data_ptr() % 16) or (m and wgp.data_ptr() % 16) or (w_c.data_ptr() % 16) or (stride % 16):
+        rows = w_c.data_ptr() + np.arange(n, dtype=np.uint64) * np.uint64(stride)
+        return align_shared(rows, wg, wgp, M, mode, rt)
+    with rt.timed("align", float(esz) * M * (n + (2 if m else 1))):
+        rt.call(rt.lib.fs_sign_align_rows(w_c.data_ptr(), stride, wg.data_ptr(), wgp.data_ptr() if m else None, n, M,
+                                          m, esz, out.data_ptr(), rt.stream), "fs_sign_align_rows")
     return out[:n]
 
 
