@@ -50,6 +50,9 @@ int fs_abi_version(void);
 /* dst[0..n) = value (device, stream-ordered): per-request launch arguments
  * that are one value for a whole round (start model pointer, step size bits) */
 int fs_fill_u64(uint64_t* dst, uint64_t value, int64_t n, void* stream);
+/* flag[0] = value after all work queued before it on `stream` (release store):
+ * publishes a chunk of an upload to kernels polling on other streams     */
+int fs_publish_flag(int32_t* flag, int32_t value, void* stream);
 /* stream-ordered device-to-device copy (engine-owned model versions -> caller tensors) */
 int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 
@@ -147,6 +150,12 @@ typedef struct fs_train_desc {
   const uint64_t* w_prev;
   int32_t align_mode;
   int32_t done_tag;
+  /* bf16 unit-major trainer only: the shards are still being uploaded in
+   * chunks; request r reads its rows after data_flags[data_chunk[r]] ==
+   * data_tag (NULL: resident)                                             */
+  const int32_t* data_flags;
+  const int32_t* data_chunk;
+  int32_t data_tag;
 } fs_train_desc;
 
 typedef struct {

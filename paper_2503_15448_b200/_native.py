@@ -76,6 +76,9 @@ class TrainDesc(ctypes.Structure):
         ("w_prev", _c_vp),
         ("align_mode", _c_i32),
         ("done_tag", _c_i32),
+        ("data_flags", _c_vp),
+        ("data_chunk", _c_vp),
+        ("data_tag", _c_i32),
     ]
 
 
@@ -84,6 +87,7 @@ _SIGNATURES = {
     "fs_abi_version": (ctypes.c_int, []),
     "fs_memcpy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_fill_u64": (ctypes.c_int, [_c_vp, _c_u64, _c_i64, _c_vp]),
+    "fs_publish_flag": (ctypes.c_int, [_c_vp, _c_i32, _c_vp]),
     "fs_derive_seed_host": (ctypes.c_int, [_c_u64, ctypes.POINTER(ctypes.c_uint32), _c_i32, ctypes.POINTER(_c_u64)]),
     "fs_train_seeds_host": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),

@@ -64,6 +64,22 @@ extern "C" int fs_fill_u64(uint64_t* dst, uint64_t value, int64_t n, void* strea
   return fs::check_launch("fill_u64_kernel");
 }
 
+namespace {
+__global__ void publish_flag_kernel(int32_t* flag, int32_t v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+}  // namespace
+
+extern "C" int fs_publish_flag(int32_t* flag, int32_t value, void* stream) {
+  if (!flag) {
+    fs::set_error("fs_publish_flag: null flag");
+    return FS_EINVAL;
+  }
+  publish_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  return fs::check_launch("publish_flag_kernel");
+}
+
 extern "C" int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return FS_OK;
   if (!dst || !src) {

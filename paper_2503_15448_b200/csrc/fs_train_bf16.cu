@@ -971,11 +971,14 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.w_prev = d->w_prev;
   a.align_mode = d->done ? d->align_mode : -1;
   a.done_tag = d->done_tag;
+  a.data_flags = d->data_flags;
+  a.data_chunk = d->data_chunk;
+  a.data_tag = d->data_tag;
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
-  if (a.mask_flags || a.done) {
+  if (a.mask_flags || a.done || a.data_flags) {
     set_error("fs_train_bf16: flagged keep bits / completion records need the unit-major kernel's layer shapes");
     return FS_EINVAL;
   }

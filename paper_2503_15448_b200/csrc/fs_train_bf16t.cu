@@ -333,6 +333,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     const int spe = (n + B - 1) / B;
     float* W = a.w_out + (int64_t)rq * a.ldw;
     const float* Ws = reinterpret_cast<const float*>(a.w_start[rq]);
+    if (a.data_flags) wait_mask_step(a.data_flags + a.data_chunk[rq], a.data_tag);  // this client's rows uploaded
     FS_PROF(30);
 
     // ---------------- client start: masters and bf16 tiles from the start row
@@ -447,7 +448,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         } else if (tid < R) {
           const int64_t row = tid < rows ? row_off + perm_e[s * B + row0 + tid] : -1;
           s_rowidx[tid] = row;
-          y_sh[tid] = row >= 0 ? a.labels[row] : 0.f;
+          y_sh[tid] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
         }
         __syncthreads();
         FS_PROF(0);
@@ -459,7 +460,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
             uint4 v = xnext[u];
             if (!have_next) {
               v = make_uint4(0, 0, 0, 0);
-              if (r < rows) v = __ldg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * fp0 + c));
+              if (r < rows) v = __ldcg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * fp0 + c));
             }
             st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
           }
@@ -557,7 +558,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           const int nr0 = nch * R;
           const int64_t row = t < min(R, nrows_step - nr0) ? row_off + perm_c[(int64_t)ne * n + ns * B + nr0 + t] : -1;
           s_rowidx_next[t] = row;
-          s_y_next[t] = row >= 0 ? a.labels[row] : 0.f;
+          s_y_next[t] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
         }
         {
           const int hh = warp >> 2, m = q * 32 + lane;
@@ -617,7 +618,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
             xnext[u] = make_uint4(0, 0, 0, 0);
             if (i < R * cpr) {
               const int64_t row = s_rowidx_next[i / cpr];
-              if (row >= 0) xnext[u] = __ldg(reinterpret_cast<const uint4*>(a.feat + row * fp0 + (i % cpr) * 8));
+              if (row >= 0) xnext[u] = __ldcg(reinterpret_cast<const uint4*>(a.feat + row * fp0 + (i % cpr) * 8));
             }
           }
           have_next = true;

@@ -200,15 +200,21 @@ class HostPack:
     with ``pin=True`` the buffers are page-locked, so uploads are plain async
     DMA copies (the bench's end-to-end leg re-uploads them every round)."""
 
-    def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True, bf16: bool = False):
+    def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True, bf16: bool = False,
+                 order: np.ndarray | None = None, chunk_bytes: int = 0):
         n_rows = np.array([f.shape[0] for f in features], dtype=np.int64)
         self.n_rows = n_rows.astype(np.int32)
+        # clients are packed in `order` (default: index order); row_off stays per client
+        order = np.arange(len(features)) if order is None else np.asarray(order, dtype=np.int64)
         self.row_off = np.zeros(len(features), dtype=np.int64)
-        if len(features) > 1:
-            self.row_off[1:] = np.cumsum(n_rows)[:-1]
+        if len(features):
+            packed_off = np.zeros(len(features), dtype=np.int64)
+            packed_off[1:] = np.cumsum(n_rows[order])[:-1]
+            self.row_off[order] = packed_off
         self.dim = features[0].shape[1] if features else 0
-        x = np.ascontiguousarray(np.concatenate(features, axis=0), dtype=np.float64) if features else np.zeros((0, self.dim))
-        y = (np.ascontiguousarray(np.concatenate([np.asarray(l, dtype=np.float64) for l in labels]))
+        x = (np.ascontiguousarray(np.concatenate([features[i] for i in order], axis=0), dtype=np.float64)
+             if features else np.zeros((0, self.dim)))
+        y = (np.ascontiguousarray(np.concatenate([np.asarray(labels[i], dtype=np.float64) for i in order]))
              if labels else np.zeros(0))
         self.x = torch.from_numpy(x.reshape(-1, self.dim) if self.dim else x)
         self.y = torch.from_numpy(y)
@@ -226,6 +232,23 @@ class HostPack:
         if pin:
             self.x = self.x.pin_memory()
             self.y = self.y.pin_memory()
+        # upload chunks: consecutive clients of the packing order, ~chunk_bytes
+        # each; chunk_of[client] tells a trainer which chunk holds its rows
+        self.chunk_of = np.zeros(len(features), dtype=np.int32)
+        self.chunks = [(0, int(self.x.shape[0]))]
+        if chunk_bytes > 0 and len(features):
+            row_bytes = self.x.element_size() * (self.x.shape[1] if self.x.dim() == 2 else 1)
+            bounds, start, acc = [], 0, 0
+            for i in order:
+                self.chunk_of[i] = len(bounds)
+                acc += int(n_rows[i]) * row_bytes
+                if acc >= chunk_bytes:
+                    end = int(self.row_off[i] + n_rows[i])
+                    bounds.append((start, end))
+                    start, acc = end, 0
+            if start < self.x.shape[0] or not bounds:
+                bounds.append((start, int(self.x.shape[0])))
+            self.chunks = bounds
 
     def to_device(self, t: torch.Tensor, rt: Runtime) -> torch.Tensor:
         if t.numel() == 0:
@@ -321,7 +344,8 @@ class TrainPlan:
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
                  dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
-                 pool: dict | None = None, stage: "Stage | None" = None, defer_masks: bool = False):
+                 pool: dict | None = None, stage: "Stage | None" = None, defer_masks: bool = False,
+                 data_chunk: np.ndarray | None = None):
         rt = rt or Runtime.get()
         self.rt = rt
         self.stage = stage
@@ -374,7 +398,11 @@ class TrainPlan:
         self._pool = pool
         with torch.cuda.stream(torch_stream):
             i64 = np.concatenate([shards.row_off[cl], perm_off, mask_off, self.seeds.view(np.int64)])
-            i32 = np.concatenate([n_rows, self.batch, start, end, order]).astype(np.int32)
+            self.has_chunks = data_chunk is not None
+            parts = [n_rows, self.batch, start, end, order]
+            if self.has_chunks:
+                parts.append(np.asarray(data_chunk, dtype=np.int64)[cl])
+            i32 = np.concatenate(parts).astype(np.int32)
             if stage is not None:
                 self.d_i64 = self.d_i32 = None
                 p64, p32 = stage.put(i64), stage.put(i32)
@@ -405,6 +433,7 @@ class TrainPlan:
                          if use_masks and self.epochs > 0 else None)
         self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
         self.n_rows_p, self.batch_p, self.start_p, self.end_p, self.order_p = (p32 + 4 * n * k for k in range(5))
+        self.chunk_p = p32 + 4 * n * 5 if self.has_chunks else None
         if self.epochs > 0:
             rt.call(lib.fs_shuffle_perms(self.seeds_p, self.n_rows_p, self.perm_off_p, n, self.epochs,
                                          int(n_rows.max()), self.perm.data_ptr(), s_handle), "fs_shuffle_perms")
@@ -538,6 +567,14 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.order = plan.order_p
     desc.status = status.data_ptr()
     desc.grid = TRAIN_GRID
+    up = getattr(plan.shards, "upload", None)  # a chunked upload still in flight (DeviceWorld.refill)
+    if up is not None and up["pending"]:
+        if bf16 and plan.chunk_p is not None and eval_bf16_supported(dims):
+            desc.data_flags = up["flags"].data_ptr()
+            desc.data_chunk = plan.chunk_p
+            desc.data_tag = up["tag"]
+        else:  # trainers without per-client data waits take the whole upload first
+            stream.wait_event(up["done"])
     if plan.mask_flags is not None:
         if not plan.mask_tag:
             raise ValueError("deferred keep bits: launch_masks() must run before the trainer")
