@@ -11,6 +11,7 @@
 #include "fs_rng.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace fs {
 
@@ -170,38 +171,43 @@ __device__ void mask_stream(U128 base_state, U128 inc, int64_t n_draws, uint64_t
 // SeedSequence hashing + PCG64 seeding), then all threads fill their words.
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
-                        const int64_t* mask_off, int epochs, int sum_hidden, uint64_t thresh,
+                        const int64_t* mask_off, int n_req, int epochs, int sum_hidden, uint64_t thresh,
                         uint32_t* bits) {
+  // work item = (request, y-split); a throttled launch (fewer CTAs than items)
+  // strides over them, so the mask generation can be given a bounded share
+  // of the SMs it shares with the trainer and the round's tail kernels
   __shared__ U128 sh_state[32], sh_inc[32];
-  const int r = blockIdx.x;
-  const int n = n_rows[r], B = batch[r];
-  const int spe = (n + B - 1) / B;
-  const int total = epochs * spe;
-  const int64_t slot = ((int64_t)B * sum_hidden + 31) / 32;
-  const uint64_t train_seed = seeds[r];
   const LcgJump jt = lcg_jump(32ull * threadIdx.x);
   const LcgJump j1 = lcg_jump(32ull * MASK_THREADS);
   const LcgJump jr = lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32);
-  uint32_t* out_r = bits + mask_off[r];
-  for (int k0 = 0;; k0 += 32) {
-    const int st0 = blockIdx.y + k0 * MASK_YSPLIT;
-    if (st0 >= total) break;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int st = st0 + threadIdx.x * MASK_YSPLIT;
-      if (st < total) {
-        const Pcg64 g = pcg_from_seed(derive_mask_seed(train_seed, (uint32_t)(st / spe), (uint32_t)(st % spe)));
-        sh_state[threadIdx.x] = g.state;
-        sh_inc[threadIdx.x] = g.inc;
+  for (int item = blockIdx.x; item < n_req * MASK_YSPLIT; item += gridDim.x) {
+    const int r = item / MASK_YSPLIT, ysplit = item % MASK_YSPLIT;
+    const int n = n_rows[r], B = batch[r];
+    const int spe = (n + B - 1) / B;
+    const int total = epochs * spe;
+    const int64_t slot = ((int64_t)B * sum_hidden + 31) / 32;
+    const uint64_t train_seed = seeds[r];
+    uint32_t* out_r = bits + mask_off[r];
+    for (int k0 = 0;; k0 += 32) {
+      const int st0 = ysplit + k0 * MASK_YSPLIT;
+      if (st0 >= total) break;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int st = st0 + threadIdx.x * MASK_YSPLIT;
+        if (st < total) {
+          const Pcg64 g = pcg_from_seed(derive_mask_seed(train_seed, (uint32_t)(st / spe), (uint32_t)(st % spe)));
+          sh_state[threadIdx.x] = g.state;
+          sh_inc[threadIdx.x] = g.inc;
+        }
       }
-    }
-    __syncthreads();
-    for (int j = 0; j < 32; ++j) {
-      const int st = st0 + j * MASK_YSPLIT;
-      if (st >= total) break;
-      const int rows = min(B, n - (st % spe) * B);
-      mask_stream(sh_state[j], sh_inc[j], (int64_t)rows * sum_hidden, thresh, out_r + (int64_t)st * slot, jt, j1,
-                  jr);
+      __syncthreads();
+      for (int j = 0; j < 32; ++j) {
+        const int st = st0 + j * MASK_YSPLIT;
+        if (st >= total) break;
+        const int rows = min(B, n - (st % spe) * B);
+        mask_stream(sh_state[j], sh_inc[j], (int64_t)rows * sum_hidden, thresh, out_r + (int64_t)st * slot, jt, j1,
+                    jr);
+      }
     }
   }
 }
@@ -321,9 +327,11 @@ extern "C" int fs_dropout_bits(const uint64_t* seeds, const int32_t* n_rows, con
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0) return FS_OK;
-  dim3 grid(n_req, MASK_YSPLIT);
-  dropout_bits_kernel<<<grid, MASK_THREADS, 0, (cudaStream_t)stream>>>(
-      seeds, n_rows, batch, mask_off, epochs, sum_hidden, keep_threshold(keep), bits_out);
+  int64_t items = (int64_t)n_req * MASK_YSPLIT, blocks = items;
+  static const int64_t cap = getenv("FS_K3_BLOCKS") ? atoll(getenv("FS_K3_BLOCKS")) : 0;
+  if (cap > 0 && blocks > cap) blocks = cap;
+  dropout_bits_kernel<<<(unsigned)blocks, MASK_THREADS, 0, (cudaStream_t)stream>>>(
+      seeds, n_rows, batch, mask_off, n_req, epochs, sum_hidden, keep_threshold(keep), bits_out);
   return check_launch("dropout_bits_kernel");
 }
 
