@@ -535,8 +535,8 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         w_arr = np.broadcast_to(np.asarray(w_start, dtype=np.uint64), (n,))
         lr_arr = np.broadcast_to(np.asarray(lr, dtype=np.float64).reshape(-1, 1) if np.ndim(lr) == 1 else
                                  np.asarray(lr, dtype=np.float64), (n, max(plan.epochs, 1)))
-        d_run = rt.h2d(np.ascontiguousarray(w_arr).view(np.int64))
-        d_lr = rt.h2d(np.ascontiguousarray(lr_arr))
+        d_run = rt.h2d(np.array(w_arr, dtype=np.uint64).view(np.int64))  # writable copies of the views
+        d_lr = rt.h2d(np.array(lr_arr, dtype=np.float64))
         run_p, lr_p = d_run.data_ptr(), d_lr.data_ptr()
     desc = N.TrainDesc()
     desc.n_dims = len(dims)
