@@ -320,7 +320,11 @@ def test_async_engines_agree(golden, monkeypatch, name, engine):
     assert len(state.history) == sum(1 for r in eng.timeline.log if r["kind"] == "aggregate")
 
 
-def test_async_engines_agree_bf16():
+@pytest.mark.parametrize("extra", [{}, {"dropout_rate": 0.3, "checkpoint": {"enabled": True, "total_time_s": 60.0,
+                                                                           "recovery_s": 2.0}},
+                                   {"dropout_rate": 0.3}, {"aggregation": {"k_min": 1}}],
+                         ids=["plain", "fail_ckpt", "fail_lost", "k_min1"])
+def test_async_engines_agree_bf16(extra):
     """bf16 mode: the three async engines make the same decisions and produce
     the same float32 global model bitwise (same kernels, same order)."""
     from paper_2503_15448_b200 import server
@@ -333,6 +337,7 @@ def test_async_engines_agree_bf16():
                         "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
                         "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
                         "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}}}
+    cfg.update(extra)
     out = {}
     saved = server._ASYNC_ENGINE
     try:
