@@ -22,8 +22,10 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <map>
 #include <queue>
 #include <vector>
 
@@ -391,7 +393,7 @@ struct DeviceExec {
   size_t next_stream = 0;
   std::vector<std::pair<void*, cudaEvent_t>> deferred_free;  // freed once the event completes
   int32_t low_version = 0;                    // versions below are released
-  double t_poll = 0;
+  double t_poll = 0, t_jobs = 0, t_batch = 0, t_look = 0, t_alloc = 0, t_copy = 0, t_launch = 0;
   int64_t perm_at(int32_t ci, int32_t p) const { return p * perm_sum + perm_pre[ci]; }
   int64_t mask_at(int32_t ci, int32_t p) const { return p * mask_sum + mask_pre[ci]; }
   static double now_s() {
@@ -399,6 +401,10 @@ struct DeviceExec {
   }
 
   ~DeviceExec() {
+    if (getenv("FS_ASYNC_PROF"))
+      fprintf(stderr, "async host s: prep %.4f wait %.4f | jobs %.4f batch %.4f (alloc %.4f copy %.4f launch %.4f "
+              "lookahead %.4f) flushes %lld\n", t_prep, t_wait, t_jobs, t_batch, t_alloc, t_copy, t_launch, t_look,
+              (long long)flushes);
     for (cudaStream_t ps : stream_pool) {
       cudaStreamSynchronize(ps);
       cudaStreamDestroy(ps);
@@ -409,6 +415,17 @@ struct DeviceExec {
       cudaEventDestroy(f.second);
     }
     for (auto* h : rec_host) cudaFreeHost(h);
+    if (main_ev) cudaEventDestroy(main_ev);
+    cudaStreamSynchronize(st);
+    for (auto& b : arena_pending) {  // every release is complete after the syncs above
+      cudaEventDestroy(b.ready);
+      arena_free.push_back(ArenaBlock{b.p, b.cls, nullptr});
+    }
+    for (auto& bm : batch_mem) {  // blocks of launches whose rows were never all dropped
+      cudaEventDestroy(bm.end);
+      arena_free.push_back(ArenaBlock{bm.mem, arena_cls[bm.mem], nullptr});
+    }
+    for (auto ev : event_pool) cudaEventDestroy(ev);
     for (auto& b : blocks)
       if (b.ptr) cudaFreeAsync(b.ptr, st);
     if (d_perm) cudaFreeAsync(d_perm, st);
@@ -632,6 +649,11 @@ struct DeviceExec {
   int launch_jobs(fs_async_engine* e) {
     const int32_t nj = (int32_t)e->job_version.size();
     if (nj == 0) return FS_OK;
+    struct Acc {
+      double& t;
+      double t0;
+      ~Acc() { t += now_s() - t0; }
+    } acc_{t_jobs, now_s()};
     const int64_t nrows = e->job_off[nj];
     int32_t max_k = 1;
     for (int32_t j = 0; j < nj; ++j) max_k = std::max<int32_t>(max_k, (int32_t)(e->job_off[j + 1] - e->job_off[j]));
@@ -946,6 +968,11 @@ struct DeviceExec {
 
   // one trainer launch for every pending cycle not launched yet, on its own stream
   int launch_batch(fs_async_engine* e) {
+    struct Acc {
+      double& t;
+      double t0;
+      ~Acc() { t += now_s() - t0; }
+    } acc_{t_batch, now_s()};
     if ((int64_t)launched.size() < (int64_t)e->deferred.size()) {
       const size_t n = e->deferred.size() * 2 + 16;
       row_ptr.resize(n, 0);
@@ -990,12 +1017,6 @@ struct DeviceExec {
     }
     if (side_used)
       if (int rc = cuda(cudaStreamWaitEvent(bs, side_done, 0), "event")) return rc;
-    // versions written by aggregation jobs on the main stream
-    cudaEvent_t main_ev;
-    cudaEventCreateWithFlags(&main_ev, cudaEventDisableTiming);
-    cudaEventRecord(main_ev, st);
-    cudaStreamWaitEvent(bs, main_ev, 0);
-    cudaEventDestroy(main_ev);
     if (!miss_ci.empty()) {
       misses += (int64_t)miss_ci.size();
       // generate() stages through the shared arena; copies go on the batch stream
@@ -1050,7 +1071,16 @@ struct DeviceExec {
     const size_t rows_b = (size_t)k * ldw * esz;
     const size_t status_b = (4 * (size_t)k + 255) / 256 * 256;
     uint8_t* mem = nullptr;
-    if (int rc = cuda(cudaMallocAsync((void**)&mem, meta + wsb + status_b + rows_b, bs), "batch memory")) return rc;
+    double ta = now_s();
+    // allocated (and later freed) on the main stream: the pool then reuses
+    // memory without cross-stream dependencies (allocating on the batch
+    // streams cost ~50-100 us per launch); the batch stream waits for main,
+    // which also orders it after the versions the aggregation jobs wrote
+    if (int rc = arena_get(meta + wsb + status_b + rows_b, &mem)) return rc;
+    if (!main_ev) cudaEventCreateWithFlags(&main_ev, cudaEventDisableTiming);
+    cudaEventRecord(main_ev, st);
+    cudaStreamWaitEvent(bs, main_ev, 0);
+    t_alloc += now_s() - ta;
     std::vector<uint8_t> h(meta);
     size_t o = 0;
     auto put_h = [&](const void* src, size_t n) {
@@ -1065,7 +1095,9 @@ struct DeviceExec {
     const uint64_t ppv = put_h(wpv.data(), 8 * (size_t)k);
     const uint64_t pdn = put_h(dn.data(), 8 * (size_t)k);
     const uint64_t p32 = put_h(i32.data(), 4 * i32.size());
+    ta = now_s();
     if (int rc = cuda(cudaMemcpyAsync(mem, h.data(), meta, cudaMemcpyHostToDevice, bs), "batch metadata")) return rc;
+    t_copy += now_s() - ta;
     int32_t* status = (int32_t*)(mem + meta + wsb);
     if (int rc = cuda(cudaMemsetAsync(status, 0, 4 * (size_t)k, bs), "status")) return rc;
     uint8_t* rows = mem + meta + wsb + status_b;
@@ -1094,7 +1126,9 @@ struct DeviceExec {
     t.align_mode = d.align_mode;
     t.done_tag = 1;
     launches += 1;
+    ta = now_s();
     if (int rc = fs_train_bf16(&t, d.features, (const float*)d.labels, bs)) return rc;
+    t_launch += now_s() - ta;
     // rows stay until aggregated (accepted) or collected (rejected); one block per batch
     blocks.push_back(DevBlock{nullptr, k});
     const int64_t blk = (int64_t)blocks.size() - 1;
@@ -1103,8 +1137,7 @@ struct DeviceExec {
       row_block[ids[i]] = blk;
       launched[ids[i]] = 1;
     }
-    cudaEvent_t end_ev;
-    cudaEventCreateWithFlags(&end_ev, cudaEventDisableTiming);
+    cudaEvent_t end_ev = get_event();
     cudaEventRecord(end_ev, bs);
     batch_mem.push_back({blk, mem, end_ev});
     // lookahead: K2/K3 of every launched client's next cycle
@@ -1115,8 +1148,10 @@ struct DeviceExec {
         ncy.push_back(cyc[i] + 1);
         nsl.push_back(1 - slot[i]);
       }
+    ta = now_s();
     if (!nci.empty())
       if (int rc = generate(nci.data(), ncy.data(), nsl.data(), (int32_t)nci.size(), side)) return rc;
+    t_look += now_s() - ta;
     inflight.push_back(Batch{bs, ids, k});
     flushes += 1;
     return FS_OK;
@@ -1128,6 +1163,73 @@ struct DeviceExec {
     cudaEvent_t end;  // recorded right behind the batch's trainer kernel
   };
   std::vector<BatchMem> batch_mem;
+  cudaEvent_t main_ev = nullptr;
+  // batch memory arena: power-of-two blocks (>= 1 MB) recycled by the host
+  // once the event recorded at their release has completed (stream-ordered
+  // allocations cost ~45 us per launch here)
+  struct ArenaBlock {
+    uint8_t* p;
+    int cls;
+    cudaEvent_t ready;  // null: free now
+  };
+  // process-wide (one device per process): blocks outlive an engine, so a new
+  // run starts warm; the pending list is per engine and drains at destroy
+  static std::vector<ArenaBlock>& arena_free_list() {
+    static std::vector<ArenaBlock> v;
+    return v;
+  }
+  static std::map<uint8_t*, int>& arena_classes() {
+    static std::map<uint8_t*, int> m;
+    return m;
+  }
+  std::vector<ArenaBlock>& arena_free = arena_free_list();
+  std::vector<ArenaBlock> arena_pending;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t ev = event_pool.back();
+      event_pool.pop_back();
+      return ev;
+    }
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    return ev;
+  }
+  static int arena_class(size_t bytes) {
+    int c = 20;
+    while (((size_t)1 << c) < bytes) ++c;
+    return c;
+  }
+  int arena_get(size_t bytes, uint8_t** out) {
+    const int cls = arena_class(bytes);
+    for (size_t i = 0; i < arena_pending.size();) {  // recycle completed releases
+      if (cudaEventQuery(arena_pending[i].ready) == cudaSuccess) {
+        event_pool.push_back(arena_pending[i].ready);
+        arena_pending[i].ready = nullptr;
+        arena_free.push_back(arena_pending[i]);
+        arena_pending[i] = arena_pending.back();
+        arena_pending.pop_back();
+      } else {
+        ++i;
+      }
+    }
+    for (size_t i = 0; i < arena_free.size(); ++i)
+      if (arena_free[i].cls == cls) {
+        *out = arena_free[i].p;
+        arena_free[i] = arena_free.back();
+        arena_free.pop_back();
+        return FS_OK;
+      }
+    if (int rc = cuda(cudaMalloc((void**)out, (size_t)1 << cls), "batch arena")) return rc;
+    arena_cls[*out] = cls;
+    return FS_OK;
+  }
+  std::map<uint8_t*, int>& arena_cls = arena_classes();
+  void arena_release(uint8_t* p) {  // after everything queued on the main stream so far
+    cudaEvent_t ev = get_event();
+    cudaEventRecord(ev, st);
+    arena_pending.push_back(ArenaBlock{p, arena_cls[p], ev});
+  }
 
   void drop_row(int32_t id) {  // the row of a collected cycle is no longer needed
     const int64_t b = row_block[id];
@@ -1139,8 +1241,8 @@ struct DeviceExec {
           // after the aggregations queued on the main stream and the batch's own kernel
           // (whose CTAs still claim work items from the workspace after their last client)
           cudaStreamWaitEvent(st, batch_mem[i].end, 0);
-          cudaEventDestroy(batch_mem[i].end);
-          cudaFreeAsync(batch_mem[i].mem, st);
+          event_pool.push_back(batch_mem[i].end);  // re-recorded only after this wait was queued
+          arena_release(batch_mem[i].mem);
           batch_mem.erase(batch_mem.begin() + i);
           break;
         }
