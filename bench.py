@@ -419,6 +419,46 @@ C5_SHARE = {
 }
 
 
+def measure_small_configs(precision: str):
+    """BASELINE configs[1] (C2: 100 UNSW clients, async_filtered, dynamic batch,
+    delta_sign) and configs[2] (C3: 256 ROAD-shaped CAN-window clients, d = 64,
+    sync_filtered + async_filtered, b = 64): throughput of full runs after a
+    warm-up run, CUDA events on the launching stream."""
+    import torch
+
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    base = {"epochs": 5, "theta": 0.65, "seed": 1, "selection_mode": "delta_sign", "profiles": C4_SYNC["profiles"],
+            "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}}
+    cfgs = {
+        "c2_async": dict(base, num_clients=100, rounds=5, mode="async_filtered",
+                         dataset=C4_SYNC["dataset"], batch=C4_SYNC["batch"]),
+        "c3_sync": dict(base, num_clients=256, rounds=5, mode="sync_filtered", batch={"policy": "fixed", "size": 64},
+                        dataset={"kind": "synthetic", "d": 64, "samples_per_client": 256, "anomaly_frac": 0.1,
+                                 "separation": 2.0, "test_frac": 0.2}),
+    }
+    cfgs["c3_async"] = dict(cfgs["c3_sync"], mode="async_filtered")
+    out = {}
+    for name, cfg in cfgs.items():
+        world, init = build_world(ExperimentConfig.from_dict(cfg), precision=precision)
+        world.device_state()
+        FederationEngine(world).run(init)  # warm-up
+        torch.cuda.synchronize()
+        eng = FederationEngine(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.run(init)
+        b.record()
+        torch.cuda.synchronize()
+        sec = a.elapsed_time(b) / 1e3
+        out[name] = {"clients": cfg["num_clients"], "rounds": cfg["rounds"], "rounds_per_s": cfg["rounds"] / sec,
+                     "client_updates_per_s": eng.trainings / sec, "trainings": eng.trainings,
+                     "digest": eng.timeline.digest()}
+    return out
+
+
 def measure_c5_share(precision: str, rounds: int = 2):
     """BASELINE configs[4] (WIDE MLP 42-1024x4-1, 8192 clients over 8 GPUs):
     the 1024-client share one GPU owns, ~21 rows per client (data scaled 1/8),
@@ -510,9 +550,10 @@ def run_b200(args, rank: int, world_size: int) -> None:
     async_c4 = None
     if world_size == 1 and not args.no_async:
         async_c4 = measure_async(args.precision)
-    c5_share = None
+    c5_share = small = None
     if world_size == 1 and not args.no_c5:
         c5_share = measure_c5_share(args.precision)
+        small = measure_small_configs(args.precision)
     cpu = None
     if world_size == 1 and not args.no_cpu:
         per_round, detail = oracle_round_sample(world, initial, args.cpu_sample)
@@ -544,6 +585,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
         "fp64_parity": parity,
         "async_c4": async_c4,
         "c5_share_1gpu": c5_share,
+        "c2_c3_1gpu": small,
         "cpu_baseline": cpu,
         "gpu_launches": int(m["abi_calls"]),
         "gpu_launches_note": "kernel-launching C-ABI calls in the timed region (a CUB sort counts as one)",
