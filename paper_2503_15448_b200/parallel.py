@@ -88,5 +88,7 @@ class ShardComm:
         import torch.distributed as dist
 
         if not dist.is_initialized():
-            dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+            # FS_DIST_BACKEND=gloo lets several ranks share one GPU (tests)
+            backend = os.environ.get("FS_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+            dist.init_process_group(backend)
         return cls(dist.get_rank(), dist.get_world_size())

@@ -377,3 +377,24 @@ def test_engine_matches_oracle_at_road_shape(mode):
     wg = sim.run(init.values)
     assert eng.timeline.digest() == sim.digest()
     assert rel_err(st.w_g.values, wg) < 1e-12
+
+
+@pytest.mark.parametrize("prec", ["fp64", "bf16"])
+def test_client_sharded_rounds_match_single_process(prec):
+    """Two ranks (sharing the one GPU over gloo) run the client-sharded sync
+    engine (parallel.py: LPT ownership, one packed all-reduce per round) and
+    reproduce the single-process event log and global model."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, FS_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr",
+                          "127.0.0.1", "--master-port", str(port), os.path.join(root, "scripts", "sharded_check.py"),
+                          prec], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert "SHARDED OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
