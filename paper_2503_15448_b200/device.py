@@ -568,7 +568,7 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.status = status.data_ptr()
     desc.grid = TRAIN_GRID
     up = getattr(plan.shards, "upload", None)  # a chunked upload still in flight (DeviceWorld.refill)
-    if up is not None and up["pending"]:
+    if up is not None and up["pending"] and up["flags"] is not None:
         if bf16 and plan.chunk_p is not None and eval_bf16_supported(dims):
             desc.data_flags = up["flags"].data_ptr()
             desc.data_chunk = plan.chunk_p
