@@ -17,8 +17,10 @@ from paper_2503_15448_b200.parallel import ShardComm  # noqa: E402
 from paper_2503_15448_b200.server import FederationEngine  # noqa: E402
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp64"
+mode = sys.argv[2] if len(sys.argv) > 2 else "sync_filtered"
+sel = sys.argv[3] if len(sys.argv) > 3 else "delta_sign"
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
-cfg = {"num_clients": 40, "rounds": 3, "epochs": 1, "mode": "sync_filtered", "selection_mode": "delta_sign",
+cfg = {"num_clients": 40, "rounds": 3, "epochs": 1, "mode": mode, "selection_mode": sel,
        "dataset": {"n": 12000, "d": 42}, "batch": {"policy": "dynamic"}, "seed": 11,
        "profiles": {"speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
                     "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
@@ -37,7 +39,8 @@ if comm is None or comm.rank == 0:
     err = float(np.max(np.abs(wg - st1.w_g.values) / np.maximum(np.abs(st1.w_g.values), 1.0)))
     same_log = digest == ref.timeline.digest()
     tol = 1e-12 if prec == "fp64" else 1e-5
-    print(f"SHARDED {prec} ranks={comm.size if comm else 1} digest_equal={same_log} max_rel_err={err:.3e}")
+    print(f"SHARDED {prec} {mode} {sel} ranks={comm.size if comm else 1} digest_equal={same_log} "
+          f"max_rel_err={err:.3e} trainings={eng.trainings}")
     assert same_log, "sharded event log differs from the single-process run"
     assert err < tol, f"sharded global model differs ({err:.3e})"
     print("SHARDED OK")
