@@ -319,6 +319,15 @@ def measure_e2e(world, eng, state, reps: int, barrier):
     return 1000.0 / float(np.mean(e2e_ms)), int(h2d), int(d2h)
 
 
+def _ncu_traffic():
+    """dram__bytes_read+write of the trainer from the committed ncu capture (per launch)."""
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_train_kernel.json")
+    try:
+        return json.load(open(f))["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = None, reps: int = 10):
     """K6/K7 standalone (default: the C5 WIDE-MLP row length), float32 rows,
     `n_agg` of the rows aggregated: achieved GB/s. Arguments are staged on the
@@ -373,11 +382,12 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = N
     return out
 
 
-def measure_async(precision: str, windows: int = 2):
+def measure_async(precision: str, windows: int = 2, reps: int = 5):
     """C4 `async_filtered` (the reference's buffered asynchronous engine: C++
     event loop driving the device executor, deferred batched training): windows
     of 1024 applied updates per second. One untimed warm-up run first (module
-    load, memory pools), then the timed run, CUDA events on the launching stream."""
+    load, memory pools), then `reps` timed runs (median reported: single runs
+    vary 0.14-0.6 s with host scheduling), CUDA events on the launching stream."""
     import torch
 
     from paper_2503_15448_b200.config import ExperimentConfig
@@ -388,17 +398,22 @@ def measure_async(precision: str, windows: int = 2):
     cfg.update({"mode": "async_filtered", "rounds": windows})
     world, init = build_world(ExperimentConfig.from_dict(cfg), precision=precision)
     world.device_state()
-    FederationEngine(world).run(init)  # warm-up
+    for _ in range(2):  # warm-up (module load, memory arena, pools)
+        FederationEngine(world).run(init)
     torch.cuda.synchronize()
-    eng = FederationEngine(world)
     stream = torch.cuda.current_stream()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    eng.run(init)
-    b.record(stream)
-    torch.cuda.synchronize()
-    sec = a.elapsed_time(b) / 1e3
+    runs = []
+    for _ in range(reps):
+        eng = FederationEngine(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.run(init)
+        b.record(stream)
+        torch.cuda.synchronize()
+        runs.append(a.elapsed_time(b) / 1e3)
+    sec = float(np.median(runs))
     return {"value": windows / sec, "unit": "rounds/s (windows of 1024 applied updates)",
+            "run_s": runs, "statistic": f"median of {reps} full runs (each {windows} windows)",
             "client_updates_per_s": eng.trainings / sec, "trainings": eng.trainings,
             "device_batches": eng.device_batches, "events": len(eng.timeline.log), "windows": windows,
             "precision": precision, "gpu_launches": getattr(eng, "async_launches", None),
@@ -531,7 +546,9 @@ def run_b200(args, rank: int, world_size: int) -> None:
         roofline = {"kernel": "fs::f64::train_kernel (K5, fp64 parity)", "bound": "fp64"}
     roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if achieved else None, "peak_source": src,
-                     "traffic": None, "algorithmic_flops_per_launch": tr.get("work_per_launch"),
+                     "traffic": _ncu_traffic() if args.precision == "bf16" else None,
+                     "traffic_source": "profiles/r1_ncu_train_kernel.json (dram read+write bytes, one ncu --set full launch)",
+                     "algorithmic_flops_per_launch": tr.get("work_per_launch"),
                      "share_of_round": tr.get("total_ms", 0.0) / (m["ms_per_round"] * args.steps) if tr else None})
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     kernels = {}

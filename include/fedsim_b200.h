@@ -292,6 +292,10 @@ int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes,
 size_t fs_eval_workspace_bytes(int32_t n);
 int fs_eval_metrics(const double* scores, const int8_t* labels, int32_t n, double threshold,
                     int64_t* counts_out, void* workspace, size_t workspace_bytes, void* stream);
+/* Same counts when every score is a widened float (the bf16 evaluation,
+ * fs_forward_bf16): ranks on float keys, half the radix-sort passes.      */
+int fs_eval_metrics_f32(const double* scores, const int8_t* labels, int32_t n, double threshold,
+                        int64_t* counts_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- f2 async event engine
  * Host-side (all pointers HOST memory; no CUDA): the event loop of

@@ -130,6 +130,7 @@ _SIGNATURES = {
     "fs_mean_finish": (ctypes.c_int, [_c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_eval_workspace_bytes": (_c_sz, [_c_i32]),
     "fs_eval_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_f64, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "fs_eval_metrics_f32": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_f64, _c_vp, _c_vp, _c_sz, _c_vp]),
 }
 
 # host event engine (bound with its ctypes structs in async_loop.py)

@@ -403,8 +403,8 @@ struct DeviceExec {
   ~DeviceExec() {
     if (getenv("FS_ASYNC_PROF"))
       fprintf(stderr, "async host s: prep %.4f wait %.4f | jobs %.4f batch %.4f (alloc %.4f copy %.4f launch %.4f "
-              "lookahead %.4f) flushes %lld\n", t_prep, t_wait, t_jobs, t_batch, t_alloc, t_copy, t_launch, t_look,
-              (long long)flushes);
+              "lookahead %.4f) flushes %lld arena mallocs %lld\n", t_prep, t_wait, t_jobs, t_batch, t_alloc, t_copy,
+              t_launch, t_look, (long long)flushes, (long long)arena_mallocs);
     for (cudaStream_t ps : stream_pool) {
       cudaStreamSynchronize(ps);
       cudaStreamDestroy(ps);
@@ -1213,18 +1213,26 @@ struct DeviceExec {
         ++i;
       }
     }
+    // the smallest free block that fits (at most 4x the request): a fresh
+    // cudaMalloc costs ~0.1-1 ms and synchronises with the device
+    size_t best = arena_free.size();
     for (size_t i = 0; i < arena_free.size(); ++i)
-      if (arena_free[i].cls == cls) {
-        *out = arena_free[i].p;
-        arena_free[i] = arena_free.back();
-        arena_free.pop_back();
-        return FS_OK;
-      }
+      if (arena_free[i].cls >= cls && arena_free[i].cls <= cls + 2 &&
+          (best == arena_free.size() || arena_free[i].cls < arena_free[best].cls))
+        best = i;
+    if (best < arena_free.size()) {
+      *out = arena_free[best].p;
+      arena_free[best] = arena_free.back();
+      arena_free.pop_back();
+      return FS_OK;
+    }
+    ++arena_mallocs;
     if (int rc = cuda(cudaMalloc((void**)out, (size_t)1 << cls), "batch arena")) return rc;
     arena_cls[*out] = cls;
     return FS_OK;
   }
   std::map<uint8_t*, int>& arena_cls = arena_classes();
+  int64_t arena_mallocs = 0;
   void arena_release(uint8_t* p) {  // after everything queued on the main stream so far
     cudaEvent_t ev = get_event();
     cudaEventRecord(ev, st);

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -335,6 +336,11 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
         w_out=w_out, rt=rt)
 
 
+# launch K3 before K2 when building a plan (FS_K3_FIRST=1; measured: the trainer
+# then slows by as much as the round tail gains)
+K3_FIRST = os.environ.get("FS_K3_FIRST", "0") == "1"
+
+
 class TrainPlan:
     """The data-independent half of a training launch: per-request metadata in
     HBM plus the K2 permutations and K3 dropout keep-bits. It depends only on
@@ -344,12 +350,16 @@ class TrainPlan:
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
                  dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
+                 mask_stream=None,
                  pool: dict | None = None, stage: "Stage | None" = None, defer_masks: bool = False,
                  data_chunk: np.ndarray | None = None):
         rt = rt or Runtime.get()
         self.rt = rt
         self.stage = stage
         self.mask_flags = None   # set when K3 runs later, concurrently with the trainer (launch_masks)
+        self._desc = None        # (precision, static TrainDesc) built by static_desc()
+        self.workspace_need = 0
+        self.prefilled = None    # (precision, lr, desc, w_out, status, run) prepared by prefill()
         self.mask_tag = 0
         lib = rt.lib
         self.dims = tuple(int(x) for x in spec_dims)
@@ -366,6 +376,7 @@ class TrainPlan:
         if n == 0:
             return
         torch_stream = stream if stream is not None else torch.cuda.current_stream(rt.device)
+        self.stream = torch_stream
         s_handle = torch_stream.cuda_stream
         sum_hidden = sum(self.dims[1:-1])
         n_rows = shards.n_rows[cl].astype(np.int64)
@@ -434,14 +445,44 @@ class TrainPlan:
         self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
         self.n_rows_p, self.batch_p, self.start_p, self.end_p, self.order_p = (p32 + 4 * n * k for k in range(5))
         self.chunk_p = p32 + 4 * n * 5 if self.has_chunks else None
-        if self.epochs > 0:
-            rt.call(lib.fs_shuffle_perms(self.seeds_p, self.n_rows_p, self.perm_off_p, n, self.epochs,
-                                         int(n_rows.max()), self.perm.data_ptr(), s_handle), "fs_shuffle_perms")
+        k3_stream = torch_stream
+        if mask_stream is not None and use_masks and self.epochs > 0 and not defer_masks:
+            # K3 (ALU-bound) and K2 (latency-bound) are independent: run them
+            # side by side so both finish under the trainer they overlap
+            copied = torch.cuda.Event()
+            copied.record(torch_stream)
+            mask_stream.wait_event(copied)
+            k3_stream = mask_stream
         self.scale = 1.0
         self.max_steps = int(end.max()) if n else 0
         self.sum_hidden = sum_hidden
+        keep = 1.0 - self.dropout_rate
+        k3_now = self.bits is not None and not defer_masks
+
+        def launch_k2():
+            if self.epochs > 0:
+                rt.call(lib.fs_shuffle_perms(self.seeds_p, self.n_rows_p, self.perm_off_p, n, self.epochs,
+                                             int(n_rows.max()), self.perm.data_ptr(), s_handle), "fs_shuffle_perms")
+
+        def launch_k3():
+            rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n,
+                                        self.epochs, sum_hidden, keep, self.bits.data_ptr(),
+                                        k3_stream.cuda_stream), "fs_dropout_bits")
+            if k3_stream is not torch_stream:
+                masks_done = torch.cuda.Event()
+                masks_done.record(k3_stream)
+                torch_stream.wait_event(masks_done)
+
+        # K3 (the longer, ALU-bound one) first: the block scheduler drains one
+        # kernel's CTAs before the next, so the order decides which starts under the trainer
+        if k3_now and K3_FIRST:
+            launch_k3()
+            launch_k2()
+        else:
+            launch_k2()
+            if k3_now:
+                launch_k3()
         if self.bits is not None:
-            keep = 1.0 - self.dropout_rate
             self.scale = 1.0 / keep
             if defer_masks:
                 # K3 is launched with the trainer (launch_masks); steps are
@@ -453,13 +494,82 @@ class TrainPlan:
                     if pool is not None:
                         pool["flags"] = flags
                 self.mask_flags = flags
-            else:
-                rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n,
-                                            self.epochs, sum_hidden, keep, self.bits.data_ptr(), s_handle),
-                        "fs_dropout_bits")
         if stream is not None:  # consumer stream waits on this event before the trainer reads the plan
             self.ready = torch.cuda.Event()
             self.ready.record(torch_stream)
+
+    def prefill(self, lr: float, precision: str) -> None:
+        """Prepare the whole launch of a plan that one sync round will run with
+        one step size: broadcast `lr` into the pooled lr buffer and zero the
+        pooled status on the plan's own stream (before `ready`), and build the
+        complete descriptor over pooled output rows and workspace. The round
+        then launches its trainer with one fill (the start-model pointers) and
+        no descriptor work. Pools alternate by round parity (engine), so a
+        round's rows are dead before the same pool is prepared again."""
+        if not self.pooled or self.n == 0 or self.ready is None:
+            return
+        lib, st = self.rt.lib, self.stream.cuda_stream
+        with torch.cuda.stream(self.stream):  # allocated where written: a block the caching
+            # allocator hands out on another stream may still be read by that stream's queued work
+            d_lr = self.pool_buf("lr", self.n * max(self.epochs, 1), torch.float64)
+            d_st = self.pool_buf("status", self.n, torch.int32)
+        self.rt.call(lib.fs_fill_u64(d_lr.data_ptr(), int(np.float64(lr).view(np.uint64)), d_lr.numel(), st),
+                     "fs_fill_u64")
+        self.rt.call(lib.fs_fill_u64(d_st.data_ptr(), 0, (self.n + 1) // 2, st), "fs_fill_u64")
+        self.ready.record(self.stream)
+        # output rows and workspace: written and read by the consuming (current) stream
+        bf16 = precision == "bf16"
+        M = sum((a + 1) * b for a, b in zip(self.dims[:-1], self.dims[1:]))
+        esz = 4 if bf16 else 8
+        ld = (M * esz + 127) // 128 * 128 // esz
+        w_out = self.pool_buf("w_out", self.n * ld, torch.float32 if bf16 else torch.float64).view(self.n, ld)[:, :M]
+        desc = N.TrainDesc.from_buffer_copy(self.static_desc(precision))
+        ws = self.pool_buf("train_ws", self.workspace_need, torch.uint8)
+        d_run = self.pool_buf("run", self.n, torch.int64)
+        desc.lr, desc.status = d_lr.data_ptr(), d_st.data_ptr()
+        desc.w_out, desc.ldw = w_out.data_ptr(), w_out.stride(0)
+        desc.workspace, desc.workspace_bytes = ws.data_ptr(), ws.numel()
+        desc.w_start = d_run.data_ptr()
+        self.prefilled = (precision, float(lr), desc, w_out, d_st, d_run)
+
+    def static_desc(self, precision: str) -> "N.TrainDesc":
+        """The launch descriptor fields fixed by the plan (geometry, plan
+        buffers, grid) and the trainer's workspace size, built once per plan:
+        the engines call this while prefetching, off the round's critical path."""
+        if self._desc is not None and self._desc[0] == precision:
+            return self._desc[1]
+        bf16 = precision == "bf16"
+        if not bf16 and self.shards.features is None:
+            raise ValueError("these shards hold bf16 features only (tensor-core trainer input)")
+        desc = N.TrainDesc()
+        desc.n_dims = len(self.dims)
+        for i, v in enumerate(self.dims):
+            desc.dims[i] = v
+        desc.n_req = self.n
+        desc.epochs = self.epochs
+        desc.max_batch = int(self.batch.max())
+        desc.mask_mode = N.FS_MASK_BITS if self.bits is not None else N.FS_MASK_NONE
+        desc.scale = self.scale
+        desc.features = self.shards.features.data_ptr() if self.shards.features is not None else None
+        desc.labels = self.shards.labels.data_ptr() if self.shards.labels is not None else None
+        desc.row_off = self.row_off_p
+        desc.n_rows = self.n_rows_p
+        desc.batch = self.batch_p
+        desc.perm = self.perm.data_ptr()
+        desc.perm_off = self.perm_off_p
+        desc.mask_bits = self.bits.data_ptr() if self.bits is not None else None
+        desc.mask_off = self.mask_off_p
+        desc.start_step = self.start_p
+        desc.end_step = self.end_p
+        desc.order = self.order_p
+        desc.grid = TRAIN_GRID
+        lib = self.rt.lib
+        need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
+        if need == 0:
+            raise ValueError(f"layer dims {self.dims} are not supported by the {precision} trainer")
+        self.workspace_need = need
+        self._desc = (precision, desc)
+        return desc
 
     def pool_buf(self, name: str, n_elems: int, dtype) -> torch.Tensor:
         """A pooled device buffer owned by this plan's pool (stream-ordered reuse)."""
@@ -495,6 +605,38 @@ class TrainPlan:
             self.ready = None
 
 
+def _upload_waits(plan: TrainPlan, desc, up: dict, bf16: bool, stream) -> None:
+    """Order the trainer after a chunked shard upload still in flight
+    (DeviceWorld.refill): per-client chunk flags for the tcgen05 trainer,
+    the whole upload for the others. An upload without flags carries only
+    the test set (the shards went up on the trainer's own stream)."""
+    if up["flags"] is None:
+        return
+    if bf16 and plan.chunk_p is not None and eval_bf16_supported(plan.dims):
+        desc.data_flags = up["flags"].data_ptr()
+        desc.data_chunk = plan.chunk_p
+        desc.data_tag = up["tag"]
+    else:
+        stream.wait_event(up["done"])
+
+
+def _launch_trainer(plan: TrainPlan, desc, bf16: bool, stream) -> None:
+    rt, lib, dims = plan.rt, plan.rt.lib, plan.dims
+    work = 0.0
+    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
+        s, e, spe, b, nr = plan.start, plan.end, plan.spe, plan.batch, plan.n_rows
+        last = e // spe - s // spe   # epoch-final (partial) steps in [start, end)
+        rows = (e - s - last) * b + last * (nr - (spe - 1) * b)
+        work = float(rows.sum()) * mlp_flops_per_sample(dims)
+    with rt.timed("train", work):
+        if bf16:
+            xb, yf = plan.shards.bf16()
+            rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream.cuda_stream),
+                    "fs_train_bf16")
+        else:
+            rt.call(lib.fs_train_f64(ctypes.byref(desc), stream.cuda_stream), "fs_train_f64")
+
+
 def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision: str = "fp64",
                 w_out: torch.Tensor | None = None, status: torch.Tensor | None = None):
     """K5 over a prepared plan: lr [n x epochs], w_start [n] device pointers.
@@ -505,6 +647,20 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     dims = plan.dims
     M = sum((a + 1) * b for a, b in zip(dims[:-1], dims[1:]))
     bf16 = precision == "bf16"
+    pre = plan.prefilled
+    up = getattr(plan.shards, "upload", None)  # a chunked upload still in flight (DeviceWorld.refill)
+    if (pre is not None and pre[0] == precision and w_out is None and status is None and np.ndim(lr) == 0
+            and float(lr) == pre[1] and np.ndim(w_start) == 0 and plan.mask_flags is None):
+        # the launch prepared while this plan was prefetched (TrainPlan.prefill)
+        desc, w_out, status, d_run = pre[2], pre[3], pre[4], pre[5]
+        stream = torch.cuda.current_stream(rt.device)
+        plan.consume(stream)
+        desc.data_flags, desc.data_chunk, desc.data_tag = None, None, 0
+        if up is not None and up["pending"]:
+            _upload_waits(plan, desc, up, bf16, stream)
+        rt.call(lib.fs_fill_u64(d_run.data_ptr(), int(w_start), n, stream.cuda_stream), "fs_fill_u64")
+        _launch_trainer(plan, desc, bf16, stream)
+        return w_out, status
     if w_out is None:
         # rows padded to 128 bytes: 16-byte vector access to every client row
         esz = 4 if bf16 else 8
@@ -538,68 +694,24 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         d_run = rt.h2d(np.array(w_arr, dtype=np.uint64).view(np.int64))  # writable copies of the views
         d_lr = rt.h2d(np.array(lr_arr, dtype=np.float64))
         run_p, lr_p = d_run.data_ptr(), d_lr.data_ptr()
-    desc = N.TrainDesc()
-    desc.n_dims = len(dims)
-    for i, v in enumerate(dims):
-        desc.dims[i] = v
-    desc.n_req = n
-    desc.epochs = plan.epochs
-    desc.max_batch = int(plan.batch.max())
-    desc.mask_mode = N.FS_MASK_BITS if plan.bits is not None else N.FS_MASK_NONE
-    desc.scale = plan.scale
-    if not bf16 and plan.shards.features is None:
-        raise ValueError("these shards hold bf16 features only (tensor-core trainer input)")
-    desc.features = plan.shards.features.data_ptr() if plan.shards.features is not None else None
-    desc.labels = plan.shards.labels.data_ptr() if plan.shards.labels is not None else None
-    desc.row_off = plan.row_off_p
-    desc.n_rows = plan.n_rows_p
-    desc.batch = plan.batch_p
+    desc = N.TrainDesc.from_buffer_copy(plan.static_desc(precision))
     desc.lr = lr_p
     desc.w_start = run_p
     desc.w_out = w_out.data_ptr()
     desc.ldw = w_out.stride(0)
-    desc.perm = plan.perm.data_ptr()
-    desc.perm_off = plan.perm_off_p
-    desc.mask_bits = plan.bits.data_ptr() if plan.bits is not None else None
-    desc.mask_off = plan.mask_off_p
-    desc.start_step = plan.start_p
-    desc.end_step = plan.end_p
-    desc.order = plan.order_p
     desc.status = status.data_ptr()
-    desc.grid = TRAIN_GRID
-    up = getattr(plan.shards, "upload", None)  # a chunked upload still in flight (DeviceWorld.refill)
-    if up is not None and up["pending"] and up["flags"] is not None:
-        if bf16 and plan.chunk_p is not None and eval_bf16_supported(dims):
-            desc.data_flags = up["flags"].data_ptr()
-            desc.data_chunk = plan.chunk_p
-            desc.data_tag = up["tag"]
-        else:  # trainers without per-client data waits take the whole upload first
-            stream.wait_event(up["done"])
+    if up is not None and up["pending"]:
+        _upload_waits(plan, desc, up, bf16, stream)
     if plan.mask_flags is not None:
         if not plan.mask_tag:
             raise ValueError("deferred keep bits: launch_masks() must run before the trainer")
         desc.mask_flags = plan.mask_flags.data_ptr()
         desc.mask_tag = plan.mask_tag
         desc.max_steps = plan.max_steps
-    need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
-    if need == 0:
-        raise ValueError(f"layer dims {dims} are not supported by the {precision} trainer")
-    ws = rt.scratch("train", need)
+    ws = rt.scratch("train", plan.workspace_need)
     desc.workspace = ws.data_ptr()
     desc.workspace_bytes = ws.numel()
-    work = 0.0
-    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
-        s, e, spe, b, nr = plan.start, plan.end, plan.spe, plan.batch, plan.n_rows
-        last = e // spe - s // spe   # epoch-final (partial) steps in [start, end)
-        rows = (e - s - last) * b + last * (nr - (spe - 1) * b)
-        work = float(rows.sum()) * mlp_flops_per_sample(dims)
-    with rt.timed("train", work):
-        if bf16:
-            xb, yf = plan.shards.bf16()
-            rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream.cuda_stream),
-                    "fs_train_bf16")
-        else:
-            rt.call(lib.fs_train_f64(ctypes.byref(desc), stream.cuda_stream), "fs_train_f64")
+    _launch_trainer(plan, desc, bf16, stream)
     return w_out, status
 
 
@@ -843,15 +955,18 @@ def forward_probs_bf16(spec_dims, w32: torch.Tensor, xb: torch.Tensor, rt: Runti
     return probs
 
 
-def eval_counts(scores: torch.Tensor, labels_i8: torch.Tensor, threshold: float, rt: Runtime | None = None) -> torch.Tensor:
-    """K8 metrics: device int64 [3] = (#correct, 2*U_pos, n_pos)."""
+def eval_counts(scores: torch.Tensor, labels_i8: torch.Tensor, threshold: float, rt: Runtime | None = None,
+                f32_scores: bool = False) -> torch.Tensor:
+    """K8 metrics: device int64 [3] = (#correct, 2*U_pos, n_pos). `f32_scores`:
+    every score is a widened float (bf16 evaluation), ranked on float keys."""
     rt = rt or Runtime.get()
     n = scores.shape[0]
     out = torch.empty(3, dtype=torch.int64, device=rt.device)
     need = rt.lib.fs_eval_workspace_bytes(n)
     ws = rt.scratch("eval", need)
-    rt.call(rt.lib.fs_eval_metrics(scores.data_ptr(), labels_i8.data_ptr(), n, float(threshold),
-                                   out.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream), "fs_eval_metrics")
+    fn = rt.lib.fs_eval_metrics_f32 if f32_scores else rt.lib.fs_eval_metrics
+    rt.call(fn(scores.data_ptr(), labels_i8.data_ptr(), n, float(threshold),
+               out.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream), "fs_eval_metrics")
     return out
 
 

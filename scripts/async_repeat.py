@@ -16,7 +16,7 @@ cfg = dict(bench.C4_SYNC)
 cfg.update({"mode": "async_filtered", "rounds": 2})
 world, init = build_world(ExperimentConfig.from_dict(cfg), precision=prec)
 world.device_state()
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     eng = FederationEngine(world)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -1,7 +1,9 @@
-"""Host/device timeline of one C4 sync round (diagnostic)."""
+"""Device timeline of C4 bf16 sync rounds (kernel start/end per stream) via
+torch.profiler/CUPTI: where the round's time goes besides the trainer
+(diagnostic; timings under the profiler are not bench values)."""
+import json
 import os
 import sys
-import time
 
 import torch
 
@@ -9,32 +11,34 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2503_15448_b200.server import FederationEngine, GlobalState  # noqa: E402
 
-prec = sys.argv[1] if len(sys.argv) > 1 else "bf16"
-world, init = bench.build_c4_world(precision=prec)
+world, init = bench.build_c4_world(precision="bf16")
 eng = FederationEngine(world)
-st = GlobalState(round=0, w_g=init)
-for _ in range(3):
-    st = eng.run_sync_round(st)
+state = GlobalState(round=0, w_g=init)
+for _ in range(4):
+    state = eng.run_sync_round(state)
 torch.cuda.synchronize()
-E2E = os.environ.get("E2E") == "1"  # rebuild the device world from host memory each round
-if E2E:
-    world.host_pack()
-for rep in range(2):
-    eng.trace = []
-    t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    if E2E:
-        world._device = None
-        world.device_state()
-        eng._mark("device world rebuilt")
-    st = eng.run_sync_round(st)
-    if E2E:
-        _ = st.w_g.values
-    e1 = torch.cuda.Event(enable_timing=True)
-    e1.record()
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    print(f"round: host {1e3 * (t1 - t0):.2f} ms, device {e0.elapsed_time(e1):.2f} ms")
-    for label, th, ev in eng.trace:
-        print(f"  {label:36s} host +{1e3 * (th - t0):7.2f} ms   device-queue +{e0.elapsed_time(ev):7.2f} ms")
+l2 = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    for _ in range(3):
+        l2.add_(1)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("round")
+        state = eng.run_sync_round(state)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+out = os.path.join("gpurun_out", "round_trace.json")
+prof.export_chrome_trace(out)
+ev = json.load(open(out))["traceEvents"]
+keep = []
+for e in ev:
+    if e.get("ph") != "X":
+        continue
+    cat = e.get("cat", "")
+    if cat in ("kernel", "gpu_memcpy", "gpu_memset", "cuda_runtime", "cuda_driver"):
+        keep.append({"cat": cat, "name": e["name"][:70], "ts": e["ts"], "dur": e["dur"],
+                     "stream": e.get("args", {}).get("stream"), "tid": e.get("tid")})
+keep.sort(key=lambda e: e["ts"])
+json.dump(keep, open(os.path.join("gpurun_out", "round_trace_slim.json"), "w"))
+print(len(keep), "events")

@@ -287,3 +287,25 @@ def test_wide_eval_forward_tracks_fp64(dims):
     p16 = D.forward_probs_wide(spec.dims, w32, xb, rt).cpu().numpy()
     assert np.max(np.abs(p16 - p64)) < 2e-2
     assert np.mean(np.abs(p16 - p64)) < 3e-3
+
+
+@pytest.mark.parametrize("n,levels", [(1, 5), (257, 7), (43835, 1 << 20), (100003, 64)])
+def test_eval_metrics_f32_keys_match_f64_keys(n, levels):
+    """fs_eval_metrics_f32 (float ranking keys, 4 radix passes) gives the same
+    exact counts as fs_eval_metrics on widened-float scores, ties included."""
+    from paper_2503_15448_b200 import device as D
+
+    rt = D.Runtime.get()
+    g = np.random.default_rng(n)
+    s32 = (g.integers(0, levels, n) / levels).astype(np.float32)  # few levels: many ties
+    s32[g.random(n) < 0.05] = np.float32(1.0)
+    y = (g.random(n) < 0.3).astype(np.int8)
+    y[0] = 1
+    if n > 1:
+        y[1] = 0
+    sd = torch.tensor(s32.astype(np.float64), device="cuda")
+    yd = torch.tensor(y, device="cuda")
+    for thr in (0.5, float(s32[0])):
+        a = D.eval_counts(sd, yd, thr, rt).cpu().numpy()
+        b = D.eval_counts(sd, yd, thr, rt, f32_scores=True).cpu().numpy()
+        assert np.array_equal(a, b), (a, b)
