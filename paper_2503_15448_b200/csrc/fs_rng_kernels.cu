@@ -310,11 +310,15 @@ extern "C" int fs_shuffle_perms(const uint64_t* seeds, const int32_t* n_rows,
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0) return FS_OK;
+  // FS_K2_SMEM=0 swaps in the output itself (L1/L2) with one-warp CTAs
+  // instead of staging in shared memory, so more chains co-reside with the
+  // trainer; measured equal in the C4 round (the chains are latency-bound)
+  static const int staged = getenv("FS_K2_SMEM") ? atoi(getenv("FS_K2_SMEM")) : 1;
   const size_t smem = (size_t)max_rows * sizeof(int32_t);
-  const int use_smem = smem <= 200 * 1024;
+  const int use_smem = staged && smem <= 200 * 1024;
   if (use_smem && smem > 48 * 1024)
     ensure_smem(shuffle_kernel, (int)smem);
-  shuffle_kernel<<<n_req * epochs, 128, use_smem ? smem : 0, (cudaStream_t)stream>>>(
+  shuffle_kernel<<<n_req * epochs, use_smem ? 128 : 32, use_smem ? smem : 0, (cudaStream_t)stream>>>(
       seeds, n_rows, perm_off, epochs, perm_out, use_smem);
   return check_launch("shuffle_kernel");
 }
