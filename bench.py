@@ -508,6 +508,40 @@ def measure_c5_share(precision: str, rounds: int = 2):
             else "fp64 parity trainer"}
 
 
+def measure_c5_async_share(precision: str):
+    """BASELINE configs[4] is async_filtered: the same 1024-client WIDE share
+    through the async engine (C++ event loop + device executor driving the
+    batched-GEMM trainer), one window; after a warm-up run on a 64-client world.
+    Reported as client-updates/s (delta_sign rejects most WIDE updates, so the
+    run ends at the reference's cycle budget before the window fills)."""
+    import torch
+
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    warm = dict(C5_SHARE, mode="async_filtered", rounds=1, num_clients=64)
+    warm["dataset"] = dict(C5_SHARE["dataset"], n=219176 * 64 // 8192)
+    w, i = build_world(ExperimentConfig.from_dict(warm), precision=precision)
+    FederationEngine(w).run(i)
+    world, init = build_world(ExperimentConfig.from_dict(dict(C5_SHARE, mode="async_filtered", rounds=1)),
+                              precision=precision)
+    world.device_state()
+    torch.cuda.synchronize()
+    eng = FederationEngine(world)
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    eng.run(init)
+    b.record(stream)
+    torch.cuda.synchronize()
+    sec = a.elapsed_time(b) / 1e3
+    return {"workload": "C5 share, async_filtered: 1024 clients, WIDE MLP, 1 window",
+            "client_updates_per_s": eng.trainings / sec, "trainings": eng.trainings, "seconds": sec,
+            "windows_completed": len(eng.reports), "device_batches": eng.device_batches,
+            "digest": eng.timeline.digest()}
+
+
 def run_b200(args, rank: int, world_size: int) -> None:
     import torch
 
@@ -570,6 +604,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
     c5_share = small = None
     if world_size == 1 and not args.no_c5:
         c5_share = measure_c5_share(args.precision)
+        c5_share["async"] = measure_c5_async_share(args.precision)
         small = measure_small_configs(args.precision)
     cpu = None
     if world_size == 1 and not args.no_cpu:

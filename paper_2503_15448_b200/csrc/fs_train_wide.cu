@@ -47,6 +47,11 @@ struct Geo {
   size_t x_off, h_off[MAXL], d_off[MAXL], t_off, y_off, z_off;  // byte offsets inside a slot
 };
 
+// head-logit partials per row: one per warp of the last forward epilogue's
+// grid (256-thread blocks over the last hidden width), summed in a fixed order
+// by the consumer so the logits do not depend on atomic arrival order
+__host__ __device__ __forceinline__ int zparts(int n_last) { return (n_last + 255) / 256 * 8; }
+
 static bool make(const fs_train_desc* d, Geo* g) {
   if (make_layout(d->dims, d->n_dims, &g->lay) != FS_OK) return false;
   const MlpLayout& L = g->lay;
@@ -78,7 +83,7 @@ static bool make(const fs_train_desc* d, Geo* g) {
   }
   g->t_off = take((size_t)g->rb * L.max_hidden * 4);
   g->y_off = take((size_t)g->rb * 4 * 2);  // labels, dz
-  g->z_off = take((size_t)g->rb * 4);      // head logits, accumulated by the last forward epilogue
+  g->z_off = take((size_t)g->rb * zparts(L.f[L.L - 1]) * 4);  // head-logit partials (last forward epilogue)
   g->slot_bytes = (s + 255) / 256 * 256;
   return true;
 }
@@ -198,11 +203,7 @@ __global__ void gather_kernel(StepArgs a, const StepRow* rows) {
     if (r < sr.rows) v = *reinterpret_cast<const uint4*>(a.feat + (base + perm[r]) * a.dp + c * 8);
     *reinterpret_cast<uint4*>(x + (int64_t)r * a.dp + c * 8) = v;
   }
-  float* z = reinterpret_cast<float*>(sb + a.z_off);
-  for (int r = threadIdx.x; r < a.rb; r += blockDim.x) {
-    y[r] = r < sr.rows ? a.labels[base + perm[r]] : 0.f;
-    z[r] = 0.f;
-  }
+  for (int r = threadIdx.x; r < a.rb; r += blockDim.x) y[r] = r < sr.rows ? a.labels[base + perm[r]] : 0.f;
 }
 
 __device__ __forceinline__ bool keep_bit(const StepArgs& a, const StepRow& sr, int l, int r, int u) {
@@ -215,8 +216,8 @@ __device__ __forceinline__ bool keep_bit(const StepArgs& a, const StepRow& sr, i
 }
 
 // H_l = relu(Z + b_{l-1}) * keep * scale  (bf16), Z in the fp32 temp. The
-// last hidden layer also accumulates the head logits from the fp32 values
-// (as the on-chip trainers do): z[r] += sum_u H[r][u] w_h[u].
+// last hidden layer also forms the head logits from the fp32 values (as the
+// on-chip trainers do): per-warp partials of sum_u H[r][u] w_h[u].
 __global__ void fwd_epilogue_kernel(StepArgs a, const StepRow* rows, int l) {
   const StepRow sr = rows[blockIdx.y];
   const int N = a.lay.f[l];
@@ -240,7 +241,7 @@ __global__ void fwd_epilogue_kernel(StepArgs a, const StepRow* rows, int l) {
     if (last && r < sr.rows) {
       float p = v * wh;
       for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      if ((threadIdx.x & 31) == 0) atomicAdd(zacc + r, p);
+      if ((threadIdx.x & 31) == 0) zacc[(int64_t)r * zparts(N) + blockIdx.x * 8 + (threadIdx.x >> 5)] = p;
     }
   }
 }
@@ -265,7 +266,10 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   for (int r = threadIdx.x; r < a.rb; r += blockDim.x) {
     float d = 0.f;
     if (r < sr.rows) {
-      const float z = zacc[r] + bh[0];
+      const int zp = zparts(N);
+      float zs = 0.f;
+      for (int k = 0; k < zp; ++k) zs += zacc[(int64_t)r * zp + k];
+      const float z = zs + bh[0];
       const float sg = z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
       d = (sg - y[r]) / (float)sr.rows;
       if (!isfinite(z)) atomicOr(a.status + sr.req, 1);
@@ -628,14 +632,16 @@ __global__ void eval_epilogue_kernel(const float* Z, const float* b, int N, int 
   if (wh) {
     float p = u < N ? v * wh[u] : 0.f;
     for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(z + r, p);
+    if ((threadIdx.x & 31) == 0) z[(int64_t)r * zparts(N) + blockIdx.x * 8 + (threadIdx.x >> 5)] = p;
   }
 }
 
-__global__ void eval_probs_kernel(const float* z, const float* bh, int rows, double* probs) {
+__global__ void eval_probs_kernel(const float* z, int zp, const float* bh, int rows, double* probs) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
-  const float zz = z[r] + bh[0];
+  float zs = 0.f;
+  for (int k = 0; k < zp; ++k) zs += z[(int64_t)r * zp + k];
+  const float zz = zs + bh[0];
   probs[r] = (double)(zz >= 0.f ? 1.f / (1.f + __expf(-zz)) : __expf(zz) / (1.f + __expf(zz)));
 }
 
@@ -651,7 +657,8 @@ extern "C" size_t fs_forward_wide_workspace_bytes(const int32_t* dims, int32_t n
   const size_t wb = ((size_t)L.M + (size_t)(dp - L.f[0]) * L.f[1]) * 2;
   const size_t act = (size_t)rows * std::max(L.max_hidden, dp) * 2;
   return (wb + 255) / 256 * 256 + 2 * ((act + 255) / 256 * 256) +
-         (((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256) + ((size_t)rows * 4 + 256);
+         (((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256) +
+         ((size_t)rows * wide::zparts(L.f[L.L - 1]) * 4 + 256);
 }
 
 // K8 forward for layer shapes beyond the on-chip kernels (bf16 operands,
@@ -687,8 +694,7 @@ extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float*
   p += 2 * ((act + 255) / 256 * 256);
   float* Z = reinterpret_cast<float*>(p);
   p += ((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256;
-  float* z = reinterpret_cast<float*>(p);
-  if (cudaMemsetAsync(z, 0, (size_t)rows * 4, st) != cudaSuccess) return check_launch("fs_forward_wide memset");
+  float* z = reinterpret_cast<float*>(p);  // head-logit partials [rows x zparts]
   const float one = 1.f, zero = 0.f;
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(x_bf16);
   int fin_pad = dp;
@@ -715,7 +721,8 @@ extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float*
     fin_pad = fout;
   }
   (void)fin_pad;
-  wide::eval_probs_kernel<<<(rows + 255) / 256, 256, 0, st>>>(z, w + L.boff[L.L - 1], rows, probs_out);
+  wide::eval_probs_kernel<<<(rows + 255) / 256, 256, 0, st>>>(z, wide::zparts(L.f[L.L - 1]), w + L.boff[L.L - 1],
+                                                              rows, probs_out);
   return check_launch("fs_forward_wide probs");
 }
 

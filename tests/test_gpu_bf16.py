@@ -338,3 +338,27 @@ def test_host_upload_rounds_match_resident_rounds(monkeypatch, chunk_mb):
         runs.append((eng.timeline.digest(), st.w_g.values.copy()))
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_wide_runs_are_deterministic_and_async_engines_agree(monkeypatch):
+    """WIDE MLP (batched-GEMM trainer + fs_forward_wide): repeated runs give the
+    same event log and model (head logits from fixed-order partials, no float
+    atomics), and the device-mode async engine matches the Python-executor one."""
+    from paper_2503_15448_b200 import server as S
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    base = {"num_clients": 24, "rounds": 2, "epochs": 2, "selection_mode": "delta_sign", "theta": 0.65, "seed": 4,
+            "dataset": {"kind": "synthetic", "n": 4000, "d": 42, "anomaly_frac": 0.3},
+            "partition": {"alpha": 5.0}, "model": {"hidden_dims": [1024, 1024, 1024, 1024], "dropout_rate": 0.3},
+            "batch": {"policy": "fixed", "size": 64}}
+    for mode, engines in (("sync_filtered", ("device", "device")), ("async_filtered", ("device", "native"))):
+        world, init = build_world(ExperimentConfig.from_dict(dict(base, mode=mode)), precision="bf16")
+        out = []
+        for eng_name in engines:
+            monkeypatch.setattr(S, "_ASYNC_ENGINE", eng_name)
+            eng = S.FederationEngine(world)
+            st = eng.run(init)
+            out.append((eng.timeline.digest(), st.w_g.values.copy()))
+        assert out[0][0] == out[1][0], mode
+        assert np.array_equal(out[0][1], out[1][1]), mode
