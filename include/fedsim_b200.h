@@ -156,6 +156,12 @@ typedef struct fs_train_desc {
   const int32_t* data_flags;
   const int32_t* data_chunk;
   int32_t data_tag;
+  /* bf16 unit-major trainer only: when align_counts != NULL (and done ==
+   * NULL) each client's CTA writes the K6 count of its trained row against
+   * (w_start[r], w_prev[r]) under align_mode to align_counts[r] — the sync
+   * round's alignment fused into the trainer instead of a second pass over
+   * the rows (fs_sign_align_rows)                                          */
+  int64_t* align_counts;
 } fs_train_desc;
 
 typedef struct {

@@ -79,6 +79,7 @@ class TrainDesc(ctypes.Structure):
         ("data_flags", _c_vp),
         ("data_chunk", _c_vp),
         ("data_tag", _c_i32),
+        ("align_counts", _c_vp),
     ]
 
 

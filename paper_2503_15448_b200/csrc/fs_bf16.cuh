@@ -71,6 +71,7 @@ struct Args {
   const uint64_t* w_prev;     // [n_req] previous global (delta_sign) or 0
   int32_t align_mode;         // FS_ALIGN_*, or -1: no count
   int32_t done_tag;
+  int64_t* counts_out;        // [n_req] fused K6 counts (sync rounds), nullptr: off
   const int32_t* data_flags;  // chunked shard upload in flight: request r waits on data_flags[data_chunk[r]]
   const int32_t* data_chunk;
   int32_t data_tag;

@@ -969,8 +969,13 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.max_steps = d->max_steps;
   a.done = d->done;
   a.w_prev = d->w_prev;
-  a.align_mode = d->done ? d->align_mode : -1;
+  a.counts_out = d->done ? nullptr : d->align_counts;
+  a.align_mode = (d->done || d->align_counts) ? d->align_mode : -1;
   a.done_tag = d->done_tag;
+  if (a.counts_out && (a.align_mode < 0 || (a.align_mode == FS_ALIGN_DELTA_SIGN && !d->w_prev))) {
+    set_error("fs_train_bf16: align_counts needs align_mode (and w_prev for delta_sign)");
+    return FS_EINVAL;
+  }
   a.data_flags = d->data_flags;
   a.data_chunk = d->data_chunk;
   a.data_tag = d->data_tag;
@@ -978,7 +983,7 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);
-  if (a.mask_flags || a.done || a.data_flags) {
+  if (a.mask_flags || a.done || a.data_flags || a.counts_out) {
     set_error("fs_train_bf16: flagged keep bits / completion records need the unit-major kernel's layer shapes");
     return FS_EINVAL;
   }

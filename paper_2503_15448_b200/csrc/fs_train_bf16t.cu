@@ -242,12 +242,35 @@ __device__ __forceinline__ int sgn_d(float a, float b) { return (a > b) - (a < b
 // (system-scope release: the record usually lives in mapped host memory and
 // the trained row must be visible to kernels the host launches next).
 __device__ __noinline__ void client_done(int M, int mode, const float* W, const float* g, const float* p,
-                                         const int32_t* status, uint64_t rec_addr, int32_t tag, int tid) {
+                                         const int32_t* status, uint64_t rec_addr, int32_t tag, int tid,
+                                         int64_t* count_out) {
   __shared__ unsigned long long s_cnt[THREADS / 32];
   unsigned cnt = 0;
   if (mode == FS_ALIGN_DELTA_SIGN && !p) mode = -1;  // no movement history: unscored (server.py:283-284)
   if (mode >= 0) {
-    for (int j = tid; j < M; j += THREADS) {
+    // 16-byte loads, four in flight per thread: the row was just written by
+    // this CTA (L2), g and p are shared by every client (L2-resident)
+    const int M4 = (((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(g) |
+                      (p ? reinterpret_cast<uintptr_t>(p) : 0)) & 15) == 0) ? M / 4 : 0;
+    const float4* W4 = reinterpret_cast<const float4*>(W);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    if (mode == FS_ALIGN_WEIGHT_SIGN) {
+#pragma unroll 4
+      for (int j = tid; j < M4; j += THREADS) {
+        const float4 c = __ldcg(W4 + j), gv = __ldg(g4 + j);
+        cnt += (sgn_f(c.x) == sgn_f(gv.x)) + (sgn_f(c.y) == sgn_f(gv.y)) + (sgn_f(c.z) == sgn_f(gv.z)) +
+               (sgn_f(c.w) == sgn_f(gv.w));
+      }
+    } else {
+#pragma unroll 4
+      for (int j = tid; j < M4; j += THREADS) {
+        const float4 c = __ldcg(W4 + j), gv = __ldg(g4 + j), pv = __ldg(p4 + j);
+        cnt += (sgn_d(c.x, gv.x) == sgn_d(gv.x, pv.x)) + (sgn_d(c.y, gv.y) == sgn_d(gv.y, pv.y)) +
+               (sgn_d(c.z, gv.z) == sgn_d(gv.z, pv.z)) + (sgn_d(c.w, gv.w) == sgn_d(gv.w, pv.w));
+      }
+    }
+    for (int j = 4 * M4 + tid; j < M; j += THREADS) {
       const float c = __ldcg(W + j), gv = __ldg(g + j);
       cnt += mode == FS_ALIGN_WEIGHT_SIGN ? (sgn_f(c) == sgn_f(gv)) : (sgn_d(c, gv) == sgn_d(gv, __ldg(p + j)));
     }
@@ -258,6 +281,10 @@ __device__ __noinline__ void client_done(int M, int mode, const float* W, const 
   if (tid == 0) {
     unsigned long long t = 0;
     for (int w = 0; w < THREADS / 32; ++w) t += s_cnt[w];
+    if (count_out) {  // sync round: a plain count, ordered by the kernel's completion
+      *count_out = (int64_t)t;
+      return;
+    }
     fs_client_done* rec = reinterpret_cast<fs_client_done*>(rec_addr);
     rec->aligned = (int64_t)t;
     rec->status = __ldcg(status);
@@ -820,12 +847,13 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     for (int k = tid; k <= f3; k += THREADS) {
       if (k < f3) W[g.woff[3] + k] = wh[k]; else W[g.boff[3]] = wh[f3];
     }
-    if (a.done) {  // per-client completion: fused K6 count + release of the record
+    if (a.done || a.counts_out) {  // fused K6 count (+ release of the completion record)
       __threadfence();
       __syncthreads();
       client_done(g.M, a.align_mode, W, Ws,
                   a.align_mode == FS_ALIGN_DELTA_SIGN ? reinterpret_cast<const float*>(a.w_prev[rq]) : nullptr,
-                  a.status + rq, a.done[rq], a.done_tag, tid);
+                  a.status + rq, a.done ? a.done[rq] : 0, a.done_tag, tid,
+                  a.counts_out ? a.counts_out + rq : nullptr);
     }
     fence_before_sync();
     __syncthreads();

@@ -637,9 +637,33 @@ def _launch_trainer(plan: TrainPlan, desc, bf16: bool, stream) -> None:
             rt.call(lib.fs_train_f64(ctypes.byref(desc), stream.cuda_stream), "fs_train_f64")
 
 
+def _fused_align(plan: TrainPlan, desc, align, stream) -> None:
+    """K6 fused into the unit-major trainer (fs_train_desc.align_counts):
+    align = (mode, counts int64 [n] device, w_prev pointer or None)."""
+    mode, counts, wprev = align
+    m = N.FS_ALIGN_WEIGHT_SIGN if mode == "weight_sign" else N.FS_ALIGN_DELTA_SIGN
+    desc.align_mode = m
+    desc.align_counts = counts.data_ptr()
+    desc.w_prev = None
+    if m == N.FS_ALIGN_DELTA_SIGN:
+        d_prev = plan.pool_buf("w_prev", plan.n, torch.int64) if plan.pooled else \
+            torch.empty(plan.n, dtype=torch.int64, device=plan.rt.device)
+        plan.rt.call(plan.rt.lib.fs_fill_u64(d_prev.data_ptr(), int(wprev), plan.n, stream.cuda_stream),
+                     "fs_fill_u64")
+        desc.w_prev = d_prev.data_ptr()
+        plan._keep_prev = d_prev
+
+
+def fused_align_supported(dims, precision: str) -> bool:
+    """The trainer can count K6 itself (bf16 unit-major kernel shapes)."""
+    return precision == "bf16" and eval_bf16_supported(dims)
+
+
 def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision: str = "fp64",
-                w_out: torch.Tensor | None = None, status: torch.Tensor | None = None):
+                w_out: torch.Tensor | None = None, status: torch.Tensor | None = None, align=None):
     """K5 over a prepared plan: lr [n x epochs], w_start [n] device pointers.
+    `align` = (mode, counts [n] int64 device tensor, w_prev pointer | None):
+    the trainer also writes each client's K6 count (fused_align_supported).
     Returns (w_out [n x M], status int32 [n]) on the device."""
     rt = plan.rt
     lib = rt.lib
@@ -656,8 +680,11 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         stream = torch.cuda.current_stream(rt.device)
         plan.consume(stream)
         desc.data_flags, desc.data_chunk, desc.data_tag = None, None, 0
+        desc.align_counts, desc.w_prev, desc.align_mode = None, None, -1
         if up is not None and up["pending"]:
             _upload_waits(plan, desc, up, bf16, stream)
+        if align is not None:
+            _fused_align(plan, desc, align, stream)
         rt.call(lib.fs_fill_u64(d_run.data_ptr(), int(w_start), n, stream.cuda_stream), "fs_fill_u64")
         _launch_trainer(plan, desc, bf16, stream)
         return w_out, status
@@ -702,6 +729,8 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     desc.status = status.data_ptr()
     if up is not None and up["pending"]:
         _upload_waits(plan, desc, up, bf16, stream)
+    if align is not None:
+        _fused_align(plan, desc, align, stream)
     if plan.mask_flags is not None:
         if not plan.mask_tag:
             raise ValueError("deferred keep bits: launch_masks() must run before the trainer")

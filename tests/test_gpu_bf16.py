@@ -362,3 +362,27 @@ def test_wide_runs_are_deterministic_and_async_engines_agree(monkeypatch):
             out.append((eng.timeline.digest(), st.w_g.values.copy()))
         assert out[0][0] == out[1][0], mode
         assert np.array_equal(out[0][1], out[1][1]), mode
+
+
+@pytest.mark.parametrize("mode", ["weight_sign", "delta_sign"])
+def test_fused_alignment_matches_separate_pass(monkeypatch, mode):
+    """Sync rounds with K6 counted inside the trainer (fs_train_desc.align_counts)
+    give the same counts, log and model as the separate fs_sign_align_rows pass."""
+    from paper_2503_15448_b200 import server as S
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    cfg = {"num_clients": 40, "rounds": 3, "epochs": 2, "mode": "sync_filtered", "selection_mode": mode,
+           "theta": 0.6, "seed": 6, "dataset": {"kind": "synthetic", "n": 8000, "d": 42, "anomaly_frac": 0.3},
+           "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}, "batch": {"policy": "fixed", "size": 64}}
+    out = []
+    for fused in (False, True):
+        monkeypatch.setattr(S, "_FUSED_ALIGN", fused)
+        world, init = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+        eng = S.FederationEngine(world)
+        st = eng.run(init)
+        out.append((eng.timeline.digest(), st.w_g.values.copy(),
+                    [r.to_record() for r in eng.reports]))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
