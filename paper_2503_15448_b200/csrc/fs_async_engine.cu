@@ -27,6 +27,7 @@
 #include <cmath>
 #include <map>
 #include <queue>
+#include <mutex>
 #include <vector>
 
 #include "fs_common.cuh"
@@ -330,6 +331,43 @@ struct DevBlock {
 
 }  // namespace
 
+// Page-locked host buffers outlive an engine: cudaFreeHost unpins pages and
+// took up to 0.9 s at engine teardown, so freed buffers go back to a
+// process-wide cache (one per allocation flag set) and later engines reuse them.
+struct PinnedCache {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free_default, free_mapped;
+};
+static PinnedCache& pinned_cache() {
+  static PinnedCache c;
+  return c;
+}
+static int pinned_get(size_t bytes, unsigned flags, void** out, size_t* got) {
+  PinnedCache& c = pinned_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto& v = flags & cudaHostAllocMapped ? c.free_mapped : c.free_default;
+    size_t best = v.size();
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].second >= bytes && (best == v.size() || v[i].second < v[best].second)) best = i;
+    if (best < v.size()) {
+      *out = v[best].first;
+      *got = v[best].second;
+      v.erase(v.begin() + best);
+      return FS_OK;
+    }
+  }
+  if (cudaHostAlloc(out, bytes, flags) != cudaSuccess) return FS_ECUDA;
+  *got = bytes;
+  return FS_OK;
+}
+static void pinned_put(void* p, size_t bytes, unsigned flags) {
+  if (!p) return;
+  PinnedCache& c = pinned_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  (flags & cudaHostAllocMapped ? c.free_mapped : c.free_default).push_back({p, bytes});
+}
+
 struct DeviceExec {
   fs_async_device d;
   cudaStream_t st;
@@ -339,6 +377,7 @@ struct DeviceExec {
   std::vector<int32_t> n_rows, batch;
   // pinned staging + device mirror (one copy per flush)
   uint8_t* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0, stage_off = 0, stage_done = 0;  // [stage_done, stage_off) not yet copied
   // pooled device buffers
@@ -405,6 +444,10 @@ struct DeviceExec {
       fprintf(stderr, "async host s: prep %.4f wait %.4f | jobs %.4f batch %.4f (alloc %.4f copy %.4f launch %.4f "
               "lookahead %.4f) flushes %lld arena mallocs %lld\n", t_prep, t_wait, t_jobs, t_batch, t_alloc, t_copy,
               t_launch, t_look, (long long)flushes, (long long)arena_mallocs);
+    const bool prof = getenv("FS_ASYNC_PROF") != nullptr;
+    double tt[8];
+    int nt = 0;
+    tt[nt++] = now_s();
     for (cudaStream_t ps : stream_pool) {
       cudaStreamSynchronize(ps);
       cudaStreamDestroy(ps);
@@ -414,7 +457,9 @@ struct DeviceExec {
       cudaFree(f.first);
       cudaEventDestroy(f.second);
     }
-    for (auto* h : rec_host) cudaFreeHost(h);
+    tt[nt++] = now_s();
+    for (auto* h : rec_host) pinned_put(h, sizeof(fs_client_done) * kRecChunk, cudaHostAllocMapped);
+    tt[nt++] = now_s();
     if (main_ev) cudaEventDestroy(main_ev);
     cudaStreamSynchronize(st);
     for (auto& b : arena_pending) {  // every release is complete after the syncs above
@@ -425,6 +470,7 @@ struct DeviceExec {
       cudaEventDestroy(bm.end);
       arena_free.push_back(ArenaBlock{bm.mem, arena_cls[bm.mem], nullptr});
     }
+    tt[nt++] = now_s();
     for (auto ev : event_pool) cudaEventDestroy(ev);
     for (auto& b : blocks)
       if (b.ptr) cudaFreeAsync(b.ptr, st);
@@ -442,9 +488,17 @@ struct DeviceExec {
     if (side_done) cudaEventDestroy(side_done);
     if (d_perm_all) cudaFreeAsync(d_perm_all, st);
     if (d_bits_all) cudaFreeAsync(d_bits_all, st);
+    tt[nt++] = now_s();
     cudaStreamSynchronize(st);
-    if (h_stage) cudaFreeHost(h_stage);
-    if (h_res) cudaFreeHost(h_res);
+    tt[nt++] = now_s();
+    pinned_put(h_stage, h_stage_bytes, cudaHostAllocDefault);
+    pinned_put(h_res, 1 << 20, cudaHostAllocDefault);
+    if (prof) {
+      tt[nt++] = now_s();
+      fprintf(stderr, "async destroy s:");
+      for (int i = 1; i < nt; ++i) fprintf(stderr, " %.4f", tt[i] - tt[i - 1]);
+      fprintf(stderr, "\n");
+    }
   }
 
   static int cuda(cudaError_t e, const char* what) {
@@ -492,13 +546,16 @@ struct DeviceExec {
     if (int rc = cuda(cudaStreamSynchronize(st), "staging grow")) return rc;
     if (side)
       if (int rc = cuda(cudaStreamSynchronize(side), "staging grow")) return rc;
-    if (h_stage) cudaFreeHost(h_stage);
+    pinned_put(h_stage, h_stage_bytes, cudaHostAllocDefault);
     if (d_stage) cudaFreeAsync(d_stage, st);
     h_stage = nullptr;
     d_stage = nullptr;
     stage_cap = stage_off = stage_done = 0;
     const size_t n = 2 * more + 4096;
-    if (int rc = cuda(cudaHostAlloc((void**)&h_stage, n, cudaHostAllocDefault), "pinned staging")) return rc;
+    if (pinned_get(n, cudaHostAllocDefault, (void**)&h_stage, &h_stage_bytes) != FS_OK) {
+      fs::set_error("fs_async: pinned staging allocation failed");
+      return FS_ECUDA;
+    }
     if (int rc = cuda(cudaMallocAsync((void**)&d_stage, n, st), "device staging")) return rc;
     stage_cap = n;
     return FS_OK;
@@ -540,7 +597,11 @@ struct DeviceExec {
       uint64_t keep = UINT64_MAX;  // keep freed blocks cached across synchronisations
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    if (int rc = cuda(cudaHostAlloc((void**)&h_res, 1 << 20, cudaHostAllocDefault), "pinned results")) return rc;
+    size_t h_res_got = 0;
+    if (pinned_get(1 << 20, cudaHostAllocDefault, (void**)&h_res, &h_res_got) != FS_OK) {
+      fs::set_error("fs_async: pinned results allocation failed");
+      return FS_ECUDA;
+    }
     if (int rc = stage_reserve(1 << 19)) return rc;
     // lookahead plan slots
     E = d.epochs;
@@ -919,7 +980,8 @@ struct DeviceExec {
     const size_t c = (size_t)id / kRecChunk, o = (size_t)id % kRecChunk;
     while (rec_host.size() <= c) {
       void* h = nullptr;
-      if (cudaHostAlloc(&h, sizeof(fs_client_done) * kRecChunk, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+      size_t got = 0;
+      if (pinned_get(sizeof(fs_client_done) * kRecChunk, cudaHostAllocMapped, &h, &got) != FS_OK) return nullptr;
       memset(h, 0, sizeof(fs_client_done) * kRecChunk);
       void* dv = nullptr;
       cudaHostGetDevicePointer(&dv, h, 0);
