@@ -171,7 +171,21 @@ class _SmiSampler:
 
 
 # ------------------------------------------------------------------ CPU sides
-def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None, workers: int = 1):
+_ORACLE_JOB = None
+
+
+def _oracle_cycles(clients):
+    """Worker process body: oracle client cycles (accepted flag + params only)."""
+    sim, r, w0, wp = _ORACLE_JOB
+    out = []
+    for ci in clients:
+        o = sim.cycle(ci, r, r, w0, wp)
+        out.append({"accepted": o["accepted"], "res": {"params": o["res"]["params"]}})
+    return out
+
+
+def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None, workers: int = 1,
+                        processes: int = 1):
     """Time the oracle (reference algorithm, numpy, 1 thread) on a bounded
     sample of one C4 sync round: `sample_clients` client cycles (training +
     delta_sign scoring), FedAvg of their updates, and one full evaluation.
@@ -183,13 +197,28 @@ def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 
     w0 = initial.values
     wp = w_prev if w_prev is not None else w0 * 0.999
     picks = [int(i) for i in np.linspace(0, n - 1, sample_clients).round()]
-    t0 = time.perf_counter()
-    if workers > 1:  # the reference's own fan-out: a thread pool over clients (server.py:412-415)
-        with ThreadPoolExecutor(max_workers=workers) as pool:
-            outs = list(pool.map(lambda ci: sim.cycle(ci, round_index, round_index, w0, wp), picks))
+    if processes > 1:
+        # every host core: one forked worker process per core, clients dealt
+        # round-robin (the reference's own thread pool is GIL-bound, see top)
+        import multiprocessing as mp
+
+        global _ORACLE_JOB
+        _ORACLE_JOB = (sim, round_index, w0, wp)
+        ctx = mp.get_context("fork")
+        with ctx.Pool(processes) as pool:
+            pool.map(_oracle_cycles, [[0]] * processes)  # workers up (fork, imports) before the clock
+            t0 = time.perf_counter()
+            chunks = [picks[i::processes] for i in range(processes)]
+            outs = [o for part in pool.map(_oracle_cycles, chunks) for o in part]
+            t_train = time.perf_counter() - t0
     else:
-        outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
-    t_train = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        if workers > 1:  # the reference's own fan-out: a thread pool over clients (server.py:412-415)
+            with ThreadPoolExecutor(max_workers=workers) as pool:
+                outs = list(pool.map(lambda ci: sim.cycle(ci, round_index, round_index, w0, wp), picks))
+        else:
+            outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
+        t_train = time.perf_counter() - t0
     ups = [o["res"]["params"] for o in outs if o["accepted"]]
     t0 = time.perf_counter()
     O.fedavg(ups if ups else [w0])
@@ -211,10 +240,14 @@ def run_reference(args, rank: int, world_size: int) -> None:
         return
     world, initial = build_c4_world()
     sample = args.ref_sample
+    procs = args.ref_procs if args.ref_procs > 0 else (os.cpu_count() or 1)
     threads = max(1, args.ref_workers)
+    if procs > 1:
+        sample = max(sample, 8 * procs)
     times = []
     for i in range(args.warmup + args.steps):
-        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0, workers=threads)
+        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0, workers=threads,
+                                                processes=procs)
         if i >= args.warmup:
             times.append(per_round)
     sec = float(np.mean(times))
@@ -225,10 +258,11 @@ def run_reference(args, rank: int, world_size: int) -> None:
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients, MLP 42-256-128-64-1, E=5, "
                                "dynamic batch, delta_sign theta=0.65"},
-        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": max(procs, threads), "kind": "port",
                          "sample": f"{sample} of 1024 client cycles of round 0 + FedAvg + full eval per step, "
-                                   f"extrapolated x1024/sample (oracle/fl_oracle.py, numpy, {threads} worker thread(s) "
-                                   "over clients like the reference's `workers`; 1 BLAS thread; more threads were slower)",
+                                   f"extrapolated x1024/sample (oracle/fl_oracle.py, numpy, 1 BLAS thread; "
+                                   + (f"{procs} forked worker processes over clients, one per host core)" if procs > 1
+                                      else f"{threads} worker thread(s) over clients like the reference's `workers`)"),
                          "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "client_updates_per_s": value * 1024,
@@ -660,7 +694,8 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--ref-sample", type=int, default=64)
-    ap.add_argument("--ref-workers", type=int, default=1)
+    ap.add_argument("--ref-workers", type=int, default=1, help="thread pool over clients (GIL-bound)")
+    ap.add_argument("--ref-procs", type=int, default=0, help="worker processes for the reference arm (0: all cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
     ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity-mode measurement")
