@@ -202,7 +202,7 @@ class HostPack:
     DMA copies (the bench's end-to-end leg re-uploads them every round)."""
 
     def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True, bf16: bool = False,
-                 order: np.ndarray | None = None, chunk_bytes: int = 0):
+                 order: np.ndarray | None = None, chunk_bytes: int = 0, first_chunk_bytes: int = 0):
         n_rows = np.array([f.shape[0] for f in features], dtype=np.int64)
         self.n_rows = n_rows.astype(np.int32)
         # clients are packed in `order` (default: index order); row_off stays per client
@@ -233,20 +233,24 @@ class HostPack:
         if pin:
             self.x = self.x.pin_memory()
             self.y = self.y.pin_memory()
-        # upload chunks: consecutive clients of the packing order, ~chunk_bytes
-        # each; chunk_of[client] tells a trainer which chunk holds its rows
+        # upload chunks: consecutive clients of the packing order, growing
+        # geometrically from ~first_chunk_bytes to ~chunk_bytes (the trainer's
+        # first clients land early; later chunks amortise the copy overhead);
+        # chunk_of[client] tells a trainer which chunk holds its rows
         self.chunk_of = np.zeros(len(features), dtype=np.int32)
         self.chunks = [(0, int(self.x.shape[0]))]
         if chunk_bytes > 0 and len(features):
             row_bytes = self.x.element_size() * (self.x.shape[1] if self.x.dim() == 2 else 1)
+            target = min(first_chunk_bytes, chunk_bytes) if first_chunk_bytes > 0 else chunk_bytes
             bounds, start, acc = [], 0, 0
             for i in order:
                 self.chunk_of[i] = len(bounds)
                 acc += int(n_rows[i]) * row_bytes
-                if acc >= chunk_bytes:
+                if acc >= target:
                     end = int(self.row_off[i] + n_rows[i])
                     bounds.append((start, end))
                     start, acc = end, 0
+                    target = min(2 * target, chunk_bytes)
             if start < self.x.shape[0] or not bounds:
                 bounds.append((start, int(self.x.shape[0])))
             self.chunks = bounds
