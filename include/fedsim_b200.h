@@ -162,6 +162,12 @@ typedef struct fs_train_desc {
    * round's alignment fused into the trainer instead of a second pass over
    * the rows (fs_sign_align_rows)                                          */
   int64_t* align_counts;
+  /* bf16 unit-major trainer only: w_start == NULL and w_start_all != NULL
+   * starts every request from the one model w_start_all (a sync round);
+   * counter_zeroed = 1 promises the workspace's work counter is already 0
+   * (prepared ahead on another stream), so no memset precedes the launch   */
+  const void* w_start_all;
+  int32_t counter_zeroed;
 } fs_train_desc;
 
 typedef struct {

@@ -80,6 +80,8 @@ class TrainDesc(ctypes.Structure):
         ("data_chunk", _c_vp),
         ("data_tag", _c_i32),
         ("align_counts", _c_vp),
+        ("w_start_all", _c_vp),
+        ("counter_zeroed", _c_i32),
     ]
 
 

@@ -51,6 +51,7 @@ struct Args {
   const int32_t* batch;
   const double* lr;           // [n_req x epochs]
   const uint64_t* w_start;    // fp32 flat start parameters
+  const float* w_all;         // unit-major kernel: the start model of every request when w_start == nullptr
   float* w_out;               // fp32 flat, ldw floats per request
   int64_t ldw;
   const int32_t* perm;

@@ -925,8 +925,13 @@ extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
 extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, const float* labels_f32,
                              void* stream) {
   Geo g;
-  if (d && make_geo(d->dims, d->n_dims, &g) != FS_OK && fs_bf16_supported(d->dims, d->n_dims) == 2)
+  if (d && make_geo(d->dims, d->n_dims, &g) != FS_OK && fs_bf16_supported(d->dims, d->n_dims) == 2) {
+    if (!d->w_start && d->n_req > 0) {
+      set_error("fs_train_bf16 (wide): w_start is NULL");
+      return FS_EINVAL;
+    }
     return wide_train(d, features_bf16, labels_f32, (cudaStream_t)stream);
+  }
   if (!d || make_geo(d->dims, d->n_dims, &g) != FS_OK) {
     set_error("fs_train_bf16: unsupported layer dims for the tensor-core trainer");
     return FS_EINVAL;
@@ -979,7 +984,14 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.data_flags = d->data_flags;
   a.data_chunk = d->data_chunk;
   a.data_tag = d->data_tag;
-  if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
+  a.w_all = reinterpret_cast<const float*>(d->w_start_all);
+  const bool v3 = g_bf16_force_generic == 0 && bf16t::geo_ok(g);
+  if (!a.w_start && !(v3 && a.w_all)) {
+    set_error("fs_train_bf16: w_start is NULL (w_start_all needs the unit-major kernel's layer shapes)");
+    return FS_EINVAL;
+  }
+  if (!(v3 && d->counter_zeroed) && cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess)
+    return check_launch("memset");
   int grid = d->grid > 0 ? d->grid : kNumSMs;
   if (grid > d->n_req) grid = d->n_req;
   if (g_bf16_force_generic == 0 && bf16t::geo_ok(g)) return bf16t::launch(a, grid, st);

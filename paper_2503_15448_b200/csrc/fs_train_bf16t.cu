@@ -359,7 +359,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     const int n = a.n_rows[rq], B = a.batch[rq];
     const int spe = (n + B - 1) / B;
     float* W = a.w_out + (int64_t)rq * a.ldw;
-    const float* Ws = reinterpret_cast<const float*>(a.w_start[rq]);
+    const float* Ws = a.w_start ? reinterpret_cast<const float*>(a.w_start[rq]) : a.w_all;
     if (a.data_flags) wait_mask_step(a.data_flags + a.data_chunk[rq], a.data_tag);  // this client's rows uploaded
     FS_PROF(30);
 

@@ -534,6 +534,12 @@ class TrainPlan:
         desc.w_out, desc.ldw = w_out.data_ptr(), w_out.stride(0)
         desc.workspace, desc.workspace_bytes = ws.data_ptr(), ws.numel()
         desc.w_start = d_run.data_ptr()
+        if fused_align_supported(self.dims, precision):
+            # the unit-major kernel takes the one start model directly and finds
+            # its work counter zeroed here: the round launches it with no fill/memset
+            self.rt.call(lib.fs_fill_u64(ws.data_ptr(), 0, 1, st), "fs_fill_u64")
+            self.ready.record(self.stream)
+            desc.counter_zeroed = 1
         self.prefilled = (precision, float(lr), desc, w_out, d_st, d_run)
 
     def static_desc(self, precision: str) -> "N.TrainDesc":
@@ -679,8 +685,10 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     up = getattr(plan.shards, "upload", None)  # a chunked upload still in flight (DeviceWorld.refill)
     if (pre is not None and pre[0] == precision and w_out is None and status is None and np.ndim(lr) == 0
             and float(lr) == pre[1] and np.ndim(w_start) == 0 and plan.mask_flags is None):
-        # the launch prepared while this plan was prefetched (TrainPlan.prefill)
+        # the launch prepared while this plan was prefetched (TrainPlan.prefill);
+        # used once (its work counter is zeroed for exactly one launch)
         desc, w_out, status, d_run = pre[2], pre[3], pre[4], pre[5]
+        plan.prefilled = None
         stream = torch.cuda.current_stream(rt.device)
         plan.consume(stream)
         desc.data_flags, desc.data_chunk, desc.data_tag = None, None, 0
@@ -689,7 +697,10 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
             _upload_waits(plan, desc, up, bf16, stream)
         if align is not None:
             _fused_align(plan, desc, align, stream)
-        rt.call(lib.fs_fill_u64(d_run.data_ptr(), int(w_start), n, stream.cuda_stream), "fs_fill_u64")
+        if desc.counter_zeroed:
+            desc.w_start, desc.w_start_all = None, int(w_start)
+        else:
+            rt.call(lib.fs_fill_u64(d_run.data_ptr(), int(w_start), n, stream.cuda_stream), "fs_fill_u64")
         _launch_trainer(plan, desc, bf16, stream)
         return w_out, status
     if w_out is None:
