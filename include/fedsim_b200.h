@@ -46,6 +46,10 @@ enum fs_mask_mode { FS_MASK_NONE = 0, FS_MASK_BITS = 1, FS_MASK_DENSE = 2 };
 enum fs_align_mode { FS_ALIGN_WEIGHT_SIGN = 0, FS_ALIGN_DELTA_SIGN = 1 };
 
 const char* fs_last_error(void);
+/* Layout check for bindings: sizes of the ABI structs in this build, in the
+ * order fs_train_desc, fs_client_done, fs_async_world, fs_async_yield,
+ * fs_async_logview, fs_async_device. Writes min(n, 6) entries, returns 6.  */
+int32_t fs_struct_sizes(size_t* out, int32_t n);
 int fs_abi_version(void);
 /* dst[0..n) = value (device, stream-ordered): per-request launch arguments
  * that are one value for a whole round (start model pointer, step size bits) */

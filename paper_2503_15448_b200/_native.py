@@ -87,6 +87,7 @@ class TrainDesc(ctypes.Structure):
 
 _SIGNATURES = {
     "fs_last_error": (ctypes.c_char_p, []),
+    "fs_struct_sizes": (ctypes.c_int32, [_c_vp, _c_i32]),
     "fs_abi_version": (ctypes.c_int, []),
     "fs_memcpy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_fill_u64": (ctypes.c_int, [_c_vp, _c_u64, _c_i64, _c_vp]),

@@ -30,6 +30,13 @@ int check_launch(const char* what) {
 
 extern "C" const char* fs_last_error(void) { return fs::g_err; }
 
+extern "C" int32_t fs_struct_sizes(size_t* out, int32_t n) {
+  const size_t sz[6] = {sizeof(fs_train_desc),  sizeof(fs_client_done),   sizeof(fs_async_world),
+                        sizeof(fs_async_yield), sizeof(fs_async_logview), sizeof(fs_async_device)};
+  for (int32_t i = 0; out && i < n && i < 6; ++i) out[i] = sz[i];
+  return 6;
+}
+
 extern "C" int fs_abi_version(void) { return FS_ABI_VERSION; }
 
 namespace fs {

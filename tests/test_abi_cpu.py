@@ -62,3 +62,19 @@ def test_product_has_no_oracle_import():
                     src = fh.read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
                 assert "fl_oracle" not in src, f
+
+
+def test_ctypes_structs_match_the_c_layout():
+    """The Python bindings' ctypes mirrors have the sizes the library was built
+    with (catches a field added on one side only)."""
+    from paper_2503_15448_b200 import async_loop as A
+
+    lib = N.load(require_gpu=False)
+    sizes = (ctypes.c_size_t * 6)()
+    assert lib.fs_struct_sizes(ctypes.cast(sizes, ctypes.c_void_p), 6) == 6
+
+    class ClientDone(ctypes.Structure):
+        _fields_ = [("aligned", ctypes.c_int64), ("status", ctypes.c_int32), ("tag", ctypes.c_int32)]
+
+    mirrors = [N.TrainDesc, ClientDone, A.AsyncWorld, A.AsyncYield, A.AsyncLogView, A.AsyncDevice]
+    assert [ctypes.sizeof(m) for m in mirrors] == list(sizes)
