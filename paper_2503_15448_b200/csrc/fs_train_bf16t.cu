@@ -295,6 +295,9 @@ __device__ __noinline__ void client_done(int M, int mode, const float* W, const 
 
 // 184 registers x 256 threads leaves room for one 256-thread block of the next
 // round's K3 (70 registers) on the same SM
+#ifndef FS_D3_QUARTERS
+#define FS_D3_QUARTERS 1
+#endif
 #ifndef FS_BF16T_MAXNREG
 #define FS_BF16T_MAXNREG 184
 #endif
@@ -650,6 +653,39 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           }
           have_next = true;
         }
+#if FS_D3_QUARTERS
+        // ---------------- D3^T = gate(w_h dz^T, H3^T) * scale; head-weight and b2 gradient partials.
+        // Every warp takes a (32-unit group, 16-row quarter) item; the partials
+        // go to [4][64] slots in the gb0p area (consumed by stage 2, rewritten
+        // only in stage 1)
+        if (warp < 4 * (f3 / 32)) {
+          const int ug = warp % (f3 / 32), rq4 = warp / (f3 / 32), m = ug * 32 + lane, c0 = rq4 * 16;
+          uint32_t hv[8];
+          ld_shared_v4(h3t.saddr + h3t.off(m, c0), hv[0], hv[1], hv[2], hv[3]);
+          ld_shared_v4(h3t.saddr + h3t.off(m, c0 + 8), hv[4], hv[5], hv[6], hv[7]);
+          const float w = wh[m] * dsc;
+          float d[16];
+          float gw = 0.f, gb = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float hj = (j & 1) ? bf16hi(hv[j >> 1]) : bf16lo(hv[j >> 1]);
+            const float dzj = dz_sh[c0 + j];
+            gw = fmaf(hj, dzj, gw);
+            d[j] = hj > 0.f ? dzj * w : 0.f;
+          }
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            pk[j >> 1] = pack_bf16x2(d[j], d[j + 1]);
+            gb += bf16lo(pk[j >> 1]);
+            gb += bf16hi(pk[j >> 1]);
+          }
+          st_shared_v4(h3t.saddr + h3t.off(m, c0), pk[0], pk[1], pk[2], pk[3]);
+          st_shared_v4(h3t.saddr + h3t.off(m, c0 + 8), pk[4], pk[5], pk[6], pk[7]);
+          gb0p[rq4 * 64 + m] = gw;
+          gb0p[256 + rq4 * 64 + m] = gb;
+        }
+#else
         // ---------------- D3^T = gate(w_h dz^T, H3^T) * scale; head-weight and b2 gradient partials
         if (q < f3 / 32) {
           const int hh = warp >> 2, m = q * 32 + lane;
@@ -675,6 +711,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           gwp[hh * 64 + m] = gw;
           gb2p[hh * 64 + m] = gb;
         }
+#endif
         FS_PROF(11);
 
         // ---------------- stage 2: G2 = H2^T D3 (TMEM [0,64)), D2^T = W2 D3^T (TMEM [64,128))
@@ -689,12 +726,20 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         // head and b2 updates while the MMAs run (gradients accumulate over a step's chunks)
         if (tid >= 32 && tid <= 32 + f3) {
           const int k = tid - 32;
+#if FS_D3_QUARTERS
+          const float gk = k < f3 ? (gb0p[k] + gb0p[64 + k]) + (gb0p[128 + k] + gb0p[192 + k]) : gbh[0] + gbh[1];
+#else
           const float gk = k < f3 ? gwp[k] + gwp[64 + k] : gbh[0] + gbh[1];
+#endif
           const float acc = first_chunk ? gk : ghs[k] + gk;
           if (last_chunk) wh[k] -= lr * acc; else ghs[k] = acc;
         } else if (tid >= 128 && tid < 128 + f3) {
           const int c = tid - 128;
+#if FS_D3_QUARTERS
+          const float gk = (gb0p[256 + c] + gb0p[320 + c]) + (gb0p[384 + c] + gb0p[448 + c]);
+#else
           const float gk = gb2p[c] + gb2p[64 + c];
+#endif
           const float acc = first_chunk ? gk : gbacc[f1 + f2 + c] + gk;
           if (last_chunk) bias[f1 + f2 + c] -= lr * acc; else gbacc[f1 + f2 + c] = acc;
         }
