@@ -306,9 +306,11 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
   __shared__ uint64_t mma_bar;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_item;
-  __shared__ int64_t s_rowidx[R];
-  __shared__ int64_t s_rowidx_next[R];
-  __shared__ float s_y_next[R];
+  // row ids and labels of the current chunk and the prefetched next one,
+  // ping-ponged (cur flips when a prefetched chunk becomes current: no copy,
+  // no barrier at the chunk start)
+  __shared__ int64_t s_rowidx_pp[2][R];
+  __shared__ float s_y_pp[2][R];
   __shared__ unsigned long long s_prof[32];
   long long prof_t0 = clock64();
 
@@ -318,7 +320,6 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
   const int f0 = g.f[0], fp0 = g.fp[0], f1 = g.f[1], f2 = g.f[2], f3 = g.f[3];
   const int MB = f1 / 128;
   float* fl = reinterpret_cast<float*>(smem + ly.fl);
-  float* y_sh = fl + FL_Y;
   float* dz_sh = fl + FL_DZ;
   float* zpart = fl + FL_ZP;    // [2][R]
   float* gwp = fl + FL_GW;      // [2][64] head weight gradient partials
@@ -444,6 +445,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     FS_PROF(26);
     const int64_t slot_words = ((int64_t)B * g.sum_hidden + 31) / 32;
     bool have_next = false;
+    int cur = 0;  // s_rowidx_pp / s_y_pp buffer of the current chunk
     uint4 xnext[XPRE];
     MaskRaw mrn;
     // per-client constants, loaded once (the stores into W would otherwise
@@ -471,16 +473,15 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         // ---------------- gather the chunk's rows (bf16 features) and labels
         const int cpr = fp0 / 8;
         if (have_next) {
+          cur ^= 1;
+        } else {
           if (tid < R) {
-            s_rowidx[tid] = s_rowidx_next[tid];
-            y_sh[tid] = s_y_next[tid];
+            const int64_t row = tid < rows ? row_off + perm_e[s * B + row0 + tid] : -1;
+            s_rowidx_pp[cur][tid] = row;
+            s_y_pp[cur][tid] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
           }
-        } else if (tid < R) {
-          const int64_t row = tid < rows ? row_off + perm_e[s * B + row0 + tid] : -1;
-          s_rowidx[tid] = row;
-          y_sh[tid] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
+          __syncthreads();
         }
-        __syncthreads();
         FS_PROF(0);
 #pragma unroll
         for (int u = 0; u < XPRE; ++u) {
@@ -490,7 +491,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
             uint4 v = xnext[u];
             if (!have_next) {
               v = make_uint4(0, 0, 0, 0);
-              if (r < rows) v = __ldcg(reinterpret_cast<const uint4*>(a.feat + s_rowidx[r] * fp0 + c));
+              if (r < rows) v = __ldcg(reinterpret_cast<const uint4*>(a.feat + s_rowidx_pp[cur][r] * fp0 + c));
             }
             st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
           }
@@ -587,8 +588,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           const int nrows_step = min(B, n - ns * B);
           const int nr0 = nch * R;
           const int64_t row = t < min(R, nrows_step - nr0) ? row_off + perm_c[(int64_t)ne * n + ns * B + nr0 + t] : -1;
-          s_rowidx_next[t] = row;
-          s_y_next[t] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
+          s_rowidx_pp[cur ^ 1][t] = row;
+          s_y_pp[cur ^ 1][t] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
         }
         {
           const int hh = warp >> 2, m = q * 32 + lane;
@@ -621,7 +622,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           const float z = zpart[tid] + zpart[R + tid] + wh[f3];
           float d = 0.f;
           if (tid < rows) {
-            d = (bf16::sigmoidf_stable(z) - y_sh[tid]) / (float)step_rows;
+            d = (bf16::sigmoidf_stable(z) - s_y_pp[cur][tid]) / (float)step_rows;
             if (!isfinite(z)) atomicOr(a.status + rq, 1);
           }
           dz_sh[tid] = d;
@@ -647,7 +648,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
             const int i = tid + u * THREADS;
             xnext[u] = make_uint4(0, 0, 0, 0);
             if (i < R * cpr) {
-              const int64_t row = s_rowidx_next[i / cpr];
+              const int64_t row = s_rowidx_pp[cur ^ 1][i / cpr];
               if (row >= 0) xnext[u] = __ldcg(reinterpret_cast<const uint4*>(a.feat + row * fp0 + (i % cpr) * 8));
             }
           }
