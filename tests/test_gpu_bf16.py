@@ -386,3 +386,27 @@ def test_fused_alignment_matches_separate_pass(monkeypatch, mode):
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("mode", ["weight_sign", "delta_sign"])
+def test_bf16_sync_round_with_every_update_rejected_keeps_the_model(mode):
+    """theta = 1.0 rejects every client on the device path (fs_select_rows with
+    no accepted row -> empty FedAvg job): w_g stays bitwise the start model and
+    the aggregate records count 0, as server.aggregate returning None does."""
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    cfg = {"num_clients": 24, "rounds": 2, "epochs": 1, "mode": "sync_filtered", "selection_mode": mode,
+           "theta": 1.0, "seed": 8, "dataset": {"kind": "synthetic", "n": 5000, "d": 42, "anomaly_frac": 0.3},
+           "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}, "batch": {"policy": "fixed", "size": 64}}
+    world, init = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+    eng = FederationEngine(world)
+    st = eng.run(init)
+    aggs = [r for r in eng.timeline.log if r["kind"] == "aggregate"]
+    if mode == "weight_sign":
+        assert aggs and all(a["count"] == 0 for a in aggs)
+        assert np.array_equal(np.asarray(st.w_g.values, dtype=np.float32),
+                              np.asarray(init.values, dtype=np.float32))
+    else:  # round 0 is unscored (no movement history): everyone is accepted once
+        assert aggs[0]["count"] == 24 and all(a["count"] == 0 for a in aggs[1:])
