@@ -440,14 +440,6 @@ struct DeviceExec {
   }
 
   ~DeviceExec() {
-    if (getenv("FS_ASYNC_PROF"))
-      fprintf(stderr, "async host s: prep %.4f wait %.4f | jobs %.4f batch %.4f (alloc %.4f copy %.4f launch %.4f "
-              "lookahead %.4f) flushes %lld arena mallocs %lld\n", t_prep, t_wait, t_jobs, t_batch, t_alloc, t_copy,
-              t_launch, t_look, (long long)flushes, (long long)arena_mallocs);
-    const bool prof = getenv("FS_ASYNC_PROF") != nullptr;
-    double tt[8];
-    int nt = 0;
-    tt[nt++] = now_s();
     for (cudaStream_t ps : stream_pool) {
       cudaStreamSynchronize(ps);
       cudaStreamDestroy(ps);
@@ -457,9 +449,7 @@ struct DeviceExec {
       cudaFree(f.first);
       cudaEventDestroy(f.second);
     }
-    tt[nt++] = now_s();
     for (auto* h : rec_host) pinned_put(h, sizeof(fs_client_done) * kRecChunk, cudaHostAllocMapped);
-    tt[nt++] = now_s();
     if (main_ev) cudaEventDestroy(main_ev);
     cudaStreamSynchronize(st);
     for (auto& b : arena_pending) {  // every release is complete after the syncs above
@@ -470,7 +460,6 @@ struct DeviceExec {
       cudaEventDestroy(bm.end);
       arena_free.push_back(ArenaBlock{bm.mem, arena_cls[bm.mem], nullptr});
     }
-    tt[nt++] = now_s();
     for (auto ev : event_pool) cudaEventDestroy(ev);
     for (auto& b : blocks)
       if (b.ptr) cudaFreeAsync(b.ptr, st);
@@ -488,17 +477,9 @@ struct DeviceExec {
     if (side_done) cudaEventDestroy(side_done);
     if (d_perm_all) cudaFreeAsync(d_perm_all, st);
     if (d_bits_all) cudaFreeAsync(d_bits_all, st);
-    tt[nt++] = now_s();
     cudaStreamSynchronize(st);
-    tt[nt++] = now_s();
     pinned_put(h_stage, h_stage_bytes, cudaHostAllocDefault);
     pinned_put(h_res, 1 << 20, cudaHostAllocDefault);
-    if (prof) {
-      tt[nt++] = now_s();
-      fprintf(stderr, "async destroy s:");
-      for (int i = 1; i < nt; ++i) fprintf(stderr, " %.4f", tt[i] - tt[i - 1]);
-      fprintf(stderr, "\n");
-    }
   }
 
   static int cuda(cudaError_t e, const char* what) {
@@ -629,7 +610,7 @@ struct DeviceExec {
     if (int rc = cuda(cudaEventRecord(side_done, st), "event")) return rc;
     if (int rc = cuda(cudaStreamWaitEvent(side, side_done, 0), "event")) return rc;
     percycle = d.bf16 && d.n_dims == 5 && (d.dims[1] == 128 || d.dims[1] == 256) && d.dims[2] == 128 &&
-               d.dims[3] == 64 && d.dims[0] <= 64 && !getenv("FS_ASYNC_BATCH_WAIT");
+               d.dims[3] == 64 && d.dims[0] <= 64;
     if (percycle) {
       stream_pool.resize(8);
       for (auto& ps : stream_pool)

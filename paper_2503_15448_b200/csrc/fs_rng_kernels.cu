@@ -310,12 +310,10 @@ extern "C" int fs_shuffle_perms(const uint64_t* seeds, const int32_t* n_rows,
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0) return FS_OK;
-  // FS_K2_SMEM=0 swaps in the output itself (L1/L2) with one-warp CTAs
-  // instead of staging in shared memory, so more chains co-reside with the
-  // trainer; measured equal in the C4 round (the chains are latency-bound)
-  static const int staged = getenv("FS_K2_SMEM") ? atoi(getenv("FS_K2_SMEM")) : 1;
+  // each chain is staged in shared memory when it fits (swapping in the
+  // output through L1/L2 with one-warp CTAs measured equal: latency-bound)
   const size_t smem = (size_t)max_rows * sizeof(int32_t);
-  const int use_smem = staged && smem <= 200 * 1024;
+  const int use_smem = smem <= 200 * 1024;
   if (use_smem && smem > 48 * 1024)
     ensure_smem(shuffle_kernel, (int)smem);
   shuffle_kernel<<<n_req * epochs, use_smem ? 128 : 32, use_smem ? smem : 0, (cudaStream_t)stream>>>(
@@ -331,9 +329,7 @@ extern "C" int fs_dropout_bits(const uint64_t* seeds, const int32_t* n_rows, con
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0) return FS_OK;
-  int64_t items = (int64_t)n_req * MASK_YSPLIT, blocks = items;
-  static const int64_t cap = getenv("FS_K3_BLOCKS") ? atoll(getenv("FS_K3_BLOCKS")) : 0;
-  if (cap > 0 && blocks > cap) blocks = cap;
+  const int64_t blocks = (int64_t)n_req * MASK_YSPLIT;
   dropout_bits_kernel<<<(unsigned)blocks, MASK_THREADS, 0, (cudaStream_t)stream>>>(
       seeds, n_rows, batch, mask_off, n_req, epochs, sum_hidden, keep_threshold(keep), bits_out);
   return check_launch("dropout_bits_kernel");

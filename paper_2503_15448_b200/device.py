@@ -202,7 +202,7 @@ class HostPack:
     DMA copies (the bench's end-to-end leg re-uploads them every round)."""
 
     def __init__(self, features: list[np.ndarray], labels: list[np.ndarray], pin: bool = True, bf16: bool = False,
-                 order: np.ndarray | None = None, chunk_bytes: int = 0, first_chunk_bytes: int = 0):
+                 order: np.ndarray | None = None, chunk_bytes: int = 0):
         n_rows = np.array([f.shape[0] for f in features], dtype=np.int64)
         self.n_rows = n_rows.astype(np.int32)
         # clients are packed in `order` (default: index order); row_off stays per client
@@ -233,15 +233,13 @@ class HostPack:
         if pin:
             self.x = self.x.pin_memory()
             self.y = self.y.pin_memory()
-        # upload chunks: consecutive clients of the packing order, growing
-        # geometrically from ~first_chunk_bytes to ~chunk_bytes (the trainer's
-        # first clients land early; later chunks amortise the copy overhead);
-        # chunk_of[client] tells a trainer which chunk holds its rows
+        # upload chunks: consecutive clients of the packing order, ~chunk_bytes
+        # each; chunk_of[client] tells a trainer which chunk holds its rows
         self.chunk_of = np.zeros(len(features), dtype=np.int32)
         self.chunks = [(0, int(self.x.shape[0]))]
         if chunk_bytes > 0 and len(features):
             row_bytes = self.x.element_size() * (self.x.shape[1] if self.x.dim() == 2 else 1)
-            target = min(first_chunk_bytes, chunk_bytes) if first_chunk_bytes > 0 else chunk_bytes
+            target = chunk_bytes
             bounds, start, acc = [], 0, 0
             for i in order:
                 self.chunk_of[i] = len(bounds)
@@ -250,7 +248,6 @@ class HostPack:
                     end = int(self.row_off[i] + n_rows[i])
                     bounds.append((start, end))
                     start, acc = end, 0
-                    target = min(2 * target, chunk_bytes)
             if start < self.x.shape[0] or not bounds:
                 bounds.append((start, int(self.x.shape[0])))
             self.chunks = bounds
@@ -324,8 +321,12 @@ def steps_per_epoch(n: int, b: int) -> int:
 def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], epochs: int,
                    dropout_rate: float, w_out: torch.Tensor | None = None,
                    rt: Runtime | None = None):
-    """List-of-requests front end of :func:`train_batch`."""
+    """List-of-requests front end of :func:`train_batch` (fp64 trainer: every
+    start vector must be a float64 device tensor)."""
     n = len(reqs)
+    for r in reqs:
+        if r.w_start.dtype != torch.float64 or not r.w_start.is_cuda:
+            raise ValueError(f"w_start must be a float64 CUDA tensor, got {r.w_start.dtype} on {r.w_start.device}")
     return train_batch(
         spec_dims, shards,
         clients=np.array([r.client for r in reqs], dtype=np.int64),
@@ -340,11 +341,6 @@ def train_requests(spec_dims, shards: DeviceShards, reqs: list[TrainRequest], ep
         w_out=w_out, rt=rt)
 
 
-# launch K3 before K2 when building a plan (FS_K3_FIRST=1; measured: the trainer
-# then slows by as much as the round tail gains)
-K3_FIRST = os.environ.get("FS_K3_FIRST", "0") == "1"
-
-
 class TrainPlan:
     """The data-independent half of a training launch: per-request metadata in
     HBM plus the K2 permutations and K3 dropout keep-bits. It depends only on
@@ -354,13 +350,12 @@ class TrainPlan:
 
     def __init__(self, spec_dims, shards: "DeviceShards", clients, seeds, batch, epochs: int,
                  dropout_rate: float, start=None, end=None, rt: Runtime | None = None, stream=None,
-                 mask_stream=None,
-                 pool: dict | None = None, stage: "Stage | None" = None, defer_masks: bool = False,
+                 pool: dict | None = None, stage: "Stage | None" = None,
                  data_chunk: np.ndarray | None = None):
         rt = rt or Runtime.get()
         self.rt = rt
         self.stage = stage
-        self.mask_flags = None   # set when K3 runs later, concurrently with the trainer (launch_masks)
+        self.mask_flags = None   # per-(request, step) keep-bit flags: unused by the engines (K3 runs before the trainer)
         self._desc = None        # (precision, static TrainDesc) built by static_desc()
         self.workspace_need = 0
         self.prefilled = None    # (precision, lr, desc, w_out, status, run) prepared by prefill()
@@ -449,19 +444,10 @@ class TrainPlan:
         self.row_off_p, self.perm_off_p, self.mask_off_p, self.seeds_p = (p64 + 8 * n * k for k in range(4))
         self.n_rows_p, self.batch_p, self.start_p, self.end_p, self.order_p = (p32 + 4 * n * k for k in range(5))
         self.chunk_p = p32 + 4 * n * 5 if self.has_chunks else None
-        k3_stream = torch_stream
-        if mask_stream is not None and use_masks and self.epochs > 0 and not defer_masks:
-            # K3 (ALU-bound) and K2 (latency-bound) are independent: run them
-            # side by side so both finish under the trainer they overlap
-            copied = torch.cuda.Event()
-            copied.record(torch_stream)
-            mask_stream.wait_event(copied)
-            k3_stream = mask_stream
         self.scale = 1.0
         self.max_steps = int(end.max()) if n else 0
         self.sum_hidden = sum_hidden
         keep = 1.0 - self.dropout_rate
-        k3_now = self.bits is not None and not defer_masks
 
         def launch_k2():
             if self.epochs > 0:
@@ -470,34 +456,15 @@ class TrainPlan:
 
         def launch_k3():
             rt.call(lib.fs_dropout_bits(self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, n,
-                                        self.epochs, sum_hidden, keep, self.bits.data_ptr(),
-                                        k3_stream.cuda_stream), "fs_dropout_bits")
-            if k3_stream is not torch_stream:
-                masks_done = torch.cuda.Event()
-                masks_done.record(k3_stream)
-                torch_stream.wait_event(masks_done)
+                                        self.epochs, sum_hidden, keep, self.bits.data_ptr(), s_handle),
+                    "fs_dropout_bits")
 
-        # K3 (the longer, ALU-bound one) first: the block scheduler drains one
-        # kernel's CTAs before the next, so the order decides which starts under the trainer
-        if k3_now and K3_FIRST:
-            launch_k3()
-            launch_k2()
-        else:
-            launch_k2()
-            if k3_now:
-                launch_k3()
+        # K2 then K3 on the plan's stream (K3 first or on a second stream was
+        # measured: the trainer slows by as much as the round tail gains)
+        launch_k2()
         if self.bits is not None:
+            launch_k3()
             self.scale = 1.0 / keep
-            if defer_masks:
-                # K3 is launched with the trainer (launch_masks); steps are
-                # published through per-(request, step) flags
-                flags = pool.get("flags") if pool is not None else None
-                need = n * self.max_steps
-                if flags is None or flags.numel() < need:
-                    flags = torch.zeros(int(need * 1.25) + 1, dtype=torch.int32, device=rt.device)
-                    if pool is not None:
-                        pool["flags"] = flags
-                self.mask_flags = flags
         if stream is not None:  # consumer stream waits on this event before the trainer reads the plan
             self.ready = torch.cuda.Event()
             self.ready.record(torch_stream)
@@ -588,17 +555,6 @@ class TrainPlan:
             t = torch.empty(int(n_elems * 1.25) + 1, dtype=dtype, device=self.rt.device)
             self._pool[name] = t
         return t[:n_elems]
-
-    def launch_masks(self, stream, tag: int) -> None:
-        """K3 for a deferred-mask plan on `stream`, concurrent with the trainer
-        that consumes it step by step (fs_dropout_bits_flagged)."""
-        if self.mask_flags is None:
-            return
-        self.mask_tag = int(tag)
-        self.rt.call(self.rt.lib.fs_dropout_bits_flagged(
-            self.seeds_p, self.n_rows_p, self.batch_p, self.mask_off_p, self.order_p, self.n, self.epochs,
-            self.max_steps, self.sum_hidden, 1.0 - self.dropout_rate, self.bits.data_ptr(),
-            self.mask_flags.data_ptr(), self.mask_tag, stream.cuda_stream), "fs_dropout_bits_flagged")
 
     def matches(self, clients, seeds, batch, epochs) -> bool:
         return (self.epochs == epochs and np.array_equal(self.clients, clients)
@@ -776,7 +732,7 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
     return run_trainer(plan, lr, w_start, precision, w_out)
 
 
-TRAIN_GRID = int(__import__("os").environ.get("FS_TRAIN_GRID", "0"))
+TRAIN_GRID = 0  # persistent trainer grid (0 = library default: one CTA per SM)
 
 
 # --------------------------------------------------------------- alignment

@@ -5,18 +5,23 @@ stream (dataset, stratified split, Dirichlet partition, per-client
 profiles, capacity-driven batch sizes, checkpoint interval, geometry,
 failure schedule, initial parameters), so a config yields the same world
 as in the reference; tests/golden pins the digests. ``run_experiment``
-drives the engine and returns the replay digest and final parameters
-(artifact files are control plane and not written).
+drives the engine, returns the replay digest, summary and final parameters
+and writes the reference's run-directory artifacts (except the checkpoint
+blob); ``replay_run`` re-runs a directory and compares digests.
 """
 
 from __future__ import annotations
 
 import hashlib
+import json
+import os
 import time
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import __version__
+from .backends import backend_name
 from .client import ClientProfile, assign_batch_size
 from .config import ExperimentConfig
 from .data import partition_dirichlet, stratified_split, synth_anomaly
@@ -25,7 +30,8 @@ from .model import ModelSpec, ParamVector, init_params
 from .rng import derive_rng, derive_seed
 from .selection import SelectionPolicy
 from .server import FederationEngine, World, WorldClient, finalize_client_geometry
-from .simnet import DistSpec
+from .metrics import summarize_reports, write_reports
+from .simnet import DistSpec, write_event_log
 
 
 def params_digest(params: ParamVector) -> str:
@@ -104,6 +110,7 @@ class RunResult:
     reports: list
     final_params: ParamVector
     digest: str
+    summary: dict
     wall_clock_s: float
 
     @property
@@ -115,14 +122,54 @@ class RunResult:
         return self.reports[-1].auc if self.reports else float("nan")
 
 
-def run_experiment(config: ExperimentConfig, world_and_initial=None, workers: int = 1,
-                   precision: str = "fp64") -> RunResult:
-    """Build (or take) a world and run it; ``workers`` is accepted for API
-    compatibility (clients are batched on the device, results are identical)."""
+def run_experiment(config: ExperimentConfig, out_dir: str | None = None, workers: int = 1, *,
+                   world_and_initial=None, precision: str = "fp64") -> RunResult:
+    """Build a world, run it, and (with ``out_dir``) write the run directory
+    (reference experiment.py:206-272): ``config.json``, ``events.jsonl``,
+    ``rounds.jsonl``, ``summary.csv`` and ``run_meta.json``.
+
+    ``workers`` is accepted for API compatibility (clients are batched on the
+    device; results do not depend on it). Framework extensions are
+    keyword-only: ``world_and_initial`` reuses a prebuilt ``build_world``
+    result, ``precision`` selects the fp64 parity or bf16 trainer. The
+    global-model checkpoint file (``checkpoints/``) is not written: the
+    checkpoint blob codec is outside the round-loop scope."""
+    t0 = time.perf_counter()
     world, initial = (world_and_initial if world_and_initial is not None
                       else build_world(config, workers=workers, precision=precision))
     engine = FederationEngine(world)
-    t0 = time.perf_counter()
     state = engine.run(initial)
     wall = time.perf_counter() - t0
-    return RunResult(config, world, engine, engine.reports, state.w_g, engine.timeline.digest(), wall)
+    digest = engine.timeline.digest()
+    extra = {"seed": config.seed, "mode": config.mode, "theta": world.policy.theta}
+    result = RunResult(config, world, engine, engine.reports, state.w_g, digest, {}, wall)
+    if out_dir is None:
+        result.summary = summarize_reports(engine.reports, extra)
+        return result
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "config.json"), "w", encoding="utf-8") as f:
+        f.write(config.canonical_json())
+    write_event_log(list(engine.timeline.log), os.path.join(out_dir, "events.jsonl"))
+    result.summary = write_reports(engine.reports, out_dir, extra)
+    meta = {"digest": digest, "params_digest": params_digest(state.w_g), "backend": backend_name(),
+            "version": __version__, "events": len(engine.timeline.log), "wall_clock_s": wall,
+            "workers": workers, "precision": world.precision}
+    with open(os.path.join(out_dir, "run_meta.json"), "w", encoding="utf-8") as f:
+        json.dump(meta, f, indent=2, sort_keys=True)
+    return result
+
+
+def replay_run(run_dir: str, workers: int = 1) -> tuple[bool, dict]:
+    """Re-run a run directory's config and compare the replay and parameter
+    digests with the recorded ones (reference experiment.py:275-296)."""
+    config = ExperimentConfig.from_file(os.path.join(run_dir, "config.json"))
+    with open(os.path.join(run_dir, "run_meta.json"), encoding="utf-8") as f:
+        meta = json.load(f)
+    result = run_experiment(config, None, workers, precision=meta.get("precision", "fp64"))
+    report = {"recorded_digest": meta["digest"], "replayed_digest": result.digest,
+              "recorded_params_digest": meta.get("params_digest"),
+              "replayed_params_digest": params_digest(result.final_params),
+              "recorded_backend": meta.get("backend"), "active_backend": backend_name()}
+    ok = (report["recorded_digest"] == report["replayed_digest"]
+          and report["recorded_params_digest"] == report["replayed_params_digest"])
+    return ok, report

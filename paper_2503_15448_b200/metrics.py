@@ -84,3 +84,53 @@ def accuracy(scores, labels, threshold: float = 0.5) -> float:
 
 def auc_roc(scores, labels) -> float:
     return evaluate(scores, labels).auc
+
+
+SUMMARY_FIELDS = [
+    "schema", "rounds", "accuracy", "auc", "comm_time_s", "transfer_s", "updates", "aggregations",
+    "accepted_frac", "staleness_mean", "staleness_max", "sgd_steps", "seed", "mode", "theta",
+]
+
+
+def summarize_reports(reports: list, summary_extra: dict | None = None) -> dict:
+    """The one-row run summary (metrics.py:246-275 semantics): last-round
+    accuracy/AUC/times, totals over rounds, accepted fraction over decisions."""
+    if reports:
+        last = reports[-1]
+        decided = sum(r.accepted + r.rejected for r in reports)
+        summary = {
+            "schema": REPORT_SCHEMA_VERSION, "rounds": len(reports), "accuracy": last.accuracy,
+            "auc": last.auc, "comm_time_s": last.comm_time_s, "transfer_s": last.transfer_s,
+            "updates": sum(r.updates for r in reports), "aggregations": sum(r.aggregations for r in reports),
+            "accepted_frac": sum(r.accepted for r in reports) / max(1, decided),
+            "staleness_mean": last.staleness_mean,
+            "staleness_max": max((r.staleness_max for r in reports), default=0),
+            "sgd_steps": sum(r.sgd_steps for r in reports),
+        }
+    else:
+        summary = {"schema": REPORT_SCHEMA_VERSION, "rounds": 0}
+    for key in ("seed", "mode", "theta"):
+        summary.setdefault(key, "")
+    if summary_extra:
+        summary.update(summary_extra)
+    return summary
+
+
+def write_reports(reports: list, out_dir: str, summary_extra: dict | None = None) -> dict:
+    """rounds.jsonl (one record per report) and summary.csv (header + one
+    row; header only for a zero-round run); returns the summary row."""
+    import csv
+    import json
+    import os
+
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "rounds.jsonl"), "w", encoding="utf-8") as f:
+        for rep in reports:
+            f.write(json.dumps(rep.to_record()) + "\n")
+    summary = summarize_reports(reports, summary_extra)
+    with open(os.path.join(out_dir, "summary.csv"), "w", encoding="utf-8", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=SUMMARY_FIELDS, extrasaction="ignore")
+        w.writeheader()
+        if reports:
+            w.writerow({k: summary.get(k, "") for k in SUMMARY_FIELDS})
+    return summary

@@ -13,6 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from .model import ParamVector
 
@@ -54,11 +55,15 @@ def relevance_batched(wc_rows, wg_list, wgp_list, M: int, mode: str) -> np.ndarr
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
     rt = D.Runtime.get()
+    tensors = list(wc_rows) + list(wg_list) + (list(wgp_list) if mode == "delta_sign" else [])
+    dtypes = {t.dtype for t in tensors}
+    if len(dtypes) > 1 or not dtypes <= {torch.float32, torch.float64}:
+        raise ValueError(f"parameter vectors must share one dtype (float32 or float64), got {sorted(map(str, dtypes))}")
     out = D.align_requests(
         [t.data_ptr() for t in wc_rows],
         [t.data_ptr() for t in wg_list],
         [t.data_ptr() for t in wgp_list] if mode == "delta_sign" else None,
-        M, mode, rt,
+        M, mode, rt, dtype=dtypes.pop() if dtypes else torch.float64,
     )
     return out.cpu().numpy()
 

@@ -311,16 +311,17 @@ def test_eval_metrics_f32_keys_match_f64_keys(n, levels):
         assert np.array_equal(a, b), (a, b)
 
 
-@pytest.mark.parametrize("chunk_mb", ["0", "0.02", "8"])
+@pytest.mark.parametrize("chunk_mb", [0.0, 0.02, 8.0])
 def test_host_upload_rounds_match_resident_rounds(monkeypatch, chunk_mb):
     """The public e2e path (World.upload before every sync round: shards from
     page-locked host memory, chunked with per-client flags the trainer waits
     on, test set on a copy stream) reproduces the HBM-resident run exactly."""
     from paper_2503_15448_b200.config import ExperimentConfig
     from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200 import server as S
     from paper_2503_15448_b200.server import FederationEngine, GlobalState
 
-    monkeypatch.setenv("FS_UPLOAD_CHUNK_MB", chunk_mb)
+    monkeypatch.setattr(S, "UPLOAD_CHUNK_MB", chunk_mb)
     cfg = {"num_clients": 48, "rounds": 3, "epochs": 2, "mode": "sync_filtered", "selection_mode": "delta_sign",
            "seed": 3, "dataset": {"kind": "synthetic", "n": 9000, "d": 42, "anomaly_frac": 0.3},
            "partition": {"alpha": 0.5}, "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3},
