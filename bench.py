@@ -27,7 +27,6 @@ import subprocess
 import sys
 import threading
 import time
-from concurrent.futures import ThreadPoolExecutor
 
 # CPU legs run the oracle single-threaded: the reference path is GIL-bound, and
 # a thread pool over clients (the reference's `workers`) plus BLAS threads was
@@ -54,6 +53,8 @@ C4_SYNC = {
     "lr": 0.05, "lr_decay": 0.9,
 }
 METRIC = "FL rounds/sec (1024 UNSW-shaped clients, C4 sync_filtered)"
+C4_WORKLOAD = ("C4 sync_filtered: 1024 UNSW-shaped clients (175,341 train rows, d=42), MLP 42-256-128-64-1 "
+               "dropout 0.3, E=5, dynamic batch 64..1024, delta_sign theta=0.65, FedAvg, eval on 43,835 rows")
 N_DELTA = 1  # FS_ALIGN_DELTA_SIGN
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA-core and DMMA) nominal; no measured fp64 peak exists
@@ -171,103 +172,80 @@ class _SmiSampler:
 
 
 # ------------------------------------------------------------------ CPU sides
-_ORACLE_JOB = None
+def reference_engine(workers: int):
+    """The REFERENCE package (oracle/_ref/pkg: the shipped fedsim with its
+    compiled Cython backend, built by oracle/build_ref.sh) on the C4 config:
+    its own build_world, FederationEngine and run_sync_round. With workers > 1
+    the reference's client fan-out (server.py:412-415, a GIL-bound thread
+    pool) runs in forked processes instead (oracle/ref_pool.py)."""
+    from oracle.ref_pool import patch_server_pool, use_reference
+
+    use_reference("compiled")
+    import fedsim.server
+    from fedsim.config import ExperimentConfig
+    from fedsim.experiment import build_world
+    from fedsim.server import FederationEngine, GlobalState
+
+    if workers > 1:
+        patch_server_pool(fedsim.server)
+    world, initial = build_world(ExperimentConfig.from_dict(dict(C4_SYNC)), workers=workers)
+    return FederationEngine(world), GlobalState(round=0, w_g=initial)
 
 
-def _oracle_cycles(clients):
-    """Worker process body: oracle client cycles (accepted flag + params only)."""
-    sim, r, w0, wp = _ORACLE_JOB
-    out = []
-    for ci in clients:
-        o = sim.cycle(ci, r, r, w0, wp)
-        out.append({"accepted": o["accepted"], "res": {"params": o["res"]["params"]}})
-    return out
-
-
-def oracle_round_sample(world, initial, sample_clients: int, round_index: int = 0, w_prev=None, workers: int = 1,
-                        processes: int = 1):
-    """Time the oracle (reference algorithm, numpy, 1 thread) on a bounded
-    sample of one C4 sync round: `sample_clients` client cycles (training +
-    delta_sign scoring), FedAvg of their updates, and one full evaluation.
-    Returns (extrapolated seconds per 1024-client round, detail)."""
-    from oracle import fl_oracle as O
-
-    sim = O.OracleFederation(world)
-    n = world.num_clients
-    w0 = initial.values
-    wp = w_prev if w_prev is not None else w0 * 0.999
-    picks = [int(i) for i in np.linspace(0, n - 1, sample_clients).round()]
-    if processes > 1:
-        # every host core: one forked worker process per core, clients dealt
-        # round-robin (the reference's own thread pool is GIL-bound, see top)
-        import multiprocessing as mp
-
-        global _ORACLE_JOB
-        _ORACLE_JOB = (sim, round_index, w0, wp)
-        ctx = mp.get_context("fork")
-        with ctx.Pool(processes) as pool:
-            pool.map(_oracle_cycles, [[0]] * processes)  # workers up (fork, imports) before the clock
-            t0 = time.perf_counter()
-            chunks = [picks[i::processes] for i in range(processes)]
-            outs = [o for part in pool.map(_oracle_cycles, chunks) for o in part]
-            t_train = time.perf_counter() - t0
-    else:
+def time_reference_rounds(workers: int, warmup: int, steps: int):
+    """Wall-clock seconds of `steps` consecutive full C4 sync rounds of the
+    reference (after `warmup` rounds; round 0 has no delta_sign scoring, so
+    warmup >= 1 puts only scored rounds in the timed region)."""
+    eng, state = reference_engine(workers)
+    for _ in range(warmup):
+        state = eng.run_sync_round(state)
+    times = []
+    for _ in range(steps):
         t0 = time.perf_counter()
-        if workers > 1:  # the reference's own fan-out: a thread pool over clients (server.py:412-415)
-            with ThreadPoolExecutor(max_workers=workers) as pool:
-                outs = list(pool.map(lambda ci: sim.cycle(ci, round_index, round_index, w0, wp), picks))
-        else:
-            outs = [sim.cycle(ci, round_index, round_index, w0, wp) for ci in picks]
-        t_train = time.perf_counter() - t0
-    ups = [o["res"]["params"] for o in outs if o["accepted"]]
-    t0 = time.perf_counter()
-    O.fedavg(ups if ups else [w0])
-    t_agg = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    p = O.probs(w0, world.spec.dims, np.ascontiguousarray(world.test_features))
-    O.acc_auc(p, world.test_labels)
-    t_eval = time.perf_counter() - t0
-    per_round = (t_train + t_agg) * n / len(picks) + t_eval
-    return per_round, {"t_train_s": t_train, "t_agg_s": t_agg, "t_eval_s": t_eval, "clients": len(picks)}
-
-
-def cpu_threads_used() -> int:
-    return 1  # numpy oracle; BLAS pinned to one thread below
+        state = eng.run_sync_round(state)
+        times.append(time.perf_counter() - t0)
+    rep = eng.reports[-1]
+    return times, {"round": state.round, "accuracy": rep.accuracy, "auc": rep.auc}
 
 
 def run_reference(args, rank: int, world_size: int) -> None:
     if rank != 0:
         return
-    world, initial = build_c4_world()
-    sample = args.ref_sample
     procs = args.ref_procs if args.ref_procs > 0 else (os.cpu_count() or 1)
-    threads = max(1, args.ref_workers)
-    if procs > 1:
-        sample = max(sample, 8 * procs)
-    times = []
-    for i in range(args.warmup + args.steps):
-        per_round, detail = oracle_round_sample(world, initial, sample, round_index=0, workers=threads,
-                                                processes=procs)
-        if i >= args.warmup:
-            times.append(per_round)
+    times, quality = time_reference_rounds(procs, max(1, args.warmup), args.steps)
     sec = float(np.mean(times))
     value = 1.0 / sec
+    sample = (f"{args.steps} consecutive full C4 sync rounds (1024 clients, after {max(1, args.warmup)} warm-up "
+              f"rounds) of the reference package's own FederationEngine.run_sync_round, Cython backend, "
+              f"1 BLAS thread per process; client fan-out over {procs} forked worker processes (the "
+              f"reference's thread pool, server.py:412-415, is GIL-bound)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world_size,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients, MLP 42-256-128-64-1, E=5, "
-                               "dynamic batch, delta_sign theta=0.65"},
-        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": max(procs, threads), "kind": "port",
-                         "sample": f"{sample} of 1024 client cycles of round 0 + FedAvg + full eval per step, "
-                                   f"extrapolated x1024/sample (oracle/fl_oracle.py, numpy, 1 BLAS thread; "
-                                   + (f"{procs} forked worker processes over clients, one per host core)" if procs > 1
-                                      else f"{threads} worker thread(s) over clients like the reference's `workers`)"),
-                         "host_cores": os.cpu_count()},
+        "config": {"workload": C4_WORKLOAD},
+        "cpu_baseline": {"value": value, "unit": "rounds/s", "cores": procs, "kind": "reference",
+                         "sample": sample, "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "client_updates_per_s": value * 1024,
+        "round_s": [round(t, 3) for t in times],
+        "quality": quality,
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_cpu_baseline():
+    """cpu_baseline of the b200 arm: the reference package on ONE core (its
+    default workers=1), one full C4 sync round (round 0: all 1024 clients
+    train, FedAvg, evaluation; ~20 s of CPU work)."""
+    eng, state = reference_engine(1)
+    t0 = time.perf_counter()
+    eng.run_sync_round(state)
+    sec = time.perf_counter() - t0
+    return {"value": 1.0 / sec, "unit": "rounds/s", "cores": 1, "kind": "reference",
+            "sample": "one full C4 sync round (round 0: 1024 clients train 5 epochs, FedAvg, evaluation; "
+                      "delta_sign scoring starts in round 1) of the reference package (oracle/_ref/pkg, "
+                      "Cython backend, workers=1, 1 BLAS thread)", "seconds": sec}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -305,6 +283,9 @@ def measure_rounds(world, initial, comm, steps: int, warmup: int, device_index: 
     calls0 = D.Runtime.abi_calls
     trainings0 = eng.trainings
     round_ms = []
+    import gc
+
+    gc.disable()  # no collector pauses inside the timed rounds (re-enabled below)
     with ClockSampler(device_index) as clocks:
         for _ in range(steps):
             flush_l2(l2_flush)
@@ -316,6 +297,7 @@ def measure_rounds(world, initial, comm, steps: int, warmup: int, device_index: 
             barrier()
             clocks.sample()
             round_ms.append(a.elapsed_time(b))
+    gc.enable()
     timer, D.Runtime.timer = D.Runtime.timer, None
     total_ms = float(np.sum(round_ms))
     if dist is not None:
@@ -353,9 +335,13 @@ def measure_e2e(world, eng, state, reps: int, barrier):
     return 1000.0 / float(np.mean(e2e_ms)), int(h2d), int(d2h)
 
 
+NCU_TRAFFIC_FILE = "profiles/r1_ncu_train_kernel.json"
+NCU_TRAFFIC_SOURCE = f"{NCU_TRAFFIC_FILE} (dram read+write bytes, one ncu --set full launch)"
+
+
 def _ncu_traffic():
     """dram__bytes_read+write of the trainer from the committed ncu capture (per launch)."""
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_train_kernel.json")
+    f = os.path.join(ROOT, NCU_TRAFFIC_FILE)
     try:
         return json.load(open(f))["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
@@ -576,7 +562,37 @@ def measure_c5_async_share(precision: str):
             "digest": eng.timeline.digest()}
 
 
+def reference_quality(rounds: int = 5):
+    """The reference's own per-round accuracy/AUC on C4 (committed fixture
+    tests/golden/configs.json, recorded from the reference package by
+    tests/golden/make_golden_configs.py)."""
+    f = os.path.join(ROOT, "tests", "golden", "configs.json")
+    try:
+        rep = json.load(open(f))["c4_sync"]["reports"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"round": rounds - 1, "accuracy": rep[rounds - 1]["accuracy"], "auc": rep[rounds - 1]["auc"],
+            "source": "reference package, tests/golden/configs.json (c4_sync)"}
+
+
+def measure_quality(precision: str, rounds: int = 5):
+    """Accuracy/AUC of the global model after `rounds` C4 rounds from the
+    initial model (the bench's own world, this precision)."""
+    from paper_2503_15448_b200.server import FederationEngine, GlobalState
+
+    world, initial = build_c4_world(precision=precision)
+    eng = FederationEngine(world)
+    st = GlobalState(round=0, w_g=initial)
+    for _ in range(rounds):
+        st = eng.run_sync_round(st)
+    rep = eng.reports[-1]
+    return {"round": rounds - 1, "accuracy": rep.accuracy, "auc": rep.auc,
+            "accepted": [r.accepted for r in eng.reports]}
+
+
 def run_b200(args, rank: int, world_size: int) -> None:
+    import gc
+
     import torch
 
     from paper_2503_15448_b200.parallel import ShardComm
@@ -584,6 +600,8 @@ def run_b200(args, rank: int, world_size: int) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     comm = ShardComm.from_env()
+    gc.collect()
+    gc.freeze()  # the worlds built below outlive the bench: keep them out of the collector's scans
     world, initial = build_c4_world(precision=args.precision)
     m = measure_rounds(world, initial, comm, args.steps, args.warmup, local)
     value = 1000.0 / m["ms_per_round"]
@@ -592,8 +610,10 @@ def run_b200(args, rank: int, world_size: int) -> None:
     if not args.no_parity:
         w64, i64 = build_c4_world(precision="fp64")
         p = measure_rounds(w64, i64, comm, 3, 3, local)
+        e64, h64, d64 = measure_e2e(w64, p["engine"], p["state"], 2, p["barrier"])
         parity = {"value": 1000.0 / p["ms_per_round"], "unit": "rounds/s", "ms_per_step": p["ms_per_round"],
                   "train_kernel_ms": p["kernels"].get("train", {}).get("mean_ms"),
+                  "e2e": {"value": e64, "unit": "rounds/s", "h2d_bytes_per_step": h64, "d2h_bytes_per_step": d64},
                   "note": "fp64 parity mode: event log bit-identical to the reference (tests/test_gpu_parity.py)"}
     if rank != 0:
         if comm is not None:
@@ -601,6 +621,12 @@ def run_b200(args, rank: int, world_size: int) -> None:
 
             dist.destroy_process_group()
         return
+    quality = None
+    if world_size == 1 and not args.no_quality:
+        quality = {"bf16": measure_quality("bf16"), "fp64": measure_quality("fp64"),
+                   "reference": reference_quality(),
+                   "note": "accuracy/AUC on the 43,835-row test split after 5 C4 rounds from the same initial "
+                           "model; fp64 equals the reference exactly, bf16 is tolerance-matched"}
     ksum = m["kernels"]
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     tr = ksum.get("train", {})
@@ -615,7 +641,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
     roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if achieved else None, "peak_source": src,
                      "traffic": _ncu_traffic() if args.precision == "bf16" else None,
-                     "traffic_source": "profiles/r1_ncu_train_kernel.json (dram read+write bytes, one ncu --set full launch)",
+                     "traffic_source": NCU_TRAFFIC_SOURCE,
                      "algorithmic_flops_per_launch": tr.get("work_per_launch"),
                      "share_of_round": tr.get("total_ms", 0.0) / (m["ms_per_round"] * args.steps) if tr else None})
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -642,18 +668,15 @@ def run_b200(args, rank: int, world_size: int) -> None:
         small = measure_small_configs(args.precision)
     cpu = None
     if world_size == 1 and not args.no_cpu:
-        per_round, detail = oracle_round_sample(world, initial, args.cpu_sample)
-        cpu = {"value": 1.0 / per_round, "unit": "rounds/s", "cores": cpu_threads_used(), "kind": "port",
-               "sample": f"{args.cpu_sample} of 1024 client cycles of round 0 + FedAvg + full eval, "
-                         f"extrapolated x1024/{args.cpu_sample}; oracle/fl_oracle.py numpy, 1 thread",
-               "detail": detail}
+        try:
+            cpu = reference_cpu_baseline()
+        except ImportError as e:  # oracle/_ref not shipped with this snapshot
+            cpu = {"value": None, "unit": "rounds/s", "cores": 1, "kind": "reference", "unavailable": str(e)}
     line = {
         "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world_size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": m["ms_per_round"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "f64", "data": "synthetic",
-        "config": {"workload": "C4 sync_filtered: 1024 UNSW-shaped clients (175,341 train rows, d=42), "
-                               "MLP 42-256-128-64-1 dropout 0.3, E=5, dynamic batch 64..1024, delta_sign "
-                               "theta=0.65, FedAvg, eval on 43,835 rows",
+        "config": {"workload": C4_WORKLOAD,
                    "precision": ("bf16 GEMM operands, fp32 accumulate/master weights (tolerance-matched)"
                                  if args.precision == "bf16" else "fp64 parity (digest-identical to reference)"),
                    "l2": "256 MiB buffer written between timed rounds (L2 flush)",
@@ -669,6 +692,7 @@ def run_b200(args, rank: int, world_size: int) -> None:
                                 "in_round: CUDA events around the launch inside the timed rounds, where the "
                                 "next round's K2/K3 prefetch shares the SMs (overlap by design)"},
         "fp64_parity": parity,
+        "quality": quality,
         "async_c4": async_c4,
         "c5_share_1gpu": c5_share,
         "c2_c3_1gpu": small,
@@ -686,25 +710,38 @@ def run_b200(args, rank: int, world_size: int) -> None:
         dist.destroy_process_group()
 
 
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: relaunch this command as N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=256)
-    ap.add_argument("--ref-sample", type=int, default=64)
-    ap.add_argument("--ref-workers", type=int, default=1, help="thread pool over clients (GIL-bound)")
     ap.add_argument("--ref-procs", type=int, default=0, help="worker processes for the reference arm (0: all cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
     ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity-mode measurement")
+    ap.add_argument("--no-quality", action="store_true", help="skip the 5-round accuracy/AUC check")
     ap.add_argument("--no-micro", action="store_true", help="skip the C5-shape HBM microbenchmark")
     ap.add_argument("--no-async", action="store_true", help="skip the C4 async-engine measurement")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5-share (WIDE MLP) measurement")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    world_size = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, rank, world_size)
     else:

@@ -111,3 +111,25 @@ def test_oracle_runs_replay_reference_digest(golden, name):
         assert got["accuracy"] == pytest.approx(ref["accuracy"], abs=1e-9)
         assert got["auc"] == pytest.approx(ref["auc"], abs=1e-9)
         assert got["accepted"] == ref["accepted"] and got["sgd_steps"] == ref["sgd_steps"]
+
+
+def test_oracle_replays_reference_at_road_config():
+    """BASELINE configs[2] (C3: 256 ROAD-shaped clients, sync_filtered,
+    delta_sign, 2 rounds; tests/golden/configs.json recorded from the
+    reference package): the oracle replays the digest and final model. The
+    larger configs (C1, C2, C4) are checked against the CUDA path only
+    (tests/test_gpu_configs.py); the oracle needs minutes per C4 round."""
+    import json
+    import os
+
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from tests.conftest import GOLDEN
+
+    ref = json.load(open(os.path.join(GOLDEN, "configs.json")))["c3_sync"]
+    want = np.load(os.path.join(GOLDEN, "configs_wg.npz"))["c3_sync_wg"]
+    world, init = build_world(ExperimentConfig.from_dict(ref["config"]))
+    sim = O.OracleFederation(world)
+    wg = sim.run(init.values)
+    assert sim.digest() == ref["digest"]
+    assert np.max(np.abs(wg - want) / np.maximum(np.abs(want), 1.0)) < 1e-12
