@@ -80,10 +80,16 @@ def calculate_relevance(w_c: ParamVector, w_g: ParamVector, w_g_prev: ParamVecto
             raise ValueError("delta_sign mode requires w_g_prev")
         if len(w_g_prev) != len(w_g):
             raise ValueError("w_g_prev length mismatch")
-        prev = [w_g_prev.device_tensor()]
+        prev = [w_g_prev]
     else:
         raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
-    aligned = relevance_batched([w_c.device_tensor()], [w_g.device_tensor()], prev, len(w_c), mode)
+    # the vectors' stored dtype when they share one (bf16-mode float32 rows),
+    # else float64; 3-class signs of a difference are the same either way
+    vecs = [w_c, w_g] + prev
+    ts = [v.device_native() for v in vecs]
+    if len({t.dtype for t in ts}) > 1:
+        ts = [v.device_tensor() for v in vecs]
+    aligned = relevance_batched(ts[:1], ts[1:2], ts[2:], len(w_c), mode)
     return RelevanceScore(aligned=int(aligned[0]), total=len(w_c))
 
 

@@ -402,3 +402,36 @@ def test_client_sharded_rounds_match_single_process(prec, mode, sel):
                           "127.0.0.1", "--master-port", str(port), os.path.join(root, "scripts", "sharded_check.py"),
                           prec, mode, sel], env=env, capture_output=True, text=True, timeout=600, cwd=root)
     assert "SHARDED OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
+
+
+def test_engine_keeps_caller_vectors_and_checkpoints_intact():
+    """A bf16 run does not turn the caller's float64 vector into float32
+    (device_tensor() stays float64, values unchanged); every global
+    checkpoint keeps the model of its round although only the newest one
+    stays in HBM (older ones move to host memory); a checkpoint is a separate
+    vector from the engine state."""
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine, GlobalState
+
+    cfg = {"num_clients": 12, "rounds": 4, "epochs": 1, "selection_mode": "delta_sign", "seed": 4,
+           "dataset": {"n": 4000, "d": 42}, "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}}
+    world, initial = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+    before = initial.values.copy()
+    assert initial.device_tensor().dtype == torch.float64
+    eng = FederationEngine(world)
+    st = GlobalState(round=0, w_g=initial)
+    seen = []
+    for _ in range(4):
+        st = eng.run_sync_round(st)
+        seen.append(st.w_g.values.copy())
+    assert initial.device_tensor().dtype == torch.float64
+    assert np.array_equal(initial.values, before)
+    cps = eng.global_checkpoints
+    assert [c.round for c in cps] == [0, 1, 2, 3]
+    assert [c.params.is_on_device for c in cps] == [False, False, False, True]
+    for c, want in zip(cps, seen):
+        assert np.array_equal(c.params.values, want)
+    assert cps[-1].params is not st.w_g
+    st.w_g.values = np.zeros_like(seen[-1])  # replacing the state's values leaves the checkpoint alone
+    assert np.array_equal(cps[-1].params.values, seen[-1])
