@@ -512,11 +512,15 @@ def measure_c5_share(precision: str, rounds: int = 2):
     D.Runtime.timer = D.KernelTimer()
     stream = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import gc
+
+    gc.disable()  # no collector pauses inside the timed rounds
     a.record(stream)
     for _ in range(rounds):
         st = eng.run_sync_round(st)
     b.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     ks, D.Runtime.timer = D.Runtime.timer.summary(), None
     ms = a.elapsed_time(b) / rounds
     tr = ks.get("train", {})
