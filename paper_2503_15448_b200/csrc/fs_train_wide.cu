@@ -1,89 +1,105 @@
 // K5 (bf16 mode) for MLPs whose hidden layers do not fit the on-chip
-// trainers: the WIDE shape of BASELINE configs[4] (42-1024-1024-1024-1024-1).
-// Same contract as fs_train_bf16 (client.train_local, client.py:98-172 with
-// bf16 GEMM operands and fp32 masters): K2 permutations, K3 keep bits, per
-// epoch learning rates, BCE on logits, plain SGD.
+// trainers: the WIDE shape of BASELINE configs[4] (42-1024-1024-1024-1024-1)
+// and any other layer widths. Same contract as fs_train_bf16
+// (client.train_local, client.py:98-172 with bf16 GEMM operands and fp32
+// masters): K2 permutations, K3 keep bits, per-epoch learning rates, BCE on
+// logits, plain SGD (model.py:189-221, _core.pyx:140-219).
 //
 // A 1024x1024 layer (2 MB bf16, 4 MB fp32 master) cannot stay on one SM, so
-// the clients of a launch train in lockstep instead: global SGD step t runs
-// step t of every client that has one, each layer product being ONE batched
-// GEMM over those clients (cublasGemmBatchedEx, bf16 x bf16 -> fp32; a plain
-// library GEMM), with the elementwise work fused into small kernels between
-// them:
+// the clients of a launch train in lockstep: global SGD step t runs step t
+// of every client that has one, and every layer product of that step is ONE
+// launch of a hand-written tcgen05 kernel over all those clients (grid.z =
+// client). Operands are staged by TMA (3-D tensor maps [slot][row][col]
+// over the clients' workspace slots, 128-byte swizzle, zero fill past the
+// edges) into a 4-deep shared-memory ring; one thread issues
+// tcgen05.mma (bf16 x bf16 -> fp32 in TMEM); the elementwise work is the
+// epilogue of the same kernel (TMEM -> registers -> global):
 //
-//   forward   Z_{l+1} = H_l W_l            (GEMM)  ->  H_{l+1} = relu(Z + b) * keep * scale  (fwd_epilogue)
-//   head      z = H_L w_h + b_h, dz = (sigmoid(z) - y) / rows, D_L = gate(dz w_h^T); head + b_{L-1} SGD (head_kernel)
-//   backward  dH_l = D_{l+1} W_l^T          (GEMM)  ->  D_l = dH_l * gate(H_l); b_{l-1} SGD (gate_kernel)
-//   update    W_l master += (-lr) H_l^T D_{l+1}   (GEMM with beta = 1: the SGD step IS the GEMM epilogue)
-//   refresh   bf16 copies of the updated masters for the next step (convert_kernel)
+//   fwd   Z^T[u][r] = sum_k W_l[k][u] H_l[r][k]    A = W_l (MN-major), B = H_l (K-major)
+//         -> H_{l+1}[r][u] = relu(Z + b) * keep * scale (bf16); the last
+//            hidden layer also leaves per-(row, 32-unit) head-logit partials
+//   head  logits, dz, D_H, SGD of the head and of b_{H-1} (CUDA cores)
+//   bwd   dH^T[i][r] = sum_j W_l[i][j] D_{l+1}[r][j]  A = W_l (K-major), B = D_{l+1} (K-major)
+//         -> D_l = bf16(dH * scale * [H_l > 0]), SGD of b_{l-1}
+//   upd   G[i][u] = sum_r H_l[r][i] D_{l+1}[r][u]      A = H_l (MN-major), B = D_{l+1} (MN-major)
+//         -> master W_l[i][u] -= lr * G (fp32, in the caller's output row) and
+//            its bf16 copy refreshed in the same pass (no separate convert)
 //
-// The fp32 masters live in the caller's output rows (w_out + r*ldw) from the
-// first step on; workspace slots hold each client's bf16 weight copies and
-// activations. Clients are processed in groups of at most WIDE_GROUP slots.
-#include <cublas_v2.h>
+// Units sit on the MMA's M side (128 per tile) and the step's rows on N, so
+// one tcgen05.ld row of TMEM is one unit's values across rows and the
+// activation stores of a warp are 32 consecutive units (64 B). Per
+// client-step the weights are streamed three times (fwd read, bwd read,
+// update read-modify-write + bf16 write: 14 B per parameter), so the trainer
+// is HBM-bound at the WIDE shape.
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
 #include <vector>
 
 #include "fs_common.cuh"
+#include "fs_tma.cuh"
 
 namespace fs {
 namespace wide {
 
 constexpr int WIDE_GROUP = 256;   // clients per lockstep group (workspace slots)
 constexpr int MAXL = FS_MAX_LAYERS;
+constexpr int TM = 128;           // units per tile (MMA M)
+constexpr int KC = 64;            // K chunk = one 128-byte swizzle row of bf16
+constexpr int UN = 256;           // update tile width along fan-out (MMA N)
+constexpr int STAGES = 4;         // fwd/bwd TMA ring depth
+constexpr int THREADS = 128;
+constexpr uint32_t A_BYTES = TM * KC * 2;  // 16 KB
+
+__host__ __device__ inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+// head-logit partials per row: one per 32-unit warp slice of each 128-unit tile
+__host__ __device__ __forceinline__ int zparts(int n_last) { return (n_last + TM - 1) / TM * 4; }
 
 struct Geo {
   MlpLayout lay;
-  int dp;                // input width padded to 16 (bf16 feature rows)
-  int rb;                // activation rows per slot (max batch rounded up to 16)
-  int64_t wb_off[MAXL];  // bf16 weight copy offsets (elements) inside a slot
-  int64_t wb_elems;
-  int64_t hid_base[MAXL];  // mask draw base of hidden layer l (1-based) within a step's block
+  int H;                  // hidden layers
+  int dp;                 // X row width (bf16 features padded to 16)
+  int rb;                 // activation rows per slot (multiple of nb)
+  int nb;                 // rows per fwd/bwd tile = MMA N (multiple of 16, <= 256)
+  int rtiles;             // rb / nb
+  int ld[MAXL + 1];       // row stride (elements) of the layer-l activations (0: X = dp)
+  int ldw[MAXL];          // row stride of the bf16 copy of W_l: roundup8(f_{l+1})
+  size_t wb_off[MAXL], x_off, h_off[MAXL + 1], d_off[MAXL + 1], y_off, z_off, bp_off[MAXL + 1];
   size_t slot_bytes;
-  size_t x_off, h_off[MAXL], d_off[MAXL], t_off, y_off, z_off;  // byte offsets inside a slot
 };
-
-// head-logit partials per row: one per warp of the last forward epilogue's
-// grid (256-thread blocks over the last hidden width), summed in a fixed order
-// by the consumer so the logits do not depend on atomic arrival order
-__host__ __device__ __forceinline__ int zparts(int n_last) { return (n_last + 255) / 256 * 8; }
 
 static bool make(const fs_train_desc* d, Geo* g) {
   if (make_layout(d->dims, d->n_dims, &g->lay) != FS_OK) return false;
   const MlpLayout& L = g->lay;
   if (L.L < 2 || L.L > MAXL) return false;
-  g->dp = (L.f[0] + 15) / 16 * 16;
-  g->rb = std::max(16, (d->max_batch + 15) / 16 * 16);
-  int64_t o = 0;
-  for (int l = 0; l < L.L - 1; ++l) {  // hidden weight matrices; the head stays fp32
-    g->wb_off[l] = o;
-    o += (int64_t)(l == 0 ? g->dp : L.f[l]) * L.f[l + 1];
-  }
-  g->wb_elems = o;
-  int64_t hb = 0;
-  for (int l = 1; l < L.L; ++l) {
-    g->hid_base[l] = hb;
-    hb += L.f[l];
-  }
-  size_t s = (size_t)g->wb_elems * 2;
+  g->H = L.L - 1;
+  g->dp = rup(L.f[0], 16);
+  const int mb = std::max(16, rup(d->max_batch, 16));
+  g->nb = mb <= 256 ? mb : 128;
+  g->rb = rup(mb, g->nb);
+  g->rtiles = g->rb / g->nb;
+  g->ld[0] = g->dp;
+  for (int l = 1; l <= g->H; ++l) g->ld[l] = rup(L.f[l], 8);
+  size_t s = 0;
   auto take = [&](size_t bytes) {
     s = (s + 255) / 256 * 256;
     const size_t at = s;
     s += bytes;
     return at;
   };
-  g->x_off = take((size_t)g->rb * g->dp * 2);
-  for (int l = 1; l < L.L; ++l) {
-    g->h_off[l] = take((size_t)g->rb * L.f[l] * 2);
-    g->d_off[l] = take((size_t)g->rb * L.f[l] * 2);
+  for (int l = 0; l < g->H; ++l) {
+    g->ldw[l] = rup(L.f[l + 1], 8);
+    g->wb_off[l] = take((size_t)L.f[l] * g->ldw[l] * 2);
   }
-  g->t_off = take((size_t)g->rb * L.max_hidden * 4);
+  g->x_off = take((size_t)g->rb * g->dp * 2);
+  for (int l = 1; l <= g->H; ++l) {
+    g->h_off[l] = take((size_t)g->rb * g->ld[l] * 2);
+    g->d_off[l] = take((size_t)g->rb * g->ld[l] * 2);
+    g->bp_off[l] = g->rtiles > 1 ? take((size_t)g->rtiles * L.f[l] * 4) : 0;
+  }
+  g->h_off[0] = g->x_off;
   g->y_off = take((size_t)g->rb * 4 * 2);  // labels, dz
-  g->z_off = take((size_t)g->rb * zparts(L.f[L.L - 1]) * 4);  // head-logit partials (last forward epilogue)
+  g->z_off = take((size_t)g->rb * zparts(L.f[g->H]) * 4);
   g->slot_bytes = (s + 255) / 256 * 256;
   return true;
 }
@@ -97,7 +113,7 @@ struct StepRow {
   float lr;
 };
 
-// ------------------------------------------------------------------ kernels
+// ------------------------------------------------------------------ setup kernels
 __global__ void init_master_kernel(const uint64_t* w_start, const int* reqs, int n, int64_t M, float* w_out,
                                    int64_t ldw) {
   const int a = blockIdx.y;
@@ -119,55 +135,39 @@ __global__ void init_master_kernel(const uint64_t* w_start, const int* reqs, int
 
 struct ConvArgs {
   MlpLayout lay;
-  int dp;
-  int64_t wb_off[MAXL];
+  int H;
+  int ldw[MAXL];
+  size_t wb_off[MAXL];
   size_t slot_bytes;
   uint8_t* slots;
-  float* w_out;
-  int64_t ldw;
+  const float* w_out;
+  int64_t ldw_out;
 };
 
-// bf16 copies of every hidden weight matrix of the listed clients (W_0 rows
-// padded to dp with zeros, matching the zero-padded feature columns): one
-// 16-byte read and one 8-byte write per 4 parameters (fout % 4 == 0).
+// bf16 copies of every hidden weight matrix of the listed clients (row stride ldw)
 __global__ void convert_kernel(ConvArgs c, const StepRow* rows, int n) {
   const int a = blockIdx.y;
   if (a >= n) return;
   const StepRow sr = rows[a];
-  const float* m = c.w_out + (int64_t)sr.req * c.ldw;
-  __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(c.slots + (size_t)sr.slot * c.slot_bytes);
+  const float* m = c.w_out + (int64_t)sr.req * c.ldw_out;
+  uint8_t* sb = c.slots + (size_t)sr.slot * c.slot_bytes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int l = 0; l < c.lay.L - 1; ++l) {
+  for (int l = 0; l < c.H; ++l) {
     const int fin = c.lay.f[l], fout = c.lay.f[l + 1];
     const float* src = m + c.lay.woff[l];
-    __nv_bfloat16* dst = wb + c.wb_off[l];
-    const int64_t real = (int64_t)fin * fout;
-    const int64_t total = (int64_t)(l == 0 ? c.dp : fin) * fout;
-    const bool vec = (fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(dst) & 7) == 0);
-    if (vec) {
-      for (int64_t j4 = t0; j4 < total / 4; j4 += stride) {
-        const int64_t j = j4 * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (j < real) v = __ldcs(reinterpret_cast<const float4*>(src + j));
-        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-        uint2 packed;
-        packed.x = *reinterpret_cast<uint32_t*>(&lo);
-        packed.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(dst + j) = packed;
-      }
-    } else {
-      for (int64_t j = t0; j < total; j += stride) dst[j] = __float2bfloat16_rn(j < real ? src[j] : 0.f);
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(sb + c.wb_off[l]);
+    const int64_t total = (int64_t)fin * fout;
+    for (int64_t j = t0; j < total; j += stride) {
+      const int64_t i = j / fout, u = j - i * fout;
+      dst[i * c.ldw[l] + u] = __float2bfloat16_rn(src[j]);
     }
   }
 }
 
 struct StepArgs {
   MlpLayout lay;
-  int dp, rb;
-  int64_t hid_base[MAXL];
-  size_t slot_bytes, x_off, h_off[MAXL], d_off[MAXL], t_off, y_off, z_off;
+  Geo g;
   uint8_t* slots;
   float* w_out;
   int64_t ldw;
@@ -185,88 +185,219 @@ struct StepArgs {
   int32_t* status;
 };
 
-__device__ __forceinline__ uint8_t* slot_of(const StepArgs& a, int slot) { return a.slots + (size_t)slot * a.slot_bytes; }
+__device__ __forceinline__ uint8_t* slot_of(const StepArgs& a, int slot) {
+  return a.slots + (size_t)slot * a.g.slot_bytes;
+}
 
 // X rows of the step (permuted shard rows, bf16, zero padded) and labels
 __global__ void gather_kernel(StepArgs a, const StepRow* rows) {
   const StepRow sr = rows[blockIdx.x];
   uint8_t* sb = slot_of(a, sr.slot);
-  __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(sb + a.x_off);
-  float* y = reinterpret_cast<float*>(sb + a.y_off);
+  __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(sb + a.g.x_off);
+  float* y = reinterpret_cast<float*>(sb + a.g.y_off);
   const int n = a.n_rows[sr.req], B = a.batch[sr.req];
   const int32_t* perm = a.perm + a.perm_off[sr.req] + (int64_t)sr.e * n + (int64_t)sr.s * B;
   const int64_t base = a.row_off[sr.req];
-  const int cpr = a.dp / 8;  // 16-byte chunks per row
-  for (int i = threadIdx.x; i < a.rb * cpr; i += blockDim.x) {
+  const int cpr = a.g.dp / 8;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < a.g.rb * cpr; i += blockDim.x) {
     const int r = i / cpr, c = i % cpr;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < sr.rows) v = *reinterpret_cast<const uint4*>(a.feat + (base + perm[r]) * a.dp + c * 8);
-    *reinterpret_cast<uint4*>(x + (int64_t)r * a.dp + c * 8) = v;
+    if (r < sr.rows) v = *reinterpret_cast<const uint4*>(a.feat + (base + perm[r]) * a.g.dp + c * 8);
+    *reinterpret_cast<uint4*>(x + (int64_t)r * a.g.dp + c * 8) = v;
   }
-  for (int r = threadIdx.x; r < a.rb; r += blockDim.x) y[r] = r < sr.rows ? a.labels[base + perm[r]] : 0.f;
+  for (int r = threadIdx.x; r < a.g.rb; r += blockDim.x) y[r] = r < sr.rows ? a.labels[base + perm[r]] : 0.f;
 }
 
-__device__ __forceinline__ bool keep_bit(const StepArgs& a, const StepRow& sr, int l, int r, int u) {
-  if (a.mask_mode != FS_MASK_BITS) return true;
+__device__ __forceinline__ bool keep_bit(const StepArgs& a, const StepRow& sr, int l, int r, int u,
+                                         int64_t hid_base) {
   const int B = a.batch[sr.req];
   const int64_t slot_words = ((int64_t)B * a.lay.sum_hidden + 31) / 32;
   const uint32_t* bits = a.mask_bits + a.mask_off[sr.req] + (int64_t)sr.global_step * slot_words;
-  const int64_t j = (int64_t)sr.rows * a.hid_base[l] + (int64_t)r * a.lay.f[l] + u;
+  const int64_t j = (int64_t)sr.rows * hid_base + (int64_t)r * a.lay.f[l] + u;
   return (bits[j >> 5] >> (j & 31)) & 1u;
 }
 
-// H_l = relu(Z + b_{l-1}) * keep * scale  (bf16), Z in the fp32 temp. The
-// last hidden layer also forms the head logits from the fp32 values (as the
-// on-chip trainers do): per-warp partials of sum_u H[r][u] w_h[u].
-__global__ void fwd_epilogue_kernel(StepArgs a, const StepRow* rows, int l) {
-  const StepRow sr = rows[blockIdx.y];
-  const int N = a.lay.f[l];
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool last = l == a.lay.L - 1;
-  uint8_t* sb = slot_of(a, sr.slot);
-  const float* z = reinterpret_cast<const float*>(sb + a.t_off);
-  __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(sb + a.h_off[l]);
-  float* zacc = reinterpret_cast<float*>(sb + a.z_off);
-  const float* W = a.w_out + (int64_t)sr.req * a.ldw;
-  const float b = u < N ? W[a.lay.boff[l - 1] + u] : 0.f;
-  const float wh = last && u < N ? W[a.lay.woff[l] + u] : 0.f;
-  const float sc = a.mask_mode == FS_MASK_BITS ? a.scale : 1.f;
-  for (int r = 0; r < a.rb; ++r) {
-    float v = 0.f;
-    if (r < sr.rows && u < N) {
-      v = fmaxf(z[(int64_t)r * N + u] + b, 0.f);
-      v = keep_bit(a, sr, l, r, u) ? v * sc : 0.f;
-    }
-    if (u < N) h[(int64_t)r * N + u] = __float2bfloat16_rn(v);
-    if (last && r < sr.rows) {
-      float p = v * wh;
-      for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      if ((threadIdx.x & 31) == 0) zacc[(int64_t)r * zparts(N) + blockIdx.x * 8 + (threadIdx.x >> 5)] = p;
-    }
-  }
+// ------------------------------------------------------------------ tcgen05 tile machinery
+struct Ring {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t done;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
 }
 
-// head: logits, dz, D_{L-1}, SGD on the head and on b_{L-2}; one CTA per client
+__device__ __forceinline__ void ring_init(Ring& R, uint32_t tmem_cols) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&R.full[s], 1);
+      tc::mbar_init(&R.empty[s], 1);
+    }
+    tc::mbar_init(&R.done, 1);
+    tc::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc(&R.tmem, tmem_cols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+__device__ __forceinline__ void ring_free(Ring& R, uint32_t tmem_cols) {
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc(R.tmem, tmem_cols);
+}
+
+// fwd/bwd main loop: D[128 x nb] (TMEM) = sum over kchunks of A . B.
+//   A_MN: A box = 64 units x 64 k (two per chunk, units m0 and m0+64), else
+//         one box of 64 k x 128 units; B box = 64 k x nb rows at row r0.
+template <bool A_MN>
+__device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorMap* ta, const CUtensorMap* tb,
+                                         int m0, int r0, int slot, int kchunks, int nb) {
+  const uint32_t stage_bytes = A_BYTES + (uint32_t)nb * 128u;
+  if (threadIdx.x == 0) {
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % STAGES;
+      const uint32_t ph = (uint32_t)(kc / STAGES) & 1u;
+      if (kc >= STAGES) tc::mbar_wait(&R.empty[s], ph ^ 1u);
+      uint8_t* a = smem + s * stage_bytes;
+      uint8_t* b = a + A_BYTES;
+      tma::expect_tx(&R.full[s], stage_bytes);
+      if (A_MN) {
+        tma::load_3d(a, ta, m0, kc * KC, slot, &R.full[s]);
+        tma::load_3d(a + 8192, ta, m0 + 64, kc * KC, slot, &R.full[s]);
+      } else {
+        tma::load_3d(a, ta, kc * KC, m0, slot, &R.full[s]);
+      }
+      tma::load_3d(b, tb, kc * KC, r0, slot, &R.full[s]);
+    }
+  } else if (threadIdx.x == 32) {
+    const uint32_t idesc = tc::idesc_bf16(TM, nb, A_MN, false);
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % STAGES;
+      const uint32_t ph = (uint32_t)(kc / STAGES) & 1u;
+      tc::mbar_wait(&R.full[s], ph);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(smem + s * stage_bytes), b = a + A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk) {
+        const uint64_t ad = A_MN ? tma::mnmajor(a, kk, 8192u) : tma::kmajor(a, kk);
+        tc::mma_bf16(R.tmem, ad, tma::kmajor(b, kk), idesc, (kc | kk) != 0);
+      }
+      tc::mma_commit(&R.empty[s]);
+    }
+    tc::mma_commit(&R.done);
+  }
+  tc::mbar_wait(&R.done, 0);
+  tc::fence_after_sync();
+  __syncwarp();  // producer / issuer lanes rejoin their warps before tcgen05.ld
+}
+
+__device__ __forceinline__ uint32_t lane_addr(uint32_t tmem, int col) {
+  return tmem + ((uint32_t)((threadIdx.x >> 5) * 32) << 16) + (uint32_t)col;
+}
+
+// ------------------------------------------------------------------ forward
+struct FwdArgs {
+  int l;              // output layer (1..H): H_l = relu(H_{l-1} W_{l-1} + b_{l-1})
+  int fin, fout, nb, kchunks, last, zp;
+  int64_t boff, whoff, hid_base;
+  // training: per-client slots
+  size_t h_off, z_off;
+  int ld_out;
+  // evaluation (eval = 1): one model, global buffers
+  int eval, rows_eval;
+  __nv_bfloat16* h_eval;
+  float* z_eval;
+  const float* w_eval;
+};
+
+__global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CUtensorMap ta,
+                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, FwdArgs f,
+                                                      const StepRow* rows) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Ring R;
+  uint8_t* smem = smem_base(smem_raw);
+  const int tile = blockIdx.x, m0 = tile * TM, r0 = blockIdx.y * f.nb;
+  StepRow sr{};
+  int slot = 0, nrows;
+  const float* W;
+  if (f.eval) {
+    nrows = f.rows_eval;
+    W = f.w_eval;
+  } else {
+    sr = rows[blockIdx.z];
+    slot = sr.slot;
+    nrows = sr.rows;
+    W = a.w_out + (int64_t)sr.req * a.ldw;
+  }
+  if (threadIdx.x == 0) {
+    tma::prefetch_map(&ta);
+    tma::prefetch_map(&tb);
+  }
+  const uint32_t cols = f.nb <= 32 ? 32 : f.nb <= 64 ? 64 : f.nb <= 128 ? 128 : 256;
+  ring_init(R, cols);
+  mainloop<true>(R, smem, &ta, &tb, m0, r0, slot, f.kchunks, f.nb);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = m0 + threadIdx.x;
+  const bool uok = u < f.fout;
+  const float b = uok ? W[f.boff + u] : 0.f;
+  const float wh = f.last && uok ? W[f.whoff + u] : 0.f;
+  const bool masked = !f.eval && a.mask_mode == FS_MASK_BITS;
+  const float sc = masked ? a.scale : 1.f;
+  __nv_bfloat16* h = f.eval ? f.h_eval : reinterpret_cast<__nv_bfloat16*>(slot_of(a, slot) + f.h_off);
+  float* z = f.eval ? f.z_eval : reinterpret_cast<float*>(slot_of(a, slot) + f.z_off);
+  const int rend = f.eval ? min(r0 + f.nb, nrows) : r0 + f.nb;  // training slots hold rb rows
+  for (int c0 = 0; c0 < f.nb; c0 += 32) {
+    if (r0 + c0 >= rend) break;
+    float v[32];
+    tc::tmem_ld32(lane_addr(R.tmem, c0), v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int r = r0 + c0 + j;
+      if (r >= rend) continue;  // (eval: past the last row; uniform across the warp)
+      float x = 0.f;
+      if (r < nrows && uok) {
+        x = fmaxf(v[j] + b, 0.f);
+        if (masked) x = keep_bit(a, sr, f.l, r, u, f.hid_base) ? x * sc : 0.f;
+      }
+      if (uok) h[(int64_t)r * f.ld_out + u] = __float2bfloat16_rn(x);
+      if (f.last) {
+        float p = x * wh;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if (lane == 0 && r < nrows) z[(int64_t)r * f.zp + tile * 4 + warp] = p;
+      }
+    }
+  }
+  ring_free(R, cols);
+}
+
+// ------------------------------------------------------------------ head (CUDA cores)
+// logits from the fixed-order partials, dz, D_H, SGD on the head and b_{H-1}
 __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* rows) {
   const StepRow sr = rows[blockIdx.x];
-  const int L = a.lay.L, N = a.lay.f[L - 1];
+  const int H = a.g.H, N = a.lay.f[H], ld = a.g.ld[H], rb = a.g.rb;
   uint8_t* sb = slot_of(a, sr.slot);
-  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + a.h_off[L - 1]);
-  __nv_bfloat16* dout = reinterpret_cast<__nv_bfloat16*>(sb + a.d_off[L - 1]);
-  const float* y = reinterpret_cast<const float*>(sb + a.y_off);
-  float* dz = reinterpret_cast<float*>(sb + a.y_off) + a.rb;
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + a.g.h_off[H]);
+  __nv_bfloat16* dout = reinterpret_cast<__nv_bfloat16*>(sb + a.g.d_off[H]);
+  const float* y = reinterpret_cast<const float*>(sb + a.g.y_off);
+  float* dz = reinterpret_cast<float*>(sb + a.g.y_off) + rb;
   float* W = a.w_out + (int64_t)sr.req * a.ldw;
-  float* wh = W + a.lay.woff[L - 1];
-  float* bh = W + a.lay.boff[L - 1];
-  float* bprev = W + a.lay.boff[L - 2];
+  float* wh = W + a.lay.woff[H];
+  float* bh = W + a.lay.boff[H];
+  float* bprev = W + a.lay.boff[H - 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ float s_dz[1024];
+  extern __shared__ float s_dz[];
   __shared__ float s_red[8];
-  const float* zacc = reinterpret_cast<const float*>(sb + a.z_off);
-  for (int r = threadIdx.x; r < a.rb; r += blockDim.x) {
+  const float* zacc = reinterpret_cast<const float*>(sb + a.g.z_off);
+  const int zp = zparts(N);
+  for (int r = threadIdx.x; r < rb; r += blockDim.x) {
     float d = 0.f;
     if (r < sr.rows) {
-      const int zp = zparts(N);
       float zs = 0.f;
       for (int k = 0; k < zp; ++k) zs += zacc[(int64_t)r * zp + k];
       const float z = zs + bh[0];
@@ -282,18 +413,18 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   for (int u = threadIdx.x; u < N; u += blockDim.x) {
     const float w = wh[u];
     float g = 0.f, gb = 0.f;
-    for (int r = 0; r < a.rb; ++r) {
-      const float hv = __bfloat162float(h[(int64_t)r * N + u]);
+    for (int r = 0; r < rb; ++r) {
+      const float hv = __bfloat162float(h[(int64_t)r * ld + u]);
       g = fmaf(hv, s_dz[r], g);
       const __nv_bfloat16 dv = __float2bfloat16_rn(hv > 0.f ? s_dz[r] * w * sc : 0.f);
-      dout[(int64_t)r * N + u] = dv;
+      dout[(int64_t)r * ld + u] = dv;
       gb += __bfloat162float(dv);
     }
     wh[u] = w - sr.lr * g;
     bprev[u] -= sr.lr * gb;
   }
   float t = 0.f;
-  for (int r = threadIdx.x; r < a.rb; r += blockDim.x) t += s_dz[r];
+  for (int r = threadIdx.x; r < rb; r += blockDim.x) t += s_dz[r];
   for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) s_red[warp] = t;
   __syncthreads();
@@ -304,47 +435,172 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   }
 }
 
-// D_l = dH_l * scale * [H_l > 0] (bf16) and SGD on b_{l-1}
-__global__ void gate_kernel(StepArgs a, const StepRow* rows, int l) {
-  const StepRow sr = rows[blockIdx.y];
-  const int N = a.lay.f[l];
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= N) return;
+// ------------------------------------------------------------------ backward
+struct BwdArgs {
+  int l;              // D_l from D_{l+1} through W_l (1 <= l < H)
+  int fin, fout, nb, kchunks;
+  int64_t boff;       // b_{l-1}
+  size_t h_off, d_off, bp_off;
+  int ld;
+};
+
+__global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CUtensorMap ta,
+                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, BwdArgs p,
+                                                      const StepRow* rows) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Ring R;
+  uint8_t* smem = smem_base(smem_raw);
+  const StepRow sr = rows[blockIdx.z];
+  const int m0 = blockIdx.x * TM, r0 = blockIdx.y * p.nb;
+  if (threadIdx.x == 0) {
+    tma::prefetch_map(&ta);
+    tma::prefetch_map(&tb);
+  }
+  const uint32_t cols = p.nb <= 32 ? 32 : p.nb <= 64 ? 64 : p.nb <= 128 ? 128 : 256;
+  ring_init(R, cols);
+  mainloop<false>(R, smem, &ta, &tb, m0, r0, sr.slot, p.kchunks, p.nb);
+
+  const int i = m0 + threadIdx.x;
+  const bool iok = i < p.fin;
   uint8_t* sb = slot_of(a, sr.slot);
-  const float* dh = reinterpret_cast<const float*>(sb + a.t_off);
-  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + a.h_off[l]);
-  __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(sb + a.d_off[l]);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + p.h_off);
+  __nv_bfloat16* dl = reinterpret_cast<__nv_bfloat16*>(sb + p.d_off);
   const float sc = a.mask_mode == FS_MASK_BITS ? a.scale : 1.f;
   float gb = 0.f;
-  for (int r = 0; r < a.rb; ++r) {
-    const float hv = __bfloat162float(h[(int64_t)r * N + u]);
-    const __nv_bfloat16 dv = __float2bfloat16_rn(hv > 0.f ? dh[(int64_t)r * N + u] * sc : 0.f);
-    d[(int64_t)r * N + u] = dv;
-    gb += __bfloat162float(dv);
+  for (int c0 = 0; c0 < p.nb; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(lane_addr(R.tmem, c0), v);
+    if (iok) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int64_t o = (int64_t)(r0 + c0 + j) * p.ld + i;
+        const float hv = __bfloat162float(h[o]);
+        const __nv_bfloat16 dv = __float2bfloat16_rn(hv > 0.f ? v[j] * sc : 0.f);
+        dl[o] = dv;
+        gb += __bfloat162float(dv);
+      }
+    }
   }
-  a.w_out[(int64_t)sr.req * a.ldw + a.lay.boff[l - 1] + u] -= sr.lr * gb;
+  if (iok) {
+    if (a.g.rtiles == 1) a.w_out[(int64_t)sr.req * a.ldw + p.boff + i] -= sr.lr * gb;
+    else reinterpret_cast<float*>(sb + p.bp_off)[(int64_t)blockIdx.y * p.fin + i] = gb;
+  }
+  ring_free(R, cols);
 }
 
-// ------------------------------------------------------------------ host
-static cublasHandle_t blas() {
-  static std::mutex mu;
-  static std::map<int, cublasHandle_t> per_device;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = per_device.find(dev);
-  if (it != per_device.end()) return it->second;
-  cublasHandle_t h = nullptr;
-  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-  per_device[dev] = h;
-  return h;
+// b_{l-1} SGD from the per-row-tile partial sums (row tiles > 1), in tile order
+__global__ void bias_reduce_kernel(StepArgs a, const StepRow* rows, int fin, int64_t boff, size_t bp_off) {
+  const StepRow sr = rows[blockIdx.y];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= fin) return;
+  const float* bp = reinterpret_cast<const float*>(slot_of(a, sr.slot) + bp_off);
+  float gb = 0.f;
+  for (int t = 0; t < a.g.rtiles; ++t) gb += bp[(int64_t)t * fin + i];
+  a.w_out[(int64_t)sr.req * a.ldw + boff + i] -= sr.lr * gb;
 }
 
-static int blas_ok(cublasStatus_t s, const char* what) {
-  if (s == CUBLAS_STATUS_SUCCESS) return FS_OK;
-  set_error("fs_train_bf16 (wide): %s failed (cuBLAS status %d)", what, (int)s);
-  return FS_ECUDA;
+// ------------------------------------------------------------------ update
+struct UpdArgs {
+  int l;              // W_l [fin x fout] from H_l and D_{l+1}
+  int fin, fout;
+  int64_t woff;
+  size_t wb_off;
+  int ldw;
+};
+
+__global__ void __launch_bounds__(THREADS) upd_kernel(const __grid_constant__ CUtensorMap ta,
+                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, UpdArgs p,
+                                                      const StepRow* rows) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Ring R;
+  uint8_t* smem = smem_base(smem_raw);
+  const StepRow sr = rows[blockIdx.z];
+  const int i0 = blockIdx.x * TM, u0 = blockIdx.y * UN;
+  const int nu = min(UN, p.fout - u0);
+  const int nmma = rup(nu, 16), nbox = (nu + 63) / 64;
+  const int kchunks = max(1, (sr.rows + KC - 1) / KC);
+  const uint32_t stage_bytes = A_BYTES + (uint32_t)nbox * 8192u;
+  if (threadIdx.x == 0) {
+    tma::prefetch_map(&ta);
+    tma::prefetch_map(&tb);
+  }
+  ring_init(R, 256);
+  if (threadIdx.x == 0) {
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % 2;
+      const uint32_t ph = (uint32_t)(kc / 2) & 1u;
+      if (kc >= 2) tc::mbar_wait(&R.empty[s], ph ^ 1u);
+      uint8_t* A = smem + s * (A_BYTES + 4 * 8192);
+      uint8_t* B = A + A_BYTES;
+      tma::expect_tx(&R.full[s], stage_bytes);
+      tma::load_3d(A, &ta, i0, kc * KC, sr.slot, &R.full[s]);
+      tma::load_3d(A + 8192, &ta, i0 + 64, kc * KC, sr.slot, &R.full[s]);
+      for (int j = 0; j < nbox; ++j) tma::load_3d(B + j * 8192, &tb, u0 + 64 * j, kc * KC, sr.slot, &R.full[s]);
+    }
+  } else if (threadIdx.x == 32) {
+    const uint32_t idesc = tc::idesc_bf16(TM, nmma, true, true);
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % 2;
+      const uint32_t ph = (uint32_t)(kc / 2) & 1u;
+      tc::mbar_wait(&R.full[s], ph);
+      tc::fence_after_sync();
+      const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + 4 * 8192)), B = A + A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk)
+        tc::mma_bf16(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
+      tc::mma_commit(&R.empty[s]);
+    }
+    tc::mma_commit(&R.done);
+  }
+  tc::mbar_wait(&R.done, 0);
+  tc::fence_after_sync();
+  __syncwarp();
+
+  // W_l[i][u] -= lr * G[i][u] on the fp32 master and its bf16 copy
+  const int i = i0 + threadIdx.x;
+  const bool iok = i < p.fin;
+  float* wrow = a.w_out + (int64_t)sr.req * a.ldw + p.woff + (int64_t)i * p.fout + u0;
+  __nv_bfloat16* brow =
+      reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.wb_off) + (int64_t)i * p.ldw + u0;
+  const float nlr = -sr.lr;
+  const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(wrow) & 15) == 0);
+  for (int c0 = 0; c0 < nmma; c0 += 32) {
+    float g[32];
+    tc::tmem_ld32(lane_addr(R.tmem, c0), g);
+    if (!iok) continue;
+    if (vec && c0 + 32 <= nu) {
+      float4 w4[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w4[q] = reinterpret_cast<const float4*>(wrow + c0)[q];
+      uint32_t pk[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        w4[q].x = fmaf(nlr, g[4 * q + 0], w4[q].x);
+        w4[q].y = fmaf(nlr, g[4 * q + 1], w4[q].y);
+        w4[q].z = fmaf(nlr, g[4 * q + 2], w4[q].z);
+        w4[q].w = fmaf(nlr, g[4 * q + 3], w4[q].w);
+        reinterpret_cast<float4*>(wrow + c0)[q] = w4[q];
+        pk[2 * q] = tc::pack_bf16x2(w4[q].x, w4[q].y);
+        pk[2 * q + 1] = tc::pack_bf16x2(w4[q].z, w4[q].w);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(brow + c0)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (c0 + j >= nu) continue;
+        const float w = fmaf(nlr, g[j], wrow[c0 + j]);
+        wrow[c0 + j] = w;
+        brow[c0 + j] = __float2bfloat16_rn(w);
+      }
+    }
+  }
+  ring_free(R, 256);
 }
+
+inline int fwd_smem(int nb) { return 1024 + STAGES * (int)(A_BYTES + nb * 128); }
+inline int upd_smem() { return 1024 + 2 * (int)(A_BYTES + 4 * 8192); }
 
 }  // namespace wide
 
@@ -352,8 +608,7 @@ size_t wide_workspace_bytes(const fs_train_desc* d) {
   wide::Geo g;
   if (!d || d->n_req < 1 || !wide::make(d, &g)) return 0;
   const size_t G = (size_t)std::min(d->n_req, wide::WIDE_GROUP);
-  // slots + per-step staging (rows + pointer arrays)
-  return G * g.slot_bytes + 256 + G * (sizeof(wide::StepRow) + 3 * 8 * (size_t)(3 * FS_MAX_LAYERS)) + 65536;
+  return G * g.slot_bytes + 256 + G * sizeof(wide::StepRow) + 4 * G + 1024;
 }
 
 int wide_train(const fs_train_desc* d, const void* features_bf16, const float* labels, cudaStream_t st) {
@@ -371,12 +626,6 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
     set_error("fs_train_bf16 (wide): workspace %zu < required %zu", d->workspace_bytes, need);
     return FS_EINVAL;
   }
-  cublasHandle_t h = blas();
-  if (!h) {
-    set_error("fs_train_bf16 (wide): cublasCreate failed");
-    return FS_ECUDA;
-  }
-  if (int rc = blas_ok(cublasSetStream(h, st), "cublasSetStream")) return rc;
   // per-request geometry on the host (the descriptor's arrays live in HBM)
   std::vector<int32_t> nr(n), bt(n), s0(n), s1(n);
   std::vector<double> lr((size_t)n * std::max(d->epochs, 1));
@@ -395,23 +644,13 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
   const size_t G = (size_t)std::min(n, WIDE_GROUP);
   uint8_t* ws = reinterpret_cast<uint8_t*>(d->workspace);
   uint8_t* slots = ws;
-  uint8_t* stage = ws + G * g.slot_bytes;  // device staging: StepRow[] then pointer arrays
+  uint8_t* stage = ws + G * g.slot_bytes;  // device staging: StepRow[] (+ request ids at setup)
   float* w_out = reinterpret_cast<float*>(d->w_out);
+  const int H = g.H;
 
   StepArgs sa;
   sa.lay = L;
-  sa.dp = g.dp;
-  sa.rb = g.rb;
-  for (int l = 0; l < MAXL; ++l) {
-    sa.hid_base[l] = g.hid_base[l];
-    sa.h_off[l] = g.h_off[l];
-    sa.d_off[l] = g.d_off[l];
-  }
-  sa.slot_bytes = g.slot_bytes;
-  sa.x_off = g.x_off;
-  sa.t_off = g.t_off;
-  sa.y_off = g.y_off;
-  sa.z_off = g.z_off;
+  sa.g = g;
   sa.slots = slots;
   sa.w_out = w_out;
   sa.ldw = d->ldw;
@@ -429,17 +668,45 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
   sa.status = d->status;
   ConvArgs ca;
   ca.lay = L;
-  ca.dp = g.dp;
-  for (int l = 0; l < MAXL; ++l) ca.wb_off[l] = g.wb_off[l];
+  ca.H = H;
+  for (int l = 0; l < MAXL; ++l) {
+    ca.ldw[l] = g.ldw[l];
+    ca.wb_off[l] = g.wb_off[l];
+  }
   ca.slot_bytes = g.slot_bytes;
   ca.slots = slots;
   ca.w_out = w_out;
-  ca.ldw = d->ldw;
+  ca.ldw_out = d->ldw;
 
-  const float one = 1.f, zero = 0.f;
-  const int H = L.L - 1;  // hidden layers
+  ensure_smem(fwd_kernel, fwd_smem(g.nb));
+  ensure_smem(bwd_kernel, fwd_smem(g.nb));
+  ensure_smem(upd_kernel, upd_smem());
+  int64_t hid_base[MAXL + 1] = {0};
+  for (int l = 2; l <= H; ++l) hid_base[l] = hid_base[l - 1] + L.f[l - 1];
+
   for (int g0 = 0; g0 < n; g0 += (int)G) {
     const int gn = std::min((int)G, n - g0);
+    // tensor maps over this group's slots (slot addresses are fixed for the group)
+    CUtensorMap fA[MAXL], fB[MAXL], bA[MAXL], bB[MAXL], uA[MAXL], uB[MAXL];
+    bool ok = true;
+    for (int l = 0; l < H; ++l) {
+      const int fin = L.f[l], fout = L.f[l + 1];
+      const void* wb = slots + g.wb_off[l];
+      const void* hl = slots + g.h_off[l];
+      const void* dn = slots + g.d_off[l + 1];
+      ok = ok && tma::make_map(&fA[l], wb, fout, fin, gn, g.ldw[l], g.slot_bytes, 64);
+      ok = ok && tma::make_map(&fB[l], hl, fin, g.rb, gn, g.ld[l], g.slot_bytes, g.nb);
+      ok = ok && tma::make_map(&uA[l], hl, fin, g.rb, gn, g.ld[l], g.slot_bytes, 64);
+      ok = ok && tma::make_map(&uB[l], dn, fout, g.rb, gn, g.ld[l + 1], g.slot_bytes, 64);
+      if (l >= 1) {
+        ok = ok && tma::make_map(&bA[l], wb, fout, fin, gn, g.ldw[l], g.slot_bytes, 128);
+        ok = ok && tma::make_map(&bB[l], dn, fout, g.rb, gn, g.ld[l + 1], g.slot_bytes, g.nb);
+      }
+    }
+    if (!ok) {
+      set_error("fs_train_bf16 (wide): tensor map encoding failed");
+      return FS_ECUDA;
+    }
     // masters <- start rows, then bf16 copies of every slot
     {
       std::vector<StepRow> all(gn);
@@ -450,14 +717,14 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
       }
       std::vector<int> reqs(gn);
       for (int i = 0; i < gn; ++i) reqs[i] = g0 + i;
-      const size_t rb = (sizeof(StepRow) * gn + 255) / 256 * 256;
-      std::vector<uint8_t> host(rb + 4 * (size_t)gn);
+      const size_t rbytes = (sizeof(StepRow) * gn + 255) / 256 * 256;
+      std::vector<uint8_t> host(rbytes + 4 * (size_t)gn);
       memcpy(host.data(), all.data(), sizeof(StepRow) * gn);
-      memcpy(host.data() + rb, reqs.data(), 4 * (size_t)gn);
+      memcpy(host.data() + rbytes, reqs.data(), 4 * (size_t)gn);
       cudaMemcpyAsync(stage, host.data(), host.size(), cudaMemcpyHostToDevice, st);
       dim3 grid((unsigned)std::min<int64_t>((L.M + 255) / 256, 64), (unsigned)gn);
-      init_master_kernel<<<grid, 256, 0, st>>>(d->w_start, reinterpret_cast<const int*>(stage + rb), gn, L.M, w_out,
-                                               d->ldw);
+      init_master_kernel<<<grid, 256, 0, st>>>(d->w_start, reinterpret_cast<const int*>(stage + rbytes), gn, L.M,
+                                               w_out, d->ldw);
       if (int rc = check_launch("wide init")) return rc;
       convert_kernel<<<dim3(128, (unsigned)gn), 256, 0, st>>>(ca, reinterpret_cast<const StepRow*>(stage), gn);
       if (int rc = check_launch("wide convert")) return rc;
@@ -468,7 +735,6 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
     for (int i = 0; i < gn; ++i) t_begin = std::min(t_begin, s0[g0 + i]);
     for (int t = t_begin; t < t_end; ++t) {
       std::vector<StepRow> rows;
-      int max_rows = 1;
       for (int i = 0; i < gn; ++i) {
         const int r = g0 + i;
         if (t < s0[r] || t >= s1[r]) continue;
@@ -482,127 +748,69 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
         sr.global_step = t;
         sr.lr = (float)lr[(size_t)r * std::max(d->epochs, 1) + sr.e];
         rows.push_back(sr);
-        max_rows = std::max(max_rows, sr.rows);
       }
       const int A = (int)rows.size();
       if (A == 0) continue;
-      const int nrow = (max_rows + 7) / 8 * 8;  // GEMM row extent of this step
-      // pointer arrays: fwd (A, B, C) per layer, bwd per layer, update per layer
-      std::vector<const void*> ptrs;
-      auto sb = [&](int a) { return slots + (size_t)rows[a].slot * g.slot_bytes; };
-      auto wb = [&](int a, int l) { return (const void*)(reinterpret_cast<__nv_bfloat16*>(sb(a)) + g.wb_off[l]); };
-      auto act = [&](int a, int l) {  // H_l (l = 0: X)
-        return (const void*)(l == 0 ? sb(a) + g.x_off : sb(a) + g.h_off[l]);
-      };
-      auto dlt = [&](int a, int l) { return (const void*)(sb(a) + g.d_off[l]); };
-      auto tmp = [&](int a) { return (const void*)(sb(a) + g.t_off); };
-      auto mst = [&](int a, int l) { return (const void*)(w_out + (int64_t)rows[a].req * d->ldw + L.woff[l]); };
-      const size_t rows_bytes = (sizeof(StepRow) * A + 255) / 256 * 256;
-      // offsets (in pointers) of each array block
-      std::vector<size_t> fwdA(H), fwdB(H), fwdC(H), bwdA(H), bwdB(H), bwdC(H), updA(H), updB(H), updC(H);
-      auto block = [&](auto fn) {
-        const size_t at = ptrs.size();
-        for (int a = 0; a < A; ++a) ptrs.push_back(fn(a));
-        return at;
-      };
-      for (int l = 0; l < H; ++l) {
-        fwdA[l] = block([&](int a) { return wb(a, l); });
-        fwdB[l] = block([&](int a) { return act(a, l); });
-        fwdC[l] = block([&](int a) { return tmp(a); });
-        updA[l] = block([&](int a) { return dlt(a, l + 1); });
-        updB[l] = block([&](int a) { return act(a, l); });
-        updC[l] = block([&](int a) { return mst(a, l); });
-        if (l >= 1) {
-          bwdA[l] = block([&](int a) { return wb(a, l); });
-          bwdB[l] = block([&](int a) { return dlt(a, l + 1); });
-          bwdC[l] = block([&](int a) { return tmp(a); });
-        }
-      }
-      const size_t stage_need = rows_bytes + ptrs.size() * 8;
-      if (stage_need + 256 > d->workspace_bytes - G * g.slot_bytes) {
-        set_error("fs_train_bf16 (wide): step staging exceeds the workspace");
-        return FS_EINVAL;
-      }
-      std::vector<uint8_t> host(stage_need);
-      memcpy(host.data(), rows.data(), sizeof(StepRow) * A);
-      memcpy(host.data() + rows_bytes, ptrs.data(), ptrs.size() * 8);
-      cudaMemcpyAsync(stage, host.data(), stage_need, cudaMemcpyHostToDevice, st);
+      cudaMemcpyAsync(stage, rows.data(), sizeof(StepRow) * A, cudaMemcpyHostToDevice, st);
       const StepRow* d_rows = reinterpret_cast<const StepRow*>(stage);
-      const void** d_ptrs = reinterpret_cast<const void**>(stage + rows_bytes);
       gather_kernel<<<A, 256, 0, st>>>(sa, d_rows);
       if (int rc = check_launch("wide gather")) return rc;
       // ---- forward
       for (int l = 0; l < H; ++l) {
-        const int fin = l == 0 ? g.dp : L.f[l], fout = L.f[l + 1];
-        // col-major: Z'(fout x rows) = W'(fout x fin) * H'(fin x rows)
-        if (int rc = blas_ok(cublasGemmBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, fout, nrow, fin, &one, d_ptrs + fwdA[l],
-                                                 CUDA_R_16BF, fout, d_ptrs + fwdB[l], CUDA_R_16BF, fin, &zero,
-                                                 (void* const*)(d_ptrs + fwdC[l]), CUDA_R_32F, fout, A,
-                                                 CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                             "forward GEMM"))
-          return rc;
-        fwd_epilogue_kernel<<<dim3((fout + 255) / 256, (unsigned)A), 256, 0, st>>>(sa, d_rows, l + 1);
-        if (int rc = check_launch("wide fwd epilogue")) return rc;
+        FwdArgs f{};
+        f.l = l + 1;
+        f.fin = L.f[l];
+        f.fout = L.f[l + 1];
+        f.nb = g.nb;
+        f.kchunks = (f.fin + KC - 1) / KC;
+        f.last = l + 1 == H;
+        f.zp = zparts(L.f[H]);
+        f.boff = L.boff[l];
+        f.whoff = L.woff[H];
+        f.hid_base = hid_base[l + 1];
+        f.h_off = g.h_off[l + 1];
+        f.z_off = g.z_off;
+        f.ld_out = g.ld[l + 1];
+        fwd_kernel<<<dim3((unsigned)((f.fout + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
+                     fwd_smem(g.nb), st>>>(fA[l], fB[l], sa, f, d_rows);
+        if (int rc = check_launch("wide fwd")) return rc;
       }
-      head_kernel<<<A, 256, 0, st>>>(sa, d_rows);
+      head_kernel<<<A, 256, (size_t)g.rb * 4, st>>>(sa, d_rows);
       if (int rc = check_launch("wide head")) return rc;
-      // ---- backward: dH_l = D_{l+1} W_l^T (old bf16 weights), then gates
-      for (int l = H - 1; l >= 1; --l) {
-        const int fin = L.f[l], fout = L.f[l + 1];
-        // col-major: dH'(fin x rows) = W'^T (fin x fout) * D'(fout x rows)
-        if (int rc = blas_ok(cublasGemmBatchedEx(h, CUBLAS_OP_T, CUBLAS_OP_N, fin, nrow, fout, &one, d_ptrs + bwdA[l],
-                                                 CUDA_R_16BF, fout, d_ptrs + bwdB[l], CUDA_R_16BF, fout, &zero,
-                                                 (void* const*)(d_ptrs + bwdC[l]), CUDA_R_32F, fin, A,
-                                                 CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                             "backward GEMM"))
-          return rc;
-        gate_kernel<<<dim3((fin + 255) / 256, (unsigned)A), 256, 0, st>>>(sa, d_rows, l);
-        if (int rc = check_launch("wide gate")) return rc;
-      }
-      // ---- updates: W_l master += (-lr) H_l^T D_{l+1}, one batched GEMM per distinct lr
-      std::vector<std::pair<float, std::vector<int>>> groups;
-      for (int a = 0; a < A; ++a) {
-        auto it = std::find_if(groups.begin(), groups.end(), [&](const auto& p) { return p.first == rows[a].lr; });
-        if (it == groups.end()) groups.push_back({rows[a].lr, {a}});
-        else it->second.push_back(a);
-      }
-      for (const auto& grp : groups) {
-        const float alpha = -grp.first;
-        const int ga = (int)grp.second.size();
-        const bool contiguous = ga == A;
-        for (int l = 0; l < H; ++l) {
-          const int fin = l == 0 ? g.dp : L.f[l], fout = L.f[l + 1];
-          const int fin_true = L.f[l];  // padded W_0 rows beyond f0 have no master
-          const void* const* pa = d_ptrs + updA[l];
-          const void* const* pb = d_ptrs + updB[l];
-          void* const* pc = (void* const*)(d_ptrs + updC[l]);
-          if (!contiguous) {  // sub-batch: gather its pointers into the staging tail
-            std::vector<const void*> sub;
-            for (size_t blk : {updA[l], updB[l], updC[l]})
-              for (int a : grp.second) sub.push_back(ptrs[blk + a]);
-            const size_t off = stage_need + 256 + (size_t)3 * A * 8 * l;
-            if (off + sub.size() * 8 > d->workspace_bytes - G * g.slot_bytes) {
-              set_error("fs_train_bf16 (wide): lr-group staging exceeds the workspace");
-              return FS_EINVAL;
-            }
-            cudaMemcpyAsync(stage + off, sub.data(), sub.size() * 8, cudaMemcpyHostToDevice, st);
-            const void** dp = reinterpret_cast<const void**>(stage + off);
-            pa = dp;
-            pb = dp + ga;
-            pc = (void* const*)(dp + 2 * ga);
+      // ---- backward through W_l (old bf16 copy), then that layer's update
+      for (int l = H - 1; l >= 0; --l) {
+        if (l >= 1) {
+          BwdArgs p{};
+          p.l = l;
+          p.fin = L.f[l];
+          p.fout = L.f[l + 1];
+          p.nb = g.nb;
+          p.kchunks = (p.fout + KC - 1) / KC;
+          p.boff = L.boff[l - 1];
+          p.h_off = g.h_off[l];
+          p.d_off = g.d_off[l];
+          p.bp_off = g.bp_off[l];
+          p.ld = g.ld[l];
+          bwd_kernel<<<dim3((unsigned)((p.fin + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
+                       fwd_smem(g.nb), st>>>(bA[l], bB[l], sa, p, d_rows);
+          if (int rc = check_launch("wide bwd")) return rc;
+          if (g.rtiles > 1) {
+            bias_reduce_kernel<<<dim3((unsigned)((p.fin + 255) / 256), (unsigned)A), 256, 0, st>>>(
+                sa, d_rows, p.fin, p.boff, p.bp_off);
+            if (int rc = check_launch("wide bias")) return rc;
           }
-          (void)fin;
-          // col-major: W'(fout x fin) += alpha * D'(fout x rows) * H'^T(rows x fin)
-          if (int rc = blas_ok(cublasGemmBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_T, fout, fin_true, nrow, &alpha, pa,
-                                                   CUDA_R_16BF, fout, pb, CUDA_R_16BF, l == 0 ? g.dp : L.f[l], &one,
-                                                   pc, CUDA_R_32F, fout, ga, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                               "update GEMM"))
-            return rc;
         }
+        UpdArgs u{};
+        u.l = l;
+        u.fin = L.f[l];
+        u.fout = L.f[l + 1];
+        u.woff = L.woff[l];
+        u.wb_off = g.wb_off[l];
+        u.ldw = g.ldw[l];
+        upd_kernel<<<dim3((unsigned)((u.fin + TM - 1) / TM), (unsigned)((u.fout + UN - 1) / UN), (unsigned)A),
+                     THREADS, upd_smem(), st>>>(uA[l], uB[l], sa, u, d_rows);
+        if (int rc = check_launch("wide upd")) return rc;
       }
-      // bf16 copies of the updated masters for the next step
-      convert_kernel<<<dim3(128, (unsigned)A), 256, 0, st>>>(ca, d_rows, A);
-      if (int rc = check_launch("wide convert")) return rc;
     }
   }
   return FS_OK;
@@ -612,27 +820,12 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
 // ------------------------------------------------------------------ eval forward (wide layers)
 namespace wide {
 
-__global__ void to_bf16_kernel(const float* src, int64_t rows_src, int64_t rows_dst, int cols, __nv_bfloat16* dst) {
-  const int64_t total = rows_dst * cols;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x)
-    dst[j] = __float2bfloat16_rn(j / cols < rows_src ? src[j] : 0.f);
-}
-
-// H = bf16(relu(Z + b)); the last hidden layer also accumulates the logits
-// from the fp32 values (z[r] += sum_u v * w_h[u]), as the trainers do
-__global__ void eval_epilogue_kernel(const float* Z, const float* b, int N, int rows, __nv_bfloat16* H,
-                                     const float* wh, float* z) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
-  float v = 0.f;
-  if (u < N) {
-    v = fmaxf(Z[(int64_t)r * N + u] + b[u], 0.f);
-    H[(int64_t)r * N + u] = __float2bfloat16_rn(v);
-  }
-  if (wh) {
-    float p = u < N ? v * wh[u] : 0.f;
-    for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-    if ((threadIdx.x & 31) == 0) z[(int64_t)r * zparts(N) + blockIdx.x * 8 + (threadIdx.x >> 5)] = p;
+// bf16 copy of W_l [fin x fout] with row stride ldw
+__global__ void to_bf16_kernel(const float* src, int fin, int fout, int ldw, __nv_bfloat16* dst) {
+  const int64_t total = (int64_t)fin * fout;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j / fout, u = j - i * fout;
+    dst[i * ldw + u] = __float2bfloat16_rn(src[j]);
   }
 }
 
@@ -645,6 +838,29 @@ __global__ void eval_probs_kernel(const float* z, int zp, const float* bh, int r
   probs[r] = (double)(zz >= 0.f ? 1.f / (1.f + __expf(-zz)) : __expf(zz) / (1.f + __expf(zz)));
 }
 
+constexpr int EVAL_NB = 128;
+
+struct EvalGeo {
+  int dp, ldmax, ldw[MAXL];
+  size_t wb_off[MAXL], wb_bytes, act_bytes, z_bytes;
+};
+
+static EvalGeo eval_geo(const MlpLayout& L, int rows) {
+  EvalGeo e{};
+  e.dp = rup(L.f[0], 16);
+  size_t o = 0;
+  for (int l = 0; l < L.L - 1; ++l) {
+    e.ldw[l] = rup(L.f[l + 1], 8);
+    e.wb_off[l] = o;
+    o += ((size_t)L.f[l] * e.ldw[l] * 2 + 255) / 256 * 256;
+  }
+  e.wb_bytes = o;
+  e.ldmax = rup(std::max(L.max_hidden, 8), 8);
+  e.act_bytes = ((size_t)rows * e.ldmax * 2 + 255) / 256 * 256;
+  e.z_bytes = (size_t)rows * zparts(L.f[L.L - 1]) * 4 + 256;
+  return e;
+}
+
 }  // namespace wide
 }  // namespace fs
 
@@ -652,19 +868,17 @@ using namespace fs;
 
 extern "C" size_t fs_forward_wide_workspace_bytes(const int32_t* dims, int32_t n_dims, int32_t rows) {
   MlpLayout L;
-  if (make_layout(dims, n_dims, &L) != FS_OK || rows < 0) return 0;
-  const int dp = (L.f[0] + 15) / 16 * 16;
-  const size_t wb = ((size_t)L.M + (size_t)(dp - L.f[0]) * L.f[1]) * 2;
-  const size_t act = (size_t)rows * std::max(L.max_hidden, dp) * 2;
-  return (wb + 255) / 256 * 256 + 2 * ((act + 255) / 256 * 256) +
-         (((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256) +
-         ((size_t)rows * wide::zparts(L.f[L.L - 1]) * 4 + 256);
+  if (make_layout(dims, n_dims, &L) != FS_OK || rows < 0 || L.L < 2) return 0;
+  const wide::EvalGeo e = wide::eval_geo(L, rows);
+  return e.wb_bytes + 2 * e.act_bytes + e.z_bytes;
 }
 
 // K8 forward for layer shapes beyond the on-chip kernels (bf16 operands,
-// fp32 accumulation, fp32 head): probs_out[rows] of fs_prep_features_bf16 rows.
+// fp32 accumulation, fp32 head): probs_out[rows] of fs_prep_features_bf16
+// rows, through the same tcgen05 forward kernel as the wide trainer.
 extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float* w, const void* x_bf16, int32_t rows,
                                double* probs_out, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace wide;
   MlpLayout L;
   if (make_layout(dims, n_dims, &L) != FS_OK || rows < 0 || L.L < 2) {
     set_error("fs_forward_wide: invalid dims or rows");
@@ -677,52 +891,52 @@ extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float*
     return FS_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cublasHandle_t h = wide::blas();
-  if (!h) {
-    set_error("fs_forward_wide: cublasCreate failed");
-    return FS_ECUDA;
-  }
-  if (int rc = wide::blas_ok(cublasSetStream(h, st), "cublasSetStream")) return rc;
-  const int dp = (L.f[0] + 15) / 16 * 16;
+  const EvalGeo e = eval_geo(L, rows);
   uint8_t* p = reinterpret_cast<uint8_t*>(workspace);
-  const size_t wb_bytes = ((size_t)L.M + (size_t)(dp - L.f[0]) * L.f[1]) * 2;
-  __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(p);
-  p += (wb_bytes + 255) / 256 * 256;
-  const size_t act = (size_t)rows * std::max(L.max_hidden, dp) * 2;
-  __nv_bfloat16* hbuf[2] = {reinterpret_cast<__nv_bfloat16*>(p),
-                            reinterpret_cast<__nv_bfloat16*>(p + (act + 255) / 256 * 256)};
-  p += 2 * ((act + 255) / 256 * 256);
-  float* Z = reinterpret_cast<float*>(p);
-  p += ((size_t)rows * L.max_hidden * 4 + 255) / 256 * 256;
-  float* z = reinterpret_cast<float*>(p);  // head-logit partials [rows x zparts]
-  const float one = 1.f, zero = 0.f;
-  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(x_bf16);
-  int fin_pad = dp;
-  int64_t wofs = 0;
-  for (int l = 0; l < L.L - 1; ++l) {
+  __nv_bfloat16* hbuf[2] = {reinterpret_cast<__nv_bfloat16*>(p + e.wb_bytes),
+                            reinterpret_cast<__nv_bfloat16*>(p + e.wb_bytes + e.act_bytes)};
+  float* z = reinterpret_cast<float*>(p + e.wb_bytes + 2 * e.act_bytes);
+  const int H = L.L - 1;
+  ensure_smem(fwd_kernel, fwd_smem(EVAL_NB));
+  StepArgs sa{};
+  sa.lay = L;
+  sa.mask_mode = FS_MASK_NONE;
+  const void* in = x_bf16;
+  int ld_in = e.dp;
+  for (int l = 0; l < H; ++l) {
     const int fin = L.f[l], fout = L.f[l + 1];
-    const int kin = l == 0 ? dp : fin;
-    __nv_bfloat16* wl = wb + wofs;
-    wide::to_bf16_kernel<<<256, 256, 0, st>>>(w + L.woff[l], fin, kin, fout, wl);
+    __nv_bfloat16* wl = reinterpret_cast<__nv_bfloat16*>(p + e.wb_off[l]);
+    to_bf16_kernel<<<256, 256, 0, st>>>(w + L.woff[l], fin, fout, e.ldw[l], wl);
     if (int rc = check_launch("fs_forward_wide convert")) return rc;
-    wofs += (int64_t)kin * fout;
-    // col-major: Z'(fout x rows) = W'(fout x kin) * H'(kin x rows)
-    if (int rc = wide::blas_ok(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, fout, rows, kin, &one, wl, CUDA_R_16BF, fout,
-                                            in, CUDA_R_16BF, kin, &zero, Z, CUDA_R_32F, fout, CUBLAS_COMPUTE_32F,
-                                            CUBLAS_GEMM_DEFAULT),
-                               "forward GEMM"))
-      return rc;
-    __nv_bfloat16* out = hbuf[l & 1];
-    const bool last = l == L.L - 2;
-    wide::eval_epilogue_kernel<<<dim3((fout + 255) / 256, (unsigned)rows), 256, 0, st>>>(
-        Z, w + L.boff[l], fout, rows, out, last ? w + L.woff[L.L - 1] : nullptr, z);
-    if (int rc = check_launch("fs_forward_wide epilogue")) return rc;
-    in = out;
-    fin_pad = fout;
+    CUtensorMap ta, tb;
+    if (!tma::make_map(&ta, wl, fout, fin, 1, e.ldw[l], 0, 64) ||
+        !tma::make_map(&tb, in, fin, rows, 1, ld_in, 0, EVAL_NB)) {
+      set_error("fs_forward_wide: tensor map encoding failed");
+      return FS_ECUDA;
+    }
+    const int ld_out = rup(fout, 8);
+    FwdArgs f{};
+    f.l = l + 1;
+    f.fin = fin;
+    f.fout = fout;
+    f.nb = EVAL_NB;
+    f.kchunks = (fin + KC - 1) / KC;
+    f.last = l + 1 == H;
+    f.zp = zparts(L.f[H]);
+    f.boff = L.boff[l];
+    f.whoff = L.woff[H];
+    f.ld_out = ld_out;
+    f.eval = 1;
+    f.rows_eval = rows;
+    f.h_eval = hbuf[l & 1];
+    f.z_eval = z;
+    f.w_eval = w;
+    fwd_kernel<<<dim3((unsigned)((fout + TM - 1) / TM), (unsigned)((rows + EVAL_NB - 1) / EVAL_NB), 1), THREADS,
+                 fwd_smem(EVAL_NB), st>>>(ta, tb, sa, f, nullptr);
+    if (int rc = check_launch("fs_forward_wide layer")) return rc;
+    in = hbuf[l & 1];
+    ld_in = ld_out;
   }
-  (void)fin_pad;
-  wide::eval_probs_kernel<<<(rows + 255) / 256, 256, 0, st>>>(z, wide::zparts(L.f[L.L - 1]), w + L.boff[L.L - 1],
-                                                              rows, probs_out);
+  eval_probs_kernel<<<(rows + 255) / 256, 256, 0, st>>>(z, zparts(L.f[H]), w + L.boff[H], rows, probs_out);
   return check_launch("fs_forward_wide probs");
 }
-
