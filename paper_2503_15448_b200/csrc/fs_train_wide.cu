@@ -257,6 +257,9 @@ template <bool A_MN>
 __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorMap* ta, const CUtensorMap* tb,
                                          int m0, int r0, int slot, int kchunks, int nb) {
   const uint32_t stage_bytes = A_BYTES + (uint32_t)nb * 128u;
+  // one lane of warp 0 produces, one lane of warp 1 issues; their warp
+  // siblings park at __syncwarp (a spinning sibling would steal the lane's
+  // issue slots: divergent paths of one warp are scheduled in turn)
   if (threadIdx.x == 0) {
     for (int kc = 0; kc < kchunks; ++kc) {
       const int s = kc % STAGES;
@@ -290,9 +293,9 @@ __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorM
     }
     tc::mma_commit(&R.done);
   }
+  __syncwarp();
   tc::mbar_wait(&R.done, 0);
   tc::fence_after_sync();
-  __syncwarp();  // producer / issuer lanes rejoin their warps before tcgen05.ld
 }
 
 __device__ __forceinline__ uint32_t lane_addr(uint32_t tmem, int col) {
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CU
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int r = r0 + c0 + j;
-      if (r >= rend) continue;  // (eval: past the last row; uniform across the warp)
+      if (r >= rend || c0 + j >= f.nb) continue;  // past the last row / the tile (warp-uniform)
       float x = 0.f;
       if (r < nrows && uok) {
         x = fmaxf(v[j] + b, 0.f);
@@ -473,6 +476,7 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CU
     if (iok) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
+        if (c0 + j >= p.nb) continue;  // nb % 32 == 16: the last chunk is half wide
         const int64_t o = (int64_t)(r0 + c0 + j) * p.ld + i;
         const float hv = __bfloat162float(h[o]);
         const __nv_bfloat16 dv = __float2bfloat16_rn(hv > 0.f ? v[j] * sc : 0.f);
@@ -552,9 +556,9 @@ __global__ void __launch_bounds__(THREADS) upd_kernel(const __grid_constant__ CU
     }
     tc::mma_commit(&R.done);
   }
+  __syncwarp();
   tc::mbar_wait(&R.done, 0);
   tc::fence_after_sync();
-  __syncwarp();
 
   // W_l[i][u] -= lr * G[i][u] on the fp32 master and its bf16 copy
   const int i = i0 + threadIdx.x;
