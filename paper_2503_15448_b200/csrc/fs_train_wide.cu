@@ -208,15 +208,6 @@ __global__ void gather_kernel(StepArgs a, const StepRow* rows) {
   for (int r = threadIdx.x; r < a.g.rb; r += blockDim.x) y[r] = r < sr.rows ? a.labels[base + perm[r]] : 0.f;
 }
 
-__device__ __forceinline__ bool keep_bit(const StepArgs& a, const StepRow& sr, int l, int r, int u,
-                                         int64_t hid_base) {
-  const int B = a.batch[sr.req];
-  const int64_t slot_words = ((int64_t)B * a.lay.sum_hidden + 31) / 32;
-  const uint32_t* bits = a.mask_bits + a.mask_off[sr.req] + (int64_t)sr.global_step * slot_words;
-  const int64_t j = (int64_t)sr.rows * hid_base + (int64_t)r * a.lay.f[l] + u;
-  return (bits[j >> 5] >> (j & 31)) & 1u;
-}
-
 // ------------------------------------------------------------------ tcgen05 tile machinery
 struct Ring {
   uint64_t full[STAGES];
@@ -299,7 +290,54 @@ __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorM
 }
 
 __device__ __forceinline__ uint32_t lane_addr(uint32_t tmem, int col) {
-  return tmem + ((uint32_t)((threadIdx.x >> 5) * 32) << 16) + (uint32_t)col;
+  return tmem + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) + (uint32_t)col;
+}
+
+// 32x32 bit transpose across a warp: in, lane k bit u = A[k][u]; out, lane u bit k
+__device__ __forceinline__ uint32_t bit_transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
+                                                                                                     : 0x55555555u;
+    const uint32_t t = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((t >> j) & m)) : ((x & m) | ((t << j) & ~m));
+  }
+  return x;
+}
+
+// warp reduce-scatter: lane L returns the sum over lanes of p[L] (p clobbered)
+__device__ __forceinline__ float reduce_scatter32(float (&p)[32], int lane) {
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+    const bool up = (lane & j) != 0;
+#pragma unroll
+    for (int i = 0; i < j; ++i) {
+      const float send = up ? p[i] : p[i + j];
+      const float keep = up ? p[i + j] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, j);
+    }
+  }
+  return p[0];
+}
+
+// keep bits of rows [rbase, rbase+32) for this warp's 32 units [ub, ub+32):
+// lane l fetches the 32 unit bits of row rbase+l (K3 layout: row-major
+// [rows x f_l] per hidden layer), a bit transpose hands lane u its row bits
+__device__ __forceinline__ uint32_t keep_word(const StepArgs& a, const StepRow& sr, int l, int64_t hid_base,
+                                              int rbase, int ub, int lane) {
+  const int r = rbase + lane;
+  uint32_t w = 0;
+  if (r < sr.rows && ub < a.lay.f[l]) {
+    const int B = a.batch[sr.req];
+    const int64_t slot_words = ((int64_t)B * a.lay.sum_hidden + 31) / 32;
+    const uint32_t* bits = a.mask_bits + a.mask_off[sr.req] + (int64_t)sr.global_step * slot_words;
+    const int64_t j = (int64_t)sr.rows * hid_base + (int64_t)r * a.lay.f[l] + ub;
+    const int64_t last = j + min(32, a.lay.f[l] - ub) - 1;
+    const uint32_t sh = (uint32_t)(j & 31);
+    w = bits[j >> 5] >> sh;
+    if ((last >> 5) != (j >> 5)) w |= bits[(j >> 5) + 1] << (32u - sh);
+  }
+  return bit_transpose32(w, lane);
 }
 
 // ------------------------------------------------------------------ forward
@@ -356,24 +394,24 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CU
   const int rend = f.eval ? min(r0 + f.nb, nrows) : r0 + f.nb;  // training slots hold rb rows
   for (int c0 = 0; c0 < f.nb; c0 += 32) {
     if (r0 + c0 >= rend) break;
+    const uint32_t keep = masked ? keep_word(a, sr, f.l, f.hid_base, r0 + c0, m0 + warp * 32, lane) : ~0u;
     float v[32];
     tc::tmem_ld32(lane_addr(R.tmem, c0), v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int r = r0 + c0 + j;
-      if (r >= rend || c0 + j >= f.nb) continue;  // past the last row / the tile (warp-uniform)
       float x = 0.f;
       if (r < nrows && uok) {
         x = fmaxf(v[j] + b, 0.f);
-        if (masked) x = keep_bit(a, sr, f.l, r, u, f.hid_base) ? x * sc : 0.f;
+        x = ((keep >> j) & 1u) ? x * sc : 0.f;
       }
-      if (uok) h[(int64_t)r * f.ld_out + u] = __float2bfloat16_rn(x);
-      if (f.last) {
-        float p = x * wh;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        if (lane == 0 && r < nrows) z[(int64_t)r * f.zp + tile * 4 + warp] = p;
-      }
+      if (uok && r < rend && c0 + j < f.nb) h[(int64_t)r * f.ld_out + u] = __float2bfloat16_rn(x);
+      v[j] = x * wh;
+    }
+    if (f.last) {  // head-logit partial of row r0+c0+lane over this warp's 32 units
+      const float p = reduce_scatter32(v, lane);
+      const int r = r0 + c0 + lane;
+      if (r < nrows && r < rend && c0 + lane < f.nb) z[(int64_t)r * f.zp + tile * 4 + warp] = p;
     }
   }
   ring_free(R, cols);
@@ -474,13 +512,16 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CU
     float v[32];
     tc::tmem_ld32(lane_addr(R.tmem, c0), v);
     if (iok) {
+      // every H load of the chunk before the first D store (they may alias)
+      __nv_bfloat16 hv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        hv[j] = c0 + j < p.nb ? h[(int64_t)(r0 + c0 + j) * p.ld + i] : __float2bfloat16_rn(0.f);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (c0 + j >= p.nb) continue;  // nb % 32 == 16: the last chunk is half wide
-        const int64_t o = (int64_t)(r0 + c0 + j) * p.ld + i;
-        const float hv = __bfloat162float(h[o]);
-        const __nv_bfloat16 dv = __float2bfloat16_rn(hv > 0.f ? v[j] * sc : 0.f);
-        dl[o] = dv;
+        const __nv_bfloat16 dv = __float2bfloat16_rn(__bfloat162float(hv[j]) > 0.f ? v[j] * sc : 0.f);
+        dl[(int64_t)(r0 + c0 + j) * p.ld + i] = dv;
         gb += __bfloat162float(dv);
       }
     }
@@ -512,9 +553,11 @@ struct UpdArgs {
   int ldw;
 };
 
-__global__ void __launch_bounds__(THREADS) upd_kernel(const __grid_constant__ CUtensorMap ta,
-                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, UpdArgs p,
-                                                      const StepRow* rows) {
+constexpr int UPD_THREADS = 256;  // two warps per TMEM lane quarter: the epilogue is an HBM stream
+
+__global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant__ CUtensorMap ta,
+                                                          const __grid_constant__ CUtensorMap tb, StepArgs a,
+                                                          UpdArgs p, const StepRow* rows) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Ring R;
   uint8_t* smem = smem_base(smem_raw);
@@ -560,44 +603,60 @@ __global__ void __launch_bounds__(THREADS) upd_kernel(const __grid_constant__ CU
   tc::mbar_wait(&R.done, 0);
   tc::fence_after_sync();
 
-  // W_l[i][u] -= lr * G[i][u] on the fp32 master and its bf16 copy
-  const int i = i0 + threadIdx.x;
+  // W_l[i][u] -= lr * G[i][u] on the fp32 master and its bf16 copy. Warp w
+  // owns TMEM lane quarter w & 3 (rows i) and every other 32-column chunk
+  // starting at w >> 2; the master loads of the next chunk are issued before
+  // the stores of the current one (two chunks in flight per warp).
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = i0 + (warp & 3) * 32 + lane;
   const bool iok = i < p.fin;
   float* wrow = a.w_out + (int64_t)sr.req * a.ldw + p.woff + (int64_t)i * p.fout + u0;
   __nv_bfloat16* brow =
       reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.wb_off) + (int64_t)i * p.ldw + u0;
   const float nlr = -sr.lr;
-  const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(wrow) & 15) == 0);
-  for (int c0 = 0; c0 < nmma; c0 += 32) {
-    float g[32];
-    tc::tmem_ld32(lane_addr(R.tmem, c0), g);
-    if (!iok) continue;
-    if (vec && c0 + 32 <= nu) {
-      float4 w4[8];
+  const int nchunk = (nmma + 31) / 32;
+  const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.w_out + p.woff) & 15) == 0) &&
+                   ((a.ldw & 3) == 0);
+  float4 cur[8], nxt[8];
+  auto full_chunk = [&](int c) { return vec && iok && 32 * c + 32 <= nu; };
+  auto load8 = [&](int c, float4 (&d)[8]) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) w4[q] = reinterpret_cast<const float4*>(wrow + c0)[q];
+    for (int q = 0; q < 8; ++q) d[q] = reinterpret_cast<const float4*>(wrow + 32 * c)[q];
+  };
+  int c = warp >> 2;
+  if (c < nchunk && full_chunk(c)) load8(c, cur);
+  for (; c < nchunk; c += 2) {
+    const bool has_next = c + 2 < nchunk && full_chunk(c + 2);
+    if (has_next) load8(c + 2, nxt);
+    float g[32];
+    tc::tmem_ld32(lane_addr(R.tmem, 32 * c), g);
+    if (full_chunk(c)) {
       uint32_t pk[16];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        w4[q].x = fmaf(nlr, g[4 * q + 0], w4[q].x);
-        w4[q].y = fmaf(nlr, g[4 * q + 1], w4[q].y);
-        w4[q].z = fmaf(nlr, g[4 * q + 2], w4[q].z);
-        w4[q].w = fmaf(nlr, g[4 * q + 3], w4[q].w);
-        reinterpret_cast<float4*>(wrow + c0)[q] = w4[q];
-        pk[2 * q] = tc::pack_bf16x2(w4[q].x, w4[q].y);
-        pk[2 * q + 1] = tc::pack_bf16x2(w4[q].z, w4[q].w);
+        cur[q].x = fmaf(nlr, g[4 * q + 0], cur[q].x);
+        cur[q].y = fmaf(nlr, g[4 * q + 1], cur[q].y);
+        cur[q].z = fmaf(nlr, g[4 * q + 2], cur[q].z);
+        cur[q].w = fmaf(nlr, g[4 * q + 3], cur[q].w);
+        reinterpret_cast<float4*>(wrow + 32 * c)[q] = cur[q];
+        pk[2 * q] = tc::pack_bf16x2(cur[q].x, cur[q].y);
+        pk[2 * q + 1] = tc::pack_bf16x2(cur[q].z, cur[q].w);
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(brow + c0)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    } else {
+        reinterpret_cast<uint4*>(brow + 32 * c)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    } else if (iok) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (c0 + j >= nu) continue;
-        const float w = fmaf(nlr, g[j], wrow[c0 + j]);
-        wrow[c0 + j] = w;
-        brow[c0 + j] = __float2bfloat16_rn(w);
+        if (32 * c + j >= nu) continue;
+        const float w = fmaf(nlr, g[j], wrow[32 * c + j]);
+        wrow[32 * c + j] = w;
+        brow[32 * c + j] = __float2bfloat16_rn(w);
       }
+    }
+    if (has_next) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
     }
   }
   ring_free(R, 256);
@@ -812,7 +871,7 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
         u.wb_off = g.wb_off[l];
         u.ldw = g.ldw[l];
         upd_kernel<<<dim3((unsigned)((u.fin + TM - 1) / TM), (unsigned)((u.fout + UN - 1) / UN), (unsigned)A),
-                     THREADS, upd_smem(), st>>>(uA[l], uB[l], sa, u, d_rows);
+                     UPD_THREADS, upd_smem(), st>>>(uA[l], uB[l], sa, u, d_rows);
         if (int rc = check_launch("wide upd")) return rc;
       }
     }

@@ -133,3 +133,23 @@ def test_oracle_replays_reference_at_road_config():
     wg = sim.run(init.values)
     assert sim.digest() == ref["digest"]
     assert np.max(np.abs(wg - want) / np.maximum(np.abs(want), 1.0)) < 1e-12
+
+
+def test_world_builder_matches_reference_at_c5_scale():
+    """BASELINE configs[4] world (8192 clients, alpha = 5, WIDE MLP): the
+    host world builder reproduces the reference's world digest
+    (tests/golden/c5_world.json, recorded from the reference package)."""
+    import json
+    import os
+
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from tests.conftest import GOLDEN
+    from tests.golden.make_golden import world_digest
+
+    ref = json.load(open(os.path.join(GOLDEN, "c5_world.json")))
+    world, init = build_world(ExperimentConfig.from_dict(ref["config"]))
+    assert world.num_clients == 8192 and world.spec.param_count == ref["param_count"]
+    n = [wc.n for wc in world.clients]
+    assert (min(n), max(n), sum(n)) == (ref["rows_min"], ref["rows_max"], ref["rows_total"])
+    assert world_digest(world, init) == ref["digest"]
