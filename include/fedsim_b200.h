@@ -289,13 +289,26 @@ int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jo
                       int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out, void* stream);
 
 /* filter_update on the device for a synchronous round (selection.py:77-85):
- * accepted rows (aligned[i] / M >= theta; all rows when scored == 0) in
- * client order -> rows_out, job_off = {0, k}, job_out[0] = out: the single
- * job of fs_aggregate_jobs, so FedAvg follows K6 with no host round trip.
- * Rows are base + i * stride_bytes.                                         */
-int fs_select_rows(const int64_t* aligned, int32_t n, int64_t M, double theta, int32_t scored, uint64_t base,
-                   int64_t stride_bytes, uint64_t* rows_out, int64_t* job_off, uint64_t* job_out, uint64_t out,
-                   void* stream);
+ * accepted rows (aligned[i] / den >= theta, den = M for the sign counts or
+ * FS_COSINE_SCALE for cosine scores; all rows when scored == 0) in client
+ * order -> rows_out, job_off = {0, k}, job_out[0] = out: the single job of
+ * fs_aggregate_jobs, so FedAvg follows K6 with no host round trip. Rows are
+ * base + i * stride_bytes. top_k > 0 (opt-in extension, n <= 16384) keeps
+ * only the top_k highest-scoring accepted rows (ties: lower index first).  */
+int fs_select_rows(const int64_t* aligned, int32_t n, int64_t den, double theta, int32_t scored, int32_t top_k,
+                   uint64_t base, int64_t stride_bytes, uint64_t* rows_out, int64_t* job_off, uint64_t* job_out,
+                   uint64_t out, void* stream);
+
+/* K6c, opt-in `delta_cosine` relevance (an extension; the reference counts
+ * matching signs, selection.py:53-74): score_out[r] = llrint(cos * 2^40),
+ * cos = <w_c - w_g, w_g - w_prev> / (|w_c - w_g| |w_g - w_prev|) (0 when a
+ * norm is 0), float64 with a fixed summation order. Rows are wc[r] (device
+ * pointer array) or, when wc == NULL, base + r * stride_bytes.              */
+#define FS_COSINE_SCALE 1099511627776LL /* 2^40 */
+size_t fs_cosine_align_workspace_bytes(int32_t n_req);
+int fs_cosine_align(const uint64_t* wc, uint64_t base, int64_t stride_bytes, const void* wg, const void* wg_prev,
+                    int32_t n_req, int64_t M, int32_t dtype_bytes, int64_t* score_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
                 void* stream);

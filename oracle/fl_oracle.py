@@ -154,10 +154,31 @@ def local_sgd(dims, rate, w0, X, Y, epochs, bsz, lr_of_epoch, seed, stop=None, r
 # ------------------------------------------------------------------ selection / FedAvg
 
 
+COSINE_SCALE = 1 << 40  # fixed point of the opt-in delta_cosine score (framework extension)
+
+
 def alignment(wc, wg, wgp, mode) -> int:  # selection.py:53-74
     if mode == "weight_sign":
         return sign_matches(wc, wg)
+    if mode == "delta_cosine":  # extension (not in the reference): cos(wc - wg, wg - wgp) as llrint(cos * 2^40)
+        a, b = wc - wg, wg - wgp
+        na, nb = float(a @ a), float(b @ b)
+        cs = min(1.0, max(-1.0, float(a @ b) / np.sqrt(na * nb))) if na > 0 and nb > 0 else 0.0
+        return int(np.rint(cs * COSINE_SCALE))
     return sign_matches(wc - wg, wg - wgp)
+
+
+def score_den(mode, M) -> int:
+    return COSINE_SCALE if mode == "delta_cosine" else M
+
+
+def top_k_keep(outs, k):
+    """Extension: of the accepted scored cycles keep the k highest relevances
+    (ties: lower client index); the others become rejected."""
+    cand = [i for i, o in enumerate(outs) if o["res"] is not None and o["rel"] is not None and o["accepted"]]
+    cand.sort(key=lambda i: (-outs[i]["rel"], i))
+    for i in cand[k:]:
+        outs[i]["accepted"] = False
 
 
 def fedavg(vectors):  # server.py:72-86
@@ -285,12 +306,12 @@ class OracleFederation:
             res, span = None, f_off
         accepted, rel = False, None
         if res is not None:
-            if w.policy.mode == "delta_sign" and wgp is None:
+            if w.policy.mode in ("delta_sign", "delta_cosine") and wgp is None:
                 accepted = True
             else:
                 a = alignment(res["params"], wg, wgp, w.policy.mode)
                 self.aligned_log.append((cyc, cid, a))
-                rel = a / len(wg)
+                rel = a / score_den(w.policy.mode, len(wg))
                 accepted = rel >= w.policy.theta
         return dict(cid=cid, cyc=cyc, failed=failed, recovered=recovered, f_off=f_off, span=span,
                     res=res, accepted=accepted, rel=rel, captures=captures)
@@ -331,6 +352,8 @@ class OracleFederation:
             c.at(t, "broadcast_arrive", client_id=wc.profile.id, round=r, latency_s=wc.profile.down_latency_s)
             self.transfer += wc.profile.down_latency_s
         outs = [self.cycle(ci, r, r, wg, wgp) for ci in range(len(w.clients))]
+        if getattr(w.policy, "top_k", None) is not None:
+            top_k_keep(outs, w.policy.top_k)
         kept, ends = [], []
         for t, o in zip(arr, outs):
             self._post_cycle(t, o, r)

@@ -27,6 +27,7 @@ FS_MASK_DENSE = 2
 
 FS_ALIGN_WEIGHT_SIGN = 0
 FS_ALIGN_DELTA_SIGN = 1
+FS_COSINE_SCALE = 1 << 40  # fixed-point denominator of delta_cosine scores
 
 FS_MAX_LAYERS = 8
 
@@ -128,8 +129,11 @@ _SIGNATURES = {
     "fs_canonical_order": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_aggregate_f64": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp]),
     "fs_aggregate_jobs": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp]),
-    "fs_select_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_f64, _c_i32, _c_u64, _c_i64, _c_vp, _c_vp, _c_vp,
-                                      _c_u64, _c_vp]),
+    "fs_select_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_f64, _c_i32, _c_i32, _c_u64, _c_i64, _c_vp, _c_vp,
+                                      _c_vp, _c_u64, _c_vp]),
+    "fs_cosine_align_workspace_bytes": (_c_sz, [_c_i32]),
+    "fs_cosine_align": (ctypes.c_int, [_c_vp, _c_u64, _c_i64, _c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp,
+                                       _c_sz, _c_vp]),
     "fs_sum_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_mean_finish": (ctypes.c_int, [_c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp]),
     "fs_eval_workspace_bytes": (_c_sz, [_c_i32]),

@@ -43,6 +43,15 @@ DEFAULTS: dict = {
     "lr": 0.05,
     "lr_decay": 0.9,
     "seed": 1,
+    # framework extensions (north-star opt-ins; none is on the reference's
+    # parity path and none exists in the reference schema: a config that
+    # leaves them at these defaults serialises without this section)
+    "extensions": {
+        "top_k": None,             # at most k accepted clients per sync round
+        "staleness_alpha": None,   # async FedAvg weights (1 + staleness) ** -alpha
+        "optimizer": "sgd",        # "sgd" | "adam" (local optimizer)
+        "adam": {"beta1": 0.9, "beta2": 0.999, "eps": 1e-8},
+    },
 }
 
 MODES = ("sync_baseline", "sync_filtered", "async_filtered")
@@ -100,9 +109,19 @@ def validate(cfg: dict) -> None:
         _need(_pow2(b[key]), f"batch.{key}", "must be a positive power of two")
     _need(b["b_min"] <= b["b_ref"] <= b["b_max"], "batch.b_ref", "needs b_min <= b_ref <= b_max")
     _need(cfg["mode"] in MODES, "mode", f"must be one of {MODES}")
-    _need(0 <= cfg["theta"] <= 1, "theta", "must be in [0,1]")
-    _need(cfg["selection_mode"] in ("weight_sign", "delta_sign"), "selection_mode",
-          "must be 'weight_sign' or 'delta_sign'")
+    _need(cfg["selection_mode"] in ("weight_sign", "delta_sign", "delta_cosine"), "selection_mode",
+          "must be 'weight_sign', 'delta_sign' or 'delta_cosine'")
+    lo = -1 if cfg["selection_mode"] == "delta_cosine" else 0
+    _need(lo <= cfg["theta"] <= 1, "theta", f"must be in [{lo},1]")
+    ext = cfg["extensions"]
+    _need(ext["top_k"] is None or (isinstance(ext["top_k"], int) and ext["top_k"] >= 1), "extensions.top_k",
+          "must be a positive int or null")
+    _need(ext["staleness_alpha"] is None or ext["staleness_alpha"] >= 0, "extensions.staleness_alpha",
+          "must be >= 0 or null")
+    _need(ext["optimizer"] in ("sgd", "adam"), "extensions.optimizer", "must be 'sgd' or 'adam'")
+    ad = ext["adam"]
+    _need(0 <= ad["beta1"] < 1 and 0 <= ad["beta2"] < 1 and ad["eps"] > 0, "extensions.adam",
+          "needs 0 <= beta1, beta2 < 1 and eps > 0")
     _need(0 <= cfg["dropout_rate"] <= 1, "dropout_rate", "must be in [0,1]")
     agg = cfg["aggregation"]
     _need(int(agg["k_min"]) >= 1, "aggregation.k_min", "must be >= 1")
@@ -130,10 +149,13 @@ class ExperimentConfig:
             return ExperimentConfig.from_dict(json.load(f))
 
     def to_dict(self) -> dict:
-        return copy.deepcopy(self.raw)
+        d = copy.deepcopy(self.raw)
+        if d.get("extensions") == DEFAULTS["extensions"]:
+            del d["extensions"]  # the reference schema has no such section
+        return d
 
     def canonical_json(self) -> str:
-        return json.dumps(self.raw, sort_keys=True, indent=2) + "\n"
+        return json.dumps(self.to_dict(), sort_keys=True, indent=2) + "\n"
 
     def with_overrides(self, **top) -> "ExperimentConfig":
         d = self.to_dict()

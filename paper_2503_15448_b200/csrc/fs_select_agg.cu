@@ -688,18 +688,30 @@ extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, i
 // history, server.py:283-284). The accepted rows (client order) become the
 // single job of fs_aggregate_jobs: rows_out[0..k), job_off = {0, k},
 // job_out[0] = out. One CTA, block-wide prefix sum.
-__global__ void __launch_bounds__(1024) select_rows_kernel(const int64_t* aligned, int n, int64_t M, double theta,
-                                                           int scored, uint64_t base, int64_t stride,
+__global__ void __launch_bounds__(1024) select_rows_kernel(const int64_t* aligned, int n, int64_t den, double theta,
+                                                           int scored, int top_k, uint64_t base, int64_t stride,
                                                            uint64_t* rows_out, int64_t* job_off, uint64_t* job_out,
                                                            uint64_t out) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
+  extern __shared__ int64_t s_score[];  // [n] when top_k > 0
   if (threadIdx.x == 0) carry = 0;
+  if (top_k > 0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_score[i] = aligned[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int b0 = 0; b0 < n; b0 += blockDim.x) {
     const int i = b0 + threadIdx.x;
-    const int acc = i < n && (!scored || (double)aligned[i] / (double)M >= theta);
+    int acc = i < n && (!scored || (double)aligned[i] / (double)den >= theta);
+    if (acc && top_k > 0 && scored) {  // rank among all clients: higher score first, ties by index
+      const int64_t si = s_score[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const int64_t sj = s_score[j];
+        rank += (sj > si) || (sj == si && j < i);
+      }
+      acc = rank < top_k;
+    }
     const unsigned ball = __ballot_sync(0xffffffffu, acc);
     if (lane == 0) warp_tot[warp] = __popc(ball);
     __syncthreads();
@@ -722,15 +734,109 @@ __global__ void __launch_bounds__(1024) select_rows_kernel(const int64_t* aligne
   }
 }
 
-extern "C" int fs_select_rows(const int64_t* aligned, int32_t n, int64_t M, double theta, int32_t scored,
-                              uint64_t base, int64_t stride_bytes, uint64_t* rows_out, int64_t* job_off,
-                              uint64_t* job_out, uint64_t out, void* stream) {
-  if (n < 0 || M < 1 || (scored && !aligned)) {
+extern "C" int fs_select_rows(const int64_t* aligned, int32_t n, int64_t den, double theta, int32_t scored,
+                              int32_t top_k, uint64_t base, int64_t stride_bytes, uint64_t* rows_out,
+                              int64_t* job_off, uint64_t* job_out, uint64_t out, void* stream) {
+  if (n < 0 || den < 1 || (scored && !aligned) || top_k < 0 || (top_k > 0 && n > 16384)) {
     set_error("fs_select_rows: invalid arguments");
     return FS_EINVAL;
   }
-  select_rows_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(aligned, n, M, theta, scored, base, stride_bytes,
-                                                           rows_out, job_off, job_out, out);
+  const size_t smem = top_k > 0 ? (size_t)n * sizeof(int64_t) : 0;
+  if (smem > 48 * 1024) ensure_smem(select_rows_kernel, (int)smem);
+  select_rows_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(aligned, n, den, theta, scored, top_k, base,
+                                                              stride_bytes, rows_out, job_off, job_out, out);
   return check_launch("select_rows_kernel");
+}
+
+// ---------------------------------------------------------------- K6c: cosine relevance (opt-in)
+// Opt-in `delta_cosine` selection (an extension: the reference counts
+// matching signs, selection.py:53-74): score = cos(w_c - w_g, w_g - w_prev),
+// the cosine between a client's update and the last global step, in float64
+// with a fixed summation order (block b of row r reduces the columns
+// [b*span, (b+1)*span) thread-strided, then a fixed xor-shuffle tree and warp
+// order; the finish kernel adds the blocks in order), written as the
+// fixed-point integer llrint(cos * 2^40) so the engines' integer score path
+// (accept iff score / den >= theta, den = FS_COSINE_SCALE) carries it.
+constexpr int COS_THREADS = 256, COS_BLOCKS = 32;
+
+template <class T>
+__global__ void __launch_bounds__(COS_THREADS)
+    cosine_partial_kernel(const uint64_t* wc, uint64_t base, int64_t stride, const T* __restrict__ g,
+                          const T* __restrict__ p, int64_t M, double* part) {
+  const int r = blockIdx.y, b = blockIdx.x;
+  const T* c = reinterpret_cast<const T*>(wc ? wc[r] : base + (uint64_t)r * (uint64_t)stride);
+  const int64_t span = (M + gridDim.x - 1) / gridDim.x;
+  const int64_t j0 = (int64_t)b * span, j1 = min(M, j0 + span);
+  double d = 0.0, na = 0.0, nb = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += COS_THREADS) {
+    const double gj = (double)g[j];
+    const double a = (double)__ldcs(c + j) - gj, q = gj - (double)p[j];
+    d = fma(a, q, d);
+    na = fma(a, a, na);
+    nb = fma(q, q, nb);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  __shared__ double sh[COS_THREADS / 32][3];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[warp][0] = d;
+    sh[warp][1] = na;
+    sh[warp][2] = nb;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < COS_THREADS / 32; ++w) t += sh[w][threadIdx.x];
+    part[((int64_t)r * gridDim.x + b) * 3 + threadIdx.x] = t;
+  }
+}
+
+__global__ void cosine_finish_kernel(const double* part, int n_req, int blocks, int64_t* score) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  double d = 0.0, na = 0.0, nb = 0.0;
+  for (int b = 0; b < blocks; ++b) {
+    d += part[((int64_t)r * blocks + b) * 3];
+    na += part[((int64_t)r * blocks + b) * 3 + 1];
+    nb += part[((int64_t)r * blocks + b) * 3 + 2];
+  }
+  const double cs = (na > 0.0 && nb > 0.0) ? fmin(1.0, fmax(-1.0, d / sqrt(na * nb))) : 0.0;
+  score[r] = llrint(cs * (double)FS_COSINE_SCALE);
+}
+
+extern "C" size_t fs_cosine_align_workspace_bytes(int32_t n_req) {
+  return n_req > 0 ? (size_t)n_req * COS_BLOCKS * 3 * sizeof(double) : 0;
+}
+
+extern "C" int fs_cosine_align(const uint64_t* wc, uint64_t base, int64_t stride_bytes, const void* wg,
+                               const void* wg_prev, int32_t n_req, int64_t M, int32_t dtype_bytes, int64_t* score_out,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_req < 0 || M < 1 || !wg || !wg_prev || (dtype_bytes != 4 && dtype_bytes != 8) ||
+      (!wc && (!base || stride_bytes <= 0))) {
+    set_error("fs_cosine_align: invalid arguments");
+    return FS_EINVAL;
+  }
+  if (n_req == 0) return FS_OK;
+  if (!workspace || workspace_bytes < fs_cosine_align_workspace_bytes(n_req)) {
+    set_error("fs_cosine_align: workspace %zu < required %zu", workspace_bytes, fs_cosine_align_workspace_bytes(n_req));
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = reinterpret_cast<double*>(workspace);
+  const dim3 grid(COS_BLOCKS, (unsigned)n_req);
+  if (dtype_bytes == 8)
+    cosine_partial_kernel<double><<<grid, COS_THREADS, 0, st>>>(wc, base, stride_bytes, (const double*)wg,
+                                                                (const double*)wg_prev, M, part);
+  else
+    cosine_partial_kernel<float><<<grid, COS_THREADS, 0, st>>>(wc, base, stride_bytes, (const float*)wg,
+                                                               (const float*)wg_prev, M, part);
+  if (int rc = check_launch("cosine_partial_kernel")) return rc;
+  cosine_finish_kernel<<<(n_req + 255) / 256, 256, 0, st>>>(part, n_req, COS_BLOCKS, score_out);
+  return check_launch("cosine_finish_kernel");
 }
 

@@ -604,59 +604,87 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
   tc::fence_after_sync();
 
   // W_l[i][u] -= lr * G[i][u] on the fp32 master and its bf16 copy. Warp w
-  // owns TMEM lane quarter w & 3 (rows i) and every other 32-column chunk
-  // starting at w >> 2; the master loads of the next chunk are issued before
-  // the stores of the current one (two chunks in flight per warp).
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = i0 + (warp & 3) * 32 + lane;
-  const bool iok = i < p.fin;
-  float* wrow = a.w_out + (int64_t)sr.req * a.ldw + p.woff + (int64_t)i * p.fout + u0;
-  __nv_bfloat16* brow =
-      reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.wb_off) + (int64_t)i * p.ldw + u0;
-  const float nlr = -sr.lr;
+  // owns TMEM lane quarter w & 3 (32 rows i) and every other 32-column chunk
+  // starting at w >> 2. Each chunk goes TMEM -> registers (lane = row) ->
+  // shared memory (the free operand ring) -> registers as 4 rows x 8 float4
+  // per instruction, so every global access of a warp covers whole 128-byte
+  // row segments; the next chunk's master loads are issued before the
+  // current chunk's stores.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = warp & 3;
   const int nchunk = (nmma + 31) / 32;
+  const float nlr = -sr.lr;
+  float* T = reinterpret_cast<float*>(smem) + warp * (32 * 36);  // [32 rows][36] staging, 144-byte rows
+  const int rr0 = lane >> 3, cc = (lane & 7) * 4;                 // pass p: row 4p + rr0, columns cc..cc+3
+  float* wbase = a.w_out + (int64_t)sr.req * a.ldw + p.woff + (int64_t)(i0 + q * 32) * p.fout + u0;
+  __nv_bfloat16* bbase =
+      reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.wb_off) + (int64_t)(i0 + q * 32) * p.ldw + u0;
   const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.w_out + p.woff) & 15) == 0) &&
-                   ((a.ldw & 3) == 0);
+                   ((a.ldw & 3) == 0) && (p.ldw % 4 == 0);
+  auto row_ok = [&](int pp) { return i0 + q * 32 + 4 * pp + rr0 < p.fin; };
+  auto col_ok = [&](int c) { return 32 * c + cc + 4 <= nu; };
   float4 cur[8], nxt[8];
-  auto full_chunk = [&](int c) { return vec && iok && 32 * c + 32 <= nu; };
   auto load8 = [&](int c, float4 (&d)[8]) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) d[q] = reinterpret_cast<const float4*>(wrow + 32 * c)[q];
+    for (int pp = 0; pp < 8; ++pp)
+      if (row_ok(pp) && col_ok(c))
+        d[pp] = *reinterpret_cast<const float4*>(wbase + (int64_t)(4 * pp + rr0) * p.fout + 32 * c + cc);
   };
   int c = warp >> 2;
-  if (c < nchunk && full_chunk(c)) load8(c, cur);
+  if (vec && c < nchunk) load8(c, cur);
   for (; c < nchunk; c += 2) {
-    const bool has_next = c + 2 < nchunk && full_chunk(c + 2);
+    const bool has_next = vec && c + 2 < nchunk;
     if (has_next) load8(c + 2, nxt);
     float g[32];
     tc::tmem_ld32(lane_addr(R.tmem, 32 * c), g);
-    if (full_chunk(c)) {
-      uint32_t pk[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        cur[q].x = fmaf(nlr, g[4 * q + 0], cur[q].x);
-        cur[q].y = fmaf(nlr, g[4 * q + 1], cur[q].y);
-        cur[q].z = fmaf(nlr, g[4 * q + 2], cur[q].z);
-        cur[q].w = fmaf(nlr, g[4 * q + 3], cur[q].w);
-        reinterpret_cast<float4*>(wrow + 32 * c)[q] = cur[q];
-        pk[2 * q] = tc::pack_bf16x2(cur[q].x, cur[q].y);
-        pk[2 * q + 1] = tc::pack_bf16x2(cur[q].z, cur[q].w);
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4*>(T + lane * 36 + 4 * k) = make_float4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
+    __syncwarp();
+    if (vec) {
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        if (!row_ok(pp)) continue;
+        const int row = 4 * pp + rr0;
+        if (col_ok(c)) {
+          const float4 g4 = *reinterpret_cast<const float4*>(T + row * 36 + cc);
+          float4 w = cur[pp];
+          w.x = fmaf(nlr, g4.x, w.x);
+          w.y = fmaf(nlr, g4.y, w.y);
+          w.z = fmaf(nlr, g4.z, w.z);
+          w.w = fmaf(nlr, g4.w, w.w);
+          *reinterpret_cast<float4*>(wbase + (int64_t)row * p.fout + 32 * c + cc) = w;
+          *reinterpret_cast<uint2*>(bbase + (int64_t)row * p.ldw + 32 * c + cc) =
+              make_uint2(tc::pack_bf16x2(w.x, w.y), tc::pack_bf16x2(w.z, w.w));
+        } else {
+          for (int e = 0; e < 4; ++e) {
+            const int u = 32 * c + cc + e;
+            if (u >= nu) break;
+            float* wp = wbase + (int64_t)row * p.fout + u;
+            const float w = fmaf(nlr, T[row * 36 + cc + e], *wp);
+            *wp = w;
+            bbase[(int64_t)row * p.ldw + u] = __float2bfloat16_rn(w);
+          }
+        }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(brow + 32 * c)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    } else if (iok) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (32 * c + j >= nu) continue;
-        const float w = fmaf(nlr, g[j], wrow[32 * c + j]);
-        wrow[32 * c + j] = w;
-        brow[32 * c + j] = __float2bfloat16_rn(w);
+    } else {
+#pragma unroll 1
+      for (int pp = 0; pp < 8; ++pp) {
+        if (!row_ok(pp)) continue;
+        const int row = 4 * pp + rr0;
+        for (int e = 0; e < 4; ++e) {
+          const int u = 32 * c + cc + e;
+          if (u >= nu) break;
+          float* wp = wbase + (int64_t)row * p.fout + u;
+          const float w = fmaf(nlr, T[row * 36 + cc + e], *wp);
+          *wp = w;
+          bbase[(int64_t)row * p.ldw + u] = __float2bfloat16_rn(w);
+        }
       }
     }
+    __syncwarp();
     if (has_next) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+      for (int pp = 0; pp < 8; ++pp) cur[pp] = nxt[pp];
     }
   }
   ring_free(R, 256);

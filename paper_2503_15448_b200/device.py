@@ -805,6 +805,39 @@ def align_shared(wc_ptrs, wg: torch.Tensor, wgp: torch.Tensor | None, M: int, mo
     return out[:n]
 
 
+def cosine_shared(wc_ptrs, wg: torch.Tensor, wgp: torch.Tensor, M: int, rt: Runtime | None = None) -> torch.Tensor:
+    """K6c (opt-in delta_cosine): fixed-point cosine scores [n] int64 of rows
+    (device pointers) against one shared (w_g, w_g_prev)."""
+    rt = rt or Runtime.get()
+    n = len(wc_ptrs)
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if n == 0:
+        return out[:0]
+    d = rt.h2d(np.asarray(wc_ptrs, dtype=np.uint64).view(np.int64))
+    ws = rt.scratch("cosine", rt.lib.fs_cosine_align_workspace_bytes(n))
+    with rt.timed("align", float(wg.element_size()) * M * (n + 2)):
+        rt.call(rt.lib.fs_cosine_align(d.data_ptr(), 0, 0, wg.data_ptr(), wgp.data_ptr(), n, M, wg.element_size(),
+                                       out.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream), "fs_cosine_align")
+    return out[:n]
+
+
+def cosine_rows(w_c: torch.Tensor, wg: torch.Tensor, wgp: torch.Tensor, M: int, rt: Runtime | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """K6c for every row of a trainer output block (base + i * stride)."""
+    rt = rt or Runtime.get()
+    n = w_c.shape[0]
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=rt.device)
+    if n == 0:
+        return out[:0]
+    ws = rt.scratch("cosine", rt.lib.fs_cosine_align_workspace_bytes(n))
+    with rt.timed("align", float(wg.element_size()) * M * (n + 2)):
+        rt.call(rt.lib.fs_cosine_align(None, w_c.data_ptr(), w_c.stride(0) * w_c.element_size(), wg.data_ptr(),
+                                       wgp.data_ptr(), n, M, wg.element_size(), out.data_ptr(), ws.data_ptr(),
+                                       ws.numel(), rt.stream), "fs_cosine_align")
+    return out[:n]
+
+
 # --------------------------------------------------------------- FedAvg
 _N_KEYS = 4
 

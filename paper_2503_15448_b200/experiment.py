@@ -89,7 +89,8 @@ def build_world(config: ExperimentConfig, workers: int = 1, precision: str = "fp
         spec=ModelSpec(input_dim=ds.dim, hidden_dims=tuple(cfg["model"]["hidden_dims"]),
                        dropout_rate=cfg["model"]["dropout_rate"]),
         clients=clients, test_features=ds.features[test_idx], test_labels=ds.labels[test_idx],
-        policy=SelectionPolicy(theta=theta, mode=cfg["selection_mode"]), mode=config.mode,
+        policy=SelectionPolicy(theta=theta, mode=cfg["selection_mode"], top_k=cfg["extensions"]["top_k"]),
+        mode=config.mode,
         epochs=cfg["epochs"], rounds=cfg["rounds"], base_lr=cfg["lr"], lr_decay=cfg["lr_decay"],
         agg_cost_per_update_s=cfg["aggregation"]["cost_per_update_s"], k_min=cfg["aggregation"]["k_min"],
         buffer_timeout_s=cfg["aggregation"]["timeout_s"], master_seed=seed, dropout_rate=cfg["dropout_rate"],

@@ -1,0 +1,123 @@
+"""North-star opt-in extensions (off by default; never on the parity path):
+delta_cosine relevance (K6c), top-k selection, staleness-weighted async
+FedAvg and the Adam local optimizer. Each is checked against a plain
+float64 numpy / oracle restatement of the same definition."""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+COS = 1 << 40
+
+
+def _np_cos(wc, wg, wp):
+    a, b = wc - wg, wg - wp
+    na, nb = a @ a, b @ b
+    return 0.0 if na == 0 or nb == 0 else float(np.clip((a @ b) / np.sqrt(na * nb), -1, 1))
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("M", [1, 37, 52225, 3193857])
+def test_cosine_scores_match_numpy(dtype, M):
+    from paper_2503_15448_b200 import device as D
+
+    rt = D.Runtime.get()
+    g = np.random.default_rng(M)
+    n = 5
+    wg = g.normal(size=M)
+    wp = wg - 0.01 * g.normal(size=M)
+    wc = np.stack([wg + 0.01 * (g.normal(size=M) + k * (wg - wp) * 50) for k in range(n)])
+    wc[0] = wg  # zero update: score 0
+    tg = torch.tensor(wg, dtype=dtype, device="cuda")
+    tp = torch.tensor(wp, dtype=dtype, device="cuda")
+    tc = torch.tensor(wc, dtype=dtype, device="cuda")
+    got = D.cosine_rows(tc, tg, tp, M, rt).cpu().numpy() / COS
+    cast = (lambda v: v.astype(np.float32).astype(np.float64)) if dtype == torch.float32 else (lambda v: v)
+    want = np.array([_np_cos(cast(wc[k]), cast(wg), cast(wp)) for k in range(n)])
+    assert got[0] == 0.0
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-11)
+    ptrs = [tc[k].data_ptr() for k in range(n)]
+    np.testing.assert_array_equal(D.cosine_shared(ptrs, tg, tp, M, rt).cpu().numpy() / COS, got)
+
+
+def test_calculate_relevance_delta_cosine_and_policy():
+    from paper_2503_15448_b200.model import ParamVector
+    from paper_2503_15448_b200.selection import SelectionPolicy, calculate_relevance, filter_update
+
+    g = np.random.default_rng(3)
+    wg = g.normal(size=1000)
+    wp = wg - 0.1 * g.normal(size=1000)
+    wc = wg + (wg - wp) * 0.5 + 0.01 * g.normal(size=1000)
+    sc = calculate_relevance(ParamVector(wc, "d"), ParamVector(wg, "d"), ParamVector(wp, "d"), "delta_cosine")
+    assert sc.total == COS and abs(sc.ratio - _np_cos(wc, wg, wp)) < 1e-11
+    pol = SelectionPolicy(theta=-0.5, mode="delta_cosine", top_k=3)
+    ok, _ = filter_update(type("U", (), {"params": ParamVector(wc, "d")})(), ParamVector(wg, "d"),
+                          ParamVector(wp, "d"), pol)
+    assert ok
+    with pytest.raises(ValueError):
+        SelectionPolicy(theta=-0.5, mode="delta_sign")
+    with pytest.raises(ValueError):
+        SelectionPolicy(theta=0.5, mode="delta_sign", top_k=0)
+    with pytest.raises(ValueError):
+        calculate_relevance(ParamVector(wc, "d"), ParamVector(wg, "d"), None, "delta_cosine")
+
+
+def _cfg(**kw):
+    cfg = {"num_clients": 24, "rounds": 3, "epochs": 1, "seed": 6, "dataset": {"n": 6000, "d": 42},
+           "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}, "selection_mode": "delta_sign",
+           "batch": {"policy": "dynamic"},
+           "profiles": {"capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
+                        "speed": {"distribution": "loguniform", "low": 20.0, "high": 200.0},
+                        "up_latency": {"distribution": "constant", "value": 1.0},
+                        "down_latency": {"distribution": "constant", "value": 1.0}}}
+    cfg.update(kw)
+    return cfg
+
+
+@pytest.mark.parametrize("sel,theta,top_k", [("delta_cosine", 0.0, None), ("delta_cosine", -1.0, 5),
+                                             ("delta_sign", 0.5, 4)])
+def test_sync_engine_extensions_match_oracle(sel, theta, top_k):
+    """fp64 engine (fast batched sync path) vs the oracle restatement of the
+    same opt-in rules: identical accept decisions per round, relevances
+    within 1e-11 (cosine: float64 sums in a different order), same model."""
+    from oracle.fl_oracle import OracleFederation
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    cfg = _cfg(selection_mode=sel, theta=theta, extensions={"top_k": top_k})
+    world, init = build_world(ExperimentConfig.from_dict(cfg))
+    eng = FederationEngine(world)
+    st = eng.run(init)
+    sim = OracleFederation(world)
+    wg = sim.run(init.values)
+    mine = [r for r in eng.timeline.log if r["kind"] == "train_done"]
+    theirs = [r for r in sim.clock.log if r["kind"] == "train_done"] if hasattr(sim.clock, "log") else None
+    acc_m = [(r["round"], r["client_id"], r["accepted"]) for r in mine]
+    rel_m = np.array([r["relevance"] if r["relevance"] is not None else np.nan for r in mine])
+    ids = [(c, cid, a) for (c, cid, a) in sim.aligned_log]
+    assert [r.accepted for r in eng.reports] == [r["accepted"] for r in sim.reports]
+    if top_k is not None:
+        assert all(r.accepted <= top_k for r in eng.reports[1:])
+    if theirs is not None:
+        assert acc_m == [(r["round"], r["client_id"], r["accepted"]) for r in theirs]
+        rel_t = np.array([r["relevance"] if r["relevance"] is not None else np.nan for r in theirs])
+        np.testing.assert_allclose(rel_m, rel_t, rtol=0, atol=1e-11)
+    assert len(ids) == int(np.isfinite(rel_m).sum())
+    err = np.max(np.abs(st.w_g.values - wg) / np.maximum(np.abs(wg), 1.0))
+    assert err < 1e-12, err
+
+
+def test_async_engine_rejects_sync_only_extensions():
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    world, init = build_world(ExperimentConfig.from_dict(_cfg(mode="async_filtered", selection_mode="delta_cosine",
+                                                               theta=0.0)))
+    with pytest.raises(NotImplementedError):
+        FederationEngine(world).run(init)
