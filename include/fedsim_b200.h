@@ -287,6 +287,13 @@ int fs_sign_align_rows(uint64_t base, int64_t stride_bytes, const void* wg, cons
  * max_k <= 1024; sorted_scratch holds job_off[n_jobs] pointers).         */
 int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k, int64_t M,
                       int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out, void* stream);
+/* Weighted jobs (opt-in staleness-weighted FedAvg, an extension; the
+ * reference's mean is unweighted, server.py:587-593): job j's output is
+ * sum_i w_i x_i / sum_i w_i over its rows in canonical byte order; weights
+ * [job_off[n_jobs]] float64 in job order, sorted_w the same size scratch.   */
+int fs_aggregate_jobs_weighted(const uint64_t* rows, const double* weights, const int64_t* job_off, int32_t n_jobs,
+                               int32_t max_k, int64_t M, int32_t dtype_bytes, uint64_t* sorted_scratch,
+                               double* sorted_w, const uint64_t* job_out, void* stream);
 
 /* filter_update on the device for a synchronous round (selection.py:77-85):
  * accepted rows (aligned[i] / den >= theta, den = M for the sign counts or
@@ -426,6 +433,9 @@ typedef struct {
   const void* w0;                /* version 0 (caller-owned, device) */
   const void* w0_prev;           /* w_g_prev at start (caller-owned; NULL = none) */
   void* stream;
+  /* opt-in extension (< 0 = off, the reference's unweighted mean): flush
+   * means weighted by (1 + staleness) ** -staleness_alpha                  */
+  double staleness_alpha;
 } fs_async_device;
 
 fs_async_engine* fs_async_create(const fs_async_world* world);

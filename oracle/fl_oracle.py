@@ -181,11 +181,21 @@ def top_k_keep(outs, k):
         outs[i]["accepted"] = False
 
 
-def fedavg(vectors):  # server.py:72-86
+def fedavg(vectors, weights=None):  # server.py:72-86
     if not vectors:
         return None
     ranked = sorted(range(len(vectors)), key=lambda i: vectors[i].tobytes())
-    return np.stack([vectors[i] for i in ranked]).mean(axis=0)
+    if weights is None:
+        return np.stack([vectors[i] for i in ranked]).mean(axis=0)
+    # extension (not in the reference): weighted mean in the same canonical
+    # order, sum_i w_i x_i / sum_i w_i, sequential float64, product and sum
+    # rounded separately (the kernel's __dmul_rn / __dadd_rn chain)
+    acc = np.full(len(vectors[0]), -0.0)
+    den = -0.0
+    for i in ranked:
+        acc = acc + weights[i] * vectors[i]
+        den += weights[i]
+    return acc / den
 
 
 # ------------------------------------------------------------------ metrics
@@ -481,7 +491,9 @@ class OracleFederation:
             if kind == "aggregate":
                 batch = p.pop("batch")
                 stale = [g["aggs"] - f for _, f in batch]
-                mean = fedavg([u["res"]["params"] for u, _ in batch])
+                alpha = getattr(w, "staleness_alpha", None)
+                wts = None if alpha is None else [(1.0 + s) ** -alpha for s in stale]
+                mean = fedavg([u["res"]["params"] for u, _ in batch], wts)
                 g["wgp"] = g["wg"]
                 if mean is not None:
                     g["wg"] = mean

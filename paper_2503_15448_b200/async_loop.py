@@ -69,7 +69,7 @@ class AsyncDevice(ctypes.Structure):
                 ("dropout_rate", _f64), ("align_mode", _i32), ("theta", _f64), ("master_seed", ctypes.c_uint64),
                 ("base_lr", _f64), ("lr_decay", _f64), ("grid", _i32), ("features", _vp), ("labels", _vp),
                 ("row_off_host", _vp), ("n_rows_host", _vp), ("batch_host", _vp), ("w0", _vp), ("w0_prev", _vp),
-                ("stream", _vp)]
+                ("stream", _vp), ("staleness_alpha", _f64)]
 
 
 class AsyncLogView(ctypes.Structure):

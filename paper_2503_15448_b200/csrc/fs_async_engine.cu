@@ -92,7 +92,7 @@ struct fs_async_engine {
   int32_t phase = 0;  // 0 = first run with horizon, 1 = after the horizon/cycle-cap run_end
   // ---- outputs since the last yield
   std::vector<int32_t> ev_id, ev_ci, ev_cycle, ev_version;
-  std::vector<int32_t> job_version, job_member;
+  std::vector<int32_t> job_version, job_member, job_stale;
   std::vector<int64_t> job_off{0};
   std::vector<int64_t> rep_i;
   std::vector<double> rep_d;
@@ -215,7 +215,10 @@ struct fs_async_engine {
           window_stale.push_back(agg_count - m.second);
         }
         // job: version agg_count+1 = mean of the batch's updates (server.py:590-594)
-        for (const auto& m : batch) job_member.push_back(m.first);
+        for (const auto& m : batch) {
+          job_member.push_back(m.first);
+          job_stale.push_back(agg_count - m.second);
+        }
         job_version.push_back(agg_count + 1);
         job_off.push_back((int64_t)job_member.size());
         agg_count += 1;
@@ -246,7 +249,7 @@ struct fs_async_engine {
 
   void clear_outputs() {
     ev_id.clear(); ev_ci.clear(); ev_cycle.clear(); ev_version.clear();
-    job_version.clear(); job_member.clear(); job_off.assign(1, 0);
+    job_version.clear(); job_member.clear(); job_stale.clear(); job_off.assign(1, 0);
     rep_i.clear(); rep_d.clear(); rep_off.assign(1, 0); rep_stale.clear();
   }
 
@@ -712,31 +715,45 @@ struct DeviceExec {
       }
       version.push_back({outs[j], blk});
     }
-    uint64_t p_rows, p_off, p_out;
+    // opt-in staleness weights (1 + s) ** -alpha, s = versions since the member fetched its model
+    const bool weighted = d.staleness_alpha >= 0.0;
+    std::vector<double> wts(weighted ? nrows : 0);
+    for (int64_t i = 0; i < (int64_t)wts.size(); ++i) wts[i] = std::pow(1.0 + (double)e->job_stale[i], -d.staleness_alpha);
+    const int64_t nw = weighted ? nrows : 0;
+    uint64_t p_rows, p_off, p_out, p_w = 0;
     void* tmp = nullptr;
     if (percycle) {  // no per-flush host sync in this mode: a stream-ordered temporary
-      std::vector<uint64_t> h(nrows + nj + 1 + nj);
+      std::vector<uint64_t> h(nrows + nj + 1 + nj + nw);
       memcpy(h.data(), rows.data(), 8 * nrows);
       memcpy(h.data() + nrows, e->job_off.data(), 8 * (nj + 1));
       memcpy(h.data() + nrows + nj + 1, outs.data(), 8 * nj);
+      if (nw) memcpy(h.data() + nrows + 2 * nj + 1, wts.data(), 8 * nw);
       if (int rc = cuda(cudaMallocAsync(&tmp, 8 * h.size(), st), "jobs args")) return rc;
       if (int rc = cuda(cudaMemcpyAsync(tmp, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st), "jobs args"))
         return rc;
       p_rows = (uint64_t)tmp;
       p_off = p_rows + 8 * nrows;
       p_out = p_off + 8 * (nj + 1);
+      p_w = p_out + 8 * nj;
     } else {
-      if (int rc = stage_reserve(16 * (size_t)(2 * nrows + 2 * nj + 8))) return rc;
+      if (int rc = stage_reserve(16 * (size_t)(2 * nrows + 2 * nj + 8 + nw))) return rc;
       p_rows = put(rows.data(), 8 * nrows);
       p_off = put(e->job_off.data(), 8 * (nj + 1));
       p_out = put(outs.data(), 8 * nj);
+      if (nw) p_w = put(wts.data(), 8 * nw);
       if (int rc = commit()) return rc;
     }
-    if (int rc = grow(&d_sorted, &sorted_cap, 8 * nrows, "sorted rows")) return rc;
+    if (int rc = grow(&d_sorted, &sorted_cap, (weighted ? 16 : 8) * nrows, "sorted rows")) return rc;
     launches += 1;
-    if (int rc = fs_aggregate_jobs((const uint64_t*)p_rows, (const int64_t*)p_off, nj, max_k, M, (int32_t)esz,
-                                   (uint64_t*)d_sorted, (const uint64_t*)p_out, st))
+    if (weighted) {
+      if (int rc = fs_aggregate_jobs_weighted((const uint64_t*)p_rows, (const double*)p_w, (const int64_t*)p_off, nj,
+                                              max_k, M, (int32_t)esz, (uint64_t*)d_sorted,
+                                              (double*)d_sorted + nrows, (const uint64_t*)p_out, st))
+        return rc;
+    } else if (int rc = fs_aggregate_jobs((const uint64_t*)p_rows, (const int64_t*)p_off, nj, max_k, M, (int32_t)esz,
+                                          (uint64_t*)d_sorted, (const uint64_t*)p_out, st)) {
       return rc;
+    }
     if (tmp) cudaFreeAsync(tmp, st);
     for (int64_t i = 0; i < nrows; ++i) {
       if (percycle) drop_row(e->job_member[i]);
@@ -744,6 +761,7 @@ struct DeviceExec {
     }
     e->job_version.clear();
     e->job_member.clear();
+    e->job_stale.clear();
     e->job_off.assign(1, 0);
     return FS_OK;
   }

@@ -230,11 +230,17 @@ __device__ bool row_less(const uint64_t* keys, const uint64_t* rows, int a, int 
 template <class T>
 __global__ void __launch_bounds__(SORT_MAX) canonical_order_kernel(const uint64_t* rows, int k, int64_t M,
                                                                    uint64_t* sorted_rows,
-                                                                   const int64_t* job_off = nullptr) {
+                                                                   const int64_t* job_off = nullptr,
+                                                                   const double* w_in = nullptr,
+                                                                   double* w_sorted = nullptr) {
   if (job_off) {  // one CTA per aggregation job: rows[job_off[j], job_off[j+1])
     const int64_t o = job_off[blockIdx.x];
     rows += o;
     sorted_rows += o;
+    if (w_in) {
+      w_in += o;
+      w_sorted += o;
+    }
     k = (int)(job_off[blockIdx.x + 1] - o);
   }
   __shared__ uint64_t keys[SORT_MAX * SORT_KEYS];
@@ -272,7 +278,10 @@ __global__ void __launch_bounds__(SORT_MAX) canonical_order_kernel(const uint64_
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < k; i += blockDim.x) sorted_rows[i] = rows[idx[i]];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    sorted_rows[i] = rows[idx[i]];
+    if (w_in) w_sorted[i] = w_in[idx[i]];  // per-row weights follow their rows
+  }
 }
 
 // ---------------------------------------------------------------- K7
@@ -307,9 +316,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <class T>
-__device__ __forceinline__ double ordered_column_sum(const T* const* rows, int k, int64_t j) {
+__device__ __forceinline__ double ordered_column_sum(const T* const* rows, int k, int64_t j,
+                                                     const double* w = nullptr) {
   double acc = -0.0;
-  for (int i = 0; i < k; ++i) acc += (double)__ldcs(rows[i] + j);
+  if (w)  // product and sum rounded separately (no contraction): the oracle's restatement is exact
+    for (int i = 0; i < k; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], (double)__ldcs(rows[i] + j)));
+  else
+    for (int i = 0; i < k; ++i) acc += (double)__ldcs(rows[i] + j);
   return acc;
 }
 
@@ -319,10 +332,11 @@ __device__ __forceinline__ double ordered_column_sum(const T* const* rows, int k
 template <class T, bool MEAN, class OUT>
 __global__ void __launch_bounds__(AGG_THREADS)
     ordered_rows_kernel(const uint64_t* rows, int k, int64_t M, OUT* out, const int64_t* job_off = nullptr,
-                        const uint64_t* job_out = nullptr) {
+                        const uint64_t* job_out = nullptr, const double* wts = nullptr) {
   if (job_off) {  // blockIdx.y = aggregation job: rows[job_off[j], job_off[j+1]) -> job_out[j]
     const int64_t o = job_off[blockIdx.y];
     rows += o;
+    if (wts) wts += o;
     k = (int)(job_off[blockIdx.y + 1] - o);
     out = reinterpret_cast<OUT*>(job_out[blockIdx.y]);
   }
@@ -332,25 +346,34 @@ __global__ void __launch_bounds__(AGG_THREADS)
   uint8_t* ring = agg_smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(agg_smem + AGG_RING);
   const T** sh_rows = reinterpret_cast<const T**>(full + AGG_STAGES);
+  double* sh_w = reinterpret_cast<double*>(sh_rows + k);  // weighted jobs: w[k], then their ordered sum
   const int tid = threadIdx.x;
   uint64_t mis = 0;
   for (int i = tid; i < k; i += AGG_THREADS) {
     sh_rows[i] = reinterpret_cast<const T*>(rows[i]);
     mis |= rows[i] & 15;
+    if (wts) sh_w[i] = wts[i];
   }
   if (tid == 0) {
     for (int s = 0; s < AGG_STAGES; ++s) tc::mbar_init(&full[s], 1);
     tc::fence_mbar_init();
   }
   const bool vec_ok = !__syncthreads_or(mis != 0);
+  double den = (double)k;
+  if (wts) {  // weighted mean (staleness-weighted FedAvg, opt-in): sum w_i x_i / sum w_i, both in row order
+    den = -0.0;
+    for (int i = 0; i < k; ++i) den += sh_w[i];
+  }
+  const double* wrow = wts ? sh_w : nullptr;
   const int64_t col0 = (int64_t)blockIdx.x * STRIP_COLS;
   const int64_t ncols = min(STRIP_COLS, M - col0);
   auto emit = [&](int64_t j, double s) {
-    if (MEAN) out[j] = (OUT)(s / (double)k);
+    if (MEAN) out[j] = (OUT)(s / den);
     else out[j] = (OUT)(s + 0.0);  // an all -0.0 column sums to +0.0
   };
   if (!vec_ok || ncols != STRIP_COLS) {
-    for (int64_t c = tid; c < ncols; c += AGG_THREADS) emit(col0 + c, ordered_column_sum<T>(sh_rows, k, col0 + c));
+    for (int64_t c = tid; c < ncols; c += AGG_THREADS)
+      emit(col0 + c, ordered_column_sum<T>(sh_rows, k, col0 + c, wrow));
     return;
   }
   const int nb = (k + AGG_ROWS - 1) / AGG_ROWS;
@@ -375,10 +398,19 @@ __global__ void __launch_bounds__(AGG_THREADS)
       tc::mbar_wait(&full[s], (uint32_t)((b / AGG_STAGES) & 1));
       const int nr = min(AGG_ROWS, k - b * AGG_ROWS);
       const T* st = reinterpret_cast<const T*>(ring + s * AGG_ROWS * AGG_STRIP) + tid * CPT;
-      for (int r = 0; r < nr; ++r) {
-        const T* e = st + r * STRIP_COLS;
+      if (wrow) {
+        for (int r = 0; r < nr; ++r) {
+          const T* e = st + r * STRIP_COLS;
+          const double w = wrow[b * AGG_ROWS + r];
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) acc[c] += (double)e[c];
+          for (int c = 0; c < CPT; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w, (double)e[c]));
+        }
+      } else {
+        for (int r = 0; r < nr; ++r) {
+          const T* e = st + r * STRIP_COLS;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) acc[c] += (double)e[c];
+        }
       }
       __syncthreads();  // stage s fully read
       if (tid < 32 && b + AGG_STAGES < nb) {
@@ -401,7 +433,7 @@ static int launch_ordered_rows(const uint64_t* rows, int k, int64_t M, OUT* out,
   auto kern = ordered_rows_kernel<T, MEAN, OUT>;
   ensure_smem(kern, (int)smem);
   const int64_t strips = (M * (int64_t)sizeof(T) + AGG_STRIP - 1) / AGG_STRIP;
-  kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out, nullptr, nullptr);
+  kern<<<(unsigned)strips, AGG_THREADS, smem, st>>>(rows, k, M, out, nullptr, nullptr, nullptr);
   return check_launch(what);
 }
 
@@ -647,11 +679,11 @@ extern "C" int fs_canonical_order(const uint64_t* rows, int32_t k, int64_t M, in
 // rows rows[job_off[j] .. job_off[j+1]) in canonical byte order into
 // job_out[j]. K9 orders every job's rows (one CTA per job) into
 // sorted_scratch, then K7 runs with one grid row per job.
-extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k,
-                                 int64_t M, int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out,
-                                 void* stream) {
+static int aggregate_jobs_impl(const uint64_t* rows, const double* weights, const int64_t* job_off, int32_t n_jobs,
+                               int32_t max_k, int64_t M, int32_t dtype_bytes, uint64_t* sorted_scratch,
+                               double* sorted_w, const uint64_t* job_out, void* stream) {
   if (n_jobs < 0 || max_k < 1 || max_k > SORT_MAX || M < 1 || (dtype_bytes != 4 && dtype_bytes != 8) ||
-      n_jobs > 65535) {
+      n_jobs > 65535 || (weights && !sorted_w)) {
     set_error("fs_aggregate_jobs: need 0 <= n_jobs <= 65535 jobs of 1..%d rows, M >= 1", SORT_MAX);
     return FS_EINVAL;
   }
@@ -661,24 +693,53 @@ extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, i
   while (threads < max_k && threads < SORT_MAX) threads <<= 1;
   const int esz = dtype_bytes;
   if (esz == 8)
-    canonical_order_kernel<double><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+    canonical_order_kernel<double><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off, weights, sorted_w);
   else
-    canonical_order_kernel<float><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+    canonical_order_kernel<float><<<n_jobs, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off, weights, sorted_w);
   int rc = check_launch("canonical_order_kernel (jobs)");
   if (rc != FS_OK) return rc;
-  const size_t smem = AGG_RING + AGG_STAGES * sizeof(uint64_t) + (size_t)max_k * sizeof(void*);
+  const size_t smem = AGG_RING + AGG_STAGES * sizeof(uint64_t) + (size_t)max_k * (sizeof(void*) + sizeof(double));
   const int64_t strips = (M * (int64_t)esz + AGG_STRIP - 1) / AGG_STRIP;
   const dim3 grid((unsigned)strips, (unsigned)n_jobs);
+  const double* w = weights ? sorted_w : nullptr;
   if (esz == 8) {
     auto kern = ordered_rows_kernel<double, true, double>;
     ensure_smem(kern, (int)smem);
-    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
+    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out, w);
   } else {
     auto kern = ordered_rows_kernel<float, true, float>;
     ensure_smem(kern, (int)smem);
-    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out);
+    kern<<<grid, AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out, w);
   }
   return check_launch("ordered_rows_kernel (jobs)");
+}
+
+// Many independent FedAvg means in one launch pair (the aggregations an
+// asynchronous run queues between two training flushes): job j averages the
+// rows rows[job_off[j] .. job_off[j+1]) in canonical byte order into
+// job_out[j]. K9 orders every job's rows (one CTA per job) into
+// sorted_scratch, then K7 runs with one grid row per job.
+extern "C" int fs_aggregate_jobs(const uint64_t* rows, const int64_t* job_off, int32_t n_jobs, int32_t max_k,
+                                 int64_t M, int32_t dtype_bytes, uint64_t* sorted_scratch, const uint64_t* job_out,
+                                 void* stream) {
+  return aggregate_jobs_impl(rows, nullptr, job_off, n_jobs, max_k, M, dtype_bytes, sorted_scratch, nullptr,
+                             job_out, stream);
+}
+
+// Weighted variant (opt-in staleness-weighted FedAvg): job j's output is
+// sum_i w_i x_i / sum_i w_i over its rows in canonical byte order (weights
+// follow their rows through the ordering; float64 products and sums, each
+// rounded, then the ordered weight sum). sorted_w holds job_off[n_jobs] doubles of scratch.
+extern "C" int fs_aggregate_jobs_weighted(const uint64_t* rows, const double* weights, const int64_t* job_off,
+                                          int32_t n_jobs, int32_t max_k, int64_t M, int32_t dtype_bytes,
+                                          uint64_t* sorted_scratch, double* sorted_w, const uint64_t* job_out,
+                                          void* stream) {
+  if (!weights) {
+    set_error("fs_aggregate_jobs_weighted: weights required");
+    return FS_EINVAL;
+  }
+  return aggregate_jobs_impl(rows, weights, job_off, n_jobs, max_k, M, dtype_bytes, sorted_scratch, sorted_w,
+                             job_out, stream);
 }
 
 // ---------------------------------------------------------------- selection on device
@@ -696,7 +757,7 @@ __global__ void __launch_bounds__(1024) select_rows_kernel(const int64_t* aligne
   __shared__ int carry;
   extern __shared__ int64_t s_score[];  // [n] when top_k > 0
   if (threadIdx.x == 0) carry = 0;
-  if (top_k > 0)
+  if (top_k > 0 && scored)
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_score[i] = aligned[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -741,7 +802,7 @@ extern "C" int fs_select_rows(const int64_t* aligned, int32_t n, int64_t den, do
     set_error("fs_select_rows: invalid arguments");
     return FS_EINVAL;
   }
-  const size_t smem = top_k > 0 ? (size_t)n * sizeof(int64_t) : 0;
+  const size_t smem = top_k > 0 && scored ? (size_t)n * sizeof(int64_t) : 0;
   if (smem > 48 * 1024) ensure_smem(select_rows_kernel, (int)smem);
   select_rows_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(aligned, n, den, theta, scored, top_k, base,
                                                               stride_bytes, rows_out, job_off, job_out, out);

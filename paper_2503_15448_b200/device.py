@@ -945,6 +945,26 @@ def aggregate_rows(rows: list[torch.Tensor], M: int, rt: Runtime | None = None) 
     return aggregate_ptrs(ptrs, M, rows[0].dtype, rt, row_of=lambda i: rows[i])
 
 
+def aggregate_rows_weighted(rows: list[torch.Tensor], weights, M: int, rt: Runtime | None = None) -> torch.Tensor:
+    """Extension: sum_i w_i x_i / sum_i w_i of k device rows in canonical byte
+    order (one fs_aggregate_jobs_weighted job)."""
+    rt = rt or Runtime.get()
+    k = len(rows)
+    dt = rows[0].dtype
+    esz = rows[0].element_size()
+    out = torch.empty(M, dtype=dt, device=rt.device)
+    meta = np.concatenate([np.array([r.data_ptr() for r in rows], dtype=np.uint64),
+                           np.array([0, k], dtype=np.uint64), np.array([out.data_ptr()], dtype=np.uint64)])
+    d = rt.h2d(meta.view(np.int64))
+    w = rt.h2d(np.asarray(weights, dtype=np.float64))
+    scratch = rt.scratch("agg_weighted", 16 * k)
+    p = d.data_ptr()
+    rt.call(rt.lib.fs_aggregate_jobs_weighted(p, w.data_ptr(), p + 8 * k, 1, k, M, esz, scratch.data_ptr(),
+                                              scratch.data_ptr() + 8 * k, p + 8 * (k + 2), rt.stream),
+            "fs_aggregate_jobs_weighted")
+    return out
+
+
 # --------------------------------------------------------------- eval
 def forward_probs(spec_dims, w: torch.Tensor, x: torch.Tensor, dense_masks: torch.Tensor | None = None,
                   rt: Runtime | None = None) -> torch.Tensor:

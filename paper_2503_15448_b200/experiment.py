@@ -99,6 +99,8 @@ def build_world(config: ExperimentConfig, workers: int = 1, precision: str = "fp
         checkpointing=ck["enabled"], recovery_s=ck["recovery_s"], step_overhead_s=cfg["step_overhead_s"],
         workers=workers, horizon_s=cfg["async_run"]["horizon_s"], cycle_cap=cfg["async_run"]["cycle_cap"],
         precision=precision,
+        staleness_alpha=cfg["extensions"]["staleness_alpha"], optimizer=cfg["extensions"]["optimizer"],
+        adam=(cfg["extensions"]["adam"]["beta1"], cfg["extensions"]["adam"]["beta2"], cfg["extensions"]["adam"]["eps"]),
     )
     return world, init_params(world.spec, derive_seed(seed, "model-init"))
 
