@@ -172,7 +172,19 @@ typedef struct fs_train_desc {
    * (prepared ahead on another stream), so no memset precedes the launch   */
   const void* w_start_all;
   int32_t counter_zeroed;
+  /* opt-in local optimizer (an extension; the reference is plain SGD,
+   * model.py:215-221): FS_OPT_SGD, or FS_OPT_ADAM with moments m, v in
+   * opt_state [n_req x 2 x ldw] of the parameter dtype (m at r*2*ldw, v at
+   * r*2*ldw + ldw), zeroed at each request's start; step t = global step + 1,
+   * p -= lr * m_hat / (sqrt(v_hat) + eps). fp64 trainer and the wide bf16
+   * trainer (fs_train_bf16 routes Adam requests there).                     */
+  int32_t optimizer;
+  double adam_beta1, adam_beta2, adam_eps;
+  void* opt_state;
 } fs_train_desc;
+
+#define FS_OPT_SGD 0
+#define FS_OPT_ADAM 1
 
 typedef struct {
   int64_t aligned;

@@ -120,8 +120,12 @@ def keep_masks(hidden, rate, rows, seed):  # model.py:153-166
 # client.py:98-172 (+ model.loss_and_grad / sgd_step, model.py:189-221)
 
 
-def local_sgd(dims, rate, w0, X, Y, epochs, bsz, lr_of_epoch, seed, stop=None, resume=None):
-    """Returns dict(params, steps, epoch, batch, samples, stopped)."""
+def local_sgd(dims, rate, w0, X, Y, epochs, bsz, lr_of_epoch, seed, stop=None, resume=None, adam=None):
+    """Returns dict(params, steps, epoch, batch, samples, stopped).
+
+    adam = (beta1, beta2, eps) selects the framework's opt-in Adam (not in
+    the reference): moments from zero, t = step + 1,
+    p -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)."""
     n = X.shape[0]
     hidden = dims[1:-1]
     theta = w0 if resume is None else resume["params"]
@@ -130,6 +134,9 @@ def local_sgd(dims, rate, w0, X, Y, epochs, bsz, lr_of_epoch, seed, stop=None, r
     e0 = 0 if resume is None else resume["epoch"]
     b0 = 0 if resume is None else resume["batch"]
     per_epoch = math.ceil(n / bsz)
+    if adam is not None:
+        b1, b2, eps = adam
+        m1, m2 = np.zeros_like(theta), np.zeros_like(theta)
     for e in range(e0, epochs):
         order = sub_rng(seed, "shuffle", e).permutation(n)
         lr = lr_of_epoch(e)
@@ -143,7 +150,13 @@ def local_sgd(dims, rate, w0, X, Y, epochs, bsz, lr_of_epoch, seed, stop=None, r
             loss, g = bce_grad(theta, dims, xb, yb, masks)
             if not np.isfinite(loss):
                 raise FloatingPointError("loss became non-finite")
-            theta = theta - lr * g
+            if adam is None:
+                theta = theta - lr * g
+            else:
+                t = e * per_epoch + s + 1
+                m1 = b1 * m1 + (1.0 - b1) * g
+                m2 = b2 * m2 + (1.0 - b2) * g * g
+                theta = theta - lr * (m1 * (1.0 / (1.0 - b1 ** t))) / (np.sqrt(m2 * (1.0 / (1.0 - b2 ** t))) + eps)
             steps += 1
             samples += len(pick)
     if stop is not None and steps >= stop:
@@ -294,7 +307,8 @@ class OracleFederation:
 
         def train(**kw):
             return local_sgd(dims, rate, wg, wc.features, wc.labels, w.epochs, wc.batch_size,
-                             lambda e: lr, seed, **kw)
+                             lambda e: lr, seed, adam=(tuple(w.adam) if getattr(w, "optimizer", "sgd") == "adam"
+                                                       else None), **kw)
 
         captures, redo, recovered = [], 0.0, False
         if not failed:

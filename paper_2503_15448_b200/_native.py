@@ -25,6 +25,9 @@ FS_MASK_NONE = 0
 FS_MASK_BITS = 1
 FS_MASK_DENSE = 2
 
+FS_OPT_SGD = 0
+FS_OPT_ADAM = 1
+
 FS_ALIGN_WEIGHT_SIGN = 0
 FS_ALIGN_DELTA_SIGN = 1
 FS_COSINE_SCALE = 1 << 40  # fixed-point denominator of delta_cosine scores
@@ -83,6 +86,11 @@ class TrainDesc(ctypes.Structure):
         ("align_counts", _c_vp),
         ("w_start_all", _c_vp),
         ("counter_zeroed", _c_i32),
+        ("optimizer", _c_i32),
+        ("adam_beta1", _c_f64),
+        ("adam_beta2", _c_f64),
+        ("adam_eps", _c_f64),
+        ("opt_state", _c_vp),
     ]
 
 

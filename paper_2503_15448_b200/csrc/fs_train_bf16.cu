@@ -916,6 +916,8 @@ extern "C" int fs_forward_bf16(const int32_t* dims, int32_t n_dims, const float*
 extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
   Geo g;
   if (!d || d->n_req < 1) return 0;
+  if (d->optimizer == FS_OPT_ADAM)  // the opt-in Adam runs on the wide (lockstep) trainer for every shape
+    return fs_bf16_supported(d->dims, d->n_dims) ? wide_workspace_bytes(d) : 0;
   if (make_geo(d->dims, d->n_dims, &g) != FS_OK) return fs_bf16_supported(d->dims, d->n_dims) == 2 ? wide_workspace_bytes(d) : 0;
   const int grid = d->grid > 0 ? d->grid : kNumSMs;
   const int gg = grid < d->n_req ? grid : d->n_req;
@@ -925,7 +927,8 @@ extern "C" size_t fs_train_bf16_workspace_bytes(const fs_train_desc* d) {
 extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, const float* labels_f32,
                              void* stream) {
   Geo g;
-  if (d && make_geo(d->dims, d->n_dims, &g) != FS_OK && fs_bf16_supported(d->dims, d->n_dims) == 2) {
+  if (d && ((make_geo(d->dims, d->n_dims, &g) != FS_OK && fs_bf16_supported(d->dims, d->n_dims) == 2) ||
+            (d->optimizer == FS_OPT_ADAM && fs_bf16_supported(d->dims, d->n_dims)))) {
     if (!d->w_start && d->n_req > 0) {
       set_error("fs_train_bf16 (wide): w_start is NULL");
       return FS_EINVAL;

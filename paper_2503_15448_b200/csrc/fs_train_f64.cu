@@ -183,6 +183,24 @@ struct StepBufs {
 
 enum StepMode { STEP_TRAIN = 0, STEP_GRAD = 1 };
 
+// The parameter update of a training step: plain SGD p - lr*g written as the
+// reference's two roundings (model.py:215-221), or the opt-in Adam with
+// per-parameter moments m, v (same layout as W) and bias corrections
+// c1 = 1 / (1 - b1^t), c2 = 1 / (1 - b2^t) of this step.
+struct Opt {
+  int adam;
+  double b1, b2, eps, c1, c2;
+  double *m, *v;
+  __device__ __forceinline__ double apply(double w, int64_t i, double lr, double g) const {
+    if (!adam) return __dsub_rn(w, __dmul_rn(lr, g));
+    const double mi = b1 * m[i] + (1.0 - b1) * g;
+    const double vi = b2 * v[i] + (1.0 - b2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    return w - lr * (mi * c1) / (sqrt(vi * c2) + eps);
+  }
+};
+
 // Shared-memory per-step context (set up by the caller).
 struct StepShared {
   int64_t* rowidx;  // [rows] absolute feature rows (nullptr-free: identity filled)
@@ -196,7 +214,7 @@ struct StepShared {
 template <int MODE>
 __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, const double* X,
                          int rows, const StepShared& ss, const MaskView& mk, const StepBufs& bufs,
-                         GemmSmem& sm, int* status, double* loss_out) {
+                         GemmSmem& sm, int* status, double* loss_out, const Opt& opt = Opt{}) {
   const int L = lay.L;
   const int tid = threadIdx.x;
   const int d0 = lay.f[0];
@@ -283,14 +301,14 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
       if (MODE == STEP_GRAD)
         G[lay.woff[L - 1] + k] = g;
       else
-        wh_mut[k] = __dsub_rn(wh_mut[k], __dmul_rn(lr, g));
+        wh_mut[k] = opt.apply(wh_mut[k], lay.woff[L - 1] + k, lr, g);
     }
     if (tid == THREADS - 1) {
       const double gb = np_pairwise_sum(ss.dz, rows, 1);
       if (MODE == STEP_GRAD)
         G[lay.boff[L - 1]] = gb;
       else
-        W[lay.boff[L - 1]] = __dsub_rn(W[lay.boff[L - 1]], __dmul_rn(lr, gb));
+        W[lay.boff[L - 1]] = opt.apply(W[lay.boff[L - 1]], lay.boff[L - 1], lr, gb);
     }
   }
   __syncthreads();
@@ -328,8 +346,8 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
         cta_gemm<false, true>(K, N, rows, ColMajor{bufs.H[l], K}, RowMajor{Dn, N}, epi, sm);
     } else {
       auto epi = [&](int m, int n, double acc) {
-        double* p = Wl + (int64_t)m * N + n;
-        *p = __dsub_rn(*p, __dmul_rn(lr, acc));
+        const int64_t i = (int64_t)m * N + n;
+        Wl[i] = opt.apply(Wl[i], lay.woff[l] + i, lr, acc);
       };
       if (l == 0)
         cta_gemm<false, true>(K, N, rows, GatherRowsT{X, ss.rowidx, d0}, RowMajor{Dn, N}, epi, sm);
@@ -350,7 +368,7 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
       if (MODE == STEP_GRAD)
         G[lay.boff[l] + n] = gb;
       else
-        bl[n] = __dsub_rn(bl[n], __dmul_rn(lr, gb));
+        bl[n] = opt.apply(bl[n], lay.boff[l] + n, lr, gb);
     }
     __syncthreads();
   }
@@ -457,6 +475,16 @@ __global__ void __launch_bounds__(THREADS) train_kernel(TrainArgs a) {
     const double* W0 = reinterpret_cast<const double*>(d.w_start[r]);
     if (W0 != W)
       for (int64_t j = threadIdx.x; j < lay.M; j += THREADS) W[j] = W0[j];
+    Opt opt{};
+    if (d.optimizer == FS_OPT_ADAM) {  // moments start at zero for each request
+      opt.adam = 1;
+      opt.b1 = d.adam_beta1;
+      opt.b2 = d.adam_beta2;
+      opt.eps = d.adam_eps;
+      opt.m = reinterpret_cast<double*>(d.opt_state) + (int64_t)r * 2 * d.ldw;
+      opt.v = opt.m + d.ldw;
+      for (int64_t j = threadIdx.x; j < lay.M; j += THREADS) opt.m[j] = opt.v[j] = 0.0;
+    }
     __syncthreads();
 
     const int64_t slot_words = ((int64_t)B * lay.sum_hidden + 31) / 32;
@@ -482,8 +510,12 @@ __global__ void __launch_bounds__(THREADS) train_kernel(TrainArgs a) {
         acc += lay.f[l];
       }
       __syncthreads();
+      if (opt.adam) {
+        opt.c1 = 1.0 / (1.0 - pow(opt.b1, (double)(step + 1)));
+        opt.c2 = 1.0 / (1.0 - pow(opt.b2, (double)(step + 1)));
+      }
       mlp_step<STEP_TRAIN>(lay, W, nullptr, lr, d.features, rows, ss, mk, bufs, sm,
-                           d.status + r, nullptr);
+                           d.status + r, nullptr, opt);
     }
     __syncthreads();
   }
@@ -604,6 +636,11 @@ extern "C" int fs_train_f64(const fs_train_desc* d, void* stream) {
   }
   if (d->mask_mode != FS_MASK_NONE && d->mask_mode != FS_MASK_BITS) {
     set_error("fs_train_f64: mask_mode must be NONE or BITS");
+    return FS_EINVAL;
+  }
+  if ((d->optimizer != FS_OPT_SGD && d->optimizer != FS_OPT_ADAM) ||
+      (d->optimizer == FS_OPT_ADAM && (!d->opt_state || d->adam_eps <= 0.0))) {
+    set_error("fs_train_f64: optimizer must be SGD, or ADAM with opt_state and eps > 0");
     return FS_EINVAL;
   }
   const size_t need = fs_train_workspace_bytes(d);

@@ -183,7 +183,25 @@ struct StepArgs {
   int mask_mode;
   float scale;
   int32_t* status;
+  // opt-in Adam (fs_train_desc.optimizer): moments [n_req][2][ldw] fp32
+  int adam;
+  float b1, b2, eps;
+  float* opt;
 };
+
+// SGD as the fp32 masters always did, or the opt-in Adam step of parameter
+// `idx` of request sr.req at step t = global_step + 1
+__device__ __forceinline__ float opt_apply(const StepArgs& a, const StepRow& sr, int64_t idx, float w, float g) {
+  if (!a.adam) return w - sr.lr * g;
+  float* m = a.opt + (int64_t)sr.req * 2 * a.ldw;
+  float* v = m + a.ldw;
+  const float t = (float)(sr.global_step + 1);
+  const float c1 = 1.f / (1.f - powf(a.b1, t)), c2 = 1.f / (1.f - powf(a.b2, t));
+  const float mi = a.b1 * m[idx] + (1.f - a.b1) * g, vi = a.b2 * v[idx] + (1.f - a.b2) * g * g;
+  m[idx] = mi;
+  v[idx] = vi;
+  return w - sr.lr * (mi * c1) / (sqrtf(vi * c2) + a.eps);
+}
 
 __device__ __forceinline__ uint8_t* slot_of(const StepArgs& a, int slot) {
   return a.slots + (size_t)slot * a.g.slot_bytes;
@@ -461,8 +479,13 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
       dout[(int64_t)r * ld + u] = dv;
       gb += __bfloat162float(dv);
     }
-    wh[u] = w - sr.lr * g;
-    bprev[u] -= sr.lr * gb;
+    if (a.adam) {
+      wh[u] = opt_apply(a, sr, a.lay.woff[H] + u, w, g);
+      bprev[u] = opt_apply(a, sr, a.lay.boff[H - 1] + u, bprev[u], gb);
+    } else {
+      wh[u] = w - sr.lr * g;
+      bprev[u] -= sr.lr * gb;
+    }
   }
   float t = 0.f;
   for (int r = threadIdx.x; r < rb; r += blockDim.x) t += s_dz[r];
@@ -472,7 +495,8 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int w2 = 0; w2 < 8; ++w2) s += s_red[w2];
-    bh[0] -= sr.lr * s;
+    if (a.adam) bh[0] = opt_apply(a, sr, a.lay.boff[H], bh[0], s);
+    else bh[0] -= sr.lr * s;
   }
 }
 
@@ -527,7 +551,11 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CU
     }
   }
   if (iok) {
-    if (a.g.rtiles == 1) a.w_out[(int64_t)sr.req * a.ldw + p.boff + i] -= sr.lr * gb;
+    if (a.g.rtiles == 1) {
+      float* b = a.w_out + (int64_t)sr.req * a.ldw + p.boff + i;
+      if (a.adam) *b = opt_apply(a, sr, p.boff + i, *b, gb);
+      else *b -= sr.lr * gb;
+    }
     else reinterpret_cast<float*>(sb + p.bp_off)[(int64_t)blockIdx.y * p.fin + i] = gb;
   }
   ring_free(R, cols);
@@ -541,7 +569,9 @@ __global__ void bias_reduce_kernel(StepArgs a, const StepRow* rows, int fin, int
   const float* bp = reinterpret_cast<const float*>(slot_of(a, sr.slot) + bp_off);
   float gb = 0.f;
   for (int t = 0; t < a.g.rtiles; ++t) gb += bp[(int64_t)t * fin + i];
-  a.w_out[(int64_t)sr.req * a.ldw + boff + i] -= sr.lr * gb;
+  float* b = a.w_out + (int64_t)sr.req * a.ldw + boff + i;
+  if (a.adam) *b = opt_apply(a, sr, boff + i, *b, gb);
+  else *b -= sr.lr * gb;
 }
 
 // ------------------------------------------------------------------ update
@@ -618,7 +648,7 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
   float* wbase = a.w_out + (int64_t)sr.req * a.ldw + p.woff + (int64_t)(i0 + q * 32) * p.fout + u0;
   __nv_bfloat16* bbase =
       reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.wb_off) + (int64_t)(i0 + q * 32) * p.ldw + u0;
-  const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.w_out + p.woff) & 15) == 0) &&
+  const bool vec = !a.adam && (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.w_out + p.woff) & 15) == 0) &&
                    ((a.ldw & 3) == 0) && (p.ldw % 4 == 0);
   auto row_ok = [&](int pp) { return i0 + q * 32 + 4 * pp + rr0 < p.fin; };
   auto col_ok = [&](int c) { return 32 * c + cc + 4 <= nu; };
@@ -640,7 +670,22 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
     for (int k = 0; k < 8; ++k)
       *reinterpret_cast<float4*>(T + lane * 36 + 4 * k) = make_float4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
     __syncwarp();
-    if (vec) {
+    if (a.adam) {  // opt-in Adam: moments read-modify-written beside the master (scalar path)
+#pragma unroll 1
+      for (int pp = 0; pp < 8; ++pp) {
+        if (!row_ok(pp)) continue;
+        const int row = 4 * pp + rr0;
+        for (int e = 0; e < 4; ++e) {
+          const int u = 32 * c + cc + e;
+          if (u >= nu) break;
+          const int64_t idx = p.woff + (int64_t)(i0 + q * 32 + row) * p.fout + u0 + u;
+          float* wp = wbase + (int64_t)row * p.fout + u;
+          const float w = opt_apply(a, sr, idx, *wp, T[row * 36 + cc + e]);
+          *wp = w;
+          bbase[(int64_t)row * p.ldw + u] = __float2bfloat16_rn(w);
+        }
+      }
+    } else if (vec) {
 #pragma unroll
       for (int pp = 0; pp < 8; ++pp) {
         if (!row_ok(pp)) continue;
@@ -757,6 +802,15 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
   sa.mask_mode = d->mask_mode;
   sa.scale = (float)d->scale;
   sa.status = d->status;
+  sa.adam = d->optimizer == FS_OPT_ADAM;
+  sa.b1 = (float)d->adam_beta1;
+  sa.b2 = (float)d->adam_beta2;
+  sa.eps = (float)d->adam_eps;
+  sa.opt = reinterpret_cast<float*>(d->opt_state);
+  if (sa.adam && (!sa.opt || d->adam_eps <= 0.0)) {
+    set_error("fs_train_bf16 (wide): Adam needs opt_state and eps > 0");
+    return FS_EINVAL;
+  }
   ConvArgs ca;
   ca.lay = L;
   ca.H = H;
@@ -817,6 +871,10 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
       init_master_kernel<<<grid, 256, 0, st>>>(d->w_start, reinterpret_cast<const int*>(stage + rbytes), gn, L.M,
                                                w_out, d->ldw);
       if (int rc = check_launch("wide init")) return rc;
+      if (sa.adam &&  // moments of this group's requests start at zero
+          cudaMemsetAsync(sa.opt + (int64_t)g0 * 2 * d->ldw, 0, sizeof(float) * (size_t)gn * 2 * d->ldw, st) !=
+              cudaSuccess)
+        return check_launch("wide adam moments");
       convert_kernel<<<dim3(128, (unsigned)gn), 256, 0, st>>>(ca, reinterpret_cast<const StepRow*>(stage), gn);
       if (int rc = check_launch("wide convert")) return rc;
     }

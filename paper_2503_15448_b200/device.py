@@ -359,6 +359,7 @@ class TrainPlan:
         self._desc = None        # (precision, static TrainDesc) built by static_desc()
         self.workspace_need = 0
         self.prefilled = None    # (precision, lr, desc, w_out, status, run) prepared by prefill()
+        self.opt = None          # opt-in Adam (beta1, beta2, eps); None = SGD (set before static_desc)
         self.mask_tag = 0
         lib = rt.lib
         self.dims = tuple(int(x) for x in spec_dims)
@@ -501,7 +502,9 @@ class TrainPlan:
         desc.w_out, desc.ldw = w_out.data_ptr(), w_out.stride(0)
         desc.workspace, desc.workspace_bytes = ws.data_ptr(), ws.numel()
         desc.w_start = d_run.data_ptr()
-        if fused_align_supported(self.dims, precision):
+        if self.opt is not None:
+            desc.opt_state = self.pool_buf("opt", 2 * self.n * ld, w_out.dtype).data_ptr()
+        if fused_align_supported(self.dims, precision) and self.opt is None:
             # the unit-major kernel takes the one start model directly and finds
             # its work counter zeroed here: the round launches it with no fill/memset
             self.rt.call(lib.fs_fill_u64(ws.data_ptr(), 0, 1, st), "fs_fill_u64")
@@ -540,6 +543,9 @@ class TrainPlan:
         desc.end_step = self.end_p
         desc.order = self.order_p
         desc.grid = TRAIN_GRID
+        if self.opt is not None:
+            desc.optimizer = N.FS_OPT_ADAM
+            desc.adam_beta1, desc.adam_beta2, desc.adam_eps = (float(v) for v in self.opt)
         lib = self.rt.lib
         need = (lib.fs_train_bf16_workspace_bytes if bf16 else lib.fs_train_workspace_bytes)(ctypes.byref(desc))
         if need == 0:
@@ -578,7 +584,7 @@ def _upload_waits(plan: TrainPlan, desc, up: dict, bf16: bool, stream) -> None:
     the test set (the shards went up on the trainer's own stream)."""
     if up["flags"] is None:
         return
-    if bf16 and plan.chunk_p is not None and eval_bf16_supported(plan.dims):
+    if bf16 and plan.chunk_p is not None and eval_bf16_supported(plan.dims) and plan.opt is None:
         desc.data_flags = up["flags"].data_ptr()
         desc.data_chunk = plan.chunk_p
         desc.data_tag = up["tag"]
@@ -711,6 +717,8 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
     ws = rt.scratch("train", plan.workspace_need)
     desc.workspace = ws.data_ptr()
     desc.workspace_bytes = ws.numel()
+    if plan.opt is not None:  # Adam moments, [n][2][ldw] of the parameter dtype, zeroed by the trainer
+        desc.opt_state = rt.scratch("opt_state", 2 * n * w_out.stride(0) * w_out.element_size()).data_ptr()
     _launch_trainer(plan, desc, bf16, stream)
     return w_out, status
 
@@ -718,7 +726,8 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
 def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.ndarray, lr: np.ndarray,
                 w_start: np.ndarray, batch: np.ndarray, epochs: int, dropout_rate: float,
                 start: np.ndarray | None = None, end: np.ndarray | None = None,
-                w_out: torch.Tensor | None = None, rt: Runtime | None = None, precision: str = "fp64"):
+                w_out: torch.Tensor | None = None, rt: Runtime | None = None, precision: str = "fp64",
+                opt: tuple | None = None):
     """Batched K2 -> K3 -> K5 over n requests given as arrays.
 
     clients [n] shard index, seeds [n] uint64 train seeds, lr [n x epochs],
@@ -729,6 +738,7 @@ def train_batch(spec_dims, shards: DeviceShards, clients: np.ndarray, seeds: np.
     Returns (w_out [n x M], status int32 [n]) on the device.
     """
     plan = TrainPlan(spec_dims, shards, clients, seeds, batch, epochs, dropout_rate, start, end, rt)
+    plan.opt = opt  # opt-in Adam (beta1, beta2, eps); None = SGD
     return run_trainer(plan, lr, w_start, precision, w_out)
 
 

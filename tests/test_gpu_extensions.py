@@ -151,3 +151,87 @@ def test_staleness_weighted_async_fedavg_matches_oracle(monkeypatch, engine):
         assert max(stale) > 0  # weights differ from 1 somewhere
         digests.append(eng.timeline.digest())
     assert digests[0] != digests[1]
+
+
+@pytest.mark.parametrize("dims,rate", [((42, 256, 128, 64, 1), 0.3), ((12, 16, 8, 1), 0.0)])
+def test_adam_fp64_trainer_matches_oracle(dims, rate):
+    """Opt-in Adam in the fp64 trainer against the oracle's float64
+    restatement of the same update (same batches, masks and step counter)."""
+    from oracle.fl_oracle import local_sgd
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=dims[0], hidden_dims=dims[1:-1], dropout_rate=rate)
+    g = np.random.default_rng(11)
+    sizes, B, E = [70, 130, 9], 32, 3
+    feats = [g.normal(size=(n, dims[0])) for n in sizes]
+    labs = [(g.random(n) < 0.4).astype(np.int8) for n in sizes]
+    rt = D.Runtime.get()
+    shards = D.DeviceShards(feats, labs, rt)
+    w0 = init_params(spec, 5).values
+    wd = torch.tensor(w0, device="cuda")
+    k = len(sizes)
+    lr = np.tile(np.array([0.01, 0.008, 0.006]), (k, 1))
+    seeds = np.arange(k, dtype=np.uint64) + 40
+    adam = (0.9, 0.999, 1e-8)
+    out, st = D.train_batch(spec.dims, shards, np.arange(k), seeds, lr, np.full(k, wd.data_ptr(), dtype=np.uint64),
+                            np.full(k, B), E, rate, rt=rt, opt=adam)
+    assert int(st.sum()) == 0
+    for i in range(k):
+        want = local_sgd(spec.dims, rate, w0, feats[i], labs[i], E, B, lambda e: float(lr[i, e]), int(seeds[i]),
+                         adam=adam)["params"]
+        got = out[i].cpu().numpy()
+        err = np.max(np.abs(got - want) / np.maximum(np.abs(want), 1.0))
+        assert err < 1e-9, (i, err)
+        assert np.abs(got - w0).max() > 1e-3  # Adam moved the weights
+
+
+@pytest.mark.parametrize("dims", [(42, 256, 128, 64, 1), (42, 1024, 1024, 1)])
+def test_adam_bf16_trainer_tracks_fp64_adam(dims):
+    """Opt-in Adam in bf16 mode (the lockstep tcgen05 trainer with the Adam
+    step in its epilogues; fp32 masters and moments) stays within the bf16
+    budget of the fp64 Adam trainer."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=dims[0], hidden_dims=dims[1:-1], dropout_rate=0.3)
+    g = np.random.default_rng(12)
+    sizes, B, E = [64, 100], 64, 2
+    feats = [g.normal(size=(n, dims[0])) + 0.3 for n in sizes]
+    labs = [(g.random(n) < 0.3).astype(np.int8) for n in sizes]
+    rt = D.Runtime.get()
+    shards = D.DeviceShards(feats, labs, rt)
+    w64 = torch.tensor(init_params(spec, 2).values, device="cuda")
+    w32 = w64.float()
+    k = len(sizes)
+    args = dict(clients=np.arange(k), seeds=np.arange(k, dtype=np.uint64) + 3, lr=np.full((k, E), 0.002),
+                batch=np.full(k, B), epochs=E, dropout_rate=0.3, rt=rt, opt=(0.9, 0.999, 1e-8))
+    o64, s64 = D.train_batch(spec.dims, shards, w_start=np.full(k, w64.data_ptr(), dtype=np.uint64), **args)
+    o32, s32 = D.train_batch(spec.dims, shards, w_start=np.full(k, w32.data_ptr(), dtype=np.uint64),
+                             precision="bf16", **args)
+    assert int(s64.sum()) == 0 and int(s32.sum()) == 0
+    for i in range(k):
+        d64 = o64[i] - w64
+        d32 = o32[i].double() - w64
+        rel = ((d32 - d64).norm() / d64.norm()).item()
+        assert rel < 0.1, (i, rel)
+
+
+def test_sync_engine_adam_matches_oracle():
+    from oracle.fl_oracle import OracleFederation
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200.server import FederationEngine
+
+    cfg = _cfg(selection_mode="delta_sign", theta=0.3, extensions={"optimizer": "adam"}, lr=0.002)
+    world, init = build_world(ExperimentConfig.from_dict(cfg))
+    eng = FederationEngine(world)
+    st = eng.run(init)
+    sim = OracleFederation(world)
+    wg = sim.run(init.values)
+    assert [r.accepted for r in eng.reports] == [r["accepted"] for r in sim.reports]
+    err = np.max(np.abs(st.w_g.values - wg) / np.maximum(np.abs(wg), 1.0))
+    assert err < 1e-9, err
+    world2, init2 = build_world(ExperimentConfig.from_dict(dict(cfg, mode="async_filtered")))
+    with pytest.raises(NotImplementedError):
+        FederationEngine(world2).run(init2)
