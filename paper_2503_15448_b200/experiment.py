@@ -6,8 +6,8 @@ profiles, capacity-driven batch sizes, checkpoint interval, geometry,
 failure schedule, initial parameters), so a config yields the same world
 as in the reference; tests/golden pins the digests. ``run_experiment``
 drives the engine, returns the replay digest, summary and final parameters
-and writes the reference's run-directory artifacts (except the checkpoint
-blob); ``replay_run`` re-runs a directory and compares digests.
+and writes the reference's run-directory artifacts; ``replay_run`` re-runs
+a directory and compares digests.
 """
 
 from __future__ import annotations
@@ -25,7 +25,8 @@ from .backends import backend_name
 from .client import ClientProfile, assign_batch_size
 from .config import ExperimentConfig
 from .data import partition_dirichlet, stratified_split, synth_anomaly
-from .fault import CheckpointPolicy, WeibullModel, failure_offsets, inject_dropout, optimal_interval
+from .fault import (CheckpointPolicy, WeibullModel, failure_offsets, inject_dropout, optimal_interval,
+                    write_checkpoint_file)
 from .model import ModelSpec, ParamVector, init_params
 from .rng import derive_rng, derive_seed
 from .selection import SelectionPolicy
@@ -129,14 +130,13 @@ def run_experiment(config: ExperimentConfig, out_dir: str | None = None, workers
                    world_and_initial=None, precision: str = "fp64") -> RunResult:
     """Build a world, run it, and (with ``out_dir``) write the run directory
     (reference experiment.py:206-272): ``config.json``, ``events.jsonl``,
-    ``rounds.jsonl``, ``summary.csv`` and ``run_meta.json``.
+    ``rounds.jsonl``, ``summary.csv``, ``run_meta.json`` and the final global
+    checkpoint (``checkpoints/`` + MANIFEST.json).
 
     ``workers`` is accepted for API compatibility (clients are batched on the
     device; results do not depend on it). Framework extensions are
     keyword-only: ``world_and_initial`` reuses a prebuilt ``build_world``
-    result, ``precision`` selects the fp64 parity or bf16 trainer. The
-    global-model checkpoint file (``checkpoints/``) is not written: the
-    checkpoint blob codec is outside the round-loop scope."""
+    result, ``precision`` selects the fp64 parity or bf16 trainer."""
     t0 = time.perf_counter()
     world, initial = (world_and_initial if world_and_initial is not None
                       else build_world(config, workers=workers, precision=precision))
@@ -159,6 +159,8 @@ def run_experiment(config: ExperimentConfig, out_dir: str | None = None, workers
             "workers": workers, "precision": world.precision}
     with open(os.path.join(out_dir, "run_meta.json"), "w", encoding="utf-8") as f:
         json.dump(meta, f, indent=2, sort_keys=True)
+    if engine.global_checkpoints:
+        write_checkpoint_file(engine.global_checkpoints[-1], os.path.join(out_dir, "checkpoints"))
     return result
 
 

@@ -435,3 +435,34 @@ def test_engine_keeps_caller_vectors_and_checkpoints_intact():
     assert cps[-1].params is not st.w_g
     st.w_g.values = np.zeros_like(seen[-1])  # replacing the state's values leaves the checkpoint alone
     assert np.array_equal(cps[-1].params.values, seen[-1])
+
+
+def test_run_experiment_writes_reference_run_directory(tmp_path):
+    """run_experiment(config, out_dir) writes the reference's run directory
+    (config.json, events.jsonl, rounds.jsonl, summary.csv, run_meta.json,
+    checkpoints/ with MANIFEST.json) and replay_run reproduces it."""
+    import json
+    import os
+
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import params_digest, replay_run, run_experiment
+    from paper_2503_15448_b200.fault import read_checkpoint_file
+    from paper_2503_15448_b200.simnet import log_digest
+
+    cfg = ExperimentConfig.from_dict({"num_clients": 6, "rounds": 2, "epochs": 1, "dataset": {"n": 1500, "d": 12},
+                                      "model": {"hidden_dims": [16, 8], "dropout_rate": 0.3}, "seed": 3})
+    res = run_experiment(cfg, str(tmp_path))
+    names = set(os.listdir(tmp_path))
+    assert {"config.json", "events.jsonl", "rounds.jsonl", "summary.csv", "run_meta.json", "checkpoints"} <= names
+    meta = json.load(open(tmp_path / "run_meta.json"))
+    assert meta["digest"] == res.digest and meta["backend"] == "b200"
+    events = [json.loads(x) for x in open(tmp_path / "events.jsonl")]
+    assert log_digest(events) == res.digest
+    assert res.summary["rounds"] == 2 and "accuracy" in res.summary
+    ck_dir = tmp_path / "checkpoints"
+    files = [f for f in os.listdir(ck_dir) if f.endswith(".ckpt")]
+    assert len(files) == 1 and "MANIFEST.json" in os.listdir(ck_dir)
+    ck = read_checkpoint_file(str(ck_dir / files[0]))
+    assert params_digest(ck.params) == meta["params_digest"] == params_digest(res.final_params)
+    ok, report = replay_run(str(tmp_path))
+    assert ok, report
