@@ -367,6 +367,9 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = N
     d_agg = rt.h2d(ptr_c[:k].view(np.int64))
     counts = torch.empty(n_clients, dtype=torch.int64, device=rt.device)
     res = torch.empty(M, dtype=torch.float32, device=rt.device)
+    d_job = rt.h2d(np.array([0, k, res.data_ptr()], dtype=np.uint64).view(np.int64))  # job_off {0, k}, job_out
+    d_sorted = torch.empty(k, dtype=torch.int64, device=rt.device)
+    ws = rt.scratch("agg_rowsplit_bench", rt.lib.fs_aggregate_rowsplit_workspace_bytes(M))
     stream = torch.cuda.current_stream()
     launch = {
         "align": (lambda: rt.call(rt.lib.fs_sign_align_shared(d_all.data_ptr(), wg.data_ptr(), wp.data_ptr(),
@@ -375,6 +378,10 @@ def hbm_microbench(M: int = 3193857, n_clients: int = 256, n_agg: int | None = N
                   4.0 * M * (n_clients + 2)),
         "aggregate": (lambda: rt.call(rt.lib.fs_aggregate_f32(d_agg.data_ptr(), k, M, res.data_ptr(), rt.stream),
                                       "agg"), 4.0 * M * (k + 1)),
+        # bf16 sync rounds' FedAvg (row-split, canonical order + 16 row groups)
+        "aggregate_rowsplit": (lambda: rt.call(rt.lib.fs_aggregate_rowsplit_f32(
+            d_agg.data_ptr(), d_job.data_ptr(), k, M, d_sorted.data_ptr(), d_job.data_ptr() + 16, ws.data_ptr(),
+            ws.numel(), rt.stream), "agg_split"), 4.0 * M * (k + 1)),
     }
     flush = torch.zeros(64 << 20, dtype=torch.float32, device=rt.device)
     out = {}

@@ -329,6 +329,15 @@ int fs_cosine_align(const uint64_t* wc, uint64_t base, int64_t stride_bytes, con
                     int32_t n_req, int64_t M, int32_t dtype_bytes, int64_t* score_out, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* bf16-mode FedAvg of one fs_select_rows job of float32 rows: canonical
+ * order, then the rows cut into 16 groups summed in parallel (float64
+ * partials, groups added in order): deterministic, tolerance-matched (the
+ * numpy order is the fp64 parity mode's contract, fs_aggregate_jobs).      */
+size_t fs_aggregate_rowsplit_workspace_bytes(int64_t M);
+int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M,
+                              uint64_t* sorted_scratch, const uint64_t* job_out, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
 int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
                 void* stream);
 int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out, void* stream);

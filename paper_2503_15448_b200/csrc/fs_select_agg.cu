@@ -742,6 +742,93 @@ extern "C" int fs_aggregate_jobs_weighted(const uint64_t* rows, const double* we
                              job_out, stream);
 }
 
+// ---------------------------------------------------------------- K7, row-split (bf16 mode, one job)
+// FedAvg of a synchronous round's accepted float32 rows when the numpy
+// summation order is not the contract (bf16 mode is tolerance-matched): the
+// k rows (canonical order, count read on the device from job_off[1]) are cut
+// into SPLIT_G contiguous groups; CTA (strip, g) sums its group's rows over a
+// 1024-column strip into float64 partials (4 columns per thread, 4 rows per
+// load batch), and the finish pass adds the groups in order and divides by k.
+// Deterministic for a given k; SPLIT_G x the column-strip parallelism of the
+// sequential K7, which at the C4 row length has only 205 strips.
+constexpr int SPLIT_G = 16, SPLIT_THREADS = 256, SPLIT_COLS = 4 * SPLIT_THREADS;
+
+__global__ void __launch_bounds__(SPLIT_THREADS)
+    rowsplit_partial_kernel(const uint64_t* rows, const int64_t* job_off, int64_t M, double* part) {
+  const int k = (int)job_off[1];
+  const int g = blockIdx.y;
+  const int r0 = (int)((int64_t)k * g / SPLIT_G), r1 = (int)((int64_t)k * (g + 1) / SPLIT_G);
+  const int64_t c = (int64_t)blockIdx.x * SPLIT_COLS + 4 * threadIdx.x;
+  if (c >= M) return;
+  double a0 = -0.0, a1 = -0.0, a2 = -0.0, a3 = -0.0;
+  const bool vec = c + 4 <= M;
+  int r = r0;
+  if (vec) {
+    for (; r + 4 <= r1; r += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(rows[r + q]) + c));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a0 += (double)v[q].x;
+        a1 += (double)v[q].y;
+        a2 += (double)v[q].z;
+        a3 += (double)v[q].w;
+      }
+    }
+  }
+  for (; r < r1; ++r) {
+    const float* row = reinterpret_cast<const float*>(rows[r]) + c;
+    a0 += (double)row[0];
+    if (c + 1 < M) a1 += (double)row[1];
+    if (c + 2 < M) a2 += (double)row[2];
+    if (c + 3 < M) a3 += (double)row[3];
+  }
+  double* p = part + (int64_t)g * M + c;
+  p[0] = a0;
+  if (c + 1 < M) p[1] = a1;
+  if (c + 2 < M) p[2] = a2;
+  if (c + 3 < M) p[3] = a3;
+}
+
+__global__ void rowsplit_finish_kernel(const double* part, const int64_t* job_off, int64_t M, const uint64_t* job_out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = (int)job_off[1];
+  if (j >= M || k == 0) return;
+  double s = -0.0;
+#pragma unroll
+  for (int g = 0; g < SPLIT_G; ++g) s += part[(int64_t)g * M + j];
+  reinterpret_cast<float*>(job_out[0])[j] = (float)(s / (double)k);
+}
+
+extern "C" size_t fs_aggregate_rowsplit_workspace_bytes(int64_t M) {
+  return M > 0 ? (size_t)SPLIT_G * (size_t)M * sizeof(double) : 0;
+}
+
+// One job (fs_select_rows output: rows, job_off = {0, k}, job_out[0]) of
+// float32 rows: K9 canonical order into sorted_scratch (max_k entries), then
+// the row-split mean above. k = 0 writes nothing.
+extern "C" int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M,
+                                         uint64_t* sorted_scratch, const uint64_t* job_out, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (max_k < 1 || max_k > SORT_MAX || M < 1 || !workspace ||
+      workspace_bytes < fs_aggregate_rowsplit_workspace_bytes(M)) {
+    set_error("fs_aggregate_rowsplit_f32: invalid arguments or workspace");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int threads = 32;
+  while (threads < max_k && threads < SORT_MAX) threads <<= 1;
+  canonical_order_kernel<float><<<1, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+  if (int rc = check_launch("canonical_order_kernel (rowsplit)")) return rc;
+  double* part = reinterpret_cast<double*>(workspace);
+  rowsplit_partial_kernel<<<dim3((unsigned)((M + SPLIT_COLS - 1) / SPLIT_COLS), SPLIT_G), SPLIT_THREADS, 0, st>>>(
+      sorted_scratch, job_off, M, part);
+  if (int rc = check_launch("rowsplit_partial_kernel")) return rc;
+  rowsplit_finish_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, job_off, M, job_out);
+  return check_launch("rowsplit_finish_kernel");
+}
+
 // ---------------------------------------------------------------- selection on device
 // filter_update (selection.py:77-85) for a synchronous round without a host
 // round trip: accept[i] = aligned[i] / M >= theta (float64, inclusive), or

@@ -411,3 +411,30 @@ def test_bf16_sync_round_with_every_update_rejected_keeps_the_model(mode):
                               np.asarray(init.values, dtype=np.float32))
     else:  # round 0 is unscored (no movement history): everyone is accepted once
         assert aggs[0]["count"] == 24 and all(a["count"] == 0 for a in aggs[1:])
+
+
+@pytest.mark.parametrize("k,M", [(1, 52225), (37, 1000), (400, 52225), (1024, 3)])
+def test_rowsplit_fedavg_matches_float64_mean(k, M):
+    """bf16-mode FedAvg (fs_aggregate_rowsplit_f32: canonical order, 16 row
+    groups with float64 partials added in order) equals the float64 mean of
+    the float32 rows to float32 rounding, and is deterministic."""
+    from paper_2503_15448_b200 import device as D
+
+    rt = D.Runtime.get()
+    g = torch.Generator(device="cuda").manual_seed(k * 7 + M)
+    ld = (M * 4 + 127) // 128 * 128 // 4
+    rows = torch.randn(k, ld, device="cuda", generator=g, dtype=torch.float32)[:, :M]
+    outs = []
+    for _ in range(2):
+        out = torch.empty(M, dtype=torch.float32, device="cuda")
+        ptrs = rows.data_ptr() + np.arange(k, dtype=np.uint64) * np.uint64(ld * 4)
+        d_rows = rt.h2d(ptrs.view(np.int64))
+        d_job = rt.h2d(np.array([0, k, out.data_ptr()], dtype=np.uint64).view(np.int64))
+        sorted_ = torch.empty(k, dtype=torch.int64, device="cuda")
+        ws = rt.scratch("t_rowsplit", rt.lib.fs_aggregate_rowsplit_workspace_bytes(M))
+        rt.call(rt.lib.fs_aggregate_rowsplit_f32(d_rows.data_ptr(), d_job.data_ptr(), k, M, sorted_.data_ptr(),
+                                                 d_job.data_ptr() + 16, ws.data_ptr(), ws.numel(), rt.stream), "rs")
+        outs.append(out.cpu())
+    want = rows.double().mean(0).float().cpu()
+    assert torch.equal(outs[0], outs[1])
+    assert (outs[0] - want).abs().max().item() <= 1e-6 * max(1.0, want.abs().max().item())
