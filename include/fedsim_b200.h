@@ -329,10 +329,11 @@ int fs_cosine_align(const uint64_t* wc, uint64_t base, int64_t stride_bytes, con
                     int32_t n_req, int64_t M, int32_t dtype_bytes, int64_t* score_out, void* workspace,
                     size_t workspace_bytes, void* stream);
 
-/* bf16-mode FedAvg of one fs_select_rows job of float32 rows: canonical
- * order, then the rows cut into 16 groups summed in parallel (float64
- * partials, groups added in order): deterministic, tolerance-matched (the
- * numpy order is the fp64 parity mode's contract, fs_aggregate_jobs).      */
+/* bf16-mode FedAvg of one fs_select_rows job of float32 rows: the rows
+ * (client order) cut into 16 groups summed in parallel (float64 partials,
+ * groups added in order): deterministic, tolerance-matched (the canonical
+ * numpy order is the fp64 parity mode's contract, fs_aggregate_jobs).
+ * sorted_scratch is unused.                                                 */
 size_t fs_aggregate_rowsplit_workspace_bytes(int64_t M);
 int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M,
                               uint64_t* sorted_scratch, const uint64_t* job_out, void* workspace,
@@ -340,6 +341,21 @@ int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* job_off, int3
 
 int fs_sum_rows(const uint64_t* rows, int32_t k, int64_t M, int32_t dtype_bytes, double* out,
                 void* stream);
+
+/* Client-sharded synchronous round on the device (parallel.py): no host
+ * round trip before the all-reduce.
+ *   fs_sum_job          canonical-order float64 sum of one fs_select_rows job
+ *                       (k read on the device) -> *job_out[0] (double [M]);
+ *   fs_pack_exchange    tail[0..2N] = {counts scattered to own_idx | k |
+ *                       status scattered to own_idx} (zeros elsewhere);
+ *   fs_mean_finish_dev  out = sum / k (k = *k_dev, after the all-reduce), or
+ *                       keep (the previous model) when k == 0.               */
+int fs_sum_job(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M, int32_t dtype_bytes,
+               uint64_t* sorted_scratch, const uint64_t* job_out, void* stream);
+int fs_pack_exchange(const int64_t* counts, const int32_t* status, const int32_t* own_idx, int32_t k, int32_t N,
+                     const int64_t* job_off, double* tail, void* stream);
+int fs_mean_finish_dev(const double* sum, const double* k_dev, int64_t M, int32_t dtype_bytes, const void* keep,
+                       void* out, void* stream);
 int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t dtype_bytes, void* out, void* stream);
 
 /* ---------------------------------------------------------------- K8 metrics

@@ -139,6 +139,9 @@ _SIGNATURES = {
     "fs_aggregate_jobs": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp]),
     "fs_aggregate_rowsplit_workspace_bytes": (_c_sz, [_c_i64]),
     "fs_aggregate_rowsplit_f32": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_i64, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "fs_sum_job": (ctypes.c_int, [_c_vp, _c_vp, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp]),
+    "fs_pack_exchange": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp]),
+    "fs_mean_finish_dev": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp]),
     "fs_aggregate_jobs_weighted": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i32, _c_i32, _c_i64, _c_i32, _c_vp, _c_vp,
                                                   _c_vp, _c_vp]),
     "fs_select_rows": (ctypes.c_int, [_c_vp, _c_i32, _c_i64, _c_f64, _c_i32, _c_i32, _c_u64, _c_i64, _c_vp, _c_vp,

@@ -596,6 +596,90 @@ extern "C" int fs_mean_finish(const double* sum, int64_t k, int64_t M, int32_t d
   return check_launch("mean_finish_kernel");
 }
 
+// ---------------------------------------------------------------- client-sharded rounds, on the device
+// One rank's share of a sharded synchronous round without a host round trip
+// before the collective: its accepted rows (fs_select_rows job) are summed in
+// canonical order into the exchange buffer's float64 head (fs_sum_job), its
+// per-client counts / status / accepted count are scattered into the tail
+// (fs_pack_exchange), the caller all-reduces the buffer (NCCL on the stream),
+// and fs_mean_finish_dev writes sum / k -- or keeps the previous model when
+// no rank accepted anything -- reading k from the reduced buffer.
+extern "C" int fs_sum_job(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M, int32_t dtype_bytes,
+                          uint64_t* sorted_scratch, const uint64_t* job_out, void* stream) {
+  if (max_k < 1 || max_k > SORT_MAX || M < 1 || (dtype_bytes != 4 && dtype_bytes != 8)) {
+    set_error("fs_sum_job: need 1 <= max_k <= %d, M >= 1", SORT_MAX);
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int threads = 32;
+  while (threads < max_k && threads < SORT_MAX) threads <<= 1;
+  const size_t smem = AGG_RING + AGG_STAGES * sizeof(uint64_t) + (size_t)max_k * (sizeof(void*) + sizeof(double));
+  const int64_t strips = (M * (int64_t)dtype_bytes + AGG_STRIP - 1) / AGG_STRIP;
+  if (dtype_bytes == 8) {
+    canonical_order_kernel<double><<<1, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+    auto kern = ordered_rows_kernel<double, false, double>;
+    ensure_smem(kern, (int)smem);
+    kern<<<dim3((unsigned)strips, 1), AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out,
+                                                                nullptr);
+  } else {
+    canonical_order_kernel<float><<<1, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
+    auto kern = ordered_rows_kernel<float, false, double>;
+    ensure_smem(kern, (int)smem);
+    kern<<<dim3((unsigned)strips, 1), AGG_THREADS, smem, st>>>(sorted_scratch, 0, M, nullptr, job_off, job_out,
+                                                                nullptr);
+  }
+  return check_launch("fs_sum_job");
+}
+
+__global__ void pack_exchange_kernel(const int64_t* counts, const int32_t* status, const int32_t* own_idx, int k,
+                                     int N, const int64_t* job_off, double* tail) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) {
+    const int c = own_idx[i];
+    tail[c] = counts ? (double)counts[i] : 0.0;
+    tail[N + 1 + c] = (double)status[i];
+  }
+  if (i == 0) tail[N] = (double)job_off[1];
+}
+
+extern "C" int fs_pack_exchange(const int64_t* counts, const int32_t* status, const int32_t* own_idx, int32_t k,
+                                int32_t N, const int64_t* job_off, double* tail, void* stream) {
+  if (k < 0 || N < 1 || k > N || !status || !own_idx || !job_off || !tail) {
+    set_error("fs_pack_exchange: invalid arguments");
+    return FS_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(tail, 0, sizeof(double) * (2 * (size_t)N + 1), st) != cudaSuccess)
+    return check_launch("memset exchange tail");
+  pack_exchange_kernel<<<(unsigned)((k + 255) / 256 > 0 ? (k + 255) / 256 : 1), 256, 0, st>>>(counts, status, own_idx,
+                                                                                          k, N, job_off, tail);
+  return check_launch("pack_exchange_kernel");
+}
+
+template <class T>
+__global__ void mean_finish_dev_kernel(const double* sum, const double* kp, int64_t M, const T* keep, T* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  const double k = *kp;
+  out[j] = k > 0.0 ? (T)(sum[j] / k) : keep[j];
+}
+
+extern "C" int fs_mean_finish_dev(const double* sum, const double* k_dev, int64_t M, int32_t dtype_bytes,
+                                  const void* keep, void* out, void* stream) {
+  if (M < 1 || (dtype_bytes != 4 && dtype_bytes != 8) || !sum || !k_dev || !keep || !out) {
+    set_error("fs_mean_finish_dev: invalid arguments");
+    return FS_EINVAL;
+  }
+  const unsigned blocks = (unsigned)((M + 255) / 256);
+  if (dtype_bytes == 8)
+    mean_finish_dev_kernel<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(sum, k_dev, M, (const double*)keep,
+                                                                             (double*)out);
+  else
+    mean_finish_dev_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(sum, k_dev, M, (const float*)keep,
+                                                                            (float*)out);
+  return check_launch("mean_finish_dev_kernel");
+}
+
 template <class T>
 static int sign_align_shared_impl(const uint64_t* wc, const void* wg, const void* wgp, int32_t n_req, int64_t M,
                                   int32_t mode, int64_t* aligned_out, void* stream, uint64_t base = 0,
@@ -805,9 +889,11 @@ extern "C" size_t fs_aggregate_rowsplit_workspace_bytes(int64_t M) {
   return M > 0 ? (size_t)SPLIT_G * (size_t)M * sizeof(double) : 0;
 }
 
-// One job (fs_select_rows output: rows, job_off = {0, k}, job_out[0]) of
-// float32 rows: K9 canonical order into sorted_scratch (max_k entries), then
-// the row-split mean above. k = 0 writes nothing.
+// One job (fs_select_rows output: rows in client order, job_off = {0, k},
+// job_out[0]) of float32 rows, summed in that (deterministic) order: the
+// canonical byte order only matters for numpy-bitwise parity, which is the
+// fp64 mode's contract, so no K9 sort here. k = 0 writes nothing.
+// sorted_scratch is unused (kept for the ABI).
 extern "C" int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* job_off, int32_t max_k, int64_t M,
                                          uint64_t* sorted_scratch, const uint64_t* job_out, void* workspace,
                                          size_t workspace_bytes, void* stream) {
@@ -817,13 +903,10 @@ extern "C" int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* jo
     return FS_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  int threads = 32;
-  while (threads < max_k && threads < SORT_MAX) threads <<= 1;
-  canonical_order_kernel<float><<<1, threads, 0, st>>>(rows, 0, M, sorted_scratch, job_off);
-  if (int rc = check_launch("canonical_order_kernel (rowsplit)")) return rc;
+  (void)sorted_scratch;
   double* part = reinterpret_cast<double*>(workspace);
   rowsplit_partial_kernel<<<dim3((unsigned)((M + SPLIT_COLS - 1) / SPLIT_COLS), SPLIT_G), SPLIT_THREADS, 0, st>>>(
-      sorted_scratch, job_off, M, part);
+      rows, job_off, M, part);
   if (int rc = check_launch("rowsplit_partial_kernel")) return rc;
   rowsplit_finish_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, job_off, M, job_out);
   return check_launch("rowsplit_finish_kernel");
