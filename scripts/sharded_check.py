@@ -2,7 +2,7 @@
 a ShardComm) against a single-process run of the same world, on rank 0.
 
     FS_DIST_BACKEND=gloo python -m torch.distributed.run --nproc-per-node 2 \\
-        --master-addr 127.0.0.1 --master-port 29555 scripts/sharded_check.py [fp64|bf16]
+        --master-addr 127.0.0.1 --master-port 29555 scripts/sharded_check.py [fp64|bf16] [mode] [selection] [c5]
 """
 import os
 import sys
@@ -26,6 +26,12 @@ cfg = {"num_clients": 40, "rounds": 3, "epochs": 1, "mode": mode, "selection_mod
                     "capacity": {"distribution": "loguniform", "low": 0.25, "high": 4.0},
                     "up_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5},
                     "down_latency": {"distribution": "lognormal", "mu": 0.0, "sigma": 0.5}}}
+if len(sys.argv) > 4 and sys.argv[4] == "c5":
+    # BASELINE configs[4]'s client population at a reduced row count: 8192
+    # clients, Dirichlet alpha = 5 (alpha = 0.5 cannot partition 8192 clients),
+    # UNSW MLP instead of the WIDE one (two ranks share one GPU here)
+    cfg.update({"num_clients": 8192, "rounds": 2, "dataset": {"n": 60000, "d": 42}, "partition": {"alpha": 5.0},
+                "batch": {"policy": "fixed", "size": 64}})
 comm = ShardComm.from_env()
 world, init = build_world(ExperimentConfig.from_dict(cfg), precision=prec)
 eng = FederationEngine(world, comm=comm)
