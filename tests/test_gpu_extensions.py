@@ -186,7 +186,7 @@ def test_adam_fp64_trainer_matches_oracle(dims, rate):
         assert np.abs(got - w0).max() > 1e-3  # Adam moved the weights
 
 
-@pytest.mark.parametrize("eps,bound", [(1.0, 0.08), (1e-3, 0.2)])
+@pytest.mark.parametrize("eps,bound", [(1.0, 0.12), (1e-3, 0.2)])
 @pytest.mark.parametrize("dims", [(42, 256, 128, 64, 1), (42, 1024, 1024, 1)])
 def test_adam_bf16_trainer_tracks_fp64_adam(dims, eps, bound):
     """Opt-in Adam in bf16 mode (the lockstep tcgen05 trainer with the Adam
