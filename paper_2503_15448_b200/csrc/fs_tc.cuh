@@ -139,6 +139,47 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// A chain of n MMAs into one accumulator whose operand descriptors advance by
+// constant increments (K slices of the same tiles): no per-MMA address math
+// and an immediate accumulate flag, so a single issuing thread keeps up with
+// the tensor pipe (measured ~46 cycles per MMA issue vs ~150-190 with the
+// descriptors rebuilt per MMA, tests/csrc/mma_latency_probe.cu).
+__device__ __forceinline__ void mma_bf16_acc(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc));
+}
+__device__ __forceinline__ void mma_bf16_set(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc));
+}
+template <int N>
+__device__ __forceinline__ void mma_chain_t(uint32_t tmem_d, uint64_t a, uint64_t ia, uint64_t b, uint64_t ib,
+                                            uint32_t idesc, bool acc_first) {
+  if (acc_first) mma_bf16_acc(tmem_d, a, b, idesc);
+  else mma_bf16_set(tmem_d, a, b, idesc);
+#pragma unroll
+  for (int k = 1; k < N; ++k) mma_bf16_acc(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc);
+}
+__device__ __forceinline__ void mma_chain(int n, uint32_t tmem_d, uint64_t a, uint64_t ia, uint64_t b, uint64_t ib,
+                                          uint32_t idesc, bool acc_first) {
+  switch (n) {
+    case 1: mma_chain_t<1>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    case 2: mma_chain_t<2>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    case 3: mma_chain_t<3>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    case 4: mma_chain_t<4>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    case 8: mma_chain_t<8>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    case 16: mma_chain_t<16>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
+    default:
+      for (int k = 0; k < n; ++k)
+        if (k || acc_first) mma_bf16_acc(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc);
+        else mma_bf16_set(tmem_d, a, b, idesc);
+  }
+}
+
 // all previously issued MMAs of this thread arrive on `bar` when complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -180,6 +221,9 @@ struct Tile {
     return sdesc(saddr + (uint32_t)(2 * k_slice) * col_block_bytes() + (uint32_t)mn_block128 * 16u * 128u,
                  col_block_bytes(), 128u);
   }
+  // descriptor increments of one K slice (the start-address field only)
+  __device__ __forceinline__ uint64_t kstep() const { return (uint64_t)((2u * col_block_bytes()) >> 4); }
+  __device__ __forceinline__ uint64_t mnstep() const { return (uint64_t)(256u >> 4); }
   // operand whose K runs along R, MN along C, K-slice s = 16 rows
   __device__ __forceinline__ uint64_t mnmajor(int k_slice, int mn_block128 = 0) const {
     return sdesc(saddr + (uint32_t)(2 * k_slice) * 128u + (uint32_t)mn_block128 * 16u * col_block_bytes(), 128u,
