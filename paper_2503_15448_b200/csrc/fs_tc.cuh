@@ -140,44 +140,15 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 // A chain of n MMAs into one accumulator whose operand descriptors advance by
-// constant increments (K slices of the same tiles): no per-MMA address math
-// and an immediate accumulate flag, so a single issuing thread keeps up with
-// the tensor pipe (measured ~46 cycles per MMA issue vs ~150-190 with the
-// descriptors rebuilt per MMA, tests/csrc/mma_latency_probe.cu).
-__device__ __forceinline__ void mma_bf16_acc(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc));
-}
-__device__ __forceinline__ void mma_bf16_set(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc));
-}
-template <int N>
-__device__ __forceinline__ void mma_chain_t(uint32_t tmem_d, uint64_t a, uint64_t ia, uint64_t b, uint64_t ib,
-                                            uint32_t idesc, bool acc_first) {
-  if (acc_first) mma_bf16_acc(tmem_d, a, b, idesc);
-  else mma_bf16_set(tmem_d, a, b, idesc);
-#pragma unroll
-  for (int k = 1; k < N; ++k) mma_bf16_acc(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc);
-}
+// constant increments (K slices of the same tiles): no per-MMA descriptor
+// rebuild in the issuing thread (tests/csrc/mma_latency_probe.cu measures
+// the issue cost per MMA both ways). A templated, fully unrolled variant and
+// chains over two MN-major operands crash ptxas 12.9 (segfault) in the
+// trainer; those stay plain loops.
 __device__ __forceinline__ void mma_chain(int n, uint32_t tmem_d, uint64_t a, uint64_t ia, uint64_t b, uint64_t ib,
                                           uint32_t idesc, bool acc_first) {
-  switch (n) {
-    case 1: mma_chain_t<1>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    case 2: mma_chain_t<2>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    case 3: mma_chain_t<3>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    case 4: mma_chain_t<4>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    case 8: mma_chain_t<8>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    case 16: mma_chain_t<16>(tmem_d, a, ia, b, ib, idesc, acc_first); break;
-    default:
-      for (int k = 0; k < n; ++k)
-        if (k || acc_first) mma_bf16_acc(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc);
-        else mma_bf16_set(tmem_d, a, b, idesc);
-  }
+  for (int k = 0; k < n; ++k)
+    mma_bf16(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc, (k || acc_first) ? 1u : 0u);
 }
 
 // all previously issued MMAs of this thread arrive on `bar` when complete

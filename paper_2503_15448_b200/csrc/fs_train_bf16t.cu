@@ -551,7 +551,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         stage_sync();
         if (tid == 0) {
           const uint32_t id = idesc_bf16(128, R, true, true);
-          mma_chain(f1 / 16, tbase + T_ACC, w1t.mnmajor(0), w1t.mnstep(), h1t.mnmajor(0), h1t.mnstep(), id, false);
+          for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16(tbase + T_ACC, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
           mma_commit(&mma_bar);
         }
         {
@@ -577,7 +577,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         stage_sync();
         if (tid == 0) {
           const uint32_t id = idesc_bf16(128, R, true, true);  // M = 128 over 64 units (upper half unused)
-          mma_chain(f2 / 16, tbase + T_ACC, w2t.mnmajor(0), w2t.mnstep(), h2t.mnmajor(0), h2t.mnstep(), id, false);
+          for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase + T_ACC, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
           mma_commit(&mma_bar);
         }
         if (next_ok && tid >= 64 && tid < 64 + R) {
@@ -1029,7 +1029,7 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     stage_sync();
     if (tid == 0) {
       const uint32_t id = idesc_bf16(128, R, true, true);
-      mma_chain(f1 / 16, tbase, w1t.mnmajor(0), w1t.mnstep(), h1t.mnmajor(0), h1t.mnstep(), id, false);
+      for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16(tbase, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
       mma_commit(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     stage_sync();
     if (tid == 0) {
       const uint32_t id = idesc_bf16(128, R, true, true);
-      mma_chain(f2 / 16, tbase, w2t.mnmajor(0), w2t.mnstep(), h2t.mnmajor(0), h2t.mnstep(), id, false);
+      for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
       mma_commit(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
