@@ -14,7 +14,13 @@ reported under "fp64_parity".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Prints ONE JSON line (rank 0). See DESIGN.md §Measurement for every field.
+--gpus N outside torchrun re-launches itself as N ranks (torch.distributed.run,
+127.0.0.1). --impl reference times the REFERENCE package itself
+(oracle/_ref/pkg, built by oracle/build_ref.sh): K consecutive full C4 rounds
+of its own FederationEngine.run_sync_round, its client fan-out on forked
+workers over every host core. The b200 arm's cpu_baseline is the same
+package on one core, one full round. Prints ONE JSON line (rank 0); see
+DESIGN.md §8 for every field.
 """
 
 from __future__ import annotations
@@ -28,10 +34,9 @@ import sys
 import threading
 import time
 
-# CPU legs run the oracle single-threaded: the reference path is GIL-bound, and
-# a thread pool over clients (the reference's `workers`) plus BLAS threads was
-# measured 3.6x SLOWER on 8 cores (0.0154 vs 0.055 rounds/s); --ref-workers N
-# reproduces that variant.
+# CPU legs pin BLAS to one thread per process: the reference path is GIL- and
+# per-call-overhead-bound (8 BLAS threads gave no speed-up);
+# the reference arm gets every core through forked worker processes instead.
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 
 import numpy as np
