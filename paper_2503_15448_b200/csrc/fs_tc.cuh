@@ -139,18 +139,6 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-// A chain of n MMAs into one accumulator whose operand descriptors advance by
-// constant increments (K slices of the same tiles): no per-MMA descriptor
-// rebuild in the issuing thread (tests/csrc/mma_latency_probe.cu measures
-// the issue cost per MMA both ways). A templated, fully unrolled variant and
-// chains over two MN-major operands crash ptxas 12.9 (segfault) in the
-// trainer; those stay plain loops.
-__device__ __forceinline__ void mma_chain(int n, uint32_t tmem_d, uint64_t a, uint64_t ia, uint64_t b, uint64_t ib,
-                                          uint32_t idesc, bool acc_first) {
-  for (int k = 0; k < n; ++k)
-    mma_bf16(tmem_d, a + (uint64_t)k * ia, b + (uint64_t)k * ib, idesc, (k || acc_first) ? 1u : 0u);
-}
-
 // all previously issued MMAs of this thread arrive on `bar` when complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -192,9 +180,6 @@ struct Tile {
     return sdesc(saddr + (uint32_t)(2 * k_slice) * col_block_bytes() + (uint32_t)mn_block128 * 16u * 128u,
                  col_block_bytes(), 128u);
   }
-  // descriptor increments of one K slice (the start-address field only)
-  __device__ __forceinline__ uint64_t kstep() const { return (uint64_t)((2u * col_block_bytes()) >> 4); }
-  __device__ __forceinline__ uint64_t mnstep() const { return (uint64_t)(256u >> 4); }
   // operand whose K runs along R, MN along C, K-slice s = 16 rows
   __device__ __forceinline__ uint64_t mnmajor(int k_slice, int mn_block128 = 0) const {
     return sdesc(saddr + (uint32_t)(2 * k_slice) * 128u + (uint32_t)mn_block128 * 16u * col_block_bytes(), 128u,

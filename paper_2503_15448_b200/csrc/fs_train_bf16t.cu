@@ -517,9 +517,9 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         stage_sync();
         if (tid == 0) {
           const uint32_t id = idesc_bf16(128, R, false, false);
-          for (int mb = 0; mb < MB; ++mb)
-            mma_chain(fp0 / 16, tbase + T_ACC + (uint32_t)(mb * R), w0t.kmajor(0, mb), w0t.kstep(), xt.kmajor(0),
-                      xt.kstep(), id, false);
+          for (int ks = 0; ks < fp0 / 16; ++ks)
+            for (int mb = 0; mb < MB; ++mb)
+              mma_bf16(tbase + T_ACC + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
           mma_commit(&mma_bar);
         }
         {
@@ -719,9 +719,9 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         stage_sync();
         if (tid == 0) {
           const uint32_t idg = idesc_bf16(128, f3, false, false);
-          mma_chain(R / 16, tbase + T_ACC, h2t.kmajor(0), h2t.kstep(), h3t.kmajor(0), h3t.kstep(), idg, false);
+          for (int ks = 0; ks < R / 16; ++ks) mma_bf16(tbase + T_ACC, h2t.kmajor(ks), h3t.kmajor(ks), idg, ks > 0);
           const uint32_t idd = idesc_bf16(128, R, false, true);
-          mma_chain(f3 / 16, tbase + T_D2, w2t.kmajor(0), w2t.kstep(), h3t.mnmajor(0), h3t.mnstep(), idd, false);
+          for (int ks = 0; ks < f3 / 16; ++ks) mma_bf16(tbase + T_D2, w2t.kmajor(ks), h3t.mnmajor(ks), idd, ks > 0);
           mma_commit(&mma_bar);
         }
         // head and b2 updates while the MMAs run (gradients accumulate over a step's chunks)
@@ -762,12 +762,12 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         if (tid == 0) {
           const uint32_t idg = idesc_bf16(128, f2, false, false);
           for (int mb = 0; mb < MB; ++mb)
-            mma_chain(R / 16, tbase + T_W1 + (uint32_t)(mb * f2), h1t.kmajor(0, mb), h1t.kstep(), h2t.kmajor(0),
-                      h2t.kstep(), idg, true);
+            for (int ks = 0; ks < R / 16; ++ks)
+              mma_bf16(tbase + T_W1 + (uint32_t)(mb * f2), h1t.kmajor(ks, mb), h2t.kmajor(ks), idg, 1u);
           const uint32_t idd = idesc_bf16(128, R, false, true);
           for (int mb = 0; mb < MB; ++mb)
-            mma_chain(f2 / 16, tbase + T_ACC + (uint32_t)(mb * R), w1t.kmajor(0, mb), w1t.kstep(), h2t.mnmajor(0),
-                      h2t.mnstep(), idd, false);
+            for (int ks = 0; ks < f2 / 16; ++ks)
+              mma_bf16(tbase + T_ACC + (uint32_t)(mb * R), w1t.kmajor(ks, mb), h2t.mnmajor(ks), idd, ks > 0);
           mma_commit(&mma_bar);
         }
         if (tid >= 128 && tid < 128 + f2) {  // b1 += sum(-lr D2)
@@ -801,8 +801,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         if (tid == 0) {
           const uint32_t idg = idesc_bf16(128, fp0, false, true);
           for (int mb = 0; mb < MB; ++mb)
-            mma_chain(R / 16, tbase + T_W0 + (uint32_t)(mb * fp0), h1t.kmajor(0, mb), h1t.kstep(), xt.mnmajor(0),
-                      xt.mnstep(), idg, true);
+            for (int ks = 0; ks < R / 16; ++ks)
+              mma_bf16(tbase + T_W0 + (uint32_t)(mb * fp0), h1t.kmajor(ks, mb), xt.mnmajor(ks), idg, 1u);
           mma_commit(&mma_bar);
         }
         if (tid < f1) {  // b0 += sum(-lr D1)
@@ -1009,9 +1009,9 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     stage_sync();
     if (tid == 0) {
       const uint32_t id = idesc_bf16(128, R, false, false);
-      for (int mb = 0; mb < MB; ++mb)
-        mma_chain(fp0 / 16, tbase + (uint32_t)(mb * R), w0t.kmajor(0, mb), w0t.kstep(), xt.kmajor(0), xt.kstep(), id,
-                  false);
+      for (int ks = 0; ks < fp0 / 16; ++ks)
+        for (int mb = 0; mb < MB; ++mb)
+          mma_bf16(tbase + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
       mma_commit(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
