@@ -66,6 +66,31 @@ template <bool A_KCONTIG, bool B_NCONTIG, class LA, class LB, class EPI>
 __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const EPI& epi,
                          GemmSmem& sm) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  constexpr int QA = (TM * TK) / THREADS, QB = (TN * TK) / THREADS;
+  // each thread stages QA elements of the A chunk and QB of the B chunk;
+  // the next chunk's global (L2) loads are issued into registers before the
+  // current chunk's FMAs, so their latency hides behind the compute. The k
+  // order of every output's FMA chain is unchanged (bitwise the same result).
+  auto a_pos = [&](int q, int& m, int& k) {
+    const int idx = tid + q * THREADS;
+    if (A_KCONTIG) {
+      k = idx & (TK - 1);
+      m = idx / TK;
+    } else {
+      m = idx & (TM - 1);
+      k = idx / TM;
+    }
+  };
+  auto b_pos = [&](int q, int& n, int& k) {
+    const int idx = tid + q * THREADS;
+    if (B_NCONTIG) {
+      n = idx & (TN - 1);
+      k = idx / TN;
+    } else {
+      k = idx & (TK - 1);
+      n = idx / TK;
+    }
+  };
   for (int tm = 0; tm < M; tm += TM) {
     for (int tn = 0; tn < N; tn += TN) {
       double acc[4][4];
@@ -73,36 +98,43 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-      for (int k0 = 0; k0 < K; k0 += TK) {
+      double ra[QA], rb[QB];
+      auto fetch = [&](int k0) {
 #pragma unroll
-        for (int q = 0; q < (TM * TK) / THREADS; ++q) {
-          const int idx = tid + q * THREADS;
+        for (int q = 0; q < QA; ++q) {
           int m, k;
-          if (A_KCONTIG) {
-            k = idx & (TK - 1);
-            m = idx / TK;
-          } else {
-            m = idx & (TM - 1);
-            k = idx / TM;
-          }
+          a_pos(q, m, k);
           const int gm = tm + m, gk = k0 + k;
-          sm.As[k][m] = (gm < M && gk < K) ? la(gm, gk) : 0.0;
+          ra[q] = (gm < M && gk < K) ? la(gm, gk) : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < (TN * TK) / THREADS; ++q) {
-          const int idx = tid + q * THREADS;
+        for (int q = 0; q < QB; ++q) {
           int n, k;
-          if (B_NCONTIG) {
-            n = idx & (TN - 1);
-            k = idx / TN;
-          } else {
-            k = idx & (TK - 1);
-            n = idx / TK;
-          }
+          b_pos(q, n, k);
           const int gn = tn + n, gk = k0 + k;
-          sm.Bs[k][n] = (gn < N && gk < K) ? lb(gk, gn) : 0.0;
+          rb[q] = (gn < N && gk < K) ? lb(gk, gn) : 0.0;
         }
-        __syncthreads();
+      };
+      auto stage = [&]() {
+#pragma unroll
+        for (int q = 0; q < QA; ++q) {
+          int m, k;
+          a_pos(q, m, k);
+          sm.As[k][m] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          int n, k;
+          b_pos(q, n, k);
+          sm.Bs[k][n] = rb[q];
+        }
+      };
+      fetch(0);
+      stage();
+      __syncthreads();
+      for (int k0 = 0; k0 < K; k0 += TK) {
+        const bool more = k0 + TK < K;
+        if (more) fetch(k0 + TK);
         const int kmax = min(TK, K - k0);
         for (int k = 0; k < kmax; ++k) {
           double a[4], b[4];
@@ -116,6 +148,10 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
             for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
+        if (more) {
+          stage();
+          __syncthreads();
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -446,7 +482,7 @@ __host__ __device__ inline int64_t scratch_doubles(const MlpLayout& lay, int max
   return s + 2 * (int64_t)max_rows * mh;
 }
 
-__global__ void __launch_bounds__(THREADS) train_kernel(TrainArgs a) {
+__global__ void __launch_bounds__(THREADS, 2) train_kernel(TrainArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GemmSmem& sm = *reinterpret_cast<GemmSmem*>(smem_raw);
   const int maxb = a.d.max_batch;
