@@ -467,7 +467,8 @@ C5_SHARE = {
 
 
 def measure_small_configs(precision: str):
-    """BASELINE configs[1] (C2: 100 UNSW clients, async_filtered, dynamic batch,
+    """BASELINE configs[0] (C1: 10 UNSW clients, sync_baseline, b = 64),
+    configs[1] (C2: 100 UNSW clients, async_filtered, dynamic batch,
     delta_sign) and configs[2] (C3: 256 ROAD-shaped CAN-window clients, d = 64,
     sync_filtered + async_filtered, b = 64): throughput of full runs after a
     warm-up run, CUDA events on the launching stream."""
@@ -480,6 +481,10 @@ def measure_small_configs(precision: str):
     base = {"epochs": 5, "theta": 0.65, "seed": 1, "selection_mode": "delta_sign", "profiles": C4_SYNC["profiles"],
             "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}}
     cfgs = {
+        # BASELINE configs[0] (the reference's CPU run): 10 clients, 5 sync_baseline
+        # rounds, b = 64; a 55k-row client's 4.3k sequential steps bound each round
+        "c1_sync": dict(base, num_clients=10, rounds=5, mode="sync_baseline", selection_mode="weight_sign",
+                        dataset=C4_SYNC["dataset"], batch={"policy": "fixed", "size": 64}),
         "c2_async": dict(base, num_clients=100, rounds=5, mode="async_filtered",
                          dataset=C4_SYNC["dataset"], batch=C4_SYNC["batch"]),
         "c3_sync": dict(base, num_clients=256, rounds=5, mode="sync_filtered", batch={"policy": "fixed", "size": 64},
