@@ -33,7 +33,17 @@ constexpr int TM = 64, TN = 64, TK = 16;
 struct GemmSmem {
   double As[TK][TM + 1];
   double Bs[TK][TN + 1];
+  double Es[16][THREADS];  // per-thread epilogue operands, fetched by cp.async
 };
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- operand views
 struct RowMajor {  // (r, c) -> p[r*ld + c]
@@ -62,9 +72,17 @@ struct GatherRowsT {  // transposed: (m, k) -> X[rowidx[k]*d + m]
 // C[M x N] = A[M x K] . B[K x N], handed element-wise to `epi`.  The k sum
 // of every output runs sequentially 0..K-1 with FMA, so a given shape
 // always rounds identically (shared by the batched and per-call paths).
-template <bool A_KCONTIG, bool B_NCONTIG, class LA, class LB, class EPI>
-__device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const EPI& epi,
-                         GemmSmem& sm) {
+//
+// The epilogue is split in two: src(m, n) names the one double the output
+// needs from memory (its bias, its previous W, its gating activation; nullptr
+// for none), which the thread copies into its own shared-memory slots with
+// cp.async when the tile starts, and fin(m, n, acc, e) combines and stores.
+// The operand fetch so overlaps the tile's FMAs without holding registers;
+// loaded inside fin instead, each of a thread's 16 outputs paid its own L2
+// round trip (the stores may alias the loads as far as the compiler knows).
+template <bool A_KCONTIG, bool B_NCONTIG, class LA, class LB, class SRC, class FIN>
+__device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const SRC& src,
+                         const FIN& fin, GemmSmem& sm) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   constexpr int QA = (TM * TK) / THREADS, QB = (TN * TK) / THREADS;
   // each thread stages QA elements of the A chunk and QB of the B chunk;
@@ -98,6 +116,14 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int m = tm + ty + 16 * i, n = tn + tx + 16 * j;
+          const double* e = (m < M && n < N) ? src(m, n) : nullptr;
+          if (e) cp_async8(&sm.Es[i * 4 + j][tid], e);
+        }
       double ra[QA], rb[QB];
       auto fetch = [&](int k0) {
 #pragma unroll
@@ -153,12 +179,13 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
           __syncthreads();
         }
       }
+      cp_async_wait_all();
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int m = tm + ty + 16 * i, n = tn + tx + 16 * j;
-          if (m < M && n < N) epi(m, n, acc[i][j]);
+          if (m < M && n < N) fin(m, n, acc[i][j], sm.Es[i * 4 + j][tid]);
         }
     }
   }
@@ -262,16 +289,17 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
     const double* bl = W + lay.boff[l];
     double* Hout = bufs.H[l + 1];
     const int hl = l;
-    auto epi = [&](int m, int n, double acc) {
-      double v = acc + bl[n];
+    auto src = [&](int, int n) { return bl + n; };
+    auto fin = [&](int m, int n, double acc, double b) {
+      double v = acc + b;
       v = v > 0.0 ? v : 0.0;
       if (mk.mode != FS_MASK_NONE) v = v * mk.val(hl, m, n, N);
       Hout[(int64_t)m * N + n] = v;
     };
     if (l == 0)
-      cta_gemm<true, true>(rows, N, K, GatherRows{X, ss.rowidx, d0}, RowMajor{Wl, N}, epi, sm);
+      cta_gemm<true, true>(rows, N, K, GatherRows{X, ss.rowidx, d0}, RowMajor{Wl, N}, src, fin, sm);
     else
-      cta_gemm<true, true>(rows, N, K, RowMajor{bufs.H[l], K}, RowMajor{Wl, N}, epi, sm);
+      cta_gemm<true, true>(rows, N, K, RowMajor{bufs.H[l], K}, RowMajor{Wl, N}, src, fin, sm);
     __syncthreads();
   }
 
@@ -359,9 +387,9 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
       double* Dl = bufs.D[l & 1];
       const double* Hl = bufs.H[l];
       const int hl = l - 1;
-      auto epi = [&](int m, int n, double acc) {
+      auto src = [&](int m, int n) { return Hl + (int64_t)m * K + n; };
+      auto fin = [&](int m, int n, double acc, double h) {
         double v = acc;
-        const double h = Hl[(int64_t)m * K + n];
         if (h > 0.0) {
           if (mk.mode != FS_MASK_NONE) v = v * mk.val(hl, m, n, K);
         } else {
@@ -369,26 +397,28 @@ __device__ void mlp_step(const MlpLayout& lay, double* W, double* G, double lr, 
         }
         Dl[(int64_t)m * K + n] = v;
       };
-      cta_gemm<true, false>(rows, K, N, RowMajor{Dn, N}, ColMajor{Wl, N}, epi, sm);
+      cta_gemm<true, false>(rows, K, N, RowMajor{Dn, N}, ColMajor{Wl, N}, src, fin, sm);
       __syncthreads();
     }
     // G_l = H_l^T . D_{l+1}, fused with W_l -= lr * G_l
     if (MODE == STEP_GRAD) {
       double* Gl = G + lay.woff[l];
-      auto epi = [&](int m, int n, double acc) { Gl[(int64_t)m * N + n] = acc; };
+      auto src = [](int, int) -> const double* { return nullptr; };
+      auto fin = [&](int m, int n, double acc, double) { Gl[(int64_t)m * N + n] = acc; };
       if (l == 0)
-        cta_gemm<false, true>(K, N, rows, GatherRowsT{X, ss.rowidx, d0}, RowMajor{Dn, N}, epi, sm);
+        cta_gemm<false, true>(K, N, rows, GatherRowsT{X, ss.rowidx, d0}, RowMajor{Dn, N}, src, fin, sm);
       else
-        cta_gemm<false, true>(K, N, rows, ColMajor{bufs.H[l], K}, RowMajor{Dn, N}, epi, sm);
+        cta_gemm<false, true>(K, N, rows, ColMajor{bufs.H[l], K}, RowMajor{Dn, N}, src, fin, sm);
     } else {
-      auto epi = [&](int m, int n, double acc) {
+      auto src = [&](int m, int n) -> const double* { return Wl + (int64_t)m * N + n; };
+      auto fin = [&](int m, int n, double acc, double w) {
         const int64_t i = (int64_t)m * N + n;
-        Wl[i] = opt.apply(Wl[i], lay.woff[l] + i, lr, acc);
+        Wl[i] = opt.apply(w, lay.woff[l] + i, lr, acc);
       };
       if (l == 0)
-        cta_gemm<false, true>(K, N, rows, GatherRowsT{X, ss.rowidx, d0}, RowMajor{Dn, N}, epi, sm);
+        cta_gemm<false, true>(K, N, rows, GatherRowsT{X, ss.rowidx, d0}, RowMajor{Dn, N}, src, fin, sm);
       else
-        cta_gemm<false, true>(K, N, rows, ColMajor{bufs.H[l], K}, RowMajor{Dn, N}, epi, sm);
+        cta_gemm<false, true>(K, N, rows, ColMajor{bufs.H[l], K}, RowMajor{Dn, N}, src, fin, sm);
     }
     // bias gradient: column sums of D_{l+1}, rows accumulated in order
     // (ndarray.sum(axis=0) adds rows in order, except that a single column
@@ -423,16 +453,17 @@ __device__ void mlp_forward(const MlpLayout& lay, const double* W, const double*
     const double* bl = W + lay.boff[l];
     double* Hout = bufs.H[l + 1];
     const int hl = l;
-    auto epi = [&](int m, int n, double acc) {
-      double v = acc + bl[n];
+    auto src = [&](int, int n) { return bl + n; };
+    auto fin = [&](int m, int n, double acc, double b) {
+      double v = acc + b;
       v = v > 0.0 ? v : 0.0;
       if (mk.mode != FS_MASK_NONE) v = v * mk.val(hl, m, n, N);
       Hout[(int64_t)m * N + n] = v;
     };
     if (l == 0)
-      cta_gemm<true, true>(rows, N, K, GatherRows{X, rowidx, d0}, RowMajor{Wl, N}, epi, sm);
+      cta_gemm<true, true>(rows, N, K, GatherRows{X, rowidx, d0}, RowMajor{Wl, N}, src, fin, sm);
     else
-      cta_gemm<true, true>(rows, N, K, RowMajor{bufs.H[l], K}, RowMajor{Wl, N}, epi, sm);
+      cta_gemm<true, true>(rows, N, K, RowMajor{bufs.H[l], K}, RowMajor{Wl, N}, src, fin, sm);
     __syncthreads();
   }
   const int FL = lay.f[L - 1];
@@ -757,6 +788,8 @@ extern "C" int fs_forward_f64(const int32_t* dims, int32_t n_dims, const double*
   FwdArgs a{lay, w, x, rows, dense_masks, probs_out, reinterpret_cast<double*>(workspace),
             scratch_doubles(lay, FWD_CHUNK)};
   const size_t smem = sizeof(GemmSmem) + FWD_CHUNK * sizeof(int64_t);
+  if (smem > 48 * 1024)
+    ensure_smem(forward_kernel, (int)smem);
   forward_kernel<<<grid, THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("forward_kernel");
 }
