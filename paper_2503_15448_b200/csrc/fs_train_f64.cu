@@ -11,8 +11,8 @@
 // a client runs without a host round trip.  The client's parameters stay
 // in its own HBM row (L2-resident while it trains: 418 KB for the
 // 42-256-128-64-1 MLP), activations live in a per-CTA L2-resident scratch,
-// and every layer product is a CTA-tiled fp64 FMA GEMM (64x64 tiles, 16-deep
-// k chunks staged in shared memory, 4x4 register micro-tiles).  The SGD
+// and every layer product is a CTA-tiled fp64 tensor-core GEMM (64x64 tiles,
+// 16-deep k chunks staged in shared memory, mma.sync m8n8k4 f64 per warp).  The SGD
 // update p - lr*g is fused into the weight-gradient GEMM epilogue, written
 // as an explicit (round(lr*g), then round(p - .)) pair so it matches the
 // reference's `params.values - lr * grad.values` rounding.  Dropout
@@ -27,13 +27,17 @@
 namespace fs {
 namespace f64 {
 
-constexpr int THREADS = 256;
-constexpr int TM = 64, TN = 64, TK = 16;
+constexpr int THREADS = 512;
+constexpr int TM = 64, TN = 64, TK = 32;
+// warps tile the 64 x 64 CTA tile as WARPS_M x 4, each owning MB x 2 DMMA tiles
+constexpr int WARPS_M = THREADS / 128, MB = 8 / WARPS_M, SLOTS = MB * 2 * 2;
+static_assert(THREADS == 256 || THREADS == 512 || THREADS == 1024, "cta_gemm warp tiling");
+constexpr int SPAD = 4;  // row padding: conflict-free DMMA fragment loads (rows k..k+3 x 8 columns)
 
 struct GemmSmem {
-  double As[TK][TM + 1];
-  double Bs[TK][TN + 1];
-  double Es[16][THREADS];  // per-thread epilogue operands, fetched by cp.async
+  double As[TK][TM + SPAD];
+  double Bs[TK][TN + SPAD];
+  double Es[SLOTS][THREADS];  // per-thread epilogue operands, fetched by cp.async
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -43,6 +47,16 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// fp64 tensor-core MMA, D[8x8] += A[8x4] . B[4x8]: lane (g = lane/4, t = lane%4)
+// holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1]. Each output's four products
+// are added in k order with one rounding each, bit-identical to a chain of
+// fma() over k (tests/test_gpu_dmma_probe.py).
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
 // ---------------------------------------------------------------- operand views
@@ -69,26 +83,34 @@ struct GatherRowsT {  // transposed: (m, k) -> X[rowidx[k]*d + m]
   __device__ __forceinline__ double operator()(int m, int k) const { return X[rowidx[k] * d + m]; }
 };
 
-// C[M x N] = A[M x K] . B[K x N], handed element-wise to `epi`.  The k sum
-// of every output runs sequentially 0..K-1 with FMA, so a given shape
-// always rounds identically (shared by the batched and per-call paths).
+// C[M x N] = A[M x K] . B[K x N], handed element-wise to the epilogue. The k
+// sum of every output runs sequentially 0..K-1, one rounding per product
+// (fp64 DMMA over whole k4 slices, fma for a chunk's last K % 4), so a given
+// shape always rounds identically, and like the reference's BLAS (shared by
+// the batched and per-call paths).
+//
+// 64 x 64 CTA tile, 16-deep k chunks staged in shared memory (the next
+// chunk's global loads are issued into registers before the current chunk's
+// MMAs); the warps as WARPS_M x 4, each owning an 8MB x 16 block = MB x 2
+// DMMA tiles.
 //
 // The epilogue is split in two: src(m, n) names the one double the output
 // needs from memory (its bias, its previous W, its gating activation; nullptr
 // for none), which the thread copies into its own shared-memory slots with
 // cp.async when the tile starts, and fin(m, n, acc, e) combines and stores.
-// The operand fetch so overlaps the tile's FMAs without holding registers;
+// The operand fetch so overlaps the tile's MMAs without holding registers;
 // loaded inside fin instead, each of a thread's 16 outputs paid its own L2
 // round trip (the stores may alias the loads as far as the compiler knows).
 template <bool A_KCONTIG, bool B_NCONTIG, class LA, class LB, class SRC, class FIN>
 __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const SRC& src,
                          const FIN& fin, GemmSmem& sm) {
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * (8 * MB), wn = (warp & 3) * 16;
+  // output slot s = (mb*2 + nb)*2 + c  ->  row wm + 8mb + g, column wn + 8nb + 2t + c
+  auto out_m = [&](int s) { return wm + 8 * (s >> 2) + g; };
+  auto out_n = [&](int s) { return wn + 8 * ((s >> 1) & 1) + 2 * t + (s & 1); };
   constexpr int QA = (TM * TK) / THREADS, QB = (TN * TK) / THREADS;
-  // each thread stages QA elements of the A chunk and QB of the B chunk;
-  // the next chunk's global (L2) loads are issued into registers before the
-  // current chunk's FMAs, so their latency hides behind the compute. The k
-  // order of every output's FMA chain is unchanged (bitwise the same result).
   auto a_pos = [&](int q, int& m, int& k) {
     const int idx = tid + q * THREADS;
     if (A_KCONTIG) {
@@ -111,19 +133,14 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
   };
   for (int tm = 0; tm < M; tm += TM) {
     for (int tn = 0; tn < N; tn += TN) {
-      double acc[4][4];
+      double acc[SLOTS];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int m = tm + ty + 16 * i, n = tn + tx + 16 * j;
-          const double* e = (m < M && n < N) ? src(m, n) : nullptr;
-          if (e) cp_async8(&sm.Es[i * 4 + j][tid], e);
-        }
+      for (int s = 0; s < SLOTS; ++s) {
+        acc[s] = 0.0;
+        const int m = tm + out_m(s), n = tn + out_n(s);
+        const double* e = (m < M && n < N) ? src(m, n) : nullptr;
+        if (e) cp_async8(&sm.Es[s][tid], e);
+      }
       double ra[QA], rb[QB];
       auto fetch = [&](int k0) {
 #pragma unroll
@@ -162,16 +179,21 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
         const bool more = k0 + TK < K;
         if (more) fetch(k0 + TK);
         const int kmax = min(TK, K - k0);
-        for (int k = 0; k < kmax; ++k) {
-          double a[4], b[4];
+        const int k4 = kmax & ~3;
+        for (int k = 0; k < k4; k += 4) {
+          double a[MB], b[2];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = sm.As[k][ty + 16 * i];
+          for (int mb = 0; mb < MB; ++mb) a[mb] = sm.As[k + t][wm + 8 * mb + g];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = sm.Bs[k][tx + 16 * j];
+          for (int nb = 0; nb < 2; ++nb) b[nb] = sm.Bs[k + t][wn + 8 * nb + g];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            for (int nb = 0; nb < 2; ++nb) dmma_8x8x4(acc[(mb * 2 + nb) * 2], acc[(mb * 2 + nb) * 2 + 1], a[mb], b[nb]);
+        }
+        for (int k = k4; k < kmax; ++k) {  // the chunk's last K % 4 products
+#pragma unroll
+          for (int s = 0; s < SLOTS; ++s) acc[s] = fma(sm.As[k][out_m(s)], sm.Bs[k][out_n(s)], acc[s]);
         }
         __syncthreads();
         if (more) {
@@ -181,12 +203,10 @@ __device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const 
       }
       cp_async_wait_all();
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int m = tm + ty + 16 * i, n = tn + tx + 16 * j;
-          if (m < M && n < N) fin(m, n, acc[i][j], sm.Es[i * 4 + j][tid]);
-        }
+      for (int s = 0; s < SLOTS; ++s) {
+        const int m = tm + out_m(s), n = tn + out_n(s);
+        if (m < M && n < N) fin(m, n, acc[s], sm.Es[s][tid]);
+      }
     }
   }
 }
@@ -513,11 +533,20 @@ __host__ __device__ inline int64_t scratch_doubles(const MlpLayout& lay, int max
   return s + 2 * (int64_t)max_rows * mh;
 }
 
-__global__ void __launch_bounds__(THREADS, 2) train_kernel(TrainArgs a) {
+// Per-CTA global scratch of the batched trainer: the step buffers, then the
+// batch's row indices, labels, logits and dz (L1/L2-resident; kept out of
+// shared memory so TRAIN_CTAS_PER_SM CTAs fit on an SM at any max_batch).
+constexpr int TRAIN_CTAS_PER_SM = 1;
+__host__ __device__ inline int64_t train_scratch_doubles(const MlpLayout& lay, int max_rows) {
+  return scratch_doubles(lay, max_rows) + 4 * (int64_t)max_rows;
+}
+
+__global__ void __launch_bounds__(THREADS, TRAIN_CTAS_PER_SM) train_kernel(TrainArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GemmSmem& sm = *reinterpret_cast<GemmSmem*>(smem_raw);
   const int maxb = a.d.max_batch;
-  int64_t* rowidx = reinterpret_cast<int64_t*>(smem_raw + sizeof(GemmSmem));
+  double* cta_scratch = a.scratch + (int64_t)blockIdx.x * a.scratch_per_cta;
+  int64_t* rowidx = reinterpret_cast<int64_t*>(cta_scratch + scratch_doubles(a.lay, maxb));
   double* ysm = reinterpret_cast<double*>(rowidx + maxb);
   double* zsm = ysm + maxb;
   double* dzsm = zsm + maxb;
@@ -525,7 +554,7 @@ __global__ void __launch_bounds__(THREADS, 2) train_kernel(TrainArgs a) {
 
   const MlpLayout& lay = a.lay;
   const fs_train_desc& d = a.d;
-  const StepBufs bufs = carve(lay, a.scratch + (int64_t)blockIdx.x * a.scratch_per_cta, maxb);
+  const StepBufs bufs = carve(lay, cta_scratch, maxb);
   const StepShared ss{rowidx, ysm, zsm, dzsm};
 
   while (true) {
@@ -675,7 +704,7 @@ static size_t train_smem_bytes(int max_batch) {
 }
 
 static int train_grid(const fs_train_desc* d) {
-  int g = d->grid > 0 ? d->grid : 2 * kNumSMs;
+  int g = d->grid > 0 ? d->grid : TRAIN_CTAS_PER_SM * kNumSMs;
   return g < d->n_req ? g : d->n_req;
 }
 
@@ -687,7 +716,7 @@ extern "C" size_t fs_train_workspace_bytes(const fs_train_desc* d) {
   MlpLayout lay;
   if (!d || make_layout(d->dims, d->n_dims, &lay) != FS_OK || d->n_req < 1) return 0;
   const int grid = train_grid(d);
-  return 256 + (size_t)grid * scratch_doubles(lay, d->max_batch) * sizeof(double);
+  return 256 + (size_t)grid * train_scratch_doubles(lay, d->max_batch) * sizeof(double);
 }
 
 extern "C" int fs_train_f64(const fs_train_desc* d, void* stream) {
@@ -719,11 +748,11 @@ extern "C" int fs_train_f64(const fs_train_desc* d, void* stream) {
   TrainArgs a;
   a.lay = lay;
   a.d = *d;
-  a.scratch_per_cta = scratch_doubles(lay, d->max_batch);
+  a.scratch_per_cta = train_scratch_doubles(lay, d->max_batch);
   a.counter = reinterpret_cast<int*>(d->workspace);
   a.scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(d->workspace) + 256);
   if (cudaMemsetAsync(a.counter, 0, sizeof(int), st) != cudaSuccess) return check_launch("memset");
-  const size_t smem = train_smem_bytes(d->max_batch);
+  const size_t smem = sizeof(GemmSmem);
   if (smem > 48 * 1024)
     ensure_smem(train_kernel, (int)smem);
   train_kernel<<<train_grid(d), THREADS, smem, st>>>(a);
