@@ -473,6 +473,20 @@ typedef struct {
   /* opt-in extension (< 0 = off, the reference's unweighted mean): flush
    * means weighted by (1 + staleness) ** -staleness_alpha                  */
   double staleness_alpha;
+  /* client sharding over the ranks of a node (world_size > 1; parallel.py
+   * ownership, server.py:409-417 call sites): every rank runs the same event
+   * loop; a flush trains only the cycles of clients with owner_host[ci] ==
+   * rank, and `exchange` sums a device float64 buffer over the ranks in
+   * place (an all-reduce; called after `stream` is synchronised, must
+   * return with the sum written): once per flush for [aligned | status] of
+   * every pending cycle and once for the float64 partial sums of the
+   * aggregation jobs (each rank sums its own members in canonical order).
+   * world_size <= 1: unsharded, the other fields are ignored.              */
+  int32_t rank;
+  int32_t world_size;
+  const int32_t* owner_host;     /* [n_clients] */
+  int (*exchange)(void* ctx, double* buf, int64_t n, void* stream);
+  void* exchange_ctx;
 } fs_async_device;
 
 fs_async_engine* fs_async_create(const fs_async_world* world);

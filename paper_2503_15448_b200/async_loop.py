@@ -69,7 +69,12 @@ class AsyncDevice(ctypes.Structure):
                 ("dropout_rate", _f64), ("align_mode", _i32), ("theta", _f64), ("master_seed", ctypes.c_uint64),
                 ("base_lr", _f64), ("lr_decay", _f64), ("grid", _i32), ("features", _vp), ("labels", _vp),
                 ("row_off_host", _vp), ("n_rows_host", _vp), ("batch_host", _vp), ("w0", _vp), ("w0_prev", _vp),
-                ("stream", _vp), ("staleness_alpha", _f64)]
+                ("stream", _vp), ("staleness_alpha", _f64), ("rank", _i32), ("world_size", _i32),
+                ("owner_host", _vp), ("exchange", _vp), ("exchange_ctx", _vp)]
+
+
+# fs_async_device.exchange: sums a device float64 buffer over the ranks in place
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _vp, _i64, _vp)
 
 
 class AsyncLogView(ctypes.Structure):

@@ -435,6 +435,14 @@ struct DeviceExec {
   size_t next_stream = 0;
   std::vector<std::pair<void*, cudaEvent_t>> deferred_free;  // freed once the event completes
   int32_t low_version = 0;                    // versions below are released
+  // ---- client sharding (fs_async_device.world_size > 1): this rank trains
+  // the cycles of the clients it owns; outcomes and aggregation partials are
+  // summed over the ranks through d.exchange (ShardedAsyncExecutor's scheme)
+  bool sharded = false;
+  std::vector<int32_t> owner;
+  std::vector<uint8_t> row_owned;             // deferred id -> this rank holds its accepted row
+  double* d_x = nullptr;                      // exchange buffer
+  size_t x_cap = 0;
   double t_poll = 0, t_jobs = 0, t_batch = 0, t_look = 0, t_alloc = 0, t_copy = 0, t_launch = 0;
   int64_t perm_at(int32_t ci, int32_t p) const { return p * perm_sum + perm_pre[ci]; }
   int64_t mask_at(int32_t ci, int32_t p) const { return p * mask_sum + mask_pre[ci]; }
@@ -471,6 +479,7 @@ struct DeviceExec {
     if (d_ws) cudaFreeAsync(d_ws, st);
     if (d_sorted) cudaFreeAsync(d_sorted, st);
     if (d_res) cudaFreeAsync(d_res, st);
+    if (d_x) cudaFreeAsync(d_x, st);
     if (d_stage) cudaFreeAsync(d_stage, st);
     if (side) {
       cudaStreamSynchronize(side);
@@ -612,18 +621,43 @@ struct DeviceExec {
     // the side stream may only touch the slots once they are allocated
     if (int rc = cuda(cudaEventRecord(side_done, st), "event")) return rc;
     if (int rc = cuda(cudaStreamWaitEvent(side, side_done, 0), "event")) return rc;
-    percycle = d.bf16 && d.n_dims == 5 && (d.dims[1] == 128 || d.dims[1] == 256) && d.dims[2] == 128 &&
-               d.dims[3] == 64 && d.dims[0] <= 64;
+    sharded = d.world_size > 1;
+    if (sharded) {
+      if (!d.owner_host || !d.exchange || d.rank < 0 || d.rank >= d.world_size || d.staleness_alpha >= 0.0) {
+        fs::set_error("async device: sharding needs owner_host, exchange and 0 <= rank < world_size "
+                      "(staleness weighting runs unsharded)");
+        return FS_EINVAL;
+      }
+      owner.assign(d.owner_host, d.owner_host + n_clients);
+    }
+    percycle = !sharded && d.bf16 && d.n_dims == 5 && (d.dims[1] == 128 || d.dims[1] == 256) &&
+               d.dims[2] == 128 && d.dims[3] == 64 && d.dims[0] <= 64;
     if (percycle) {
       stream_pool.resize(8);
       for (auto& ps : stream_pool)
         if (int rc = cuda(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "pool stream")) return rc;
     }
     // cycle 0 of every client, in bulk, while the caller still prepares
-    std::vector<int32_t> all(n_clients), zero(n_clients, 0), slot(n_clients, 0);
-    for (int32_t i = 0; i < n_clients; ++i) all[i] = i;
-    if (C > 0)
-      if (int rc = generate(all.data(), zero.data(), slot.data(), n_clients, side)) return rc;
+    std::vector<int32_t> all, zero, slot;
+    for (int32_t i = 0; i < n_clients; ++i)
+      if (mine(i)) {
+        all.push_back(i);
+        zero.push_back(0);
+        slot.push_back(0);
+      }
+    if (C > 0 && !all.empty())
+      if (int rc = generate(all.data(), zero.data(), slot.data(), (int32_t)all.size(), side)) return rc;
+    return FS_OK;
+  }
+
+  bool mine(int32_t ci) const { return !sharded || owner[ci] == d.rank; }
+  // sum n doubles at d_x over the ranks (the callback runs the collective)
+  int exchange(int64_t n) {
+    if (int rc = cuda(cudaStreamSynchronize(st), "exchange")) return rc;
+    if (d.exchange(d.exchange_ctx, d_x, n, st) != 0) {
+      fs::set_error("async device: exchange callback failed");
+      return FS_EINVAL;
+    }
     return FS_OK;
   }
 
@@ -691,9 +725,79 @@ struct DeviceExec {
   }
 
   // aggregation jobs queued by the event loop, one launch pair
+  // sharded aggregation jobs: this rank's members of every job summed in
+  // canonical order into float64 partials, one exchange, means on every rank
+  // (model versions stay replicated; the sum re-associates across ranks, so
+  // they are tolerance-matched to one GPU like the sync path)
+  int launch_jobs_sharded(fs_async_engine* e) {
+    const int32_t nj = (int32_t)e->job_version.size();
+    int64_t blk;
+    void* base;
+    if (int rc = alloc_block((size_t)nj * ldw * esz, nj, &blk, &base)) return rc;
+    std::vector<uint64_t> outs(nj);
+    for (int32_t j = 0; j < nj; ++j) {
+      outs[j] = (uint64_t)base + (uint64_t)j * ldw * esz;
+      if ((int32_t)version.size() != e->job_version[j]) {
+        fs::set_error("async device: versions out of order");
+        return FS_EINVAL;
+      }
+      version.push_back({outs[j], blk});
+    }
+    if (int rc = grow((void**)&d_x, &x_cap, 8 * (size_t)nj * M, "exchange buffer")) return rc;
+    if (int rc = cuda(cudaMemsetAsync(d_x, 0, 8 * (size_t)nj * M, st), "partials")) return rc;
+    std::vector<std::vector<uint64_t>> own(nj);
+    size_t staged = 0, max_own = 1;
+    for (int32_t j = 0; j < nj; ++j) {
+      for (int64_t i = e->job_off[j]; i < e->job_off[j + 1]; ++i) {
+        const int32_t m = e->job_member[i];
+        if (m < (int32_t)row_owned.size() && row_owned[m]) own[j].push_back(row_ptr[m]);
+      }
+      staged += 16 * own[j].size() + 16;
+      max_own = std::max(max_own, own[j].size());
+    }
+    if (int rc = stage_reserve(staged + 64)) return rc;
+    std::vector<uint64_t> p_rows(nj, 0);
+    for (int32_t j = 0; j < nj; ++j)
+      if (!own[j].empty()) p_rows[j] = put(own[j].data(), 8 * own[j].size());
+    if (int rc = commit()) return rc;
+    if (int rc = grow(&d_sorted, &sorted_cap, 8 * max_own, "sorted rows")) return rc;
+    for (int32_t j = 0; j < nj; ++j) {
+      const int32_t k = (int32_t)own[j].size();
+      if (k == 0) continue;
+      const uint64_t* rows = (const uint64_t*)p_rows[j];
+      if (k > 1) {
+        launches += 1;
+        if (int rc = fs_canonical_order(rows, k, M, (int32_t)esz, (uint64_t*)d_sorted, st)) return rc;
+        rows = (const uint64_t*)d_sorted;
+      }
+      launches += 1;
+      if (int rc = fs_sum_rows(rows, k, M, (int32_t)esz, d_x + (size_t)j * M, st)) return rc;
+    }
+    if (int rc = exchange((int64_t)nj * M)) return rc;
+    for (int32_t j = 0; j < nj; ++j) {
+      launches += 1;
+      if (int rc = fs_mean_finish(d_x + (size_t)j * M, e->job_off[j + 1] - e->job_off[j], M, (int32_t)esz,
+                                  (void*)outs[j], st))
+        return rc;
+    }
+    for (int64_t i = 0; i < e->job_off[nj]; ++i) {
+      const int32_t m = e->job_member[i];
+      if (m < (int32_t)row_owned.size() && row_owned[m]) {
+        row_owned[m] = 0;
+        unref(row_block[m]);
+      }
+    }
+    e->job_version.clear();
+    e->job_member.clear();
+    e->job_stale.clear();
+    e->job_off.assign(1, 0);
+    return FS_OK;
+  }
+
   int launch_jobs(fs_async_engine* e) {
     const int32_t nj = (int32_t)e->job_version.size();
     if (nj == 0) return FS_OK;
+    if (sharded) return launch_jobs_sharded(e);
     struct Acc {
       double& t;
       double t0;
@@ -767,10 +871,18 @@ struct DeviceExec {
   }
 
   // one deferred flush: train + score every pending cycle, hand outcomes back
+  // (sharded: this rank's cycles, then one exchange of every outcome)
   int flush(fs_async_engine* e) {
     const double t0 = now_s();
     if (int rc = launch_jobs(e)) return rc;
-    const std::vector<int32_t> ids = e->unevaluated;
+    const std::vector<int32_t>& pending = e->unevaluated;
+    const int32_t K = (int32_t)pending.size();
+    std::vector<int32_t> ids, pos;  // this rank's pending cycles and their index in `pending`
+    for (int32_t i = 0; i < K; ++i)
+      if (mine(e->deferred[pending[i]].ci)) {
+        ids.push_back(pending[i]);
+        pos.push_back(i);
+      }
     const int32_t k = (int32_t)ids.size();
     const int32_t E = d.epochs;
     std::vector<int32_t> ci(k), cyc(k), ver(k);
@@ -778,150 +890,152 @@ struct DeviceExec {
       const Deferred& q = e->deferred[ids[i]];
       ci[i] = q.ci; cyc[i] = q.cycle; ver[i] = q.version;
     }
-    // ---- TrainPlan (device.TrainPlan): slots, offsets, LPT order
-    std::vector<int64_t> i64(3 * (size_t)k);
-    std::vector<int32_t> i32(5 * (size_t)k), slot(k);
-    std::vector<uint64_t> wst(k);
-    std::vector<double> lr((size_t)k * std::max(E, 1));
-    int64_t max_b = 1;
-    std::vector<int64_t> work(k);
-    std::vector<int32_t> miss_ci, miss_cyc, miss_slot;
-    for (int32_t i = 0; i < k; ++i) {
-      const int32_t c = ci[i];
-      if (gen_cycle[2 * (size_t)c] == cyc[i]) slot[i] = 0;
-      else if (gen_cycle[2 * (size_t)c + 1] == cyc[i]) slot[i] = 1;
-      else {  // not generated ahead (first use after a skipped cycle): now, on the main stream
-        slot[i] = gen_cycle[2 * (size_t)c] < gen_cycle[2 * (size_t)c + 1] ? 0 : 1;
-        miss_ci.push_back(c);
-        miss_cyc.push_back(cyc[i]);
-        miss_slot.push_back(slot[i]);
+    int64_t blk = -1;
+    void* wout = nullptr;
+    std::vector<int32_t> scored_ix;
+    if (k > 0) {
+      // ---- TrainPlan (device.TrainPlan): slots, offsets, LPT order
+      std::vector<int64_t> i64(3 * (size_t)k);
+      std::vector<int32_t> i32(5 * (size_t)k), slot(k);
+      std::vector<uint64_t> wst(k);
+      std::vector<double> lr((size_t)k * std::max(E, 1));
+      int64_t max_b = 1;
+      std::vector<int64_t> work(k);
+      std::vector<int32_t> miss_ci, miss_cyc, miss_slot;
+      for (int32_t i = 0; i < k; ++i) {
+        const int32_t c = ci[i];
+        if (gen_cycle[2 * (size_t)c] == cyc[i]) slot[i] = 0;
+        else if (gen_cycle[2 * (size_t)c + 1] == cyc[i]) slot[i] = 1;
+        else {  // not generated ahead (first use after a skipped cycle): now, on the main stream
+          slot[i] = gen_cycle[2 * (size_t)c] < gen_cycle[2 * (size_t)c + 1] ? 0 : 1;
+          miss_ci.push_back(c);
+          miss_cyc.push_back(cyc[i]);
+          miss_slot.push_back(slot[i]);
+        }
       }
-    }
-    if (side_used)  // lookahead of earlier flushes: ordered before this trainer (and any miss writes)
-      if (int rc = cuda(cudaStreamWaitEvent(st, side_done, 0), "event")) return rc;
-    if (!miss_ci.empty()) {
-      misses += (int64_t)miss_ci.size();
-      if (int rc = generate(miss_ci.data(), miss_cyc.data(), miss_slot.data(), (int32_t)miss_ci.size(), st))
+      if (side_used)  // lookahead of earlier flushes: ordered before this trainer (and any miss writes)
+        if (int rc = cuda(cudaStreamWaitEvent(st, side_done, 0), "event")) return rc;
+      if (!miss_ci.empty()) {
+        misses += (int64_t)miss_ci.size();
+        if (int rc = generate(miss_ci.data(), miss_cyc.data(), miss_slot.data(), (int32_t)miss_ci.size(), st))
+          return rc;
+      }
+      for (int32_t i = 0; i < k; ++i) {
+        const int64_t nr = n_rows[ci[i]], b = batch[ci[i]];
+        const int64_t spe = (nr + b - 1) / b, total = (int64_t)E * spe;
+        i64[i] = row_off[ci[i]];
+        i64[k + i] = perm_at(ci[i], slot[i]);
+        i64[2 * k + i] = mask_at(ci[i], slot[i]);
+        i32[i] = (int32_t)nr;
+        i32[k + i] = (int32_t)b;
+        i32[2 * k + i] = 0;
+        i32[3 * k + i] = (int32_t)total;
+        work[i] = total * b;
+        max_b = std::max(max_b, b);
+        const int32_t r = std::min(cyc[i], e->rounds - 1);
+        const double l = d.base_lr * std::pow(d.lr_decay, (double)r);  // lr_schedule (model.py:224-230)
+        for (int32_t ep = 0; ep < std::max(E, 1); ++ep) lr[(size_t)i * std::max(E, 1) + ep] = l;
+        wst[i] = version[ver[i]].first;
+      }
+      std::vector<int32_t> order(k);  // longest client first (LPT)
+      for (int32_t i = 0; i < k; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+      for (int32_t i = 0; i < k; ++i) i32[4 * k + i] = order[i];
+      // ---- rows + alignment requests
+      if (int rc = alloc_block((size_t)k * ldw * esz, 1, &blk, &wout)) return rc;
+      std::vector<uint64_t> pc, pg, pp;
+      for (int32_t i = 0; i < k; ++i) {
+        const uint64_t prev = prev_of(ver[i]);
+        if (d.align_mode == FS_ALIGN_DELTA_SIGN && prev == 0) continue;  // no movement history: accept
+        scored_ix.push_back(i);
+        pc.push_back((uint64_t)wout + (uint64_t)i * ldw * esz);
+        pg.push_back(wst[i]);
+        pp.push_back(prev);
+      }
+      const int32_t ns = (int32_t)scored_ix.size();
+      if (int rc = stage_reserve(64 * (size_t)k * (8 + std::max(E, 1)) + 4096)) return rc;
+      const uint64_t p64 = put(i64.data(), 8 * i64.size());
+      const uint64_t p32 = put(i32.data(), 4 * i32.size());
+      const uint64_t plr = put(lr.data(), 8 * lr.size());
+      const uint64_t pws = put(wst.data(), 8 * (size_t)k);
+      uint64_t palign = 0;
+      if (ns) {
+        std::vector<uint64_t> ap(pc);
+        ap.insert(ap.end(), pg.begin(), pg.end());
+        ap.insert(ap.end(), pp.begin(), pp.end());
+        palign = put(ap.data(), 8 * ap.size());
+      }
+      if (int rc = commit()) return rc;
+      const uint64_t row_off_p = p64, perm_off_p = p64 + 8 * k, mask_off_p = p64 + 16 * k;
+      const uint64_t n_rows_p = p32, batch_p = p32 + 4 * k, start_p = p32 + 8 * k, end_p = p32 + 12 * k,
+                     order_p = p32 + 16 * k;
+      const bool masks = d.dropout_rate > 0.0 && E > 0;
+      // ---- K5
+      if (int rc = grow((void**)&d_res, &res_cap, 8 * (size_t)(2 * k + 2), "results")) return rc;
+      int32_t* status = (int32_t*)(d_res + k);
+      if (int rc = cuda(cudaMemsetAsync(status, 0, 4 * (size_t)k, st), "status")) return rc;
+      fs_train_desc t;
+      memset(&t, 0, sizeof(t));
+      t.n_dims = d.n_dims;
+      for (int l = 0; l < d.n_dims; ++l) t.dims[l] = d.dims[l];
+      t.n_req = k;
+      t.epochs = E;
+      t.max_batch = (int32_t)max_b;
+      t.mask_mode = masks ? FS_MASK_BITS : FS_MASK_NONE;
+      t.scale = masks ? 1.0 / (1.0 - d.dropout_rate) : 1.0;
+      t.features = (const double*)d.features;
+      t.labels = (const double*)d.labels;
+      t.row_off = (const int64_t*)row_off_p;
+      t.n_rows = (const int32_t*)n_rows_p;
+      t.batch = (const int32_t*)batch_p;
+      t.lr = (const double*)plr;
+      t.w_start = (const uint64_t*)pws;
+      t.w_out = (double*)wout;
+      t.ldw = ldw;
+      t.perm = (const int32_t*)d_perm_all;
+      t.perm_off = (const int64_t*)perm_off_p;
+      t.mask_bits = masks ? (const uint32_t*)d_bits_all : nullptr;
+      t.mask_off = (const int64_t*)mask_off_p;
+      t.start_step = (const int32_t*)start_p;
+      t.end_step = (const int32_t*)end_p;
+      t.order = (const int32_t*)order_p;
+      t.status = status;
+      t.grid = d.grid;
+      const size_t need = d.bf16 ? fs_train_bf16_workspace_bytes(&t) : fs_train_workspace_bytes(&t);
+      if (need == 0) {
+        fs::set_error("async device: layer dims not supported by the trainer");
+        return FS_EINVAL;
+      }
+      if (int rc = grow(&d_ws, &ws_cap, need, "trainer workspace")) return rc;
+      t.workspace = d_ws;
+      t.workspace_bytes = ws_cap;
+      launches += 1;
+      if (int rc = d.bf16 ? fs_train_bf16(&t, d.features, (const float*)d.labels, st) : fs_train_f64(&t, st))
+        return rc;
+      // ---- lookahead: K2/K3 of every trained client's next cycle, on the side stream
+      {
+        std::vector<int32_t> nci, ncy, nsl;
+        for (int32_t i = 0; i < k; ++i)
+          if (cyc[i] + 1 < C) {
+            nci.push_back(ci[i]);
+            ncy.push_back(cyc[i] + 1);
+            nsl.push_back(1 - slot[i]);
+          }
+        if (!nci.empty())
+          if (int rc = generate(nci.data(), ncy.data(), nsl.data(), (int32_t)nci.size(), side)) return rc;
+      }
+      // ---- K6
+      if (ns) {
+        launches += 1;
+        const uint64_t* a = (const uint64_t*)palign;
+        const int rc = d.bf16 ? fs_sign_align_f32(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st)
+                              : fs_sign_align_f64(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st);
+        if (rc) return rc;
+      }
+      if (int rc = cuda(cudaMemcpyAsync(h_res, d_res, 8 * (size_t)k + 4 * (size_t)k, cudaMemcpyDeviceToHost, st),
+                        "results D2H"))
         return rc;
     }
-    for (int32_t i = 0; i < k; ++i) {
-      const int64_t nr = n_rows[ci[i]], b = batch[ci[i]];
-      const int64_t spe = (nr + b - 1) / b, total = (int64_t)E * spe;
-      i64[i] = row_off[ci[i]];
-      i64[k + i] = perm_at(ci[i], slot[i]);
-      i64[2 * k + i] = mask_at(ci[i], slot[i]);
-      i32[i] = (int32_t)nr;
-      i32[k + i] = (int32_t)b;
-      i32[2 * k + i] = 0;
-      i32[3 * k + i] = (int32_t)total;
-      work[i] = total * b;
-      max_b = std::max(max_b, b);
-      const int32_t r = std::min(cyc[i], e->rounds - 1);
-      const double l = d.base_lr * std::pow(d.lr_decay, (double)r);  // lr_schedule (model.py:224-230)
-      for (int32_t ep = 0; ep < std::max(E, 1); ++ep) lr[(size_t)i * std::max(E, 1) + ep] = l;
-      wst[i] = version[ver[i]].first;
-    }
-    std::vector<int32_t> order(k);  // longest client first (LPT)
-    for (int32_t i = 0; i < k; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-    for (int32_t i = 0; i < k; ++i) i32[4 * k + i] = order[i];
-    // ---- rows + alignment requests
-    int64_t blk;
-    void* wout;
-    if (int rc = alloc_block((size_t)k * ldw * esz, 1, &blk, &wout)) return rc;
-    std::vector<uint64_t> pc, pg, pp;
-    std::vector<int32_t> scored_ix;
-    for (int32_t i = 0; i < k; ++i) {
-      const uint64_t prev = prev_of(ver[i]);
-      if (d.align_mode == FS_ALIGN_DELTA_SIGN && prev == 0) continue;  // no movement history: accept
-      scored_ix.push_back(i);
-      pc.push_back((uint64_t)wout + (uint64_t)i * ldw * esz);
-      pg.push_back(wst[i]);
-      pp.push_back(prev);
-    }
-    const int32_t ns = (int32_t)scored_ix.size();
-    if (int rc = stage_reserve(64 * (size_t)k * (8 + std::max(E, 1)) + 4096)) return rc;
-    const uint64_t p64 = put(i64.data(), 8 * i64.size());
-    const uint64_t p32 = put(i32.data(), 4 * i32.size());
-    const uint64_t plr = put(lr.data(), 8 * lr.size());
-    const uint64_t pws = put(wst.data(), 8 * (size_t)k);
-    uint64_t palign = 0;
-    if (ns) {
-      std::vector<uint64_t> ap(pc);
-      ap.insert(ap.end(), pg.begin(), pg.end());
-      ap.insert(ap.end(), pp.begin(), pp.end());
-      palign = put(ap.data(), 8 * ap.size());
-    }
-    if (int rc = commit()) return rc;
-    const uint64_t row_off_p = p64, perm_off_p = p64 + 8 * k, mask_off_p = p64 + 16 * k;
-    const uint64_t n_rows_p = p32, batch_p = p32 + 4 * k, start_p = p32 + 8 * k, end_p = p32 + 12 * k,
-                   order_p = p32 + 16 * k;
-    const bool masks = d.dropout_rate > 0.0 && E > 0;
-    // ---- K5
-    if (int rc = grow((void**)&d_res, &res_cap, 8 * (size_t)(2 * k + 2), "results")) return rc;
-    int32_t* status = (int32_t*)(d_res + k);
-    if (int rc = cuda(cudaMemsetAsync(status, 0, 4 * (size_t)k, st), "status")) return rc;
-    fs_train_desc t;
-    memset(&t, 0, sizeof(t));
-    t.n_dims = d.n_dims;
-    for (int l = 0; l < d.n_dims; ++l) t.dims[l] = d.dims[l];
-    t.n_req = k;
-    t.epochs = E;
-    t.max_batch = (int32_t)max_b;
-    t.mask_mode = masks ? FS_MASK_BITS : FS_MASK_NONE;
-    t.scale = masks ? 1.0 / (1.0 - d.dropout_rate) : 1.0;
-    t.features = (const double*)d.features;
-    t.labels = (const double*)d.labels;
-    t.row_off = (const int64_t*)row_off_p;
-    t.n_rows = (const int32_t*)n_rows_p;
-    t.batch = (const int32_t*)batch_p;
-    t.lr = (const double*)plr;
-    t.w_start = (const uint64_t*)pws;
-    t.w_out = (double*)wout;
-    t.ldw = ldw;
-    t.perm = (const int32_t*)d_perm_all;
-    t.perm_off = (const int64_t*)perm_off_p;
-    t.mask_bits = masks ? (const uint32_t*)d_bits_all : nullptr;
-    t.mask_off = (const int64_t*)mask_off_p;
-    t.start_step = (const int32_t*)start_p;
-    t.end_step = (const int32_t*)end_p;
-    t.order = (const int32_t*)order_p;
-    t.status = status;
-    t.grid = d.grid;
-    const size_t need = d.bf16 ? fs_train_bf16_workspace_bytes(&t) : fs_train_workspace_bytes(&t);
-    if (need == 0) {
-      fs::set_error("async device: layer dims not supported by the trainer");
-      return FS_EINVAL;
-    }
-    if (int rc = grow(&d_ws, &ws_cap, need, "trainer workspace")) return rc;
-    t.workspace = d_ws;
-    t.workspace_bytes = ws_cap;
-    launches += 1;
-    if (int rc = d.bf16 ? fs_train_bf16(&t, d.features, (const float*)d.labels, st) : fs_train_f64(&t, st))
-      return rc;
-    // ---- lookahead: K2/K3 of every trained client's next cycle, on the side stream
-    {
-      std::vector<int32_t> nci, ncy, nsl;
-      for (int32_t i = 0; i < k; ++i)
-        if (cyc[i] + 1 < C) {
-          nci.push_back(ci[i]);
-          ncy.push_back(cyc[i] + 1);
-          nsl.push_back(1 - slot[i]);
-        }
-      if (!nci.empty())
-        if (int rc = generate(nci.data(), ncy.data(), nsl.data(), (int32_t)nci.size(), side)) return rc;
-    }
-    // ---- K6
-    if (ns) {
-      launches += 1;
-      const uint64_t* a = (const uint64_t*)palign;
-      const int rc = d.bf16 ? fs_sign_align_f32(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st)
-                            : fs_sign_align_f64(a, a + ns, a + 2 * ns, ns, M, d.align_mode, d_res, st);
-      if (rc) return rc;
-    }
-    if (int rc = cuda(cudaMemcpyAsync(h_res, d_res, 8 * (size_t)k + 4 * (size_t)k, cudaMemcpyDeviceToHost, st),
-                      "results D2H"))
-      return rc;
     const double t1 = now_s();
     if (int rc = cuda(cudaStreamSynchronize(st), "flush")) return rc;
     const double t2 = now_s();
@@ -929,40 +1043,72 @@ struct DeviceExec {
     t_wait += t2 - t1;
     stage_reset();
     flushes += 1;
-    const int32_t* h_status = (const int32_t*)(h_res + k);
-    for (int32_t i = 0; i < k; ++i)
-      if (h_status[i]) {  // lowest pending index, as the serial reference would meet it
-        div_client = e->cid[ci[i]];
-        div_cycle = cyc[i];
+    // ---- outcomes of every pending cycle: [aligned | status] by position in `pending`
+    std::vector<int64_t> aligned(K, 0), stat(K, 0);
+    {
+      const int32_t* h_status = (const int32_t*)(h_res + k);
+      for (int32_t s = 0; s < (int32_t)scored_ix.size(); ++s) aligned[pos[scored_ix[s]]] = h_res[s];
+      for (int32_t i = 0; i < k; ++i) stat[pos[i]] = h_status[i];
+    }
+    if (sharded) {  // every rank's outcomes (counts < 2^53: exact in float64)
+      if (int rc = grow((void**)&d_x, &x_cap, 16 * (size_t)std::max(K, 1), "exchange buffer")) return rc;
+      std::vector<double> hx(2 * (size_t)K);
+      for (int32_t i = 0; i < K; ++i) {
+        hx[i] = (double)aligned[i];
+        hx[K + i] = (double)stat[i];
+      }
+      if (K > 0) {
+        if (int rc = cuda(cudaMemcpyAsync(d_x, hx.data(), 16 * (size_t)K, cudaMemcpyHostToDevice, st), "outcomes"))
+          return rc;
+        if (int rc = exchange(2 * (int64_t)K)) return rc;
+        if (int rc = cuda(cudaMemcpyAsync(hx.data(), d_x, 16 * (size_t)K, cudaMemcpyDeviceToHost, st), "outcomes"))
+          return rc;
+        if (int rc = cuda(cudaStreamSynchronize(st), "outcomes")) return rc;
+      }
+      for (int32_t i = 0; i < K; ++i) {
+        aligned[i] = (int64_t)hx[i];
+        stat[i] = (int64_t)hx[K + i];
+      }
+    }
+    for (int32_t i = 0; i < K; ++i)
+      if (stat[i]) {  // lowest pending index, as the serial reference would meet it
+        const Deferred& q = e->deferred[pending[i]];
+        div_client = e->cid[q.ci];
+        div_cycle = q.cycle;
         fs::set_error("loss became non-finite training client %d cycle %d", div_client, div_cycle);
         return FS_EDIVERGED;
       }
     // ---- outcomes (selection.filter_update: ratio >= theta, inclusive)
-    std::vector<uint8_t> acc(k, 1);
-    std::vector<double> rel(k, NAN);
-    for (int32_t s = 0; s < ns; ++s) {
-      const int32_t i = scored_ix[s];
-      const double r = (double)h_res[s] / (double)M;
+    std::vector<uint8_t> acc(K, 1);
+    std::vector<double> rel(K, NAN);
+    for (int32_t i = 0; i < K; ++i) {
+      const Deferred& q = e->deferred[pending[i]];
+      if (d.align_mode == FS_ALIGN_DELTA_SIGN && prev_of(q.version) == 0) continue;  // unscored: accepted
+      const double r = (double)aligned[i] / (double)M;
       rel[i] = r;
       acc[i] = r >= d.theta;
     }
-    int64_t n_acc = 0;
     if ((int64_t)row_ptr.size() < (int64_t)e->deferred.size()) {
       row_ptr.resize(e->deferred.size() * 2 + 16, 0);
       row_block.resize(e->deferred.size() * 2 + 16, -1);
     }
+    if (sharded && row_owned.size() < row_ptr.size()) row_owned.resize(row_ptr.size(), 0);
+    int64_t n_acc = 0;
     for (int32_t i = 0; i < k; ++i)
-      if (acc[i]) {
+      if (acc[pos[i]]) {
         row_ptr[ids[i]] = (uint64_t)wout + (uint64_t)i * ldw * esz;
         row_block[ids[i]] = blk;
+        if (sharded) row_owned[ids[i]] = 1;
         ++n_acc;
       }
-    blocks[blk].refs = n_acc;
-    if (n_acc == 0) {  // nothing to aggregate from this flush
-      cudaFreeAsync(blocks[blk].ptr, st);
-      blocks[blk].ptr = nullptr;
+    if (blk >= 0) {
+      blocks[blk].refs = n_acc;
+      if (n_acc == 0) {  // nothing to aggregate from this flush
+        cudaFreeAsync(blocks[blk].ptr, st);
+        blocks[blk].ptr = nullptr;
+      }
     }
-    e->provide(k, acc.data(), rel.data());
+    e->provide(K, acc.data(), rel.data());
     t_post += now_s() - t2;
     // every deferred cycle is trained: later ones fetch the newest version
     const int32_t latest = (int32_t)version.size() - 1;

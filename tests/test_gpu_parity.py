@@ -379,18 +379,23 @@ def test_engine_matches_oracle_at_road_shape(mode):
     assert rel_err(st.w_g.values, wg) < 1e-12
 
 
-@pytest.mark.parametrize("prec,mode,sel,shape", [("fp64", "sync_filtered", "delta_sign", ""),
-                                                 ("bf16", "sync_filtered", "delta_sign", ""),
-                                                 ("fp64", "async_filtered", "weight_sign", ""),
-                                                 ("bf16", "async_filtered", "weight_sign", ""),
-                                                 ("fp64", "sync_filtered", "delta_sign", "c5"),
-                                                 ("bf16", "sync_filtered", "delta_sign", "c5")])
-def test_client_sharded_rounds_match_single_process(prec, mode, sel, shape):
+@pytest.mark.parametrize("prec,mode,sel,shape,engine", [("fp64", "sync_filtered", "delta_sign", "-", "device"),
+                                                        ("bf16", "sync_filtered", "delta_sign", "-", "device"),
+                                                        ("fp64", "async_filtered", "weight_sign", "-", "device"),
+                                                        ("bf16", "async_filtered", "weight_sign", "-", "device"),
+                                                        ("bf16", "async_filtered", "delta_sign", "-", "device"),
+                                                        ("fp64", "async_filtered", "weight_sign", "-", "native"),
+                                                        ("bf16", "async_filtered", "weight_sign", "-", "native"),
+                                                        ("fp64", "sync_filtered", "delta_sign", "c5", "device"),
+                                                        ("bf16", "sync_filtered", "delta_sign", "c5", "device")])
+def test_client_sharded_rounds_match_single_process(prec, mode, sel, shape, engine):
     """Two ranks (sharing the one GPU over gloo) run the client-sharded engines
     (parallel.py ownership; sync: selection, partial sum, packing and one
     all-reduce per round on the device; async: one all-reduce of the outcomes
-    per flush and of the job partial sums) and reproduce the single-process
-    event log and global model; "c5": 8192 clients at Dirichlet alpha 5."""
+    per flush and of the job partial sums — "device": inside the C++ engine's
+    own executor through its exchange hook, "native": ShardedAsyncExecutor)
+    and reproduce the single-process event log and global model; "c5": 8192
+    clients at Dirichlet alpha 5."""
     import os
     import socket
     import subprocess
@@ -403,7 +408,7 @@ def test_client_sharded_rounds_match_single_process(prec, mode, sel, shape):
     env = dict(os.environ, FS_DIST_BACKEND="gloo")
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr",
                           "127.0.0.1", "--master-port", str(port), os.path.join(root, "scripts", "sharded_check.py"),
-                          prec, mode, sel, shape], env=env, capture_output=True, text=True, timeout=900, cwd=root)
+                          prec, mode, sel, shape, engine], env=env, capture_output=True, text=True, timeout=900, cwd=root)
     assert "SHARDED OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
 
 
