@@ -181,6 +181,12 @@ typedef struct fs_train_desc {
   int32_t optimizer;
   double adam_beta1, adam_beta2, adam_eps;
   void* opt_state;
+  /* max over requests of n_rows[r], or 0 (unknown). The wide bf16 trainer
+   * sizes its factored (low-rank history) mode from it: with SGD and
+   * epochs * max_rows history rows well under the layer width, a client's
+   * weights are kept as its start model plus its own step rows, and the
+   * trained row is written once (fs_train_wide.cu). 0 = dense lockstep.   */
+  int32_t max_rows;
 } fs_train_desc;
 
 #define FS_OPT_SGD 0

@@ -91,6 +91,7 @@ class TrainDesc(ctypes.Structure):
         ("adam_beta2", _c_f64),
         ("adam_eps", _c_f64),
         ("opt_state", _c_vp),
+        ("max_rows", _c_i32),
     ]
 
 

@@ -981,6 +981,7 @@ struct DeviceExec {
       t.n_req = k;
       t.epochs = E;
       t.max_batch = (int32_t)max_b;
+      for (int32_t i = 0; i < k; ++i) t.max_rows = std::max(t.max_rows, n_rows[ci[i]]);
       t.mask_mode = masks ? FS_MASK_BITS : FS_MASK_NONE;
       t.scale = masks ? 1.0 / (1.0 - d.dropout_rate) : 1.0;
       t.features = (const double*)d.features;

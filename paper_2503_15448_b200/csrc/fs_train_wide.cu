@@ -25,6 +25,22 @@
 //         -> master W_l[i][u] -= lr * G (fp32, in the caller's output row) and
 //            its bf16 copy refreshed in the same pass (no separate convert)
 //
+// Factored mode (SGD, few rows per client: BASELINE configs[4]'s ~21-row
+// clients on 1024-wide layers). A client's weights after t steps are its start
+// model plus a low-rank sum, W_l = W0_l - sum_t lr_t H_l(t)^T D_{l+1}(t), of
+// rank <= its rows so far. Instead of streaming and rewriting every client's
+// dense W each step, the trainer keeps W0 (bf16, one copy per distinct start
+// model, L2-resident and shared by every client of the launch) and each
+// client's history rows H_l(t), D_{l+1}(t) (the step's own activations,
+// packed one step after another). A layer product of step t is the shared-W0
+// product plus the history term as extra K chunks of the same MMA chain:
+//   fwd   Z^T = W0^T H^T + Dhist^T P^T,  P[r][q] = -lr H[r] . Hhist[q]  (gram_kernel)
+//   bwd   dH^T = W0 D^T + Hhist^T Q^T,   Q[r][q] = -lr D[r] . Dhist[q]
+// and the trained row is written once, at the end: W_l = W0_l - lr Hhist^T
+// Dhist (mat_kernel). Same SGD (the history term is exact, rounded in fp32
+// instead of through a bf16 copy of W per step); 4 B per parameter per client
+// written once instead of 14 B per parameter per client-step.
+//
 // Units sit on the MMA's M side (128 per tile) and the step's rows on N, so
 // one tcgen05.ld row of TMEM is one unit's values across rows and the
 // activation stores of a warp are 32 consecutive units (64 B). Per
@@ -49,6 +65,7 @@ constexpr int KC = 64;            // K chunk = one 128-byte swizzle row of bf16
 constexpr int UN = 256;           // update tile width along fan-out (MMA N)
 constexpr int STAGES = 4;         // fwd/bwd TMA ring depth
 constexpr int THREADS = 128;
+constexpr int UPD_THREADS_F = 256;         // mat_kernel (the factored mode's weight write)
 constexpr uint32_t A_BYTES = TM * KC * 2;  // 16 KB
 
 __host__ __device__ inline int rup(int x, int m) { return (x + m - 1) / m * m; }
@@ -66,9 +83,19 @@ struct Geo {
   int ldw[MAXL];          // row stride of the bf16 copy of W_l: roundup8(f_{l+1})
   size_t wb_off[MAXL], x_off, h_off[MAXL + 1], d_off[MAXL + 1], y_off, z_off, bp_off[MAXL + 1];
   size_t slot_bytes;
+  // factored mode (fact = 1): activations are history buffers of rha rows
+  // (every step's rows packed), P/Q of one layer [rb x ldpq], and the bf16
+  // start weights live in version blocks of ver_bytes (wb_off within a block)
+  int fact, rha, ldpq;
+  size_t pq_off, ver_bytes;
 };
 
-static bool make(const fs_train_desc* d, Geo* g) {
+constexpr int FACT_MAX_HIST = 512;  // history rows per client (E x rows) the factored mode takes
+constexpr int FACT_VERSIONS = 8;    // distinct start models per launch (bf16 version blocks)
+constexpr int FACT_GROUP = 512;     // clients per factored lockstep group
+
+// fact_hist > 0: factored geometry for histories of up to fact_hist rows
+static bool make(const fs_train_desc* d, Geo* g, int fact_hist = 0) {
   if (make_layout(d->dims, d->n_dims, &g->lay) != FS_OK) return false;
   const MlpLayout& L = g->lay;
   if (L.L < 2 || L.L > MAXL) return false;
@@ -80,6 +107,9 @@ static bool make(const fs_train_desc* d, Geo* g) {
   g->rtiles = g->rb / g->nb;
   g->ld[0] = g->dp;
   for (int l = 1; l <= g->H; ++l) g->ld[l] = rup(L.f[l], 8);
+  g->fact = fact_hist > 0;
+  g->rha = g->fact ? rup(fact_hist + g->rb, KC) : g->rb;
+  g->ldpq = g->rha;
   size_t s = 0;
   auto take = [&](size_t bytes) {
     s = (s + 255) / 256 * 256;
@@ -87,19 +117,29 @@ static bool make(const fs_train_desc* d, Geo* g) {
     s += bytes;
     return at;
   };
-  for (int l = 0; l < g->H; ++l) {
-    g->ldw[l] = rup(L.f[l + 1], 8);
-    g->wb_off[l] = take((size_t)L.f[l] * g->ldw[l] * 2);
+  for (int l = 0; l < g->H; ++l) g->ldw[l] = rup(L.f[l + 1], 8);
+  if (g->fact) {  // start weights: one bf16 copy per version block, not per slot
+    size_t v = 0;
+    for (int l = 0; l < g->H; ++l) {
+      v = (v + 255) / 256 * 256;
+      g->wb_off[l] = v;
+      v += (size_t)L.f[l] * g->ldw[l] * 2;
+    }
+    g->ver_bytes = (v + 255) / 256 * 256;
+  } else {
+    for (int l = 0; l < g->H; ++l) g->wb_off[l] = take((size_t)L.f[l] * g->ldw[l] * 2);
+    g->ver_bytes = 0;
   }
-  g->x_off = take((size_t)g->rb * g->dp * 2);
+  g->x_off = take((size_t)g->rha * g->dp * 2);
   for (int l = 1; l <= g->H; ++l) {
-    g->h_off[l] = take((size_t)g->rb * g->ld[l] * 2);
-    g->d_off[l] = take((size_t)g->rb * g->ld[l] * 2);
+    g->h_off[l] = take((size_t)g->rha * g->ld[l] * 2);
+    g->d_off[l] = take((size_t)g->rha * g->ld[l] * 2);
     g->bp_off[l] = g->rtiles > 1 ? take((size_t)g->rtiles * L.f[l] * 4) : 0;
   }
   g->h_off[0] = g->x_off;
   g->y_off = take((size_t)g->rb * 4 * 2);  // labels, dz
   g->z_off = take((size_t)g->rb * zparts(L.f[g->H]) * 4);
+  g->pq_off = g->fact ? take((size_t)g->rb * g->ldpq * 2) : 0;
   g->slot_bytes = (s + 255) / 256 * 256;
   return true;
 }
@@ -111,6 +151,8 @@ struct StepRow {
   int e, s;          // epoch, step within the epoch
   int global_step;
   float lr;
+  int off;           // factored: first history row of this step (= history rows before it); else 0
+  int wslot;         // factored: version block of the client's start weights
 };
 
 // ------------------------------------------------------------------ setup kernels
@@ -187,6 +229,7 @@ struct StepArgs {
   int adam;
   float b1, b2, eps;
   float* opt;
+  const uint64_t* w_start;    // [n_req] fp32 start rows (factored mode: W0 of the final write)
 };
 
 // SGD as the fp32 masters always did, or the opt-in Adam step of parameter
@@ -211,7 +254,7 @@ __device__ __forceinline__ uint8_t* slot_of(const StepArgs& a, int slot) {
 __global__ void gather_kernel(StepArgs a, const StepRow* rows) {
   const StepRow sr = rows[blockIdx.x];
   uint8_t* sb = slot_of(a, sr.slot);
-  __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(sb + a.g.x_off);
+  __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(sb + a.g.x_off) + (int64_t)sr.off * a.g.dp;
   float* y = reinterpret_cast<float*>(sb + a.g.y_off);
   const int n = a.n_rows[sr.req], B = a.batch[sr.req];
   const int32_t* perm = a.perm + a.perm_off[sr.req] + (int64_t)sr.e * n + (int64_t)sr.s * B;
@@ -259,35 +302,49 @@ __device__ __forceinline__ void ring_free(Ring& R, uint32_t tmem_cols) {
   if (threadIdx.x < 32) tc::tmem_dealloc(R.tmem, tmem_cols);
 }
 
-// fwd/bwd main loop: D[128 x nb] (TMEM) = sum over kchunks of A . B.
-//   A_MN: A box = 64 units x 64 k (two per chunk, units m0 and m0+64), else
-//         one box of 64 k x 128 units; B box = 64 k x nb rows at row r0.
-template <bool A_MN>
-__device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorMap* ta, const CUtensorMap* tb,
-                                         int m0, int r0, int slot, int kchunks, int nb) {
+// One operand phase of a tile's MMA chain: k chunks of A . B from a pair of
+// tensor maps. A MN-major (amn): two boxes of 64 units x 64 k at (m0, k) and
+// (m0 + 64, k); else one box of 64 k x 128 units at (k, m0). B: one box of
+// 64 k x nb rows at (k, brow). aslot / bslot: the maps' 3rd coordinate.
+struct Phase {
+  const CUtensorMap* ta;
+  const CUtensorMap* tb;
+  int k;
+  bool amn;
+  int aslot, bslot, brow;
+};
+
+// fwd/bwd/gram main loop: D[128 x nb] (TMEM) = sum over p1's then p2's chunks
+__device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, int m0, int nb, const Phase& p1, const Phase& p2) {
   const uint32_t stage_bytes = A_BYTES + (uint32_t)nb * 128u;
+  const int total = p1.k + p2.k;
   // one lane of warp 0 produces, one lane of warp 1 issues; their warp
   // siblings park at __syncwarp (a spinning sibling would steal the lane's
   // issue slots: divergent paths of one warp are scheduled in turn)
   if (threadIdx.x == 0) {
-    for (int kc = 0; kc < kchunks; ++kc) {
+    for (int kc = 0; kc < total; ++kc) {
+      const bool first = kc < p1.k;
+      const Phase& P = first ? p1 : p2;
+      const int kl = first ? kc : kc - p1.k;
       const int s = kc % STAGES;
       const uint32_t ph = (uint32_t)(kc / STAGES) & 1u;
       if (kc >= STAGES) tc::mbar_wait(&R.empty[s], ph ^ 1u);
       uint8_t* a = smem + s * stage_bytes;
       uint8_t* b = a + A_BYTES;
       tma::expect_tx(&R.full[s], stage_bytes);
-      if (A_MN) {
-        tma::load_3d(a, ta, m0, kc * KC, slot, &R.full[s]);
-        tma::load_3d(a + 8192, ta, m0 + 64, kc * KC, slot, &R.full[s]);
+      if (P.amn) {
+        tma::load_3d(a, P.ta, m0, kl * KC, P.aslot, &R.full[s]);
+        tma::load_3d(a + 8192, P.ta, m0 + 64, kl * KC, P.aslot, &R.full[s]);
       } else {
-        tma::load_3d(a, ta, kc * KC, m0, slot, &R.full[s]);
+        tma::load_3d(a, P.ta, kl * KC, m0, P.aslot, &R.full[s]);
       }
-      tma::load_3d(b, tb, kc * KC, r0, slot, &R.full[s]);
+      tma::load_3d(b, P.tb, kl * KC, P.brow, P.bslot, &R.full[s]);
     }
   } else if (threadIdx.x == 32) {
-    const uint32_t idesc = tc::idesc_bf16(TM, nb, A_MN, false);
-    for (int kc = 0; kc < kchunks; ++kc) {
+    const uint32_t id1 = tc::idesc_bf16(TM, nb, p1.amn, false), id2 = tc::idesc_bf16(TM, nb, p2.amn, false);
+    for (int kc = 0; kc < total; ++kc) {
+      const bool amn = kc < p1.k ? p1.amn : p2.amn;
+      const uint32_t idesc = kc < p1.k ? id1 : id2;
       const int s = kc % STAGES;
       const uint32_t ph = (uint32_t)(kc / STAGES) & 1u;
       tc::mbar_wait(&R.full[s], ph);
@@ -295,7 +352,7 @@ __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, const CUtensorM
       const uint32_t a = tc::smem_u32(smem + s * stage_bytes), b = a + A_BYTES;
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk) {
-        const uint64_t ad = A_MN ? tma::mnmajor(a, kk, 8192u) : tma::kmajor(a, kk);
+        const uint64_t ad = amn ? tma::mnmajor(a, kk, 8192u) : tma::kmajor(a, kk);
         tc::mma_bf16(R.tmem, ad, tma::kmajor(b, kk), idesc, (kc | kk) != 0);
       }
       tc::mma_commit(&R.empty[s]);
@@ -373,8 +430,11 @@ struct FwdArgs {
   const float* w_eval;
 };
 
+// factored mode: ta2 = Dhist_{l} [q][u] (MN-major), tb2 = P [r][q] (the history term)
 __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CUtensorMap ta,
-                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, FwdArgs f,
+                                                      const __grid_constant__ CUtensorMap tb,
+                                                      const __grid_constant__ CUtensorMap ta2,
+                                                      const __grid_constant__ CUtensorMap tb2, StepArgs a, FwdArgs f,
                                                       const StepRow* rows) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Ring R;
@@ -398,7 +458,12 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CU
   }
   const uint32_t cols = f.nb <= 32 ? 32 : f.nb <= 64 ? 64 : f.nb <= 128 ? 128 : 256;
   ring_init(R, cols);
-  mainloop<true>(R, smem, &ta, &tb, m0, r0, slot, f.kchunks, f.nb);
+  {
+    const bool fact = !f.eval && a.g.fact;
+    const Phase p1{&ta, &tb, f.kchunks, true, fact ? sr.wslot : slot, slot, r0 + sr.off};
+    const Phase p2{&ta2, &tb2, fact ? (sr.off + KC - 1) / KC : 0, true, slot, slot, r0};
+    mainloop(R, smem, m0, f.nb, p1, p2);
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = m0 + threadIdx.x;
@@ -423,7 +488,7 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ CU
         x = fmaxf(v[j] + b, 0.f);
         x = ((keep >> j) & 1u) ? x * sc : 0.f;
       }
-      if (uok && r < rend && c0 + j < f.nb) h[(int64_t)r * f.ld_out + u] = __float2bfloat16_rn(x);
+      if (uok && r < rend && c0 + j < f.nb) h[(int64_t)(sr.off + r) * f.ld_out + u] = __float2bfloat16_rn(x);
       v[j] = x * wh;
     }
     if (f.last) {  // head-logit partial of row r0+c0+lane over this warp's 32 units
@@ -441,8 +506,8 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   const StepRow sr = rows[blockIdx.x];
   const int H = a.g.H, N = a.lay.f[H], ld = a.g.ld[H], rb = a.g.rb;
   uint8_t* sb = slot_of(a, sr.slot);
-  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + a.g.h_off[H]);
-  __nv_bfloat16* dout = reinterpret_cast<__nv_bfloat16*>(sb + a.g.d_off[H]);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + a.g.h_off[H]) + (int64_t)sr.off * ld;
+  __nv_bfloat16* dout = reinterpret_cast<__nv_bfloat16*>(sb + a.g.d_off[H]) + (int64_t)sr.off * ld;
   const float* y = reinterpret_cast<const float*>(sb + a.g.y_off);
   float* dz = reinterpret_cast<float*>(sb + a.g.y_off) + rb;
   float* W = a.w_out + (int64_t)sr.req * a.ldw;
@@ -509,8 +574,11 @@ struct BwdArgs {
   int ld;
 };
 
+// factored mode: ta2 = Hhist_l [q][i] (MN-major), tb2 = Q [r][q] (the history term)
 __global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CUtensorMap ta,
-                                                      const __grid_constant__ CUtensorMap tb, StepArgs a, BwdArgs p,
+                                                      const __grid_constant__ CUtensorMap tb,
+                                                      const __grid_constant__ CUtensorMap ta2,
+                                                      const __grid_constant__ CUtensorMap tb2, StepArgs a, BwdArgs p,
                                                       const StepRow* rows) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Ring R;
@@ -523,13 +591,18 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(const __grid_constant__ CU
   }
   const uint32_t cols = p.nb <= 32 ? 32 : p.nb <= 64 ? 64 : p.nb <= 128 ? 128 : 256;
   ring_init(R, cols);
-  mainloop<false>(R, smem, &ta, &tb, m0, r0, sr.slot, p.kchunks, p.nb);
+  {
+    const bool fact = a.g.fact;
+    const Phase p1{&ta, &tb, p.kchunks, false, fact ? sr.wslot : sr.slot, sr.slot, r0 + sr.off};
+    const Phase p2{&ta2, &tb2, fact ? (sr.off + KC - 1) / KC : 0, true, sr.slot, sr.slot, r0};
+    mainloop(R, smem, m0, p.nb, p1, p2);
+  }
 
   const int i = m0 + threadIdx.x;
   const bool iok = i < p.fin;
   uint8_t* sb = slot_of(a, sr.slot);
-  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + p.h_off);
-  __nv_bfloat16* dl = reinterpret_cast<__nv_bfloat16*>(sb + p.d_off);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(sb + p.h_off) + (int64_t)sr.off * p.ld;
+  __nv_bfloat16* dl = reinterpret_cast<__nv_bfloat16*>(sb + p.d_off) + (int64_t)sr.off * p.ld;
   const float sc = a.mask_mode == FS_MASK_BITS ? a.scale : 1.f;
   float gb = 0.f;
   for (int c0 = 0; c0 < p.nb; c0 += 32) {
@@ -572,6 +645,198 @@ __global__ void bias_reduce_kernel(StepArgs a, const StepRow* rows, int fin, int
   float* b = a.w_out + (int64_t)sr.req * a.ldw + boff + i;
   if (a.adam) *b = opt_apply(a, sr, boff + i, *b, gb);
   else *b -= sr.lr * gb;
+}
+
+// ------------------------------------------------------------------ factored mode
+// P[r][q] = -lr * sum_k A[q][k] cur[r][k] for the history rows q < sr.off of
+// this client (0 beyond), bf16, the B operand of the next fwd/bwd's history
+// phase: A = Hhist_l (fwd) or Dhist_{l+1} (bwd), K-major; cur = this step's
+// rows of the same buffer (at sr.off). TMEM lane = q, columns = rows.
+struct GramArgs {
+  int kchunks, nb;
+  size_t pq_off;
+  int ldpq;
+};
+
+__global__ void __launch_bounds__(THREADS) gram_kernel(const __grid_constant__ CUtensorMap ta,
+                                                       const __grid_constant__ CUtensorMap tb, StepArgs a, GramArgs p,
+                                                       const StepRow* rows) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Ring R;
+  uint8_t* smem = smem_base(smem_raw);
+  const StepRow sr = rows[blockIdx.z];
+  const int q0 = blockIdx.x * TM, r0 = blockIdx.y * p.nb;
+  if (q0 >= sr.off) return;  // this client has no history rows in the tile (uniform per CTA)
+  if (threadIdx.x == 0) {
+    tma::prefetch_map(&ta);
+    tma::prefetch_map(&tb);
+  }
+  const uint32_t cols = p.nb <= 32 ? 32 : p.nb <= 64 ? 64 : p.nb <= 128 ? 128 : 256;
+  ring_init(R, cols);
+  const Phase p1{&ta, &tb, p.kchunks, false, sr.slot, sr.slot, r0 + sr.off};
+  const Phase none{&ta, &tb, 0, false, 0, 0, 0};
+  mainloop(R, smem, q0, p.nb, p1, none);
+  const int q = q0 + threadIdx.x;
+  const float nlr = q < sr.off ? -sr.lr : 0.f;
+  __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(slot_of(a, sr.slot) + p.pq_off);
+  for (int c0 = 0; c0 < p.nb; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(lane_addr(R.tmem, c0), v);
+    if (q < p.ldpq) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < p.nb) P[(int64_t)(r0 + c0 + j) * p.ldpq + q] = __float2bfloat16_rn(nlr * v[j]);
+    }
+  }
+  ring_free(R, cols);
+}
+
+// the factored trainer's only write of the weights: W_l[i][u] = W0_l[i][u]
+// - lr * sum_q Hhist_l[q][i] Dhist_{l+1}[q][u] over the client's sr.off
+// history rows (A = Hhist MN-major, B = Dhist MN-major, as upd_kernel)
+struct MatArgs {
+  int fin, fout;
+  int64_t woff;
+};
+
+__global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb, StepArgs a,
+                                                            MatArgs p, const StepRow* rows) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Ring R;
+  uint8_t* smem = smem_base(smem_raw);
+  const StepRow sr = rows[blockIdx.z];
+  const int i0 = blockIdx.x * TM, u0 = blockIdx.y * UN;
+  const int nu = min(UN, p.fout - u0);
+  const int nmma = rup(nu, 16), nbox = (nu + 63) / 64;
+  const int kchunks = max(1, (sr.off + KC - 1) / KC);
+  const uint32_t stage_bytes = A_BYTES + (uint32_t)nbox * 8192u;
+  if (threadIdx.x == 0) {
+    tma::prefetch_map(&ta);
+    tma::prefetch_map(&tb);
+  }
+  ring_init(R, 256);
+  if (threadIdx.x == 0) {
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % 2;
+      const uint32_t ph = (uint32_t)(kc / 2) & 1u;
+      if (kc >= 2) tc::mbar_wait(&R.empty[s], ph ^ 1u);
+      uint8_t* A = smem + s * (A_BYTES + 4 * 8192);
+      uint8_t* B = A + A_BYTES;
+      tma::expect_tx(&R.full[s], stage_bytes);
+      tma::load_3d(A, &ta, i0, kc * KC, sr.slot, &R.full[s]);
+      tma::load_3d(A + 8192, &ta, i0 + 64, kc * KC, sr.slot, &R.full[s]);
+      for (int j = 0; j < nbox; ++j) tma::load_3d(B + j * 8192, &tb, u0 + 64 * j, kc * KC, sr.slot, &R.full[s]);
+    }
+  } else if (threadIdx.x == 32) {
+    const uint32_t idesc = tc::idesc_bf16(TM, nmma, true, true);
+    for (int kc = 0; kc < kchunks; ++kc) {
+      const int s = kc % 2;
+      const uint32_t ph = (uint32_t)(kc / 2) & 1u;
+      tc::mbar_wait(&R.full[s], ph);
+      tc::fence_after_sync();
+      const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + 4 * 8192)), B = A + A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk)
+        tc::mma_bf16(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
+      tc::mma_commit(&R.empty[s]);
+    }
+    tc::mma_commit(&R.done);
+  }
+  __syncwarp();
+  tc::mbar_wait(&R.done, 0);
+  tc::fence_after_sync();
+
+  // epilogue as upd_kernel's: TMEM -> registers -> shared transpose -> whole
+  // 128-byte row segments; W0 (the shared start row, L2) read, W written once
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = warp & 3;
+  const int nchunk = (nmma + 31) / 32;
+  const float nlr = -sr.lr;
+  float* T = reinterpret_cast<float*>(smem) + warp * (32 * 36);
+  const int rr0 = lane >> 3, cc = (lane & 7) * 4;
+  const int64_t base = p.woff + (int64_t)(i0 + q * 32) * p.fout + u0;
+  float* wbase = a.w_out + (int64_t)sr.req * a.ldw + base;
+  const float* w0 = reinterpret_cast<const float*>(a.w_start[sr.req]) + base;
+  const bool vec = (p.fout % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.w_out + p.woff) & 15) == 0) &&
+                   ((a.ldw & 3) == 0) && ((reinterpret_cast<uintptr_t>(w0 - base + p.woff) & 15) == 0);
+  auto row_ok = [&](int pp) { return i0 + q * 32 + 4 * pp + rr0 < p.fin; };
+  for (int c = warp >> 2; c < nchunk; c += 2) {
+    float g[32];
+    tc::tmem_ld32(lane_addr(R.tmem, 32 * c), g);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4*>(T + lane * 36 + 4 * k) = make_float4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int pp = 0; pp < 8; ++pp) {
+      if (!row_ok(pp)) continue;
+      const int row = 4 * pp + rr0;
+      if (vec && 32 * c + cc + 4 <= nu) {
+        const float4 g4 = *reinterpret_cast<const float4*>(T + row * 36 + cc);
+        float4 w = __ldg(reinterpret_cast<const float4*>(w0 + (int64_t)row * p.fout + 32 * c + cc));
+        w.x = fmaf(nlr, g4.x, w.x);
+        w.y = fmaf(nlr, g4.y, w.y);
+        w.z = fmaf(nlr, g4.z, w.z);
+        w.w = fmaf(nlr, g4.w, w.w);
+        __stcs(reinterpret_cast<float4*>(wbase + (int64_t)row * p.fout + 32 * c + cc), w);
+      } else {
+        for (int e = 0; e < 4; ++e) {
+          const int u = 32 * c + cc + e;
+          if (u >= nu) break;
+          wbase[(int64_t)row * p.fout + u] = fmaf(nlr, T[row * 36 + cc + e], w0[(int64_t)row * p.fout + u]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  ring_free(R, 256);
+}
+
+// biases and head of every listed request from its start row (factored
+// mode: the weight blocks are written by mat_kernel at the end)
+__global__ void init_small_kernel(const uint64_t* w_start, const int* reqs, int n, MlpLayout L, float* w_out,
+                                  int64_t ldw) {
+  const int a = blockIdx.y;
+  if (a >= n) return;
+  const int r = reqs[a];
+  const float* src = reinterpret_cast<const float*>(w_start[r]);
+  float* dst = w_out + (int64_t)r * ldw;
+  for (int l = 0; l < L.L; ++l) {
+    const int64_t b0 = L.boff[l], nb = L.f[l + 1];
+    for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x)
+      dst[b0 + j] = src[b0 + j];
+  }
+  const int H = L.L - 1;  // head weights [f_H]
+  for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < L.f[H]; j += (int64_t)gridDim.x * blockDim.x)
+    dst[L.woff[H] + j] = src[L.woff[H] + j];
+}
+
+// bf16 copy of the hidden weight matrices of each distinct start model
+struct VerArgs {
+  MlpLayout lay;
+  int H;
+  int ldw[MAXL];
+  size_t wb_off[MAXL];
+  size_t ver_bytes;
+  uint8_t* vers;
+  const uint64_t* src;  // [nver] fp32 start rows
+};
+
+__global__ void version_convert_kernel(VerArgs c) {
+  const float* m = reinterpret_cast<const float*>(c.src[blockIdx.y]);
+  uint8_t* vb = c.vers + (size_t)blockIdx.y * c.ver_bytes;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int l = 0; l < c.H; ++l) {
+    const int fin = c.lay.f[l], fout = c.lay.f[l + 1];
+    const float* src = m + c.lay.woff[l];
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(vb + c.wb_off[l]);
+    const int64_t total = (int64_t)fin * fout;
+    for (int64_t j = t0; j < total; j += stride) {
+      const int64_t i = j / fout, u = j - i * fout;
+      dst[i * c.ldw[l] + u] = __float2bfloat16_rn(src[j]);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ update
@@ -740,12 +1005,238 @@ inline int upd_smem() { return 1024 + 2 * (int)(A_BYTES + 4 * 8192); }
 
 }  // namespace wide
 
+namespace wide {
+// factored-mode history bound of a descriptor (0: dense only): SGD, a known
+// max_rows, and epochs x max_rows history rows well under the widest layer
+static int fact_bound(const fs_train_desc* d, const MlpLayout& L) {
+  if (d->optimizer != FS_OPT_SGD || d->max_rows < 1 || d->epochs < 1) return 0;
+  const int64_t h = (int64_t)d->epochs * d->max_rows;
+  int wmax = 0;
+  for (int l = 1; l < L.L; ++l) wmax = std::max(wmax, L.f[l]);
+  return (h <= FACT_MAX_HIST && 2 * h <= wmax) ? (int)h : 0;
+}
+static size_t stage_bytes(size_t G) { return 256 + G * sizeof(StepRow) + 4 * G + 64 * FACT_VERSIONS + 1024; }
+}  // namespace wide
+
 size_t wide_workspace_bytes(const fs_train_desc* d) {
   wide::Geo g;
   if (!d || d->n_req < 1 || !wide::make(d, &g)) return 0;
   const size_t G = (size_t)std::min(d->n_req, wide::WIDE_GROUP);
-  return G * g.slot_bytes + 256 + G * sizeof(wide::StepRow) + 4 * G + 1024;
+  size_t need = G * g.slot_bytes + wide::stage_bytes(G);
+  if (const int h = wide::fact_bound(d, g.lay)) {
+    wide::Geo gf;
+    wide::make(d, &gf, h);
+    const size_t Gf = (size_t)std::min(d->n_req, wide::FACT_GROUP);
+    need = std::max(need, Gf * gf.slot_bytes + wide::FACT_VERSIONS * gf.ver_bytes + wide::stage_bytes(Gf));
+  }
+  return need;
 }
+
+namespace wide {
+// the factored lockstep trainer (see the header comment); the caller checked
+// SGD, one lr per client, <= FACT_VERSIONS start models and the history bound
+static int train_factored(const fs_train_desc* d, const Geo& g, StepArgs sa, const std::vector<int32_t>& nr,
+                          const std::vector<int32_t>& bt, const std::vector<int32_t>& s0,
+                          const std::vector<int32_t>& s1, const std::vector<double>& lr,
+                          const std::vector<uint64_t>& wst, cudaStream_t st) {
+  const MlpLayout& L = g.lay;
+  const int n = d->n_req, H = g.H, EL = std::max(d->epochs, 1);
+  const size_t G = (size_t)std::min(n, FACT_GROUP);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d->workspace);
+  uint8_t* slots = ws;
+  uint8_t* vers = ws + G * g.slot_bytes;
+  uint8_t* stage = vers + FACT_VERSIONS * g.ver_bytes;
+  sa.slots = slots;
+  sa.g = g;
+  // distinct start models -> version blocks (bf16 W0 shared by their clients)
+  std::vector<uint64_t> vsrc;
+  std::vector<int> vslot(n);
+  for (int r = 0; r < n; ++r) {
+    auto it = std::find(vsrc.begin(), vsrc.end(), wst[r]);
+    vslot[r] = (int)(it - vsrc.begin());
+    if (it == vsrc.end()) vsrc.push_back(wst[r]);
+  }
+  const int nver = (int)vsrc.size();
+  {
+    cudaMemcpyAsync(stage, vsrc.data(), 8 * (size_t)nver, cudaMemcpyHostToDevice, st);
+    VerArgs va;
+    va.lay = L;
+    va.H = H;
+    for (int l = 0; l < MAXL; ++l) {
+      va.ldw[l] = g.ldw[l];
+      va.wb_off[l] = g.wb_off[l];
+    }
+    va.ver_bytes = g.ver_bytes;
+    va.vers = vers;
+    va.src = reinterpret_cast<const uint64_t*>(stage);
+    version_convert_kernel<<<dim3(256, (unsigned)nver), 256, 0, st>>>(va);
+    if (int rc = check_launch("wide version convert")) return rc;
+  }
+  ensure_smem(fwd_kernel, fwd_smem(g.nb));
+  ensure_smem(bwd_kernel, fwd_smem(g.nb));
+  ensure_smem(gram_kernel, fwd_smem(g.nb));
+  ensure_smem(mat_kernel, upd_smem());
+  int64_t hid_base[MAXL + 1] = {0};
+  for (int l = 2; l <= H; ++l) hid_base[l] = hid_base[l - 1] + L.f[l - 1];
+  // tensor maps over the version blocks (start weights)
+  CUtensorMap fA[MAXL], bA[MAXL];
+  bool ok = true;
+  for (int l = 0; l < H; ++l) {
+    const void* wb = vers + g.wb_off[l];
+    ok = ok && tma::make_map(&fA[l], wb, L.f[l + 1], L.f[l], nver, g.ldw[l], g.ver_bytes, 64);
+    if (l >= 1) ok = ok && tma::make_map(&bA[l], wb, L.f[l + 1], L.f[l], nver, g.ldw[l], g.ver_bytes, 128);
+  }
+  uint8_t* stage2 = stage + 64 * FACT_VERSIONS;  // StepRow[] and request ids
+  for (int g0 = 0; g0 < n; g0 += (int)G) {
+    const int gn = std::min((int)G, n - g0);
+    // per-slot maps: history rows (B of the main term, A of the history term
+    // and of the grams), P/Q
+    CUtensorMap hB[MAXL + 1], hA128[MAXL + 1], hA64[MAXL + 1], dB[MAXL + 1], dA128[MAXL + 1], dA64[MAXL + 1], pq;
+    for (int l = 0; l <= H && ok; ++l) {
+      const int w = L.f[l];
+      const void* hl = slots + g.h_off[l];
+      ok = ok && tma::make_map(&hB[l], hl, w, g.rha, gn, g.ld[l], g.slot_bytes, g.nb);
+      ok = ok && tma::make_map(&hA128[l], hl, w, g.rha, gn, g.ld[l], g.slot_bytes, 128);
+      ok = ok && tma::make_map(&hA64[l], hl, w, g.rha, gn, g.ld[l], g.slot_bytes, 64);
+      if (l >= 1) {
+        const void* dl = slots + g.d_off[l];
+        ok = ok && tma::make_map(&dB[l], dl, w, g.rha, gn, g.ld[l], g.slot_bytes, g.nb);
+        ok = ok && tma::make_map(&dA128[l], dl, w, g.rha, gn, g.ld[l], g.slot_bytes, 128);
+        ok = ok && tma::make_map(&dA64[l], dl, w, g.rha, gn, g.ld[l], g.slot_bytes, 64);
+      }
+    }
+    ok = ok && tma::make_map(&pq, slots + g.pq_off, g.ldpq, g.rb, gn, g.ldpq, g.slot_bytes, g.nb);
+    if (!ok) {
+      set_error("fs_train_bf16 (wide, factored): tensor map encoding failed");
+      return FS_ECUDA;
+    }
+    // every history row may be read before this launch writes it (the last
+    // K chunk of a history term): zero the group's slots once
+    if (cudaMemsetAsync(slots, 0, (size_t)gn * g.slot_bytes, st) != cudaSuccess) return check_launch("wide zero");
+    {
+      std::vector<int> reqs(gn);
+      for (int i = 0; i < gn; ++i) reqs[i] = g0 + i;
+      cudaMemcpyAsync(stage2, reqs.data(), 4 * (size_t)gn, cudaMemcpyHostToDevice, st);
+      init_small_kernel<<<dim3(4, (unsigned)gn), 256, 0, st>>>(d->w_start, reinterpret_cast<const int*>(stage2), gn,
+                                                             L, sa.w_out, d->ldw);
+      if (int rc = check_launch("wide init")) return rc;
+    }
+    std::vector<int> off(gn, 0);
+    int t_end = 0, t_begin = INT32_MAX;
+    for (int i = 0; i < gn; ++i) {
+      t_end = std::max(t_end, s1[g0 + i]);
+      t_begin = std::min(t_begin, s0[g0 + i]);
+    }
+    std::vector<StepRow> rows;
+    for (int t = t_begin; t < t_end; ++t) {
+      rows.clear();
+      int max_off = 0;
+      for (int i = 0; i < gn; ++i) {
+        const int r = g0 + i;
+        if (t < s0[r] || t >= s1[r]) continue;
+        const int spe = (nr[r] + bt[r] - 1) / bt[r];
+        StepRow sr{};
+        sr.req = r;
+        sr.slot = i;
+        sr.e = t / spe;
+        sr.s = t % spe;
+        sr.rows = std::min(bt[r], nr[r] - sr.s * bt[r]);
+        sr.global_step = t;
+        sr.lr = (float)lr[(size_t)r * EL + sr.e];
+        sr.off = off[i];
+        sr.wslot = vslot[r];
+        max_off = std::max(max_off, sr.off);
+        off[i] += sr.rows;
+        rows.push_back(sr);
+      }
+      const int A = (int)rows.size();
+      if (A == 0) continue;
+      cudaMemcpyAsync(stage2, rows.data(), sizeof(StepRow) * A, cudaMemcpyHostToDevice, st);
+      const StepRow* d_rows = reinterpret_cast<const StepRow*>(stage2);
+      gather_kernel<<<A, 256, 0, st>>>(sa, d_rows);
+      if (int rc = check_launch("wide gather")) return rc;
+      const unsigned qt = (unsigned)((max_off + TM - 1) / TM);
+      // ---- forward
+      for (int l = 0; l < H; ++l) {
+        if (qt) {
+          const GramArgs gp{(L.f[l] + KC - 1) / KC, g.nb, g.pq_off, g.ldpq};
+          gram_kernel<<<dim3(qt, (unsigned)g.rtiles, (unsigned)A), THREADS, fwd_smem(g.nb), st>>>(
+              hA128[l], hB[l], sa, gp, d_rows);
+          if (int rc = check_launch("wide gram")) return rc;
+        }
+        FwdArgs f{};
+        f.l = l + 1;
+        f.fin = L.f[l];
+        f.fout = L.f[l + 1];
+        f.nb = g.nb;
+        f.kchunks = (f.fin + KC - 1) / KC;
+        f.last = l + 1 == H;
+        f.zp = zparts(L.f[H]);
+        f.boff = L.boff[l];
+        f.whoff = L.woff[H];
+        f.hid_base = hid_base[l + 1];
+        f.h_off = g.h_off[l + 1];
+        f.z_off = g.z_off;
+        f.ld_out = g.ld[l + 1];
+        fwd_kernel<<<dim3((unsigned)((f.fout + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
+                     fwd_smem(g.nb), st>>>(fA[l], hB[l], dA64[l + 1], pq, sa, f, d_rows);
+        if (int rc = check_launch("wide fwd")) return rc;
+      }
+      head_kernel<<<A, 256, (size_t)g.rb * 4, st>>>(sa, d_rows);
+      if (int rc = check_launch("wide head")) return rc;
+      // ---- backward (no per-step weight update: the history is the update)
+      for (int l = H - 1; l >= 1; --l) {
+        if (qt) {
+          const GramArgs gp{(L.f[l + 1] + KC - 1) / KC, g.nb, g.pq_off, g.ldpq};
+          gram_kernel<<<dim3(qt, (unsigned)g.rtiles, (unsigned)A), THREADS, fwd_smem(g.nb), st>>>(
+              dA128[l + 1], dB[l + 1], sa, gp, d_rows);
+          if (int rc = check_launch("wide gram")) return rc;
+        }
+        BwdArgs p{};
+        p.l = l;
+        p.fin = L.f[l];
+        p.fout = L.f[l + 1];
+        p.nb = g.nb;
+        p.kchunks = (p.fout + KC - 1) / KC;
+        p.boff = L.boff[l - 1];
+        p.h_off = g.h_off[l];
+        p.d_off = g.d_off[l];
+        p.bp_off = g.bp_off[l];
+        p.ld = g.ld[l];
+        bwd_kernel<<<dim3((unsigned)((p.fin + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
+                     fwd_smem(g.nb), st>>>(bA[l], dB[l + 1], hA64[l], pq, sa, p, d_rows);
+        if (int rc = check_launch("wide bwd")) return rc;
+        if (g.rtiles > 1) {
+          bias_reduce_kernel<<<dim3((unsigned)((p.fin + 255) / 256), (unsigned)A), 256, 0, st>>>(sa, d_rows, p.fin,
+                                                                                                p.boff, p.bp_off);
+          if (int rc = check_launch("wide bias")) return rc;
+        }
+      }
+    }
+    // ---- the trained rows: W = W0 - lr Hhist^T Dhist, once per client
+    rows.clear();
+    for (int i = 0; i < gn; ++i) {
+      StepRow sr{};
+      const int r = g0 + i;
+      sr.req = r;
+      sr.slot = i;
+      sr.off = off[i];
+      const int e0 = s0[r] < s1[r] ? s0[r] / ((nr[r] + bt[r] - 1) / bt[r]) : 0;
+      sr.lr = (float)lr[(size_t)r * EL + std::min(e0, EL - 1)];
+      rows.push_back(sr);
+    }
+    cudaMemcpyAsync(stage2, rows.data(), sizeof(StepRow) * gn, cudaMemcpyHostToDevice, st);
+    const StepRow* d_rows = reinterpret_cast<const StepRow*>(stage2);
+    for (int l = 0; l < H; ++l) {
+      const MatArgs m{L.f[l], L.f[l + 1], L.woff[l]};
+      mat_kernel<<<dim3((unsigned)((m.fin + TM - 1) / TM), (unsigned)((m.fout + UN - 1) / UN), (unsigned)gn),
+                   UPD_THREADS_F, upd_smem(), st>>>(hA64[l], dA64[l + 1], sa, m, d_rows);
+      if (int rc = check_launch("wide mat")) return rc;
+    }
+  }
+  return FS_OK;
+}
+}  // namespace wide
 
 int wide_train(const fs_train_desc* d, const void* features_bf16, const float* labels, cudaStream_t st) {
   using namespace wide;
@@ -770,6 +1261,8 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
   cudaMemcpyAsync(s0.data(), d->start_step, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(s1.data(), d->end_step, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(lr.data(), d->lr, 8 * lr.size(), cudaMemcpyDeviceToHost, st);
+  std::vector<uint64_t> wst(n, 0);
+  if (d->w_start) cudaMemcpyAsync(wst.data(), d->w_start, 8 * (size_t)n, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("wide: metadata");
   for (int r = 0; r < n; ++r)
     if (bt[r] > g.rb || bt[r] < 1) {
@@ -810,6 +1303,31 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
   if (sa.adam && (!sa.opt || d->adam_eps <= 0.0)) {
     set_error("fs_train_bf16 (wide): Adam needs opt_state and eps > 0");
     return FS_EINVAL;
+  }
+  sa.w_start = d->w_start;
+  // factored mode when the launch qualifies (one lr per client, few start
+  // models, histories within the workspace's bound); else dense lockstep
+  if (const int bound = fact_bound(d, L)) {
+    const int EL = std::max(d->epochs, 1);
+    bool fact = d->w_start != nullptr;
+    int hmax = 0;
+    std::vector<uint64_t> seen;
+    for (int r = 0; r < n && fact; ++r) {
+      const int spe = (nr[r] + bt[r] - 1) / bt[r];
+      int h = 0;
+      for (int t = s0[r]; t < s1[r]; ++t) {
+        h += std::min(bt[r], nr[r] - (t % spe) * bt[r]);
+        if (lr[(size_t)r * EL + t / spe] != lr[(size_t)r * EL + s0[r] / spe]) fact = false;
+      }
+      hmax = std::max(hmax, h);
+      if (std::find(seen.begin(), seen.end(), wst[r]) == seen.end()) seen.push_back(wst[r]);
+    }
+    fact = fact && hmax <= bound && (int)seen.size() <= FACT_VERSIONS;
+    if (fact) {
+      Geo gf;
+      make(d, &gf, bound);
+      return train_factored(d, gf, sa, nr, bt, s0, s1, lr, wst, st);
+    }
   }
   ConvArgs ca;
   ca.lay = L;
@@ -888,7 +1406,7 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
         const int r = g0 + i;
         if (t < s0[r] || t >= s1[r]) continue;
         const int spe = (nr[r] + bt[r] - 1) / bt[r];
-        StepRow sr;
+        StepRow sr{};
         sr.req = r;
         sr.slot = i;
         sr.e = t / spe;
@@ -921,7 +1439,7 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
         f.z_off = g.z_off;
         f.ld_out = g.ld[l + 1];
         fwd_kernel<<<dim3((unsigned)((f.fout + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
-                     fwd_smem(g.nb), st>>>(fA[l], fB[l], sa, f, d_rows);
+                     fwd_smem(g.nb), st>>>(fA[l], fB[l], fA[l], fB[l], sa, f, d_rows);
         if (int rc = check_launch("wide fwd")) return rc;
       }
       head_kernel<<<A, 256, (size_t)g.rb * 4, st>>>(sa, d_rows);
@@ -941,7 +1459,7 @@ int wide_train(const fs_train_desc* d, const void* features_bf16, const float* l
           p.bp_off = g.bp_off[l];
           p.ld = g.ld[l];
           bwd_kernel<<<dim3((unsigned)((p.fin + TM - 1) / TM), (unsigned)g.rtiles, (unsigned)A), THREADS,
-                       fwd_smem(g.nb), st>>>(bA[l], bB[l], sa, p, d_rows);
+                       fwd_smem(g.nb), st>>>(bA[l], bB[l], bA[l], bB[l], sa, p, d_rows);
           if (int rc = check_launch("wide bwd")) return rc;
           if (g.rtiles > 1) {
             bias_reduce_kernel<<<dim3((unsigned)((p.fin + 255) / 256), (unsigned)A), 256, 0, st>>>(
@@ -1081,7 +1599,7 @@ extern "C" int fs_forward_wide(const int32_t* dims, int32_t n_dims, const float*
     f.z_eval = z;
     f.w_eval = w;
     fwd_kernel<<<dim3((unsigned)((fout + TM - 1) / TM), (unsigned)((rows + EVAL_NB - 1) / EVAL_NB), 1), THREADS,
-                 fwd_smem(EVAL_NB), st>>>(ta, tb, sa, f, nullptr);
+                 fwd_smem(EVAL_NB), st>>>(ta, tb, ta, tb, sa, f, nullptr);
     if (int rc = check_launch("fs_forward_wide layer")) return rc;
     in = hbuf[l & 1];
     ld_in = ld_out;

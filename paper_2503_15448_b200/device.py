@@ -528,6 +528,7 @@ class TrainPlan:
         desc.n_req = self.n
         desc.epochs = self.epochs
         desc.max_batch = int(self.batch.max())
+        desc.max_rows = int(self.n_rows.max())
         desc.mask_mode = N.FS_MASK_BITS if self.bits is not None else N.FS_MASK_NONE
         desc.scale = self.scale
         desc.features = self.shards.features.data_ptr() if self.shards.features is not None else None
