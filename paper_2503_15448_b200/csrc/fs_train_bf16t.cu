@@ -293,8 +293,15 @@ __device__ __noinline__ void client_done(int M, int mode, const float* W, const 
   }
 }
 
-// 184 registers x 256 threads leaves room for one 256-thread block of the next
-// round's K3 (70 registers) on the same SM
+// 184 registers x 256 threads leaves room for one 128-thread block of the next
+// round's K3 (70 registers) on the same SM. Warp 0 issues every stage's MMAs
+// warp-converged (mma_bf16_ws: elect.sync inside the instruction block); a
+// single divergent issuing thread (tid == 0) made the compiler serialise each
+// tcgen05.mma in a per-lane loop with its descriptors moved to uniform
+// registers one by one (~100-240 cycles per MMA; 12.7 -> 12.0 us per 64-row
+// step of the C4 world's longest client, scripts/chain_probe.py). A dedicated
+// ninth MMA warp was measured too: 3 warps on one SM sub-partition cap the
+// registers at 168 and the epilogues then lose more than the issue gains.
 #ifndef FS_D3_QUARTERS
 #define FS_D3_QUARTERS 1
 #endif
@@ -515,12 +522,12 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- F0: H1^T = relu(W0^T X^T + b0) * mask
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t id = idesc_bf16(128, R, false, false);
           for (int ks = 0; ks < fp0 / 16; ++ks)
             for (int mb = 0; mb < MB; ++mb)
-              mma_bf16(tbase + T_ACC + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
-          mma_commit(&mma_bar);
+              mma_bf16_ws(tbase + T_ACC + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
+          mma_commit_ws(&mma_bar);
         }
         {
           wait_mma(&mma_bar, phase);
@@ -549,10 +556,10 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- F1: H2^T = relu(W1^T H1^T + b1) * mask
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t id = idesc_bf16(128, R, true, true);
-          for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16(tbase + T_ACC, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
-          mma_commit(&mma_bar);
+          for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16_ws(tbase + T_ACC, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
+          mma_commit_ws(&mma_bar);
         }
         {
           const int hh = warp >> 2, m = q * 32 + lane;
@@ -575,10 +582,10 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- F2: H3^T = relu(W2^T H2^T + b2) * mask, head logits
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t id = idesc_bf16(128, R, true, true);  // M = 128 over 64 units (upper half unused)
-          for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase + T_ACC, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
-          mma_commit(&mma_bar);
+          for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16_ws(tbase + T_ACC, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
+          mma_commit_ws(&mma_bar);
         }
         if (next_ok && tid >= 64 && tid < 64 + R) {
           // prefetch A: next chunk's row ids and labels, by warps 2-3, which
@@ -717,12 +724,12 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- stage 2: G2 = H2^T D3 (TMEM [0,64)), D2^T = W2 D3^T (TMEM [64,128))
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t idg = idesc_bf16(128, f3, false, false);
-          for (int ks = 0; ks < R / 16; ++ks) mma_bf16(tbase + T_ACC, h2t.kmajor(ks), h3t.kmajor(ks), idg, ks > 0);
+          for (int ks = 0; ks < R / 16; ++ks) mma_bf16_ws(tbase + T_ACC, h2t.kmajor(ks), h3t.kmajor(ks), idg, ks > 0);
           const uint32_t idd = idesc_bf16(128, R, false, true);
-          for (int ks = 0; ks < f3 / 16; ++ks) mma_bf16(tbase + T_D2, w2t.kmajor(ks), h3t.mnmajor(ks), idd, ks > 0);
-          mma_commit(&mma_bar);
+          for (int ks = 0; ks < f3 / 16; ++ks) mma_bf16_ws(tbase + T_D2, w2t.kmajor(ks), h3t.mnmajor(ks), idd, ks > 0);
+          mma_commit_ws(&mma_bar);
         }
         // head and b2 updates while the MMAs run (gradients accumulate over a step's chunks)
         if (tid >= 32 && tid <= 32 + f3) {
@@ -759,16 +766,16 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- stage 1: W1 master += H1^T D2 (TMEM), D1^T = W1 D2^T (TMEM [0, MB*64))
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t idg = idesc_bf16(128, f2, false, false);
           for (int mb = 0; mb < MB; ++mb)
             for (int ks = 0; ks < R / 16; ++ks)
-              mma_bf16(tbase + T_W1 + (uint32_t)(mb * f2), h1t.kmajor(ks, mb), h2t.kmajor(ks), idg, 1u);
+              mma_bf16_ws(tbase + T_W1 + (uint32_t)(mb * f2), h1t.kmajor(ks, mb), h2t.kmajor(ks), idg, 1u);
           const uint32_t idd = idesc_bf16(128, R, false, true);
           for (int mb = 0; mb < MB; ++mb)
             for (int ks = 0; ks < f2 / 16; ++ks)
-              mma_bf16(tbase + T_ACC + (uint32_t)(mb * R), w1t.kmajor(ks, mb), h2t.mnmajor(ks), idd, ks > 0);
-          mma_commit(&mma_bar);
+              mma_bf16_ws(tbase + T_ACC + (uint32_t)(mb * R), w1t.kmajor(ks, mb), h2t.mnmajor(ks), idd, ks > 0);
+          mma_commit_ws(&mma_bar);
         }
         if (tid >= 128 && tid < 128 + f2) {  // b1 += sum(-lr D2)
           const int c = tid - 128;
@@ -798,12 +805,12 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- stage 0: W0^T master += D1^T X (TMEM)
         stage_sync();
-        if (tid == 0) {
+        if (warp == 0) {
           const uint32_t idg = idesc_bf16(128, fp0, false, true);
           for (int mb = 0; mb < MB; ++mb)
             for (int ks = 0; ks < R / 16; ++ks)
-              mma_bf16(tbase + T_W0 + (uint32_t)(mb * fp0), h1t.kmajor(ks, mb), xt.mnmajor(ks), idg, 1u);
-          mma_commit(&mma_bar);
+              mma_bf16_ws(tbase + T_W0 + (uint32_t)(mb * fp0), h1t.kmajor(ks, mb), xt.mnmajor(ks), idg, 1u);
+          mma_commit_ws(&mma_bar);
         }
         if (tid < f1) {  // b0 += sum(-lr D1)
           const float gk = gb0p[tid] + gb0p[256 + tid];
@@ -1007,12 +1014,12 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     }
     // F0
     stage_sync();
-    if (tid == 0) {
+    if (warp == 0) {
       const uint32_t id = idesc_bf16(128, R, false, false);
       for (int ks = 0; ks < fp0 / 16; ++ks)
         for (int mb = 0; mb < MB; ++mb)
-          mma_bf16(tbase + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
-      mma_commit(&mma_bar);
+          mma_bf16_ws(tbase + (uint32_t)(mb * R), w0t.kmajor(ks, mb), xt.kmajor(ks), id, ks > 0);
+      mma_commit_ws(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
     for (int it = warp; it < MB * 8; it += 8) {
@@ -1027,10 +1034,10 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     }
     // F1
     stage_sync();
-    if (tid == 0) {
+    if (warp == 0) {
       const uint32_t id = idesc_bf16(128, R, true, true);
-      for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16(tbase, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
-      mma_commit(&mma_bar);
+      for (int ks = 0; ks < f1 / 16; ++ks) mma_bf16_ws(tbase, w1t.mnmajor(ks), h1t.mnmajor(ks), id, ks > 0);
+      mma_commit_ws(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
     {
@@ -1044,10 +1051,10 @@ __global__ void __launch_bounds__(THREADS, 1) eval_kernel(Geo g, const float* __
     }
     // F2 + head
     stage_sync();
-    if (tid == 0) {
+    if (warp == 0) {
       const uint32_t id = idesc_bf16(128, R, true, true);
-      for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16(tbase, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
-      mma_commit(&mma_bar);
+      for (int ks = 0; ks < f2 / 16; ++ks) mma_bf16_ws(tbase, w2t.mnmajor(ks), h2t.mnmajor(ks), id, ks > 0);
+      mma_commit_ws(&mma_bar);
     }
     wait_mma(&mma_bar, phase);
     if (q < f3 / 32) {

@@ -13,5 +13,6 @@ for n in (64, 128):
         for nacc in (1,):
             if n * nacc > 512:
                 continue
-            row = [lib.probe_mma_latency(s, n, k, nacc, 50) for s in (0, 1, 2, 3)]
-            print(f"N={n:3d} mmas={k:2d} acc={nacc} floor={128 * n // 256 * k:5d}  none={row[0]:6d}  sw128={row[1]:6d}  none-incremental={row[2]:6d}  const={row[3]:6d}")
+            row = [lib.probe_mma_latency(s, n, k, nacc, 50) for s in (0, 1, 2, 3, 8, 11)]
+            print(f"N={n:3d} mmas={k:2d} acc={nacc} floor={128 * n // 256 * k:5d}  none={row[0]:6d}  sw128={row[1]:6d}  "
+                  f"none-incremental={row[2]:6d}  const={row[3]:6d}  | icache thrashed: none={row[4]:6d}  const={row[5]:6d}")

@@ -28,7 +28,18 @@ __device__ __forceinline__ void issue_const(uint32_t d, uint64_t ad, uint64_t bd
   for (int k = 1; k < NM; ++k) mma_acc(d, ad + k * ia, bd + k * ib, idesc);
 }
 
+// ~100 KB of straight-line code: run between repetitions it evicts the
+// instruction caches, as the bf16 trainer's loop body does between stages
+__device__ __noinline__ uint32_t icache_thrash(uint32_t x) {
+#pragma unroll
+  for (int i = 0; i < 2000; ++i) x = (x ^ (x >> 7)) * (0x9E3779B1u + 2u * (uint32_t)i);
+  return x;
+}
+
 __global__ void __launch_bounds__(128) mma_lat_kernel(int swz, int N, int n_mma, int nacc, int reps, long long* out) {
+  const bool thrash = (swz & 8) != 0;
+  swz &= 7;
+  uint32_t sink = threadIdx.x;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -50,6 +61,10 @@ __global__ void __launch_bounds__(128) mma_lat_kernel(int swz, int N, int n_mma,
   uint32_t phase = 0;
   long long total = 0;
   for (int rep = 0; rep < reps; ++rep) {
+    if (thrash) {
+      sink = icache_thrash(sink);
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       const long long t0 = clock64();
       if (swz == 3) {  // + compile-time count and accumulate flag
@@ -98,6 +113,7 @@ __global__ void __launch_bounds__(128) mma_lat_kernel(int swz, int N, int n_mma,
     __syncthreads();
   }
   if (threadIdx.x == 0) out[0] = total / reps;
+  if (sink == 0x12345678u) out[1] = sink;
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc(tbase, 512);
@@ -105,7 +121,7 @@ __global__ void __launch_bounds__(128) mma_lat_kernel(int swz, int N, int n_mma,
 
 extern "C" long long probe_mma_latency(int swz, int N, int n_mma, int nacc, int reps) {
   long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 16);
   const int smem = 1024 + 128 * 1024;
   cudaFuncSetAttribute(mma_lat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   mma_lat_kernel<<<1, 128, smem>>>(swz, N, n_mma, nacc, reps, d);
