@@ -67,6 +67,9 @@ __host__ __device__ inline Lay lay_of(const Geo& g) {
   // 16 KB past the W_2 tile, which lands in the (allocated) W_2 master
   l.w2m = s; s += (uint32_t)(g.f[2] * g.f[3] * 4);
   l.fl = s;  s += (uint32_t)(FL_N * 4);
+  // (one X tile: a second one, staged during the previous chunk's backward
+  // pass, pushes the CTA past the shared memory that lets the next round's
+  // K2 blocks co-reside, and the round loses more than the trainer gains)
   l.total = s;
   return l;
 }
@@ -455,6 +458,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
     int cur = 0;  // s_rowidx_pp / s_y_pp buffer of the current chunk
     uint4 xnext[XPRE];
     MaskRaw mrn;
+    uint32_t kw[4];   // keep words of this warp's forward items (current chunk)
+    uint32_t kwn[4];  // the same for the prefetched next chunk (transposed in the stage-2 MMA shadow)
     // per-client constants, loaded once (the stores into W would otherwise
     // force the compiler to reload them every step)
     const int64_t row_off = a.row_off[rq];
@@ -479,38 +484,41 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         const bool first_chunk = ch == 0;
         // ---------------- gather the chunk's rows (bf16 features) and labels
         const int cpr = fp0 / 8;
-        if (have_next) {
+        if (have_next) {  // staged during the previous chunk: row ids, labels, X rows, keep words
           cur ^= 1;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) kw[k] = kwn[k];
         } else {
           if (tid < R) {
             const int64_t row = tid < rows ? row_off + perm_e[s * B + row0 + tid] : -1;
             s_rowidx_pp[cur][tid] = row;
             s_y_pp[cur][tid] = row >= 0 ? __ldcg(a.labels + row) : 0.f;
           }
-          __syncthreads();
+          named_sync(THREADS);
         }
         FS_PROF(0);
+        {
 #pragma unroll
-        for (int u = 0; u < XPRE; ++u) {
-          const int i = tid + u * THREADS;
-          if (i < R * cpr) {
-            const int r = i / cpr, c = (i % cpr) * 8;
-            uint4 v = xnext[u];
-            if (!have_next) {
-              v = make_uint4(0, 0, 0, 0);
-              if (r < rows) v = __ldcg(reinterpret_cast<const uint4*>(a.feat + s_rowidx_pp[cur][r] * fp0 + c));
+          for (int u = 0; u < XPRE; ++u) {
+            const int i = tid + u * THREADS;
+            if (i < R * cpr) {
+              const int r = i / cpr, c = (i % cpr) * 8;
+              uint4 v = xnext[u];
+              if (!have_next) {
+                v = make_uint4(0, 0, 0, 0);
+                if (r < rows) v = __ldcg(reinterpret_cast<const uint4*>(a.feat + s_rowidx_pp[cur][r] * fp0 + c));
+              }
+              st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
             }
-            st_shared_v4(xt.saddr + xt.off(r, c), v.x, v.y, v.z, v.w);
           }
         }
         FS_PROF(28);
         const int hh_w = warp >> 2;  // row half of this warp's forward items
-        uint32_t kw[4];
         if (!have_next) {
           if (mbits && a.mask_flags) wait_mask_step(a.mask_flags + (int64_t)rq * a.max_steps + step, a.mask_tag);
           mask_issue(mrn, mbits, step_rows, row0, rows, f1, f2, f3, MB, q, hh_w, lane);
+          mask_finish(mrn, mbits != nullptr, step_rows, rows, f1, f2, f3, MB, q, hh_w, lane, kw);
         }
-        mask_finish(mrn, mbits != nullptr, step_rows, rows, f1, f2, f3, MB, q, hh_w, lane, kw);
         FS_PROF(29);
         have_next = false;
         int nstep = step, nch = ch + 1;
@@ -519,6 +527,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           nch = 0;
         }
         const bool next_ok = nstep < step_end;
+        const int nsr = next_ok ? min(B, n - (nstep % spe) * B) : 0;  // next chunk: its step's rows
+        const int nrows = next_ok ? min(R, nsr - nch * R) : 0;        // and its own rows
 
         // ---------------- F0: H1^T = relu(W0^T X^T + b0) * mask
         stage_sync();
@@ -640,14 +650,11 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
         }
         __syncthreads();
         FS_PROF(9);
-        if (next_ok) {  // next chunk's keep-bit words (transposed after the chunk barrier)
-          const int ns = nstep % spe;
-          const int nsr = min(B, n - ns * B);
-          const int nr0 = nch * R;
+        if (next_ok) {  // next chunk's keep-bit words (transposed in the stage-2 MMA shadow)
           if (mask_c && a.mask_flags && nch == 0)
             wait_mask_step(a.mask_flags + (int64_t)rq * a.max_steps + nstep, a.mask_tag);
-          mask_issue(mrn, mask_c ? mask_c + (int64_t)nstep * slot_words : nullptr, nsr, nr0, min(R, nsr - nr0), f1,
-                     f2, f3, MB, q, warp >> 2, lane);
+          mask_issue(mrn, mask_c ? mask_c + (int64_t)nstep * slot_words : nullptr, nsr, nch * R, nrows, f1, f2, f3,
+                     MB, q, warp >> 2, lane);
         }
         if (next_ok) {  // prefetch B: next chunk's feature rows, held in registers
 #pragma unroll
@@ -724,7 +731,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
 
         // ---------------- stage 2: G2 = H2^T D3 (TMEM [0,64)), D2^T = W2 D3^T (TMEM [64,128))
         stage_sync();
-        if (warp == 0) {
+        if (warp == 7) {  // stage 2 issued by warp 7: warp 0 transposes keep words in its shadow
           const uint32_t idg = idesc_bf16(128, f3, false, false);
           for (int ks = 0; ks < R / 16; ++ks) mma_bf16_ws(tbase + T_ACC, h2t.kmajor(ks), h3t.kmajor(ks), idg, ks > 0);
           const uint32_t idd = idesc_bf16(128, R, false, true);
@@ -751,6 +758,8 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           const float acc = first_chunk ? gk : gbacc[f1 + f2 + c] + gk;
           if (last_chunk) bias[f1 + f2 + c] -= lr * acc; else gbacc[f1 + f2 + c] = acc;
         }
+        // the next chunk's keep words, off the chunk-start path
+        if (next_ok && warp != 7) mask_finish(mrn, mask_c != nullptr, nsr, nrows, f1, f2, f3, MB, q, warp >> 2, lane, kwn);
         wait_mma(&mma_bar, phase);
         FS_PROF(14);
         {
@@ -794,6 +803,7 @@ __global__ void __maxnreg__(FS_BF16T_MAXNREG) train_kernel(Args a) {
           }
           if (last_chunk) store_row32(w2t, m, hh * 32, gv);
         }
+        if (next_ok && warp == 7) mask_finish(mrn, mask_c != nullptr, nsr, nrows, f1, f2, f3, MB, q, warp >> 2, lane, kwn);
         wait_mma(&mma_bar, phase);
         FS_PROF(13);
         for (int it = warp; it < MB * 8; it += 8) {
