@@ -169,6 +169,75 @@ __device__ void mask_stream(U128 base_state, U128 inc, int64_t n_draws, uint64_t
 // grid (request, MASK_YSPLIT): block y handles steps y, y + YSPLIT, ... of its
 // request. Warp 0 derives up to 32 step streams at once (one lane each:
 // SeedSequence hashing + PCG64 seeding), then all threads fill their words.
+// K2 for shards of up to 65536 rows: one CTA of SH_THREADS per (request,
+// epoch). The 32-bit draw stream (numpy's buffered next_uint32: low then high
+// half of each PCG64 output) is generated SH_VB values at a time by all
+// threads from LCG jumps; one thread then runs the sequential part alone:
+// random_interval's masked rejection over the buffered values and the
+// Fisher-Yates swaps on a 16-bit index array in shared memory (the next value
+// is loaded ahead of each swap, so a step costs one shared-memory round trip
+// instead of a 128-bit LCG step). Small footprint (2 KB + 2 bytes per row) so
+// these CTAs fit beside the trainer's persistent CTAs.
+constexpr int SH_THREADS = 64;
+constexpr int SH_VB = 512;                       // draws per generated batch
+constexpr int SH_M = SH_VB / 2 / SH_THREADS;     // PCG64 outputs per thread per batch
+__global__ void __launch_bounds__(SH_THREADS)
+    shuffle16_kernel(const uint64_t* seeds, const int32_t* n_rows, const int64_t* perm_off, int epochs,
+                     int32_t* perm_out) {
+  extern __shared__ __align__(16) uint8_t sh_raw[];
+  uint32_t* vbuf = reinterpret_cast<uint32_t*>(sh_raw);     // [SH_VB]
+  uint16_t* a = reinterpret_cast<uint16_t*>(vbuf + SH_VB);  // [n]
+  __shared__ U128 sh_state, sh_inc;
+  __shared__ int sh_i;
+  const int tid = threadIdx.x;
+  const int r = blockIdx.x / epochs, e = blockIdx.x % epochs;
+  const int n = n_rows[r];
+  int32_t* out = perm_out + perm_off[r] + (int64_t)e * n;
+  for (int i = tid; i < n; i += SH_THREADS) a[i] = (uint16_t)i;
+  if (tid == 0) {
+    const Pcg64 g = pcg_shuffle_stream(seeds[r], (uint32_t)e);
+    sh_state = g.state;
+    sh_inc = g.inc;
+  }
+  const LcgJump j_init = lcg_jump((uint64_t)tid * SH_M);   // this thread's first output of a batch
+  const LcgJump j_next = lcg_jump(SH_VB / 2 - SH_M);        // from its last output to the next batch
+  __syncthreads();
+  const U128 inc = sh_inc;
+  U128 st = lcg_apply(j_init, sh_state, inc);
+  int i = n - 1;  // Fisher-Yates position (thread 0)
+  while (n > 1) {
+#pragma unroll
+    for (int j = 0; j < SH_M; ++j) {
+      lcg128_step(st.hi, st.lo, inc.hi, inc.lo);
+      const uint64_t x = xsl_rr(st);
+      const int k = 2 * (tid * SH_M + j);
+      vbuf[k] = (uint32_t)x;
+      vbuf[k + 1] = (uint32_t)(x >> 32);
+    }
+    st = lcg_apply(j_next, st, inc);
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t vn = vbuf[0];
+      for (int c = 1;; ++c) {
+        const uint32_t v = vn & (0xFFFFFFFFu >> __clz(i));  // random_interval(i): smallest 2^k-1 >= i
+        if (c < SH_VB) vn = vbuf[c];
+        if (v <= (uint32_t)i) {
+          const uint16_t ai = a[i], av = a[v];
+          a[i] = av;
+          a[v] = ai;
+          if (--i == 0) break;
+        }
+        if (c == SH_VB) break;
+      }
+      sh_i = i;
+    }
+    __syncthreads();
+    if (sh_i == 0) break;
+  }
+  __syncthreads();
+  for (int k = tid; k < n; k += SH_THREADS) out[k] = a[k];
+}
+
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
                         const int64_t* mask_off, int n_req, int epochs, int sum_hidden, uint64_t thresh,
@@ -310,8 +379,15 @@ extern "C" int fs_shuffle_perms(const uint64_t* seeds, const int32_t* n_rows,
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0) return FS_OK;
-  // each chain is staged in shared memory when it fits (swapping in the
-  // output through L1/L2 with one-warp CTAs measured equal: latency-bound)
+  if (max_rows <= 65536) {
+    const size_t sm16 = SH_VB * sizeof(uint32_t) + (((size_t)max_rows * 2 + 15) & ~(size_t)15);
+    if (sm16 > 48 * 1024) ensure_smem(shuffle16_kernel, (int)sm16);
+    shuffle16_kernel<<<n_req * epochs, SH_THREADS, sm16, (cudaStream_t)stream>>>(seeds, n_rows, perm_off, epochs,
+                                                                                 perm_out);
+    return check_launch("shuffle16_kernel");
+  }
+  // larger shards: int32 chains staged in shared memory when they fit (swapping
+  // in the output through L1/L2 with one-warp CTAs measured equal: latency-bound)
   const size_t smem = (size_t)max_rows * sizeof(int32_t);
   const int use_smem = smem <= 200 * 1024;
   if (use_smem && smem > 48 * 1024)

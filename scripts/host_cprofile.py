@@ -26,3 +26,6 @@ ps = pstats.Stats(pr)
 ps.sort_stats("tottime").print_stats(25)
 ps.sort_stats("cumulative").print_callees("run_trainer")
 ps.sort_stats("cumulative").print_callees("_prefetch_plan")
+ps.sort_stats("cumulative").print_callees("_capture_global")
+ps.sort_stats("cumulative").print_callees("keep")
+ps.sort_stats("cumulative").print_callees("_emit_report")

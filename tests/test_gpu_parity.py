@@ -437,7 +437,8 @@ def test_engine_keeps_caller_vectors_and_checkpoints_intact():
     assert np.array_equal(initial.values, before)
     cps = eng.global_checkpoints
     assert [c.round for c in cps] == [0, 1, 2, 3]
-    assert [c.params.is_on_device for c in cps] == [False, False, False, True]
+    # the newest stays in HBM; the one before it is spilled during the next round's trainer
+    assert [c.params.is_on_device for c in cps] == [False, False, True, True]
     for c, want in zip(cps, seen):
         assert np.array_equal(c.params.values, want)
     assert cps[-1].params is not st.w_g
@@ -474,3 +475,29 @@ def test_run_experiment_writes_reference_run_directory(tmp_path):
     assert params_digest(ck.params) == meta["params_digest"] == params_digest(res.final_params)
     ok, report = replay_run(str(tmp_path))
     assert ok, report
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64, 511, 1000, 1659, 5000, 65536, 70001])
+def test_shuffle_perms_match_numpy_permutation(n):
+    """K2 (fs_shuffle_perms: the 16-bit shared-memory kernel up to 65536 rows,
+    the int32 one above) equals numpy's derive_rng(seed, "shuffle", e).permutation(n)
+    (client.py:136) for every epoch, including the batch-boundary rejection
+    paths of the buffered 32-bit draw stream."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.rng import derive_rng
+
+    rt = D.Runtime.get()
+    epochs = 3
+    seeds_h = np.array([0x9E3779B97F4A7C15 + n, 12345 + 7 * n], dtype=np.uint64)
+    sizes = np.array([n, max(n // 3, 1)], dtype=np.int32)
+    off_h = np.array([0, epochs * n], dtype=np.int64)
+    seeds, nr, off = rt.h2d(seeds_h.view(np.int64)), rt.h2d(sizes), rt.h2d(off_h)
+    perm = torch.empty(int(epochs * sizes.sum()), dtype=torch.int32, device=rt.device)
+    rt.call(rt.lib.fs_shuffle_perms(seeds.data_ptr(), nr.data_ptr(), off.data_ptr(), 2, epochs, int(sizes.max()),
+                                    perm.data_ptr(), rt.stream), "perms")
+    got = perm.cpu().numpy()
+    for r in range(2):
+        for e in range(epochs):
+            want = derive_rng(int(seeds_h[r]), "shuffle", e).permutation(int(sizes[r]))
+            at = int(off_h[r]) + e * int(sizes[r])
+            assert np.array_equal(got[at:at + int(sizes[r])], want), (r, e)
