@@ -340,7 +340,7 @@ def measure_e2e(world, eng, state, reps: int, barrier):
     return 1000.0 / float(np.mean(e2e_ms)), int(h2d), int(d2h)
 
 
-NCU_TRAFFIC_FILE = "profiles/r1_ncu_train_kernel.json"
+NCU_TRAFFIC_FILE = "profiles/r2_ncu_train_kernel.json"
 NCU_TRAFFIC_SOURCE = f"{NCU_TRAFFIC_FILE} (dram read+write bytes, one ncu --set full launch)"
 
 
