@@ -318,9 +318,10 @@ struct Phase {
 __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, int m0, int nb, const Phase& p1, const Phase& p2) {
   const uint32_t stage_bytes = A_BYTES + (uint32_t)nb * 128u;
   const int total = p1.k + p2.k;
-  // one lane of warp 0 produces, one lane of warp 1 issues; their warp
-  // siblings park at __syncwarp (a spinning sibling would steal the lane's
-  // issue slots: divergent paths of one warp are scheduled in turn)
+  // one lane of warp 0 produces (its siblings park at __syncwarp: a spinning
+  // sibling would steal the lane's issue slots), warp 1 issues the MMAs
+  // converged (a divergent single issuing lane serialises every tcgen05.mma
+  // in a per-lane loop)
   if (threadIdx.x == 0) {
     for (int kc = 0; kc < total; ++kc) {
       const bool first = kc < p1.k;
@@ -340,7 +341,7 @@ __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, int m0, int nb,
       }
       tma::load_3d(b, P.tb, kl * KC, P.brow, P.bslot, &R.full[s]);
     }
-  } else if (threadIdx.x == 32) {
+  } else if ((threadIdx.x >> 5) == 1) {  // warp 1 issues, converged (mma_bf16_ws: elect.sync)
     const uint32_t id1 = tc::idesc_bf16(TM, nb, p1.amn, false), id2 = tc::idesc_bf16(TM, nb, p2.amn, false);
     for (int kc = 0; kc < total; ++kc) {
       const bool amn = kc < p1.k ? p1.amn : p2.amn;
@@ -353,11 +354,11 @@ __device__ __forceinline__ void mainloop(Ring& R, uint8_t* smem, int m0, int nb,
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk) {
         const uint64_t ad = amn ? tma::mnmajor(a, kk, 8192u) : tma::kmajor(a, kk);
-        tc::mma_bf16(R.tmem, ad, tma::kmajor(b, kk), idesc, (kc | kk) != 0);
+        tc::mma_bf16_ws(R.tmem, ad, tma::kmajor(b, kk), idesc, (kc | kk) != 0);
       }
-      tc::mma_commit(&R.empty[s]);
+      tc::mma_commit_ws(&R.empty[s]);
     }
-    tc::mma_commit(&R.done);
+    tc::mma_commit_ws(&R.done);
   }
   __syncwarp();
   tc::mbar_wait(&R.done, 0);
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
       tma::load_3d(A + 8192, &ta, i0 + 64, kc * KC, sr.slot, &R.full[s]);
       for (int j = 0; j < nbox; ++j) tma::load_3d(B + j * 8192, &tb, u0 + 64 * j, kc * KC, sr.slot, &R.full[s]);
     }
-  } else if (threadIdx.x == 32) {
+  } else if ((threadIdx.x >> 5) == 1) {  // warp 1 issues, converged (mma_bf16_ws: elect.sync)
     const uint32_t idesc = tc::idesc_bf16(TM, nmma, true, true);
     for (int kc = 0; kc < kchunks; ++kc) {
       const int s = kc % 2;
@@ -738,10 +739,10 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
       const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + 4 * 8192)), B = A + A_BYTES;
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk)
-        tc::mma_bf16(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
-      tc::mma_commit(&R.empty[s]);
+        tc::mma_bf16_ws(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
+      tc::mma_commit_ws(&R.empty[s]);
     }
-    tc::mma_commit(&R.done);
+    tc::mma_commit_ws(&R.done);
   }
   __syncwarp();
   tc::mbar_wait(&R.done, 0);
@@ -879,7 +880,7 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
       tma::load_3d(A + 8192, &ta, i0 + 64, kc * KC, sr.slot, &R.full[s]);
       for (int j = 0; j < nbox; ++j) tma::load_3d(B + j * 8192, &tb, u0 + 64 * j, kc * KC, sr.slot, &R.full[s]);
     }
-  } else if (threadIdx.x == 32) {
+  } else if ((threadIdx.x >> 5) == 1) {  // warp 1 issues, converged (mma_bf16_ws: elect.sync)
     const uint32_t idesc = tc::idesc_bf16(TM, nmma, true, true);
     for (int kc = 0; kc < kchunks; ++kc) {
       const int s = kc % 2;
@@ -889,10 +890,10 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
       const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + 4 * 8192)), B = A + A_BYTES;
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk)
-        tc::mma_bf16(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
-      tc::mma_commit(&R.empty[s]);
+        tc::mma_bf16_ws(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
+      tc::mma_commit_ws(&R.empty[s]);
     }
-    tc::mma_commit(&R.done);
+    tc::mma_commit_ws(&R.done);
   }
   __syncwarp();
   tc::mbar_wait(&R.done, 0);
