@@ -450,7 +450,7 @@ def measure_async(precision: str, windows: int = 2, reps: int = 5):
             "device_batches": eng.device_batches, "events": len(eng.timeline.log), "windows": windows,
             "precision": precision, "gpu_launches": getattr(eng, "async_launches", None),
             "host_s": dict(zip(("prep", "wait", "post"), getattr(eng, "async_host_s", (None,) * 3))),
-            "engine": "C++ event loop + C++ device executor (FS_ASYNC_ENGINE=device)",
+            "engine": "C++ event loop + C++ device executor (server._ASYNC_ENGINE = \"device\")",
             "digest": eng.timeline.digest()}
 
 
