@@ -63,7 +63,10 @@ constexpr int MAXL = FS_MAX_LAYERS;
 constexpr int TM = 128;           // units per tile (MMA M)
 constexpr int KC = 64;            // K chunk = one 128-byte swizzle row of bf16
 constexpr int UN = 256;           // update tile width along fan-out (MMA N)
-constexpr int STAGES = 4;         // fwd/bwd TMA ring depth
+#ifndef FS_WIDE_STAGES
+#define FS_WIDE_STAGES 3
+#endif
+constexpr int STAGES = FS_WIDE_STAGES;  // fwd/bwd TMA ring depth
 constexpr int THREADS = 128;
 constexpr int UPD_THREADS_F = 256;         // mat_kernel (the factored mode's weight write)
 constexpr uint32_t A_BYTES = TM * KC * 2;  // 16 KB
@@ -700,6 +703,9 @@ struct MatArgs {
   int64_t woff;
 };
 
+// 128-wide fan-out tiles (64 KB ring, 128 TMEM columns): three CTAs per SM
+// keep the write stream going while other CTAs run their (short) main loops
+constexpr int UNF = 128;
 __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constant__ CUtensorMap ta,
                                                             const __grid_constant__ CUtensorMap tb, StepArgs a,
                                                             MatArgs p, const StepRow* rows) {
@@ -707,8 +713,8 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
   __shared__ Ring R;
   uint8_t* smem = smem_base(smem_raw);
   const StepRow sr = rows[blockIdx.z];
-  const int i0 = blockIdx.x * TM, u0 = blockIdx.y * UN;
-  const int nu = min(UN, p.fout - u0);
+  const int i0 = blockIdx.x * TM, u0 = blockIdx.y * UNF;
+  const int nu = min(UNF, p.fout - u0);
   const int nmma = rup(nu, 16), nbox = (nu + 63) / 64;
   const int kchunks = max(1, (sr.off + KC - 1) / KC);
   const uint32_t stage_bytes = A_BYTES + (uint32_t)nbox * 8192u;
@@ -716,13 +722,13 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
     tma::prefetch_map(&ta);
     tma::prefetch_map(&tb);
   }
-  ring_init(R, 256);
+  ring_init(R, UNF);
   if (threadIdx.x == 0) {
     for (int kc = 0; kc < kchunks; ++kc) {
       const int s = kc % 2;
       const uint32_t ph = (uint32_t)(kc / 2) & 1u;
       if (kc >= 2) tc::mbar_wait(&R.empty[s], ph ^ 1u);
-      uint8_t* A = smem + s * (A_BYTES + 4 * 8192);
+      uint8_t* A = smem + s * (A_BYTES + (UNF / 64) * 8192);
       uint8_t* B = A + A_BYTES;
       tma::expect_tx(&R.full[s], stage_bytes);
       tma::load_3d(A, &ta, i0, kc * KC, sr.slot, &R.full[s]);
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
       const uint32_t ph = (uint32_t)(kc / 2) & 1u;
       tc::mbar_wait(&R.full[s], ph);
       tc::fence_after_sync();
-      const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + 4 * 8192)), B = A + A_BYTES;
+      const uint32_t A = tc::smem_u32(smem + s * (A_BYTES + (UNF / 64) * 8192)), B = A + A_BYTES;
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk)
         tc::mma_bf16_ws(R.tmem, tma::mnmajor(A, kk, 8192u), tma::mnmajor(B, kk, 8192u), idesc, (kc | kk) != 0);
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(UPD_THREADS_F) mat_kernel(const __grid_constan
     }
     __syncwarp();
   }
-  ring_free(R, 256);
+  ring_free(R, UNF);
 }
 
 // biases and head of every listed request from its start row (factored
@@ -1003,6 +1009,7 @@ __global__ void __launch_bounds__(UPD_THREADS) upd_kernel(const __grid_constant_
 
 inline int fwd_smem(int nb) { return 1024 + STAGES * (int)(A_BYTES + nb * 128); }
 inline int upd_smem() { return 1024 + 2 * (int)(A_BYTES + 4 * 8192); }
+inline int mat_smem() { return 1024 + 2 * (int)(A_BYTES + (UNF / 64) * 8192); }
 
 }  // namespace wide
 
@@ -1076,7 +1083,7 @@ static int train_factored(const fs_train_desc* d, const Geo& g, StepArgs sa, con
   ensure_smem(fwd_kernel, fwd_smem(g.nb));
   ensure_smem(bwd_kernel, fwd_smem(g.nb));
   ensure_smem(gram_kernel, fwd_smem(g.nb));
-  ensure_smem(mat_kernel, upd_smem());
+  ensure_smem(mat_kernel, mat_smem());
   int64_t hid_base[MAXL + 1] = {0};
   for (int l = 2; l <= H; ++l) hid_base[l] = hid_base[l - 1] + L.f[l - 1];
   // tensor maps over the version blocks (start weights)
@@ -1230,8 +1237,8 @@ static int train_factored(const fs_train_desc* d, const Geo& g, StepArgs sa, con
     const StepRow* d_rows = reinterpret_cast<const StepRow*>(stage2);
     for (int l = 0; l < H; ++l) {
       const MatArgs m{L.f[l], L.f[l + 1], L.woff[l]};
-      mat_kernel<<<dim3((unsigned)((m.fin + TM - 1) / TM), (unsigned)((m.fout + UN - 1) / UN), (unsigned)gn),
-                   UPD_THREADS_F, upd_smem(), st>>>(hA64[l], dA64[l + 1], sa, m, d_rows);
+      mat_kernel<<<dim3((unsigned)((m.fin + TM - 1) / TM), (unsigned)((m.fout + UNF - 1) / UNF), (unsigned)gn),
+                   UPD_THREADS_F, mat_smem(), st>>>(hA64[l], dA64[l + 1], sa, m, d_rows);
       if (int rc = check_launch("wide mat")) return rc;
     }
   }
