@@ -538,7 +538,41 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
   }
   __syncthreads();
   const float sc = a.mask_mode == FS_MASK_BITS ? a.scale : 1.f;
-  for (int u = threadIdx.x; u < N; u += blockDim.x) {
+  // a thread takes unit pairs (bf16x2 row accesses); H and D are different
+  // buffers (__restrict__), so the row loads of a pair are issued ahead of
+  // its D stores instead of one L2 round trip per row (the same products and
+  // sums in the same row order as one unit at a time)
+  const int npair = (N % 2 == 0 && ld % 2 == 0) ? N / 2 : 0;
+  const __nv_bfloat162* __restrict__ h2 = reinterpret_cast<const __nv_bfloat162*>(h);
+  __nv_bfloat162* __restrict__ d2 = reinterpret_cast<__nv_bfloat162*>(dout);
+  auto update = [&](int u, float w, float g, float gb) {
+    if (a.adam) {
+      wh[u] = opt_apply(a, sr, a.lay.woff[H] + u, w, g);
+      bprev[u] = opt_apply(a, sr, a.lay.boff[H - 1] + u, bprev[u], gb);
+    } else {
+      wh[u] = w - sr.lr * g;
+      bprev[u] -= sr.lr * gb;
+    }
+  };
+  for (int up = threadIdx.x; up < npair; up += blockDim.x) {
+    const float w0 = wh[2 * up], w1 = wh[2 * up + 1];
+    float g0 = 0.f, g1 = 0.f, gb0 = 0.f, gb1 = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < rb; ++r) {
+      const float2 hv = __bfloat1622float2(h2[(int64_t)r * (ld / 2) + up]);
+      const float dzr = s_dz[r];
+      g0 = fmaf(hv.x, dzr, g0);
+      g1 = fmaf(hv.y, dzr, g1);
+      const __nv_bfloat162 dv = __floats2bfloat162_rn(hv.x > 0.f ? dzr * w0 * sc : 0.f, hv.y > 0.f ? dzr * w1 * sc : 0.f);
+      d2[(int64_t)r * (ld / 2) + up] = dv;
+      const float2 df = __bfloat1622float2(dv);
+      gb0 += df.x;
+      gb1 += df.y;
+    }
+    update(2 * up, w0, g0, gb0);
+    update(2 * up + 1, w1, g1, gb1);
+  }
+  for (int u = 2 * npair + threadIdx.x; u < N; u += blockDim.x) {
     const float w = wh[u];
     float g = 0.f, gb = 0.f;
     for (int r = 0; r < rb; ++r) {
@@ -548,13 +582,7 @@ __global__ void __launch_bounds__(256) head_kernel(StepArgs a, const StepRow* ro
       dout[(int64_t)r * ld + u] = dv;
       gb += __bfloat162float(dv);
     }
-    if (a.adam) {
-      wh[u] = opt_apply(a, sr, a.lay.woff[H] + u, w, g);
-      bprev[u] = opt_apply(a, sr, a.lay.boff[H - 1] + u, bprev[u], gb);
-    } else {
-      wh[u] = w - sr.lr * g;
-      bprev[u] -= sr.lr * gb;
-    }
+    update(u, w, g, gb);
   }
   float t = 0.f;
   for (int r = threadIdx.x; r < rb; r += blockDim.x) t += s_dz[r];
