@@ -496,17 +496,22 @@ def measure_small_configs(precision: str):
     for name, cfg in cfgs.items():
         world, init = build_world(ExperimentConfig.from_dict(cfg), precision=precision)
         world.device_state()
-        FederationEngine(world).run(init)  # warm-up
+        for _ in range(2):  # warm-up (first-run allocations and module state)
+            FederationEngine(world).run(init)
         torch.cuda.synchronize()
-        eng = FederationEngine(world)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        eng.run(init)
-        b.record()
-        torch.cuda.synchronize()
-        sec = a.elapsed_time(b) / 1e3
+        secs = []
+        for _ in range(3):  # median of three whole runs (single runs vary with host scheduling)
+            eng = FederationEngine(world)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            eng.run(init)
+            b.record()
+            torch.cuda.synchronize()
+            secs.append(a.elapsed_time(b) / 1e3)
+        sec = float(np.median(secs))
         out[name] = {"clients": cfg["num_clients"], "rounds": cfg["rounds"], "rounds_per_s": cfg["rounds"] / sec,
                      "client_updates_per_s": eng.trainings / sec, "trainings": eng.trainings,
+                     "run_s": secs, "statistic": "median of 3 whole runs after 2 warm-up runs",
                      "digest": eng.timeline.digest()}
     return out
 

@@ -1,0 +1,29 @@
+"""Run-to-run spread of the small-config measurements (C1, C3 sync) (diagnostic)."""
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2503_15448_b200.config import ExperimentConfig  # noqa: E402
+from paper_2503_15448_b200.experiment import build_world  # noqa: E402
+from paper_2503_15448_b200.server import FederationEngine  # noqa: E402
+
+base = {"epochs": 5, "theta": 0.65, "seed": 1, "selection_mode": "delta_sign", "profiles": bench.C4_SYNC["profiles"],
+        "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}}
+c3 = dict(base, num_clients=256, rounds=5, mode="sync_filtered", batch={"policy": "fixed", "size": 64},
+          dataset={"kind": "synthetic", "d": 64, "samples_per_client": 256, "anomaly_frac": 0.1, "separation": 2.0,
+                   "test_frac": 0.2})
+world, init = build_world(ExperimentConfig.from_dict(c3), precision="bf16")
+world.device_state()
+for rep in range(8):
+    eng = FederationEngine(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    a.record()
+    eng.run(init)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"c3 run {rep}: {a.elapsed_time(b):.2f} ms device, {1e3 * (time.perf_counter() - t0):.2f} ms host", flush=True)
