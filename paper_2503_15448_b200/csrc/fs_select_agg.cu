@@ -835,8 +835,14 @@ extern "C" int fs_aggregate_jobs_weighted(const uint64_t* rows, const double* we
 // load batch), and the finish pass adds the groups in order and divides by k.
 // Deterministic for a given k; SPLIT_G x the column-strip parallelism of the
 // sequential K7, which at the C4 row length has only 205 strips.
-constexpr int SPLIT_G = 16, SPLIT_THREADS = 256, SPLIT_COLS = 4 * SPLIT_THREADS;
+// Long rows (the WIDE model's 3.2M parameters) take 8 groups and 8-row load
+// batches: 6.05 vs 5.20 TB/s at C5; the C4 row length keeps 16 x 4 (3.28 vs
+// 2.64 TB/s for 8 x 8), measured with bench.hbm_microbench.
+constexpr int SPLIT_THREADS = 256, SPLIT_COLS = 4 * SPLIT_THREADS;
+constexpr int64_t SPLIT_LONG = 1 << 20;
+inline int split_groups(int64_t M) { return M >= SPLIT_LONG ? 8 : 16; }
 
+template <int SPLIT_G, int BATCH>
 __global__ void __launch_bounds__(SPLIT_THREADS)
     rowsplit_partial_kernel(const uint64_t* rows, const int64_t* job_off, int64_t M, double* part) {
   const int k = (int)job_off[1];
@@ -848,12 +854,13 @@ __global__ void __launch_bounds__(SPLIT_THREADS)
   const bool vec = c + 4 <= M;
   int r = r0;
   if (vec) {
-    for (; r + 4 <= r1; r += 4) {
-      float4 v[4];
+    for (; r + BATCH <= r1; r += BATCH) {
+      float4 v[BATCH];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(rows[r + q]) + c));
+      for (int q = 0; q < BATCH; ++q)
+        v[q] = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(rows[r + q]) + c));
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < BATCH; ++q) {
         a0 += (double)v[q].x;
         a1 += (double)v[q].y;
         a2 += (double)v[q].z;
@@ -875,6 +882,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS)
   if (c + 3 < M) p[3] = a3;
 }
 
+template <int SPLIT_G>
 __global__ void rowsplit_finish_kernel(const double* part, const int64_t* job_off, int64_t M, const uint64_t* job_out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int k = (int)job_off[1];
@@ -886,7 +894,7 @@ __global__ void rowsplit_finish_kernel(const double* part, const int64_t* job_of
 }
 
 extern "C" size_t fs_aggregate_rowsplit_workspace_bytes(int64_t M) {
-  return M > 0 ? (size_t)SPLIT_G * (size_t)M * sizeof(double) : 0;
+  return M > 0 ? (size_t)split_groups(M) * (size_t)M * sizeof(double) : 0;
 }
 
 // One job (fs_select_rows output: rows in client order, job_off = {0, k},
@@ -905,10 +913,16 @@ extern "C" int fs_aggregate_rowsplit_f32(const uint64_t* rows, const int64_t* jo
   cudaStream_t st = (cudaStream_t)stream;
   (void)sorted_scratch;
   double* part = reinterpret_cast<double*>(workspace);
-  rowsplit_partial_kernel<<<dim3((unsigned)((M + SPLIT_COLS - 1) / SPLIT_COLS), SPLIT_G), SPLIT_THREADS, 0, st>>>(
-      rows, job_off, M, part);
-  if (int rc = check_launch("rowsplit_partial_kernel")) return rc;
-  rowsplit_finish_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, job_off, M, job_out);
+  const unsigned strips = (unsigned)((M + SPLIT_COLS - 1) / SPLIT_COLS);
+  if (split_groups(M) == 8) {
+    rowsplit_partial_kernel<8, 8><<<dim3(strips, 8), SPLIT_THREADS, 0, st>>>(rows, job_off, M, part);
+    if (int rc = check_launch("rowsplit_partial_kernel")) return rc;
+    rowsplit_finish_kernel<8><<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, job_off, M, job_out);
+  } else {
+    rowsplit_partial_kernel<16, 4><<<dim3(strips, 16), SPLIT_THREADS, 0, st>>>(rows, job_off, M, part);
+    if (int rc = check_launch("rowsplit_partial_kernel")) return rc;
+    rowsplit_finish_kernel<16><<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, job_off, M, job_out);
+  }
   return check_launch("rowsplit_finish_kernel");
 }
 

@@ -413,7 +413,7 @@ def test_bf16_sync_round_with_every_update_rejected_keeps_the_model(mode):
         assert aggs[0]["count"] == 24 and all(a["count"] == 0 for a in aggs[1:])
 
 
-@pytest.mark.parametrize("k,M", [(1, 52225), (37, 1000), (400, 52225), (1024, 3)])
+@pytest.mark.parametrize("k,M", [(1, 52225), (37, 1000), (400, 52225), (1024, 3), (21, 1_200_001)])
 def test_rowsplit_fedavg_matches_float64_mean(k, M):
     """bf16-mode FedAvg (fs_aggregate_rowsplit_f32: canonical order, 16 row
     groups with float64 partials added in order) equals the float64 mean of
