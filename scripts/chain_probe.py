@@ -25,7 +25,18 @@ NAMES = {0: "gather", 1: "F0 mma", 2: "F1 mma", 3: "F2 mma", 5: "F0 epi", 6: "F1
          4: "F0 sync", 8: "F0 issue", 10: "B1 sync", 15: "B1 issue", 16: "B1 W2 upd", 19: "F1 sync",
          21: "F1 issue", 22: "B0 sync", 23: "B0 issue"}
 
-world, init = bench.build_c4_world(precision="bf16")
+if os.environ.get("CHAIN_C3"):  # the C3 world (256 ROAD clients, b = 64)
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    cfg = {"epochs": 5, "theta": 0.65, "seed": 1, "selection_mode": "delta_sign", "profiles": bench.C4_SYNC["profiles"],
+           "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}, "num_clients": 256, "rounds": 5,
+           "mode": "sync_filtered", "batch": {"policy": "fixed", "size": 64},
+           "dataset": {"kind": "synthetic", "d": 64, "samples_per_client": 256, "anomaly_frac": 0.1,
+                       "separation": 2.0, "test_frac": 0.2}}
+    world, init = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+else:
+    world, init = bench.build_c4_world(precision="bf16")
 dev = world.device_state()
 rt = dev.rt
 spec = world.spec

@@ -11,7 +11,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2503_15448_b200.server import FederationEngine, GlobalState  # noqa: E402
 
-world, init = bench.build_c4_world(precision="bf16")
+if os.environ.get("TRACE_C3"):  # the C3 world (256 ROAD clients, b = 64) instead of C4
+    from paper_2503_15448_b200.config import ExperimentConfig
+    from paper_2503_15448_b200.experiment import build_world
+
+    cfg = {"epochs": 5, "theta": 0.65, "seed": 1, "selection_mode": "delta_sign", "profiles": bench.C4_SYNC["profiles"],
+           "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}, "num_clients": 256, "rounds": 100,
+           "mode": "sync_filtered", "batch": {"policy": "fixed", "size": 64},
+           "dataset": {"kind": "synthetic", "d": 64, "samples_per_client": 256, "anomaly_frac": 0.1,
+                       "separation": 2.0, "test_frac": 0.2}}
+    world, init = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
+else:
+    world, init = bench.build_c4_world(precision="bf16")
 eng = FederationEngine(world)
 state = GlobalState(round=0, w_g=init)
 for _ in range(4):
