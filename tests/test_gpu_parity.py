@@ -412,16 +412,18 @@ def test_client_sharded_rounds_match_single_process(prec, mode, sel, shape, engi
     assert "SHARDED OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
 
 
-def test_engine_keeps_caller_vectors_and_checkpoints_intact():
+def test_engine_keeps_caller_vectors_and_checkpoints_intact(monkeypatch):
     """A bf16 run does not turn the caller's float64 vector into float32
     (device_tensor() stays float64, values unchanged); every global
-    checkpoint keeps the model of its round although only the newest one
-    stays in HBM (older ones move to host memory); a checkpoint is a separate
-    vector from the engine state."""
+    checkpoint keeps the model of its round although older ones move to host
+    memory once the HBM budget is exceeded; a checkpoint is a separate vector
+    from the engine state."""
     from paper_2503_15448_b200.config import ExperimentConfig
     from paper_2503_15448_b200.experiment import build_world
+    from paper_2503_15448_b200 import server as S
     from paper_2503_15448_b200.server import FederationEngine, GlobalState
 
+    monkeypatch.setattr(S._HostArchive, "DEVICE_BUDGET", 1)  # spill everything the next round does not read
     cfg = {"num_clients": 12, "rounds": 4, "epochs": 1, "selection_mode": "delta_sign", "seed": 4,
            "dataset": {"n": 4000, "d": 42}, "model": {"hidden_dims": [256, 128, 64], "dropout_rate": 0.3}}
     world, initial = build_world(ExperimentConfig.from_dict(cfg), precision="bf16")
@@ -437,7 +439,8 @@ def test_engine_keeps_caller_vectors_and_checkpoints_intact():
     assert np.array_equal(initial.values, before)
     cps = eng.global_checkpoints
     assert [c.round for c in cps] == [0, 1, 2, 3]
-    # the newest stays in HBM; the one before it is spilled during the next round's trainer
+    # with the HBM budget exhausted, the two newest stay (the next round reads them);
+    # older ones were spilled during the following rounds' trainers
     assert [c.params.is_on_device for c in cps] == [False, False, True, True]
     for c, want in zip(cps, seen):
         assert np.array_equal(c.params.values, want)
