@@ -439,8 +439,8 @@ def test_engine_keeps_caller_vectors_and_checkpoints_intact(monkeypatch):
     assert np.array_equal(initial.values, before)
     cps = eng.global_checkpoints
     assert [c.round for c in cps] == [0, 1, 2, 3]
-    # with the HBM budget exhausted, the two newest stay (the next round reads them);
-    # older ones were spilled during the following rounds' trainers
+    # with the HBM budget exhausted only the newest stays; the others were
+    # spilled during the following rounds' trainers (the state keeps its own refs)
     assert [c.params.is_on_device for c in cps] == [False, False, True, True]
     for c, want in zip(cps, seen):
         assert np.array_equal(c.params.values, want)
