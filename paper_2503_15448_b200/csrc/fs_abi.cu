@@ -78,6 +78,14 @@ __global__ void publish_flag_kernel(int32_t* flag, int32_t v) {
 }
 }  // namespace
 
+void fs::preload_flag_publisher() {
+  static const bool done = [] {
+    cudaFuncAttributes at;
+    return cudaFuncGetAttributes(&at, publish_flag_kernel) == cudaSuccess;
+  }();
+  (void)done;
+}
+
 extern "C" int fs_publish_flag(int32_t* flag, int32_t value, void* stream) {
   if (!flag) {
     fs::set_error("fs_publish_flag: null flag");

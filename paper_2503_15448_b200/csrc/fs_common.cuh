@@ -50,6 +50,12 @@ inline int make_layout(const int32_t* dims, int32_t n_dims, MlpLayout* out) {
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+// Force-load the kernels that publish flags a trainer spins on (the flagged
+// K3 and fs_publish_flag). Under CUDA lazy loading the first launch of a
+// kernel may synchronise the context; if a consumer is already spinning on
+// its flags, that first launch would never return.
+void preload_mask_producer();
+void preload_flag_publisher();
 
 // wide-layer bf16 trainer (fs_train_wide.cu), reached through fs_train_bf16
 size_t wide_workspace_bytes(const fs_train_desc* d);

@@ -294,9 +294,9 @@ __global__ void __launch_bounds__(MASK_THREADS)
 // flags[r * max_steps + step]. The trainer of the same round runs
 // concurrently and waits per step on the flag (fs_train_desc.mask_flags), so
 // the mask generation overlaps its own round's trainer instead of the
-// previous round's tail. Per-thread LCG jumps come from constant memory.
-__constant__ LcgJump c_jt[MASK_THREADS];
-__constant__ LcgJump c_j1, c_jr;
+// previous round's tail. Per-thread LCG jumps are computed in the kernel (no
+// host-side table copy, which as a synchronous cudaMemcpyToSymbol could wait
+// behind a trainer that is itself waiting for these flags).
 
 __global__ void __launch_bounds__(MASK_THREADS)
     dropout_bits_step_kernel(const uint64_t* seeds, const int32_t* n_rows, const int32_t* batch,
@@ -318,13 +318,22 @@ __global__ void __launch_bounds__(MASK_THREADS)
   const int64_t slot = ((int64_t)B * sum_hidden + 31) / 32;
   const int rows = min(B, n - (st % spe) * B);
   mask_stream(sh_state, sh_inc, (int64_t)rows * sum_hidden, thresh, bits + mask_off[r] + (int64_t)st * slot,
-              c_jt[threadIdx.x], c_j1, c_jr);
+              lcg_jump(32ull * threadIdx.x), lcg_jump(32ull * MASK_THREADS),
+              lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32));
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + (int64_t)r * max_steps + st), "r"(tag)
                  : "memory");
   }
+}
+
+void preload_mask_producer() {
+  static const bool done = [] {
+    cudaFuncAttributes at;
+    return cudaFuncGetAttributes(&at, dropout_bits_step_kernel) == cudaSuccess;
+  }();
+  (void)done;
 }
 
 // ceil(keep * 2^53): keep-bit threshold on the 53-bit integer behind random()
@@ -432,16 +441,6 @@ extern "C" int fs_dropout_bits_flagged(const uint64_t* seeds, const int32_t* n_r
     return FS_EINVAL;
   }
   if (n_req == 0 || epochs == 0 || max_steps == 0) return FS_OK;
-  static bool jumps_ready = false;  // per-thread LCG jump constants (stream independent)
-  if (!jumps_ready) {
-    LcgJump jt[MASK_THREADS];
-    for (int t = 0; t < MASK_THREADS; ++t) jt[t] = lcg_jump(32ull * t);
-    const LcgJump j1 = lcg_jump(32ull * MASK_THREADS), jr = lcg_jump(32ull * MASK_THREADS * MASK_ILP - 32);
-    if (cudaMemcpyToSymbol(c_jt, jt, sizeof(jt)) != cudaSuccess || cudaMemcpyToSymbol(c_j1, &j1, sizeof(j1)) != cudaSuccess ||
-        cudaMemcpyToSymbol(c_jr, &jr, sizeof(jr)) != cudaSuccess)
-      return check_launch("fs_dropout_bits_flagged: jump table");
-    jumps_ready = true;
-  }
   const int64_t blocks = (int64_t)n_req * max_steps;
   if (blocks > 0x7FFFFFFF) {
     set_error("fs_dropout_bits_flagged: too many (request, step) blocks");

@@ -987,6 +987,8 @@ extern "C" int fs_train_bf16(const fs_train_desc* d, const void* features_bf16, 
   a.data_flags = d->data_flags;
   a.data_chunk = d->data_chunk;
   a.data_tag = d->data_tag;
+  if (a.mask_flags) preload_mask_producer();
+  if (a.data_flags) preload_flag_publisher();
   a.w_all = reinterpret_cast<const float*>(d->w_start_all);
   const bool v3 = g_bf16_force_generic == 0 && bf16t::geo_ok(g);
   if (!a.w_start && !(v3 && a.w_all)) {

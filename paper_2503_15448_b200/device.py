@@ -725,7 +725,7 @@ def run_trainer(plan: TrainPlan, lr: np.ndarray, w_start: np.ndarray, precision:
         _fused_align(plan, desc, align, stream)
     if plan.mask_flags is not None:
         if not plan.mask_tag:
-            raise ValueError("deferred keep bits: launch_masks() must run before the trainer")
+            raise ValueError("deferred keep bits need a nonzero mask_tag (the tag fs_dropout_bits_flagged publishes)")
         desc.mask_flags = plan.mask_flags.data_ptr()
         desc.mask_tag = plan.mask_tag
         desc.max_steps = plan.max_steps

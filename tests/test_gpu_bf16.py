@@ -438,3 +438,57 @@ def test_rowsplit_fedavg_matches_float64_mean(k, M):
     want = rows.double().mean(0).float().cpu()
     assert torch.equal(outs[0], outs[1])
     assert (outs[0] - want).abs().max().item() <= 1e-6 * max(1.0, want.abs().max().item())
+
+
+def test_flagged_keep_bits_feed_the_trainer_per_step():
+    """fs_dropout_bits_flagged (K3 publishing each (client, step) through a
+    release flag) running on a side stream concurrently with the unit-major
+    trainer that waits per step on the flags (fs_train_desc.mask_flags) gives
+    the same trained rows, bit for bit, as the trainer on complete bits."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=42, hidden_dims=(256, 128, 64), dropout_rate=0.3)
+    rng = np.random.default_rng(3)
+    sizes = [300, 77, 1024, 64, 500, 129]
+    feats = [rng.normal(size=(n, 42)) for n in sizes]
+    labs = [(rng.random(n) < 0.3).astype(np.int8) for n in sizes]
+    rt = D.Runtime.get()
+    shards = D.DeviceShards(feats, labs, rt)
+    w0 = torch.tensor(init_params(spec, 5).values, dtype=torch.float32, device="cuda")
+    k = len(sizes)
+    clients, seeds = np.arange(k), np.arange(k, dtype=np.uint64) + 40
+    batch = np.array([64, 64, 128, 64, 256, 64])
+    lr = np.full((k, 5), 0.05)
+    starts = np.full(k, w0.data_ptr(), dtype=np.uint64)
+
+    ref = D.TrainPlan(spec.dims, shards, clients, seeds, batch, 5, 0.3, rt=rt)
+    want, st_want = D.run_trainer(ref, lr, starts, "bf16")
+
+    for trainer_first in (True, False):
+        plan = D.TrainPlan(spec.dims, shards, clients, seeds, batch, 5, 0.3, rt=rt)
+        torch.cuda.synchronize()
+        plan.bits.zero_()  # the flagged K3 below regenerates every word the trainer reads
+        flags = torch.zeros(k * plan.max_steps, dtype=torch.int32, device="cuda")
+        plan.mask_flags, plan.mask_tag = flags, 7
+        # both on non-default streams: the legacy default stream would serialise them
+        main, side = torch.cuda.Stream(), torch.cuda.Stream()
+        main.wait_stream(torch.cuda.current_stream())
+        side.wait_stream(torch.cuda.current_stream())
+
+        def k3():
+            rt.call(rt.lib.fs_dropout_bits_flagged(plan.seeds_p, plan.n_rows_p, plan.batch_p, plan.mask_off_p,
+                                                   plan.order_p, k, 5, plan.max_steps, plan.sum_hidden, 0.7,
+                                                   plan.bits.data_ptr(), flags.data_ptr(), 7, side.cuda_stream),
+                    "fs_dropout_bits_flagged")
+
+        if not trainer_first:
+            k3()
+        with torch.cuda.stream(main):
+            got, st_got = D.run_trainer(plan, lr, starts, "bf16")  # waits per step on the flags
+        if trainer_first:
+            k3()
+        torch.cuda.synchronize()
+        assert int((flags == 7).sum()) == int(sum(5 * -(-n // b) for n, b in zip(sizes, batch)))
+        assert torch.equal(st_got.cpu(), st_want.cpu())
+        assert torch.equal(got.cpu(), want.cpu())
