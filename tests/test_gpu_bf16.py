@@ -92,14 +92,17 @@ def kernel_mode(request):
     lib.fs_bf16_force_generic(0)
 
 
-@pytest.mark.parametrize("rows,dropout", [(64, 0.3), (37, 0.3), (64, 0.0), (150, 0.3)])
+@pytest.mark.parametrize("rows,dropout", [(64, 0.3), (37, 0.3), (64, 0.0), (150, 0.3), (1, 0.3), (65, 0.3), (256, 0.3)])
 @pytest.mark.parametrize("dims", [UNSW, (20, 128, 128, 64, 1), (64, 256, 128, 64, 1)], ids=["unsw", "f1_128", "road"])
 def test_bf16_single_step_matches_fp32_emulation(rows, dropout, dims, kernel_mode):
     w0, got, want = _one_step(dims, rows, dropout)
     delta_w = want - w0
     err = (got - want).abs().max().item()
     scale = delta_w.abs().max().item()
-    assert err <= 2e-3 * scale, (err, scale)
+    # bf16 operands: unit roundoff u = 2^-9. Summed over >= 16 rows the
+    # per-element errors average out (2e-3 of the largest delta); a one-row
+    # step's delta is a single product of ~3 rounded factors (up to ~4u)
+    assert err <= (2e-3 if rows >= 16 else 4 * 2.0 ** -9) * scale, (err, scale)
     rel = ((got - want).norm() / delta_w.norm()).item()
     assert rel < 1e-2, rel
 
