@@ -31,6 +31,23 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+class _TimedLaunch:
+    __slots__ = ("timer", "name", "work", "stream", "a", "b")
+
+    def __init__(self, timer, name, work, stream):
+        self.timer, self.name, self.work, self.stream = timer, name, work, stream
+
+    def __enter__(self):
+        self.a, self.b = self.timer._event(), self.timer._event()
+        self.a.record(self.stream)
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record(self.stream)
+        self.timer.events.setdefault(self.name, []).append((self.a, self.b, self.work))
+        return False
+
+
 class KernelTimer:
     """Optional CUDA-event brackets around the hot launches (bench/profiling).
 
@@ -39,24 +56,22 @@ class KernelTimer:
     the algorithmic work (FLOPs or bytes) each launch carried.
     """
 
-    def __init__(self):
+    def __init__(self, prealloc: int = 512):
         self.events: dict[str, list] = {}
         self.launches = 0
+        # CUDA events are created on their first record: a primed pool keeps
+        # cudaEventCreate out of the launch path of the timed rounds
+        self._pool = [torch.cuda.Event(enable_timing=True) for _ in range(prealloc)]
+        for ev in self._pool:
+            ev.record()
 
-    def record(self, name: str, work: float, stream):
-        timer = self
+    def _event(self):
+        return self._pool.pop() if self._pool else torch.cuda.Event(enable_timing=True)
 
-        class _Ctx:
-            def __enter__(self_inner):
-                self_inner.a = torch.cuda.Event(enable_timing=True)
-                self_inner.b = torch.cuda.Event(enable_timing=True)
-                self_inner.a.record(stream)
-
-            def __exit__(self_inner, *exc):
-                self_inner.b.record(stream)
-                timer.events.setdefault(name, []).append((self_inner.a, self_inner.b, work))
-
-        return _Ctx()
+    def record(self, name: str, work: float, stream) -> "_TimedLaunch":
+        """Events around the launch; `ctx.work` may be set inside the block,
+        after the launch, so the host never delays the kernel to count it."""
+        return _TimedLaunch(self, name, work, stream)
 
     def summary(self) -> dict:
         out = {}
@@ -609,19 +624,18 @@ def _upload_waits(plan: TrainPlan, desc, up: dict, bf16: bool, stream) -> None:
 
 def _launch_trainer(plan: TrainPlan, desc, bf16: bool, stream) -> None:
     rt, lib, dims = plan.rt, plan.rt.lib, plan.dims
-    work = 0.0
-    if Runtime.timer is not None:  # algorithmic FLOPs of this launch (rows actually trained)
-        s, e, spe, b, nr = plan.start, plan.end, plan.spe, plan.batch, plan.n_rows
-        last = e // spe - s // spe   # epoch-final (partial) steps in [start, end)
-        rows = (e - s - last) * b + last * (nr - (spe - 1) * b)
-        work = float(rows.sum()) * mlp_flops_per_sample(dims)
-    with rt.timed("train", work):
+    with rt.timed("train", 0.0) as tm:
         if bf16:
             xb, yf = plan.shards.bf16()
             rt.call(lib.fs_train_bf16(ctypes.byref(desc), xb.data_ptr(), yf.data_ptr(), stream.cuda_stream),
                     "fs_train_bf16")
         else:
             rt.call(lib.fs_train_f64(ctypes.byref(desc), stream.cuda_stream), "fs_train_f64")
+        if tm is not None:  # algorithmic FLOPs of this launch (rows actually trained), counted after it
+            s, e, spe, b, nr = plan.start, plan.end, plan.spe, plan.batch, plan.n_rows
+            last = e // spe - s // spe   # epoch-final (partial) steps in [start, end)
+            rows = (e - s - last) * b + last * (nr - (spe - 1) * b)
+            tm.work = float(rows.sum()) * mlp_flops_per_sample(dims)
 
 
 def _fused_align(plan: TrainPlan, desc, align, stream) -> None:
