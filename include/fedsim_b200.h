@@ -57,6 +57,14 @@ int fs_fill_u64(uint64_t* dst, uint64_t value, int64_t n, void* stream);
 /* flag[0] = value after all work queued before it on `stream` (release store):
  * publishes a chunk of an upload to kernels polling on other streams     */
 int fs_publish_flag(int32_t* flag, int32_t value, void* stream);
+/* chunked host -> device upload of two row-aligned arrays (page-locked host
+ * memory): for chunk c = rows [bounds[2c], bounds[2c+1]) the rows of a
+ * (a_row_bytes each) and of b (b_row_bytes each) are copied, then
+ * flags[c] = tag is published as by fs_publish_flag; one call per upload
+ * instead of three per chunk (the re-upload of DeviceWorld.refill)        */
+int fs_upload_chunks(void* dst_a, const void* src_a, int64_t a_row_bytes, void* dst_b, const void* src_b,
+                     int64_t b_row_bytes, const int64_t* bounds, int32_t n_chunks, int32_t* flags, int32_t tag,
+                     void* stream);
 /* stream-ordered device-to-device copy (engine-owned model versions -> caller tensors) */
 int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 

@@ -102,6 +102,8 @@ _SIGNATURES = {
     "fs_memcpy_d2d": (ctypes.c_int, [_c_vp, _c_vp, _c_sz, _c_vp]),
     "fs_fill_u64": (ctypes.c_int, [_c_vp, _c_u64, _c_i64, _c_vp]),
     "fs_publish_flag": (ctypes.c_int, [_c_vp, _c_i32, _c_vp]),
+    "fs_upload_chunks": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_vp, _c_i32,
+                                        _c_vp]),
     "fs_derive_seed_host": (ctypes.c_int, [_c_u64, ctypes.POINTER(ctypes.c_uint32), _c_i32, ctypes.POINTER(_c_u64)]),
     "fs_train_seeds_host": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp]),
     "fs_train_seeds": (ctypes.c_int, [_c_u64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp]),

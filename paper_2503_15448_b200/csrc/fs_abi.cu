@@ -95,6 +95,33 @@ extern "C" int fs_publish_flag(int32_t* flag, int32_t value, void* stream) {
   return fs::check_launch("publish_flag_kernel");
 }
 
+extern "C" int fs_upload_chunks(void* dst_a, const void* src_a, int64_t a_row_bytes, void* dst_b,
+                                const void* src_b, int64_t b_row_bytes, const int64_t* bounds, int32_t n_chunks,
+                                int32_t* flags, int32_t tag, void* stream) {
+  if (n_chunks < 0 || a_row_bytes < 0 || b_row_bytes < 0 || (n_chunks > 0 && (!bounds || !flags))) {
+    fs::set_error("fs_upload_chunks: invalid arguments");
+    return FS_EINVAL;
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  for (int32_t c = 0; c < n_chunks; ++c) {
+    const int64_t r0 = bounds[2 * c], r1 = bounds[2 * c + 1];
+    if (r1 < r0 || r0 < 0) {
+      fs::set_error("fs_upload_chunks: chunk %d has rows [%lld, %lld)", c, (long long)r0, (long long)r1);
+      return FS_EINVAL;
+    }
+    if (r1 > r0 && a_row_bytes > 0 &&
+        cudaMemcpyAsync(static_cast<char*>(dst_a) + r0 * a_row_bytes, static_cast<const char*>(src_a) + r0 * a_row_bytes,
+                        (size_t)((r1 - r0) * a_row_bytes), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return fs::check_launch("fs_upload_chunks");
+    if (r1 > r0 && b_row_bytes > 0 &&
+        cudaMemcpyAsync(static_cast<char*>(dst_b) + r0 * b_row_bytes, static_cast<const char*>(src_b) + r0 * b_row_bytes,
+                        (size_t)((r1 - r0) * b_row_bytes), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return fs::check_launch("fs_upload_chunks");
+    publish_flag_kernel<<<1, 1, 0, st>>>(flags + c, tag);
+  }
+  return fs::check_launch("fs_upload_chunks");
+}
+
 extern "C" int fs_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return FS_OK;
   if (!dst || !src) {
