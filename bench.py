@@ -314,16 +314,17 @@ def measure_rounds(world, initial, comm, steps: int, warmup: int, device_index: 
             "trainings": eng.trainings - trainings0, "clocks": clocks.summary(), "barrier": barrier}
 
 
-def measure_e2e(world, eng, state, reps: int, barrier):
+def measure_e2e(world, eng, state, reps: int, barrier, warmup: int = 3):
     """Same metric through the public API with HOST inputs: every step uploads
-    the world's shards and test set from page-locked host memory and reads w_g back."""
+    the world's shards and test set from page-locked host memory and reads w_g
+    back; `warmup` untimed steps of the same kind first."""
     import torch
 
     stream = torch.cuda.current_stream()
     world.host_pack()  # page-locked host copies prepared once, outside the timed region
     e2e_ms = []
     h2d = d2h = 0
-    for i in range(reps + 1):
+    for i in range(reps + warmup):
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -333,7 +334,7 @@ def measure_e2e(world, eng, state, reps: int, barrier):
         host_w = state.w_g.values
         b.record(stream)
         barrier()
-        if i > 0:
+        if i >= warmup:
             e2e_ms.append(a.elapsed_time(b))
         h2d = dev.h2d_bytes
         d2h = host_w.nbytes + world.num_clients * 8 * 2
@@ -636,7 +637,8 @@ def run_b200(args, rank: int, world_size: int) -> None:
     world, initial = build_c4_world(precision=args.precision)
     m = measure_rounds(world, initial, comm, args.steps, args.warmup, local)
     value = 1000.0 / m["ms_per_round"]
-    e2e_value, h2d, d2h = measure_e2e(world, m["engine"], m["state"], max(2, args.steps // 2), m["barrier"])
+    e2e_value, h2d, d2h = measure_e2e(world, m["engine"], m["state"], max(5, args.steps // 2), m["barrier"],
+                                      warmup=max(3, args.warmup))
     parity = None
     if not args.no_parity:
         w64, i64 = build_c4_world(precision="fp64")
