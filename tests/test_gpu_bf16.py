@@ -495,3 +495,33 @@ def test_flagged_keep_bits_feed_the_trainer_per_step():
         assert int((flags == 7).sum()) == int(sum(5 * -(-n // b) for n, b in zip(sizes, batch)))
         assert torch.equal(st_got.cpu(), st_want.cpu())
         assert torch.equal(got.cpu(), want.cpu())
+
+
+def test_kernel_timer_counts_trainer_work_after_the_launch():
+    """KernelTimer (bench.py's live kernel timing) brackets the trainer launch
+    with events and records its algorithmic FLOPs, counted after the launch:
+    rows actually trained x FLOP per sample."""
+    from paper_2503_15448_b200 import device as D
+    from paper_2503_15448_b200.model import ModelSpec, init_params
+
+    spec = ModelSpec(input_dim=42, hidden_dims=(256, 128, 64), dropout_rate=0.3)
+    rng = np.random.default_rng(5)
+    sizes = [300, 77, 129]
+    feats = [rng.normal(size=(n, 42)) for n in sizes]
+    labs = [(rng.random(n) < 0.3).astype(np.int8) for n in sizes]
+    rt = D.Runtime.get()
+    shards = D.DeviceShards(feats, labs, rt)
+    w0 = torch.tensor(init_params(spec, 5).values, dtype=torch.float32, device="cuda")
+    k = len(sizes)
+    D.Runtime.timer = D.KernelTimer(prealloc=4)
+    try:
+        D.train_batch(spec.dims, shards, np.arange(k), np.arange(k, dtype=np.uint64) + 3, np.full((k, 2), 0.05),
+                      np.full(k, w0.data_ptr(), dtype=np.uint64), np.array([64, 64, 128]), 2, 0.3, rt=rt,
+                      precision="bf16")
+        torch.cuda.synchronize()
+        summary = D.Runtime.timer.summary()
+    finally:
+        D.Runtime.timer = None
+    tr = summary["train"]
+    assert tr["launches"] == 1 and tr["mean_ms"] > 0
+    assert tr["work_per_launch"] == 2 * sum(sizes) * D.mlp_flops_per_sample(spec.dims)
